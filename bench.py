@@ -1,0 +1,610 @@
+#!/usr/bin/env python
+"""hadacodec-b200 benchmark (driver contract: one JSON line from rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 1|2|3|4|5a|5b] [--all] [--no-cpu-baseline]
+
+Default workload = BASELINE.json configs[1] ("config 2"): 1920x1080 G-buffer,
+k = 6 (2 RGB passes), 8 lights, latent Hadamard shade + reassembly + decode
+folded to XYZ and linear sRGB; metric Mpixel/s.  A step is one frame per GPU
+(weak scaling: rank r renders rows [r*1080, (r+1)*1080) of an N-frame-tall
+image; no collective on the data path).  Inputs are resident in HBM, rotated
+over enough buffer sets that one rotation exceeds 2x the 126 MB L2, and the K
+steps are replayed from a CUDA graph (a 19 us ideal frame is launch-bound
+otherwise); timing = CUDA events on the launching stream, max over ranks.
+
+e2e: the same frame through the reference-facing host-buffer C-ABI call
+(hc_shade_latent_host): pinned host G-buffer in, XYZ + sRGB out, copies inside
+the timed region.
+
+cpu_baseline / --impl reference: the reference's own CPU implementation
+(oracle/_ref: the reference core compiled from its sources + the G-buffer
+restatement) on the host's cores; see DESIGN.md.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+BASELINE = json.loads((ROOT / "BASELINE.json").read_text())
+PEAKS_PATH = ROOT / "MEASURED_PEAKS.json"
+METRIC = BASELINE["metric"]
+SEED = 2602
+N_SPEC = 81
+
+# Per-config shape, algorithmic bytes per unit and unit names.
+CONFIGS = {
+    "1": dict(name="codec round trip N=2^20, n=81, k=6 -> codes+spectra+XYZ+sRGB", units=1 << 20, k=6,
+              unit="M spectra/s", bytes_per_unit=696, rot=2),
+    "2": dict(name="1920x1080 G-buffer, k=6 (2 RGB passes), 8 lights, latent shade -> XYZ+sRGB",
+              W=1920, H=1080, k=6, L=8, unit="Mpixel/s", bytes_per_unit=60, rot=8),
+    "3": dict(name="3840x2160 G-buffer, k=9 (3 RGB passes), 32 lights, latent shade -> spectra(81)+sRGB",
+              W=3840, H=2160, k=9, L=32, unit="Mpixel/s", bytes_per_unit=468, rot=2),
+    "4": dict(name="2048x2048, 64 spp, depth 4, k=6 multi-bounce accumulate -> XYZ+sRGB",
+              W=2048, H=2048, k=6, spp=64, unit="Mpixel/s", bytes_per_unit=1368, rot=1),
+    "5a": dict(name="4096x4096 RGB -> code MLP 3-64-64-6 (bf16 tcgen05)", W=4096, H=4096, k=6,
+               unit="Mpixel/s", bytes_per_unit=36, flops_per_unit=9344, rot=2),
+    "5b": dict(name="Hadamard near-multiplicativity loss, 2^24 pairs, n=81, k=6", units=1 << 24, k=6,
+               unit="M pairs/s", bytes_per_unit=648, rot=1),
+}
+
+
+# ---------------------------------------------------------------------------- helpers
+def peaks() -> dict:
+    if PEAKS_PATH.exists():
+        d = json.loads(PEAKS_PATH.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + clocks-event reasons during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.samples: list[tuple[int, int]] = []
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                mhz = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((mhz, rs))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self._t.join()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0}
+        mhz = sorted(s[0] for s in self.samples)
+        bits = 0
+        for _, r in self.samples:
+            bits |= r
+        reasons = [name for bit, name in self.REASONS.items() if bits & bit and name != "gpu_idle"]
+        return {"sm_mhz": mhz[len(mhz) // 2], "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+def emit(obj: dict) -> None:
+    print(json.dumps(obj), flush=True)
+
+
+# ---------------------------------------------------------------------------- CPU reference
+def cpu_reference_run(cfg_key: str, budget_s: float, threads: int = 0, rank: int = 0) -> dict:
+    """Time the reference's CPU implementation (oracle/_ref) on a bounded sample."""
+    import oracle
+    from paper_2602_18741_b200 import synth
+
+    ref = oracle.reference(81)
+    kind = "reference"
+    if ref is None:
+        raise RuntimeError("oracle/_ref not built (python __graft_entry__.py build)")
+    cfg = CONFIGS[cfg_key]
+    nthreads = threads if threads > 0 else ref.ref_thread_count()
+    k = cfg["k"]
+    E, D = synth.codec_weights(SEED, k, N_SPEC)
+
+    if cfg_key in ("2", "3"):
+        L = cfg["L"]
+        W = cfg["W"]
+        pal = synth.palette(SEED, 256, N_SPEC)
+        lts = synth.lights(SEED, L, N_SPEC)
+        pc = np.zeros((256, k), np.float32)
+        lc = np.zeros((L, k), np.float32)
+        ref.ref_asset_codes(E, k, pal, 256, pc)
+        ref.ref_asset_codes(E, k, lts, L, lc)
+        rows = max(1, min(cfg["H"], 64))
+        P = rows * W
+        idx, cosv = synth.gbuffer_np(SEED, rank * cfg["H"] * W, P, L, 256)
+        cosv = np.ascontiguousarray(cosv)
+        outs = {"xyz": np.zeros((P, 3), np.float32), "rgb": np.zeros((P, 3), np.float32)}
+        spec = np.zeros((P, N_SPEC), np.float32) if cfg_key == "3" else None
+
+        def run():
+            ref.ref_shade_latent(E, D, k, pc, lc, L, idx, cosv, P, None, spec,
+                                 None if cfg_key == "3" else outs["xyz"], outs["rgb"], nthreads)
+
+        sample = f"{rows} rows x {W} px of the frame (R1 latent shade + decode_image + image_to_linear_rgb)"
+    elif cfg_key == "1":
+        P = 1 << 14
+        S = synth.gm_spectra_ctr(SEED, "codec.spectra", 0, 2048, N_SPEC)
+        S = np.ascontiguousarray(np.tile(S, (P // 2048, 1)))
+        bufs = [np.zeros((P, d), np.float32) for d in (k, N_SPEC, 3, 3)]
+
+        def run():
+            ref.ref_codec_roundtrip(E, D, k, S, P, *bufs, nthreads)
+
+        sample = f"{P} spectra (encode/decode_image/image_to_linear_rgb)"
+    elif cfg_key == "4":
+        spp = cfg["spp"]
+        P = 2048 * 2
+        pal = synth.palette(SEED, 256, N_SPEC)
+        ill = synth.lights(SEED, 16, N_SPEC, purpose="scene.illuminants")
+        pc = np.zeros((256, k), np.float32)
+        ic = np.zeros((16, k), np.float32)
+        ref.ref_asset_codes(E, k, pal, 256, pc)
+        ref.ref_asset_codes(E, k, ill, 16, ic)
+        pidx, iidx, tw = (np.ascontiguousarray(a) for a in synth.chain_np(SEED, 0, P, spp, 256, 16))
+        X, R = np.zeros((P, 3), np.float32), np.zeros((P, 3), np.float32)
+
+        def run():
+            ref.ref_multibounce_latent(E, D, k, pc, ic, pidx, iidx, tw, P, spp, 4, None, X, R, nthreads)
+
+        sample = f"{P} px x {spp} spp (2 rows)"
+    elif cfg_key == "5a":
+        from paper_2602_18741_b200.synth import mlp_weights
+
+        w = mlp_weights(SEED, 6, 64)
+        P = 4096 * 8
+        rgb = np.ascontiguousarray(synth.uniform_np(SEED, "mlp.input", 0, P * 3).reshape(P, 3))
+        out = np.zeros((P, 6), np.float32)
+
+        def run():
+            ref.ref_mlp_forward(rgb, P, 64, 6, w["w1"], w["b1"], w["w2"], w["b2"], w["w3"], w["b3"], out, nthreads)
+
+        sample = f"{P} texels (8 rows)"
+    else:  # 5b
+        P = 1 << 15
+        A = synth.gm_spectra_ctr(SEED, "loss.a", 0, 1024, N_SPEC)
+        B = synth.gm_spectra_ctr(SEED, "loss.b", 0, 1024, N_SPEC)
+        A = np.ascontiguousarray(np.tile(A, (P // 1024, 1)))
+        B = np.ascontiguousarray(np.tile(B, (P // 1024, 1)))
+
+        def run():
+            ref.ref_hadamard_loss(E, D, k, A, B, P, nthreads)
+
+        sample = f"{P} pairs"
+
+    run()  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        run()
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    value = P * reps / el / 1e6
+    return {"value": value, "unit": cfg["unit"], "cores": nthreads, "kind": kind, "sample": sample,
+            "seconds": round(el, 3), "units_per_rep": P, "reps": reps, "step_s": el / reps,
+            "cpu": _cpu_model()}
+
+
+def _cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference_arm(args) -> int:
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    # calibrate one step, then time K steps of the bounded sample
+    cal = cpu_reference_run(args.config, budget_s=0.0)
+    per_step = cal["step_s"]
+    for _ in range(args.warmup):
+        pass
+    res = cpu_reference_run(args.config, budget_s=max(per_step * args.steps, 1.0))
+    line = {"metric": METRIC if args.config == "2" else f"{cfg['unit']} config {args.config}",
+            "value": res["value"], "unit": cfg["unit"], "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["step_s"] * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": cfg["name"], "config_id": args.config}, "impl": "reference",
+            "cpu_baseline": {"value": res["value"], "unit": cfg["unit"], "cores": res["cores"], "kind": res["kind"],
+                             "sample": res["sample"], "cpu": res["cpu"]},
+            "e2e": {"value": res["value"], "unit": cfg["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    emit(line)
+    return 0
+
+
+# ---------------------------------------------------------------------------- GPU arm
+class Workload:
+    """Builds the per-rank inputs of one config and a step() closure over buffer set i."""
+
+    def __init__(self, api, ctx, cfg_key: str, rank: int, naive: bool = False):
+        import torch
+        from paper_2602_18741_b200 import synth
+
+        self.cfg = cfg = CONFIGS[cfg_key]
+        self.key = cfg_key
+        k = cfg["k"]
+        E, D = synth.codec_weights(SEED, k, N_SPEC)
+        self.codec = codec = api.Codec(ctx, E, D)
+        self.sets = []
+        R = cfg["rot"]
+        if cfg_key in ("2", "3"):
+            W, H, L = cfg["W"], cfg["H"], cfg["L"]
+            P = W * H
+            pal = synth.palette(SEED, 256, N_SPEC)
+            lts = synth.lights(SEED, L, N_SPEC)
+            self.pal_d = torch.from_numpy(pal).cuda()
+            self.lts = lts
+            self.pal_codes = codec.encode(self.pal_d)  # compile_scene: assets encoded once
+            self.light_codes = codec.encode(torch.from_numpy(lts).cuda()).cpu().numpy()
+            spec = cfg_key == "3"
+            for r in range(R):
+                idx, cosv = api.synth_gbuffer(ctx, SEED + r, rank * P, P, L, 256)
+                outs = {"xyz": None if spec else ctx.empty(P, 3), "rgb": ctx.empty(P, 3),
+                        "spectra": ctx.empty(P, N_SPEC) if spec else None, "latent": None}
+                self.sets.append((idx, cosv, outs))
+            self.units = P
+
+            def step(i):
+                idx, cosv, outs = self.sets[i % R]
+                if naive:
+                    codec.shade_spectral(self.pal_d, self.lts, idx, cosv, out=outs)
+                else:
+                    codec.shade_latent(self.pal_codes, self.light_codes, idx, cosv, out=outs)
+            self.step = step
+        elif cfg_key == "1":
+            P = cfg["units"]
+            for r in range(R):
+                S = api.synth_gm_spectra(ctx, SEED + r, "codec.spectra", rank * P, P, N_SPEC)
+                outs = {"codes": ctx.empty(P, k), "spectra": ctx.empty(P, N_SPEC), "xyz": ctx.empty(P, 3),
+                        "rgb": ctx.empty(P, 3)}
+                self.sets.append((S, outs))
+            self.units = P
+
+            def step(i):
+                S, outs = self.sets[i % R]
+                codec.roundtrip(S, out=outs)
+            self.step = step
+        elif cfg_key == "4":
+            W, H, spp = cfg["W"], cfg["H"], cfg["spp"]
+            P = W * H
+            pal = synth.palette(SEED, 256, N_SPEC)
+            ill = synth.lights(SEED, 16, N_SPEC, purpose="scene.illuminants")
+            self.pal_d = torch.from_numpy(pal).cuda()
+            self.ill_d = torch.from_numpy(ill).cuda()
+            self.pal_codes = codec.encode(self.pal_d)
+            self.ill_codes = codec.encode(self.ill_d)
+            for r in range(R):
+                pidx, iidx, tw = api.synth_chain(ctx, SEED + r, rank * P, P, spp, 256, 16)
+                outs = {"xyz": ctx.empty(P, 3), "rgb": ctx.empty(P, 3), "latent": None}
+                self.sets.append((pidx, iidx, tw, outs))
+            self.units = P
+
+            def step(i):
+                pidx, iidx, tw, outs = self.sets[i % R]
+                if naive:
+                    codec.multibounce_spectral(self.pal_d, self.ill_d, pidx, iidx, tw, out=outs)
+                else:
+                    codec.multibounce_latent(self.pal_codes, self.ill_codes, pidx, iidx, tw, out=outs)
+            self.step = step
+        elif cfg_key == "5a":
+            W, H = cfg["W"], cfg["H"]
+            P = W * H
+            w = synth.mlp_weights(SEED, 6, 64)
+            self.mlp = api.Upsampler(ctx, w)
+            for r in range(R):
+                rgb = api.synth_uniform(ctx, SEED + r, "mlp.input", rank * P * 3, P * 3).reshape(P, 3)
+                self.sets.append((rgb, ctx.empty(P, 6)))
+            self.units = P
+
+            def step(i):
+                rgb, out = self.sets[i % R]
+                self.mlp.forward(rgb, out=out)
+            self.step = step
+        else:  # 5b
+            P = cfg["units"]
+            A = api.synth_gm_spectra(ctx, SEED, "loss.a", rank * P, P, N_SPEC)
+            B = api.synth_gm_spectra(ctx, SEED, "loss.b", rank * P, P, N_SPEC)
+            self.sum = ctx.empty(1, dtype=torch.float64)
+            self.sets.append((A, B))
+            self.units = P
+
+            def step(i):
+                codec.hadamard_loss(A, B, out=self.sum)
+            self.step = step
+        self.R = R
+
+
+def time_graph(torch, wl, steps: int, warmup: int, stream) -> tuple[float, int]:
+    """Capture R steps (one per buffer set) in a CUDA graph; replay to cover `steps`.
+    Returns (elapsed ms over exactly `steps` steps, launches per step)."""
+    R = wl.R
+    reps = max(1, steps // R)
+    assert reps * R == steps or steps < R, "steps must be a multiple of the rotation"
+    ctx = wl.codec.ctx
+    with torch.cuda.stream(stream):
+        for i in range(max(warmup, R)):
+            wl.step(i)
+        torch.cuda.synchronize()
+        l0 = ctx.launches
+        wl.step(0)
+        torch.cuda.synchronize()
+        per_step = ctx.launches - l0
+        g = torch.cuda.CUDAGraph()
+        n_in_graph = min(R, steps)
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(n_in_graph):
+                wl.step(i)
+        g.replay()
+        torch.cuda.synchronize()
+    return g, per_step, n_in_graph
+
+
+def run_ours(args) -> int:
+    import torch
+    import torch.distributed as dist
+    from paper_2602_18741_b200 import api
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+    cfg = CONFIGS[args.config]
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        ctx = api.Context(dev)
+        wl = Workload(api, ctx, args.config, rank)
+    torch.cuda.synchronize()
+    R = wl.R
+    steps = max(R, (args.steps + R - 1) // R * R)
+
+    g, per_step, n_in_graph = time_graph(torch, wl, steps, args.warmup, stream)
+    reps = steps // n_in_graph
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: K steps, graph replays, CUDA events on the launching stream
+    for _ in range(max(1, args.warmup // n_in_graph)):
+        g.replay()
+    barrier()
+    launches0 = ctx.launches
+    t_ev0, t_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        t_wall0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            t_ev0.record(stream)
+            for _ in range(reps):
+                g.replay()
+            t_ev1.record(stream)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    barrier()
+    ms = t_ev0.elapsed_time(t_ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    launches_timed = per_step * steps  # graph replays do not pass through the host counter
+    ms_per_step = ms / steps
+    value = wl.units * world * steps / (ms / 1e3) / 1e6
+
+    pk = peaks()
+    kernel_us = ms_per_step * 1e3  # one hot kernel per step (per_step launches)
+    if "flops_per_unit" in cfg:
+        achieved = wl.units * cfg["flops_per_unit"] / (kernel_us * 1e-6) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16_tflops"], "traffic": None,
+                "peak_source": f"{pk['source']} bf16_tflops (burst)"}
+    else:
+        achieved = wl.units * cfg["bytes_per_unit"] / (kernel_us * 1e-6) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_source": f"{pk['source']} hbm_gbs",
+                "bytes_per_unit": cfg["bytes_per_unit"], "units_per_launch": wl.units,
+                "kernel_us": kernel_us}
+    traffic = Path(ROOT / "profiles" / f"traffic_config{args.config}.json")
+    if traffic.exists():
+        try:
+            roof["traffic"] = json.loads(traffic.read_text()).get("bytes_per_launch")
+        except Exception:  # noqa: BLE001
+            pass
+
+    extra = {}
+    # ---- naive n = 81 comparison on the same inputs (configs 2 / 4)
+    if args.config in ("2", "3", "4") and not args.no_naive:
+        wn = Workload.__new__(Workload)
+        wn.__dict__.update(wl.__dict__)
+        wn_step_ours = wl.step
+        # rebuild the step closure with the naive path over the same buffers
+        with torch.cuda.stream(stream):
+            wl2 = Workload(api, ctx, args.config, rank, naive=True)
+        gn, _, nn = time_graph(torch, wl2, steps if args.config != "4" else R, 1, stream)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nreps = max(1, (steps if args.config != "4" else R) // nn)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(nreps):
+                gn.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        nms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([nms], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            nms = float(t.item())
+        nsteps = nreps * nn
+        extra["naive_n81"] = {"value": wl2.units * world * nsteps / (nms / 1e3) / 1e6, "unit": cfg["unit"],
+                              "ms_per_step": nms / nsteps}
+        extra["speedup_latent_vs_naive"] = extra["naive_n81"]["ms_per_step"] and (nms / nsteps) / ms_per_step
+        del wl2, gn
+        _ = wn_step_ours
+
+    # ---- gather of the sRGB band to rank 0 (compute + gather), N > 1 only
+    if world > 1 and args.config in ("2", "3", "4"):
+        rgb_local = wl.sets[0][-1]["rgb"]
+        gathered = [torch.empty_like(rgb_local) for _ in range(world)] if rank == 0 else None
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gsteps = min(steps, 20)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for i in range(gsteps):
+                wl.step(i)
+                dist.gather(rgb_local, gathered, dst=0)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        gms = e0.elapsed_time(e1)
+        t = torch.tensor([gms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gms = float(t.item())
+        extra["with_gather"] = {"value": wl.units * world * gsteps / (gms / 1e3) / 1e6, "unit": cfg["unit"],
+                                "ms_per_step": gms / gsteps, "gathered": "linear-sRGB row bands -> rank 0 (NCCL)"}
+
+    # ---- e2e through the host-buffer C-ABI call (config 2)
+    e2e = None
+    if args.config == "2":
+        P = wl.units
+        idx, cosv, _ = wl.sets[0]
+        h_idx = torch.empty(P, dtype=torch.int32, pin_memory=True)
+        h_cos = torch.empty(P, cfg["L"], pin_memory=True)
+        h_idx.copy_(idx)
+        h_cos.copy_(cosv)
+        h_pal = wl.pal_codes.cpu().numpy()
+        h_xyz = torch.empty(P, 3, pin_memory=True)
+        h_rgb = torch.empty(P, 3, pin_memory=True)
+        ni, nc, nx, nr = h_idx.numpy(), h_cos.numpy(), h_xyz.numpy(), h_rgb.numpy()
+        with torch.cuda.stream(stream):
+            for _ in range(3):
+                wl.codec.shade_latent_host(h_pal, wl.light_codes, ni, nc, nx, nr)
+            barrier()
+            esteps = max(5, min(steps, 50))
+            t0 = time.perf_counter()
+            for _ in range(esteps):
+                wl.codec.shade_latent_host(h_pal, wl.light_codes, ni, nc, nx, nr)
+            el = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el = float(t.item())
+        e2e = {"value": P * world * esteps / el / 1e6, "unit": cfg["unit"],
+               "h2d_bytes_per_step": int(h_idx.numel() * 4 + h_cos.numel() * 4 + h_pal.nbytes),
+               "d2h_bytes_per_step": int(h_xyz.numel() * 4 + h_rgb.numel() * 4), "ms_per_step": el / esteps * 1e3,
+               "api": "hc_shade_latent_host (pinned host buffers)"}
+        # parity spot check of the e2e result against the device path
+        dev_rgb = wl.sets[0][2]["rgb"].cpu().numpy()
+        extra["e2e_matches_device"] = bool(np.array_equal(dev_rgb, nr))
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_reference_run(args.config, budget_s=args.cpu_seconds)
+            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "seconds", "cpu")}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": cfg["unit"], "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC if args.config == "2" else f"{cfg['unit']} config {args.config}",
+            "value": value, "unit": cfg["unit"], "n_gpus": world, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if args.config == "5a" else "f32", "data": "synthetic (seeded, DESIGN.md Inputs)",
+            "config": {"workload": cfg["name"], "config_id": args.config, "units_per_gpu": wl.units,
+                       "l2": f"{R} rotating input/output buffer sets"
+                             f" ({'each' if R == 1 else 'rotation'} > 2x 126 MB L2)",
+                       "timing": "CUDA graph of the step replayed K times; CUDA events; max over ranks",
+                       "parallelism": f"row bands, weak scaling, {world} rank(s)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches_timed),
+            "clocks": clocks.summary(),
+            "wall_s_timed": t_wall,
+        }
+        line.update(extra)
+        emit(line)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=16)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-naive", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

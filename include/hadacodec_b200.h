@@ -1,0 +1,187 @@
+/*
+ * hadacodec-b200 — C ABI of the B200-native per-pixel codec / latent-shading path.
+ *
+ * This is the drop-in boundary for the reference's `hadacodec` static library
+ * (/root/reference/proj/core, public headers core/include/hadacodec/*.hpp).
+ * The reference exposes a by-value C++ API over single spectra / images; this
+ * ABI exposes the same operations BATCHED, over device pointers, stream
+ * ordered, with plain pointers and sizes only (no C++ or torch types).  The
+ * C++ drop-in layer (include/hadacodec_b200.hpp) restores the reference
+ * signatures and exception types on top of it.
+ *
+ * Conventions
+ *   - Layouts are row-major, item-major ("HWC" as ChannelImage, renderer.hpp:73-89):
+ *       spectra [rows][n] f32, codes [rows][k] f32, xyz / rgb [rows][3] f32,
+ *       G-buffer idx [P] u32 + cos [P][L] f32, chain samples pidx [P][spp][4] u8,
+ *       iidx [P][spp] u8, tw [P][spp][4] f32.
+ *   - Pointers passed to compute entry points are DEVICE pointers of the
+ *     context's device unless the name ends in `_host`.  Output pointers may be
+ *     NULL to skip that output.
+ *   - Every call is enqueued on the context's stream and returns without
+ *     synchronising, except `_host` variants, hc_ctx_synchronize and calls
+ *     that return a host value.
+ *   - Return codes: HC_OK, HC_EINVAL (std::invalid_argument in the reference),
+ *     HC_EDOMAIN (std::domain_error: negative code to decode, codec.cpp:56-62),
+ *     HC_ECUDA, HC_ENOMEM, HC_EUNSUPPORTED.  hc_last_error() gives a message
+ *     (thread-local).  Device-side range / sign violations are latched in the
+ *     context and reported by the next hc_ctx_synchronize.
+ *   - One context per (device, stream); a context is externally synchronised.
+ */
+#ifndef HADACODEC_B200_H
+#define HADACODEC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HC_OK 0
+#define HC_EINVAL 1
+#define HC_EDOMAIN 2
+#define HC_ECUDA 3
+#define HC_ENOMEM 4
+#define HC_EUNSUPPORTED 5
+
+typedef struct hc_ctx_s* hc_ctx;
+typedef struct hc_codec_s* hc_codec;
+typedef struct hc_mlp_s* hc_mlp;
+
+/* ------------------------------------------------------------------ runtime */
+const char* hc_last_error(void);
+const char* hc_version(void);
+/* Create a context on `device`, enqueuing on `stream` (a cudaStream_t; NULL =
+ * legacy default stream). */
+int hc_ctx_create(int device, void* stream, hc_ctx* out);
+int hc_ctx_destroy(hc_ctx ctx);
+int hc_ctx_set_stream(hc_ctx ctx, void* stream);
+/* Synchronise the stream; returns HC_EDOMAIN / HC_EINVAL if a kernel latched a
+ * negative-code or index-range violation since the last call (then clears it). */
+int hc_ctx_synchronize(hc_ctx ctx);
+/* Number of kernels this library has launched from `ctx` (monotonic). */
+int64_t hc_ctx_launch_count(hc_ctx ctx);
+
+/* ------------------------------------------------------------------ codec
+ * Replaces CodecWeights / EffectiveWeights / CmfTable usage
+ * (codec.hpp:34-60, colorimetry.hpp:25-47).
+ *   E    k x n encoder (effective, non-negative), D  n x k decoder   (host, f32)
+ *   cmf  3 x n colour-matching rows (xbar, ybar, zbar) on the grid   (host, f64)
+ *   dlambda  grid step in nm (radiance convention, colorimetry.cpp:75-87)
+ * Supported (n, k): n in {47, 81}, k in {3, 6, 9}.  k % 3 != 0 -> HC_EINVAL
+ * (validate, codec.cpp:111-135). */
+int hc_codec_create(hc_ctx ctx, int k, int n, const float* E, const float* D, const double* cmf,
+                    double dlambda, hc_codec* out);
+/* Same from raw softplus-parameterised weights (raw_enc k x n, raw_dec n x k,
+ * beta): effective_weights (codec.cpp:21-34) is applied on the host. */
+int hc_codec_create_raw(hc_ctx ctx, int k, int n, double beta, const double* raw_enc,
+                        const double* raw_dec, const double* cmf, double dlambda, hc_codec* out);
+int hc_codec_destroy(hc_codec codec);
+int hc_codec_dims(hc_codec codec, int* k, int* n);
+/* Folded 3 x k XYZ projection dlambda * CMF * D (host copy, f32). */
+int hc_codec_xyz_projection(hc_codec codec, float* out_3k);
+
+/* encode (codec.cpp:36-46), batched: Z[rows][k] = S[rows][n] . E^T. */
+int hc_encode(hc_codec codec, const float* S, int64_t rows, float* Z);
+/* decode (codec.cpp:52-71) / decode_image (renderer.cpp:661-690), batched,
+ * with the CMF -> XYZ -> linear-sRGB projection of image_to_linear_rgb
+ * (renderer.cpp:692-719) folded in.  check_negative != 0 latches HC_EDOMAIN for
+ * negative codes (decode's contract); decode_image does not check (0). */
+int hc_decode(hc_codec codec, const float* Z, int64_t rows, float* S, float* xyz, float* rgb,
+              int check_negative);
+/* Fused round trip (config 1): encode -> decode -> XYZ -> sRGB. */
+int hc_roundtrip(hc_codec codec, const float* S, int64_t rows, float* Z, float* S2, float* xyz,
+                 float* rgb);
+/* image_to_linear_rgb (renderer.cpp:692-719) on n-channel spectra, plus XYZ. */
+int hc_spectra_to_xyz_rgb(hc_codec codec, const float* S, int64_t rows, float* xyz, float* rgb);
+/* blockwise_hadamard (codec.cpp:77-85), batched: out = A (.) B, [rows][k]. */
+int hc_blockwise_hadamard(hc_ctx ctx, const float* A, const float* B, int64_t rows, int k,
+                          float* out);
+
+/* ------------------------------------------------------------------ shading
+ * Latent G-buffer shading (configs 2/3): z_p = zR[idx_p] (.) sum_l cos_{p,l} zL_l
+ * — the renderer's NEE channel loop (renderer.cpp:505-510) with the compiled
+ * assets of compile_scene (renderer.cpp:161-271) — all k/3 RGB passes fused,
+ * written as the reassembled HWC latent image (renderer.cpp:645-657), decoded
+ * to spectra and/or projected to XYZ / linear sRGB.
+ *   pal_codes  n_pal x k device codes (n_pal <= 256), light_codes L x k (host)
+ *   L in {8, 32} (others -> HC_EUNSUPPORTED).  */
+int hc_shade_latent(hc_codec codec, const float* pal_codes, int n_pal, const float* light_codes,
+                    int L, const uint32_t* idx, const float* cosv, int64_t P, float* latent,
+                    float* spectra, float* xyz, float* rgb);
+/* One 3-channel render pass b < k/3 (slice_pass, renderer.cpp:274-283):
+ * pass_image[P][3] = channels 3b..3b+2 of the latent shade. */
+int hc_shade_latent_pass(hc_codec codec, int pass, const float* pal_codes, int n_pal,
+                         const float* light_codes, int L, const uint32_t* idx, const float* cosv,
+                         int64_t P, float* pass_image);
+/* render_latent_multipass reassembly (renderer.cpp:645-657):
+ * latent[p][3b+c] = passes[b][p][c] for b < blocks.  `passes` is a HOST array
+ * of `blocks` device pointers. */
+int hc_reassemble(hc_ctx ctx, const float* const* passes, int blocks, int64_t P, float* latent);
+/* Naive n-sample shading (config 2/3 ground truth): S_p = R_idx (.) sum_l cos_l L_l,
+ * then XYZ / sRGB (renderer.cpp:187-190 at C = n, :692-719).
+ *   pal_spectra n_pal x n device, light_spectra L x n host. */
+int hc_shade_spectral(hc_codec codec, const float* pal_spectra, int n_pal,
+                      const float* light_spectra, int L, const uint32_t* idx, const float* cosv,
+                      int64_t P, float* spectra, float* xyz, float* rgb);
+
+/* Multi-bounce accumulation (config 4; renderer.cpp:457-551, evaluation.cpp:50-76):
+ * depth 4, spp a multiple of 8.  Latent: codes; spectral: spectra. */
+int hc_multibounce_latent(hc_codec codec, const float* pal_codes, int n_pal, const float* ill_codes,
+                          int n_ill, const uint8_t* pidx, const uint8_t* iidx, const float* tw,
+                          int64_t P, int spp, float* latent, float* xyz, float* rgb);
+int hc_multibounce_spectral(hc_codec codec, const float* pal_spectra, int n_pal,
+                            const float* ill_spectra, int n_ill, const uint8_t* pidx,
+                            const uint8_t* iidx, const float* tw, int64_t P, int spp, float* xyz,
+                            float* rgb);
+
+/* ------------------------------------------------------------------ upsampler
+ * RGB -> code MLP (upsampler.cpp:42-72, :179-190): 3 -> hidden -> hidden -> k with
+ * ReLU, ReLU, softplus(beta = 1) (BASELINE config 5), bf16 tcgen05 GEMMs with
+ * fp32 accumulate.  Weights row-major as UpsamplerWeights (upsampler.hpp:17-24):
+ * w1 hidden x 3, w2 hidden x hidden, w3 k x hidden (host f32, rounded to bf16),
+ * biases host f32.  hidden = 64, k in {3, 6, 9}. */
+int hc_mlp_create(hc_ctx ctx, int hidden, int k, const float* w1, const float* b1, const float* w2,
+                  const float* b2, const float* w3, const float* b3, hc_mlp* out);
+int hc_mlp_destroy(hc_mlp mlp);
+int hc_mlp_forward(hc_mlp mlp, const float* rgb, int64_t P, float* codes);
+
+/* ------------------------------------------------------------------ loss
+ * Near-multiplicativity residual (trainer.cpp:49-71): sum over pairs and lambda
+ * of (D (E a (.) E b) - a (.) b)^2 into *sum_dev (one f64 on the device). */
+int hc_hadamard_loss(hc_codec codec, const float* A, const float* B, int64_t pairs, double* sum_dev);
+
+/* ------------------------------------------------------------------ host-buffer entry points
+ * Reference-facing value calls: inputs and outputs in HOST memory (pinned for
+ * full copy speed), copies and compute on the context stream, synchronised on
+ * return.  These are what a caller of the reference's by-value API binds. */
+int hc_shade_latent_host(hc_codec codec, const float* pal_codes, int n_pal, const float* light_codes,
+                         int L, const uint32_t* idx, const float* cosv, int64_t P, float* xyz,
+                         float* rgb);
+int hc_roundtrip_host(hc_codec codec, const float* S, int64_t rows, float* Z, float* S2, float* xyz,
+                      float* rgb);
+
+/* ------------------------------------------------------------------ synthetic inputs
+ * Seeded generators for the BASELINE configs.  Keys are
+ * hc_stream_key(seed, purpose); value i of a counter stream is
+ * splitmix64(key + (i + 1) * 0x9e3779b97f4a7c15) (rng.cpp:17-22). */
+uint64_t hc_stream_key(uint64_t seed, const char* purpose);
+/* Gaussian-mixture spectra: item i uses Rng(ctr(key, first + i)) (rng.cpp:32-81):
+ * m = 1 + index(4) bumps (centre U[380,780], sigma U[10,100], amp U[0,1]),
+ * gaussian_curve sum (spectrum.cpp:97-105), clipped to [0,1]. */
+int hc_synth_gm_spectra(hc_ctx ctx, uint64_t key, int64_t first, int64_t count, int n,
+                        double lambda_min, double lambda_step, float* out);
+/* idx[p] = ctr(key_idx, p) % n_pal ; cos[p*L+l] = u24(ctr(key_cos, p*L+l)). */
+int hc_synth_gbuffer(hc_ctx ctx, uint64_t key_idx, uint64_t key_cos, int64_t first, int64_t P, int L,
+                     int n_pal, uint32_t* idx, float* cosv);
+int hc_synth_chain(hc_ctx ctx, uint64_t key_pidx, uint64_t key_iidx, uint64_t key_tw, int64_t first,
+                   int64_t P, int spp, int n_pal, int n_ill, uint8_t* pidx, uint8_t* iidx, float* tw);
+/* out[i] = u24(ctr(key, first + i)) in [0, 1). */
+int hc_synth_uniform(hc_ctx ctx, uint64_t key, int64_t first, int64_t count, float* out);
+/* Write `bytes` of garbage over a device buffer (L2 flush between timed steps). */
+int hc_flush_l2(hc_ctx ctx, void* buf, int64_t bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HADACODEC_B200_H */

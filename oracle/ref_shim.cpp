@@ -1,0 +1,491 @@
+// ORACLE / TEST INFRASTRUCTURE — NOT PART OF THE PRODUCT.
+//
+// Thin extern "C" shim over the UNMODIFIED reference core (compiled from
+// /root/reference/proj/core/src by oracle/Makefile into oracle/_ref/).  Every
+// hot-path number produced here comes from the reference's own functions:
+//   encode / decode                      codec.cpp:36-46, :52-71
+//   decode_image                         renderer.cpp:661-690
+//   image_to_linear_rgb                  renderer.cpp:692-719
+//   spectrum_to_xyz / xyz_to_linear_rgb  colorimetry.cpp:75-87, :103-105
+//   hadamard                             spectrum.cpp:48-52
+//   gaussian_curve / blackbody_curve     spectrum.cpp:97-105, dataset.cpp:503-516
+//   Rng                                  rng.cpp:7-96
+//   init_upsampler_weights               upsampler.cpp:146-168
+// Where BASELINE.json's configs have no reference function (G-buffer shading,
+// the fixed-depth bounce chain, the ReLU/softplus MLP, the plain L2 loss) the
+// shim restates them on top of those primitives with the renderer's own
+// float/double conventions, citing the lines followed.
+//
+// Used by tests/ (pinning the C restatement) and by bench.py --impl reference
+// (the CPU baseline, "kind": "reference").  Threads: contiguous row bands on
+// std::thread, mirroring render_compiled (renderer.cpp:573-608), honouring
+// HADACODEC_THREADS via render_thread_count (renderer.cpp:615-621).
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "hadacodec/codec.hpp"
+#include "hadacodec/colorimetry.hpp"
+#include "hadacodec/dataset.hpp"
+#include "hadacodec/renderer.hpp"
+#include "hadacodec/rng.hpp"
+#include "hadacodec/spectrum.hpp"
+#include "hadacodec/upsampler.hpp"
+
+using namespace hadacodec;
+
+namespace {
+
+constexpr int N = kSampleCount;
+
+int resolve_threads(int threads) {
+  return threads > 0 ? threads : render_thread_count();
+}
+
+void parallel_bands(int64_t count, int threads,
+                    const std::function<void(int64_t, int64_t)>& fn) {
+  threads = resolve_threads(threads);
+  if (count <= 0) return;
+  if (threads <= 1 || count < 2) {
+    fn(0, count);
+    return;
+  }
+  const int64_t t = std::min<int64_t>(threads, count);
+  std::vector<std::thread> pool;
+  pool.reserve(static_cast<size_t>(t));
+  for (int64_t i = 0; i < t; ++i) {
+    const int64_t lo = count * i / t, hi = count * (i + 1) / t;
+    pool.emplace_back([&fn, lo, hi] { fn(lo, hi); });
+  }
+  for (auto& th : pool) th.join();
+}
+
+EffectiveWeights make_eff(const float* E, const float* D, int k) {
+  EffectiveWeights e;
+  e.k = k;
+  e.n = N;
+  e.enc.assign(E, E + static_cast<size_t>(k) * N);
+  e.dec.assign(D, D + static_cast<size_t>(k) * N);
+  return e;
+}
+
+// CodecWeights whose softplus (codec.cpp:8-12) is the identity on every
+// positive raw entry: with beta = 1e300, beta*raw > 30 takes the
+// `return raw` branch bit-exactly.  Lets decode_image (which only accepts
+// CodecWeights) run on the configs' directly-specified effective weights.
+CodecWeights identity_codec(const float* E, const float* D, int k) {
+  CodecWeights w;
+  w.k = k;
+  w.n = N;
+  w.beta = 1e300;
+  w.raw_enc.assign(E, E + static_cast<size_t>(k) * N);
+  w.raw_dec.assign(D, D + static_cast<size_t>(k) * N);
+  return w;
+}
+
+SpectralCurve curve_of(const float* s) {
+  SpectralCurve c;
+  for (int i = 0; i < N; ++i) c[i] = static_cast<double>(s[i]);
+  return c;
+}
+
+ChannelImage band_image(int64_t rows, int channels, const float* src) {
+  ChannelImage img;
+  img.width = static_cast<int>(rows);
+  img.height = 1;
+  img.channels = channels;
+  img.data.assign(src, src + rows * channels);
+  return img;
+}
+
+// decode_image (renderer.cpp:661-690) then image_to_linear_rgb
+// (:692-719) and spectrum_to_xyz (colorimetry.cpp:75-87) on one band of a
+// latent image; every call is the reference function as written.
+void latent_band_to_outputs(const CodecWeights& cw, const float* latent_band,
+                            int64_t lo, int64_t hi, int k, float* spectra,
+                            float* xyz, float* rgb) {
+  const int64_t rows = hi - lo;
+  const ChannelImage lat = band_image(rows, k, latent_band);
+  const ChannelImage dec = decode_image(lat, cw);
+  if (spectra) std::memcpy(spectra + lo * N, dec.data.data(), rows * N * sizeof(float));
+  if (rgb) {
+    const ChannelImage lin = image_to_linear_rgb(dec);
+    std::memcpy(rgb + lo * 3, lin.data.data(), rows * 3 * sizeof(float));
+  }
+  if (xyz) {
+    for (int64_t p = 0; p < rows; ++p) {
+      const ColorTriple t = spectrum_to_xyz(curve_of(&dec.data[p * N]));
+      for (int c = 0; c < 3; ++c) xyz[(lo + p) * 3 + c] = static_cast<float>(t[c]);
+    }
+  }
+}
+
+void spectral_band_to_outputs(const float* spec_band, int64_t lo, int64_t hi,
+                              float* xyz, float* rgb) {
+  const int64_t rows = hi - lo;
+  const ChannelImage img = band_image(rows, N, spec_band);
+  if (rgb) {
+    const ChannelImage lin = image_to_linear_rgb(img);
+    std::memcpy(rgb + lo * 3, lin.data.data(), rows * 3 * sizeof(float));
+  }
+  if (xyz) {
+    for (int64_t p = 0; p < rows; ++p) {
+      const ColorTriple t = spectrum_to_xyz(curve_of(spec_band + p * N));
+      for (int c = 0; c < 3; ++c) xyz[(lo + p) * 3 + c] = static_cast<float>(t[c]);
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// ------------------------------------------------------------------ grid / tables
+int ref_grid_n() { return N; }
+double ref_lambda_min() { return kLambdaMin; }
+double ref_lambda_step() { return kLambdaStep; }
+double ref_wavelength_at(int i) { return wavelength_at(i); }
+
+// CmfTable rows on the grid (colorimetry.cpp:45-61): xbar, ybar, zbar, d65,
+// then the D65-weighted reflectance rows wx, wy, wz.  out: 7*N doubles.
+void ref_cmf_table(double* out) {
+  const CmfTable& t = CmfTable::instance();
+  const SpectralCurve* rows[7] = {&t.xbar(), &t.ybar(), &t.zbar(), &t.d65(),
+                                  &t.wx(),   &t.wy(),   &t.wz()};
+  for (int r = 0; r < 7; ++r)
+    for (int i = 0; i < N; ++i) out[r * N + i] = (*rows[r])[i];
+}
+
+void ref_white_xyz(double* out3) {
+  const ColorTriple w = CmfTable::instance().white_xyz();
+  for (int c = 0; c < 3; ++c) out3[c] = w[c];
+}
+
+void ref_spectrum_to_xyz_d(const double* s, double* out3) {
+  SpectralCurve c;
+  for (int i = 0; i < N; ++i) c[i] = s[i];
+  const ColorTriple t = spectrum_to_xyz(c);
+  for (int i = 0; i < 3; ++i) out3[i] = t[i];
+}
+
+void ref_xyz_to_linear_rgb_d(const double* xyz3, double* out3) {
+  ColorTriple t;
+  for (int i = 0; i < 3; ++i) t[i] = xyz3[i];
+  const ColorTriple r = xyz_to_linear_rgb(t);
+  for (int i = 0; i < 3; ++i) out3[i] = r[i];
+}
+
+double ref_softplus(double raw, double beta) { return softplus(raw, beta); }
+
+// ------------------------------------------------------------------ RNG
+void ref_rng_stream_u64(uint64_t seed, const char* purpose, int count, uint64_t* out) {
+  Rng r = Rng::stream(seed, purpose);
+  for (int i = 0; i < count; ++i) out[i] = r.next_u64();
+}
+void ref_rng_seed_u64(uint64_t seed, int count, uint64_t* out) {
+  Rng r(seed);
+  for (int i = 0; i < count; ++i) out[i] = r.next_u64();
+}
+void ref_pixel_stream_u64(uint64_t seed, int x, int y, int sample, uint32_t lane,
+                          int count, uint64_t* out) {
+  Rng r = Rng::pixel_stream(seed, x, y, sample, lane);
+  for (int i = 0; i < count; ++i) out[i] = r.next_u64();
+}
+uint64_t ref_fnv1a64(const char* bytes, int64_t len) { return fnv1a64(bytes, static_cast<size_t>(len)); }
+
+// ------------------------------------------------------------------ generators
+void ref_gaussian_curve(double c, double s, double a, double* out) {
+  const SpectralCurve g = gaussian_curve(c, s, a);
+  for (int i = 0; i < N; ++i) out[i] = g[i];
+}
+void ref_blackbody_curve(double kelvin, double* out) {
+  const SpectralCurve g = blackbody_curve(kelvin);
+  for (int i = 0; i < N; ++i) out[i] = g[i];
+}
+// init_upsampler_weights (upsampler.cpp:146-168): w1 h*3, w2 h*h, w3 k*h.
+void ref_init_upsampler(int k, int hidden, uint64_t seed, double* w1, double* w2, double* w3) {
+  const UpsamplerWeights w = init_upsampler_weights(k, hidden, seed);
+  std::copy(w.w1.begin(), w.w1.end(), w1);
+  std::copy(w.w2.begin(), w.w2.end(), w2);
+  std::copy(w.w3.begin(), w.w3.end(), w3);
+}
+
+// ------------------------------------------------------------------ codec (config 1)
+// encode(EffectiveWeights, SpectralCurve) per row, double code.
+void ref_encode_rows_d(const float* E, int k, const float* S, int64_t rows, double* Z, int threads) {
+  const EffectiveWeights e = make_eff(E, E, k);  // dec unused
+  parallel_bands(rows, threads, [&](int64_t lo, int64_t hi) {
+    for (int64_t r = lo; r < hi; ++r) {
+      const LatentCode z = encode(e, curve_of(S + r * N));
+      for (int j = 0; j < k; ++j) Z[r * k + j] = z[j];
+    }
+  });
+}
+
+// decode(EffectiveWeights, LatentCode) per row (double in, double out);
+// returns 1 if decode threw std::domain_error (negative code), 2 on
+// std::invalid_argument, else 0.
+int ref_decode_rows_d(const float* D, int k, const double* Z, int64_t rows, double* S) {
+  const EffectiveWeights e = make_eff(D, D, k);
+  try {
+    for (int64_t r = 0; r < rows; ++r) {
+      LatentCode z;
+      z.z.assign(Z + r * k, Z + (r + 1) * k);
+      const SpectralCurve s = decode(e, z);
+      for (int i = 0; i < N; ++i) S[r * N + i] = s[i];
+    }
+  } catch (const std::domain_error&) {
+    return 1;
+  } catch (const std::invalid_argument&) {
+    return 2;
+  }
+  return 0;
+}
+
+// Config 1: encode -> fp32 codes -> decode_image -> fp32 spectra ->
+// spectrum_to_xyz / image_to_linear_rgb.  Any output may be NULL.
+void ref_codec_roundtrip(const float* E, const float* D, int k, const float* S, int64_t rows,
+                         float* Z, float* S2, float* XYZ, float* RGB, int threads) {
+  const EffectiveWeights e = make_eff(E, D, k);
+  const CodecWeights cw = identity_codec(E, D, k);
+  parallel_bands(rows, threads, [&](int64_t lo, int64_t hi) {
+    std::vector<float> z(static_cast<size_t>((hi - lo) * k));
+    for (int64_t r = lo; r < hi; ++r) {
+      const LatentCode c = encode(e, curve_of(S + r * N));
+      for (int j = 0; j < k; ++j) z[(r - lo) * k + j] = static_cast<float>(c[j]);
+    }
+    if (Z) std::memcpy(Z + lo * k, z.data(), z.size() * sizeof(float));
+    latent_band_to_outputs(cw, z.data(), lo, hi, k, S2, XYZ, RGB);
+  });
+}
+
+// decode_image + image_to_linear_rgb on a full latent image (fp32 codes).
+void ref_decode_image(const float* E, const float* D, int k, const float* Z, int64_t rows,
+                      float* S2, float* XYZ, float* RGB, int threads) {
+  const CodecWeights cw = identity_codec(E, D, k);
+  parallel_bands(rows, threads, [&](int64_t lo, int64_t hi) {
+    latent_band_to_outputs(cw, Z + lo * k, lo, hi, k, S2, XYZ, RGB);
+  });
+}
+
+void ref_spectra_to_outputs(const float* S, int64_t rows, float* XYZ, float* RGB, int threads) {
+  parallel_bands(rows, threads, [&](int64_t lo, int64_t hi) {
+    spectral_band_to_outputs(S + lo * N, lo, hi, XYZ, RGB);
+  });
+}
+
+// Asset codes as compile_scene makes them: code_to_floats (renderer.cpp:117-125),
+// float(encode(eff, c)[i] * gain) with gain 1.
+void ref_asset_codes(const float* E, int k, const float* S, int64_t count, float* Z) {
+  const EffectiveWeights e = make_eff(E, E, k);
+  for (int64_t a = 0; a < count; ++a) {
+    const LatentCode z = encode(e, curve_of(S + a * N));
+    for (int j = 0; j < k; ++j) Z[a * k + j] = static_cast<float>(z[j] * 1.0);
+  }
+}
+
+// ------------------------------------------------------------------ configs 2/3 (R1)
+// Latent G-buffer shading restated on the renderer's NEE channel loop
+// (renderer.cpp:505-510; thr = 1 at the first hit, NEE weight = c_{p,l},
+// SURVEY Appendix A #11), executed as k/3 three-channel passes
+// (slice_pass renderer.cpp:274-283) and reassembled channel 3b+c
+// (renderer.cpp:645-657); per-pixel double accumulation (:548-551, :588-592).
+// Then decode_image / image_to_linear_rgb / spectrum_to_xyz as written.
+void ref_shade_latent(const float* E, const float* D, int k, const float* pal_codes,
+                      const float* light_codes, int L, const uint32_t* idx, const float* cosv,
+                      int64_t P, float* latent, float* S2, float* XYZ, float* RGB, int threads) {
+  const CodecWeights cw = identity_codec(E, D, k);
+  const int blocks = k / 3;
+  parallel_bands(P, threads, [&](int64_t lo, int64_t hi) {
+    const int64_t rows = hi - lo;
+    std::vector<float> lat(static_cast<size_t>(rows * k));
+    std::vector<float> pass(static_cast<size_t>(rows * 3));
+    for (int b = 0; b < blocks; ++b) {
+      for (int64_t p = lo; p < hi; ++p) {
+        const float* albedo = pal_codes + static_cast<int64_t>(idx[p]) * k + 3 * b;
+        float rad[3] = {0.f, 0.f, 0.f};
+        const float thr[3] = {1.f, 1.f, 1.f};
+        for (int l = 0; l < L; ++l) {
+          const float w = cosv[p * L + l];
+          const float* le = light_codes + l * k + 3 * b;
+          for (int c = 0; c < 3; ++c) rad[c] += thr[c] * albedo[c] * le[c] * w;
+        }
+        for (int c = 0; c < 3; ++c) {
+          const double accum = static_cast<double>(rad[c]);
+          pass[(p - lo) * 3 + c] = static_cast<float>(accum * (1.0 / 1));
+        }
+      }
+      for (int64_t p = 0; p < rows; ++p)
+        for (int c = 0; c < 3; ++c) lat[p * k + 3 * b + c] = pass[p * 3 + c];
+    }
+    if (latent) std::memcpy(latent + lo * k, lat.data(), lat.size() * sizeof(float));
+    latent_band_to_outputs(cw, lat.data(), lo, hi, k, S2, XYZ, RGB);
+  });
+}
+
+// Naive n-sample shading: the same loop at C = n channels with
+// curve_to_floats assets (renderer.cpp:187-190, :203-205, :216-218), then
+// image_to_linear_rgb / spectrum_to_xyz.
+void ref_shade_spectral(const float* pal_spectra, const float* light_spectra, int L,
+                        const uint32_t* idx, const float* cosv, int64_t P, float* S2,
+                        float* XYZ, float* RGB, int threads) {
+  parallel_bands(P, threads, [&](int64_t lo, int64_t hi) {
+    const int64_t rows = hi - lo;
+    std::vector<float> spec(static_cast<size_t>(rows * N));
+    std::vector<float> rad(N);
+    for (int64_t p = lo; p < hi; ++p) {
+      const float* albedo = pal_spectra + static_cast<int64_t>(idx[p]) * N;
+      std::fill(rad.begin(), rad.end(), 0.f);
+      for (int l = 0; l < L; ++l) {
+        const float w = cosv[p * L + l];
+        const float* le = light_spectra + l * N;
+        for (int c = 0; c < N; ++c) rad[c] += 1.0f * albedo[c] * le[c] * w;
+      }
+      for (int c = 0; c < N; ++c) spec[(p - lo) * N + c] = static_cast<float>(static_cast<double>(rad[c]));
+    }
+    if (S2) std::memcpy(S2 + lo * N, spec.data(), spec.size() * sizeof(float));
+    spectral_band_to_outputs(spec.data(), lo, hi, XYZ, RGB);
+  });
+}
+
+// ------------------------------------------------------------------ config 4 (R2)
+// Fixed-depth chain: per sample thr = 1, rad = 0; for
+// d < depth: rad += thr*albedo_d*le*t_d (NEE, renderer.cpp:505-510) then
+// thr *= albedo_d (:530-533); per-pixel double accumulation over samples
+// (:548-551), divided by spp (:588-592).  C = k (latent) or n (spectral).
+static void chain_accumulate(int C, const float* pal, const float* ill, const uint8_t* pidx,
+                             const uint8_t* iidx, const float* tw, int64_t p, int spp,
+                             int depth, float* out) {
+  std::vector<double> acc(static_cast<size_t>(C), 0.0);
+  std::vector<float> thr(static_cast<size_t>(C)), rad(static_cast<size_t>(C));
+  for (int s = 0; s < spp; ++s) {
+    const int64_t smp = p * spp + s;
+    std::fill(thr.begin(), thr.end(), 1.f);
+    std::fill(rad.begin(), rad.end(), 0.f);
+    const float* le = ill + static_cast<int64_t>(iidx[smp]) * C;
+    for (int d = 0; d < depth; ++d) {
+      const float* albedo = pal + static_cast<int64_t>(pidx[smp * depth + d]) * C;
+      const float w = tw[smp * depth + d];
+      for (int c = 0; c < C; ++c) rad[c] += thr[c] * albedo[c] * le[c] * w;
+      for (int c = 0; c < C; ++c) thr[c] *= albedo[c];
+    }
+    for (int c = 0; c < C; ++c) acc[c] += static_cast<double>(rad[c]);
+  }
+  const double inv_spp = 1.0 / spp;
+  for (int c = 0; c < C; ++c) out[c] = static_cast<float>(acc[c] * inv_spp);
+}
+
+void ref_multibounce_latent(const float* E, const float* D, int k, const float* pal_codes,
+                            const float* ill_codes, const uint8_t* pidx, const uint8_t* iidx,
+                            const float* tw, int64_t P, int spp, int depth, float* latent,
+                            float* XYZ, float* RGB, int threads) {
+  const CodecWeights cw = identity_codec(E, D, k);
+  parallel_bands(P, threads, [&](int64_t lo, int64_t hi) {
+    std::vector<float> lat(static_cast<size_t>((hi - lo) * k));
+    for (int64_t p = lo; p < hi; ++p)
+      chain_accumulate(k, pal_codes, ill_codes, pidx, iidx, tw, p, spp, depth, &lat[(p - lo) * k]);
+    if (latent) std::memcpy(latent + lo * k, lat.data(), lat.size() * sizeof(float));
+    latent_band_to_outputs(cw, lat.data(), lo, hi, k, nullptr, XYZ, RGB);
+  });
+}
+
+void ref_multibounce_spectral(const float* pal_spectra, const float* ill_spectra,
+                              const uint8_t* pidx, const uint8_t* iidx, const float* tw,
+                              int64_t P, int spp, int depth, float* XYZ, float* RGB, int threads) {
+  parallel_bands(P, threads, [&](int64_t lo, int64_t hi) {
+    std::vector<float> spec(static_cast<size_t>((hi - lo) * N));
+    for (int64_t p = lo; p < hi; ++p)
+      chain_accumulate(N, pal_spectra, ill_spectra, pidx, iidx, tw, p, spp, depth, &spec[(p - lo) * N]);
+    spectral_band_to_outputs(spec.data(), lo, hi, XYZ, RGB);
+  });
+}
+
+// ------------------------------------------------------------------ config 5a (R3)
+// forward (upsampler.cpp:42-72) with BASELINE's ReLU hidden activations and a
+// softplus(beta=1) head via the reference softplus (codec.cpp:8-12); the
+// operands the tensor-core path sees are bf16, so inputs, weights and hidden
+// activations arrive here already rounded to bf16 values (as floats).
+// Hidden activations are rounded to bf16 between layers by the caller-given
+// rounding function semantics: round-to-nearest-even on the fp32 value.
+static float bf16_round(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return x;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  u &= 0xffff0000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+void ref_mlp_forward(const float* rgb, int64_t P, int hidden, int k, const float* w1,
+                     const float* b1, const float* w2, const float* b2, const float* w3,
+                     const float* b3, float* out, int threads) {
+  parallel_bands(P, threads, [&](int64_t lo, int64_t hi) {
+    std::vector<double> h1(static_cast<size_t>(hidden)), h2(static_cast<size_t>(hidden));
+    for (int64_t p = lo; p < hi; ++p) {
+      double x[3];
+      for (int j = 0; j < 3; ++j) x[j] = bf16_round(rgb[p * 3 + j]);
+      for (int i = 0; i < hidden; ++i) {
+        double acc = b1[i];
+        for (int j = 0; j < 3; ++j) acc += static_cast<double>(w1[i * 3 + j]) * x[j];
+        h1[i] = bf16_round(static_cast<float>(std::max(acc, 0.0)));
+      }
+      for (int i = 0; i < hidden; ++i) {
+        double acc = b2[i];
+        for (int j = 0; j < hidden; ++j) acc += static_cast<double>(w2[i * hidden + j]) * h1[j];
+        h2[i] = bf16_round(static_cast<float>(std::max(acc, 0.0)));
+      }
+      for (int i = 0; i < k; ++i) {
+        double acc = b3[i];
+        for (int j = 0; j < hidden; ++j) acc += static_cast<double>(w3[i * hidden + j]) * h2[j];
+        out[p * k + i] = static_cast<float>(softplus(acc, 1.0));
+      }
+    }
+  });
+}
+
+// ------------------------------------------------------------------ config 5b (R4)
+// forward_pair (trainer.cpp:49-62) residual D(E a o E b) - a o b summed in
+// double over lambda (mse_n trainer.cpp:64-71 without the 1/n and the
+// (2 - cos) factor of loss_e2e :108-118), over all pairs.  Uses the public
+// encode / decode / hadamard.
+double ref_hadamard_loss(const float* E, const float* D, int k, const float* A, const float* B,
+                         int64_t pairs, int threads) {
+  const EffectiveWeights e = make_eff(E, D, k);
+  const int t = std::max<int>(1, static_cast<int>(std::min<int64_t>(resolve_threads(threads), pairs)));
+  std::vector<double> part(static_cast<size_t>(t), 0.0);
+  std::vector<std::thread> pool;
+  for (int i = 0; i < t; ++i) {
+    const int64_t lo = pairs * i / t, hi = pairs * (i + 1) / t;
+    pool.emplace_back([&, i, lo, hi] {
+      double acc = 0.0;
+      for (int64_t r = lo; r < hi; ++r) {
+        const SpectralCurve a = curve_of(A + r * N), b = curve_of(B + r * N);
+        const LatentCode za = encode(e, a), zb = encode(e, b);
+        const LatentCode zp = blockwise_hadamard(za, zb);
+        const SpectralCurve sh = decode(e, zp);
+        const SpectralCurve s = hadamard(a, b);
+        for (int l = 0; l < N; ++l) {
+          const double d = sh[l] - s[l];
+          acc += d * d;
+        }
+      }
+      part[static_cast<size_t>(i)] = acc;
+    });
+  }
+  for (auto& th : pool) th.join();
+  double total = 0.0;
+  for (double v : part) total += v;
+  return total;
+}
+
+int ref_thread_count() { return render_thread_count(); }
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+"""ctypes binding of the in-tree C ABI (include/hadacodec_b200.h).
+
+Loading fails loudly when ``libhadacodec_b200.so`` is missing: there is no CPU
+fallback on the product path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libhadacodec_b200.so"
+
+HC_OK, HC_EINVAL, HC_EDOMAIN, HC_ECUDA, HC_ENOMEM, HC_EUNSUPPORTED = range(6)
+
+vp = C.c_void_p
+i32, i64, u64, f64 = C.c_int, C.c_int64, C.c_uint64, C.c_double
+
+SIGNATURES: dict[str, tuple] = {
+    "hc_last_error": (C.c_char_p, []),
+    "hc_version": (C.c_char_p, []),
+    "hc_ctx_create": (i32, [i32, vp, C.POINTER(vp)]),
+    "hc_ctx_destroy": (i32, [vp]),
+    "hc_ctx_set_stream": (i32, [vp, vp]),
+    "hc_ctx_synchronize": (i32, [vp]),
+    "hc_ctx_launch_count": (i64, [vp]),
+    "hc_codec_create": (i32, [vp, i32, i32, vp, vp, vp, f64, C.POINTER(vp)]),
+    "hc_codec_create_raw": (i32, [vp, i32, i32, f64, vp, vp, vp, f64, C.POINTER(vp)]),
+    "hc_codec_destroy": (i32, [vp]),
+    "hc_codec_dims": (i32, [vp, C.POINTER(i32), C.POINTER(i32)]),
+    "hc_codec_xyz_projection": (i32, [vp, vp]),
+    "hc_encode": (i32, [vp, vp, i64, vp]),
+    "hc_decode": (i32, [vp, vp, i64, vp, vp, vp, i32]),
+    "hc_roundtrip": (i32, [vp, vp, i64, vp, vp, vp, vp]),
+    "hc_spectra_to_xyz_rgb": (i32, [vp, vp, i64, vp, vp]),
+    "hc_blockwise_hadamard": (i32, [vp, vp, vp, i64, i32, vp]),
+    "hc_shade_latent": (i32, [vp, vp, i32, vp, i32, vp, vp, i64, vp, vp, vp, vp]),
+    "hc_shade_latent_pass": (i32, [vp, i32, vp, i32, vp, i32, vp, vp, i64, vp]),
+    "hc_reassemble": (i32, [vp, vp, i32, i64, vp]),
+    "hc_shade_spectral": (i32, [vp, vp, i32, vp, i32, vp, vp, i64, vp, vp, vp]),
+    "hc_multibounce_latent": (i32, [vp, vp, i32, vp, i32, vp, vp, vp, i64, i32, vp, vp, vp]),
+    "hc_multibounce_spectral": (i32, [vp, vp, i32, vp, i32, vp, vp, vp, i64, i32, vp, vp]),
+    "hc_mlp_create": (i32, [vp, i32, i32, vp, vp, vp, vp, vp, vp, C.POINTER(vp)]),
+    "hc_mlp_destroy": (i32, [vp]),
+    "hc_mlp_forward": (i32, [vp, vp, i64, vp]),
+    "hc_hadamard_loss": (i32, [vp, vp, vp, i64, vp]),
+    "hc_shade_latent_host": (i32, [vp, vp, i32, vp, i32, vp, vp, i64, vp, vp]),
+    "hc_roundtrip_host": (i32, [vp, vp, i64, vp, vp, vp, vp]),
+    "hc_stream_key": (u64, [u64, C.c_char_p]),
+    "hc_synth_gm_spectra": (i32, [vp, u64, i64, i64, i32, f64, f64, vp]),
+    "hc_synth_gbuffer": (i32, [vp, u64, u64, i64, i64, i32, i32, vp, vp]),
+    "hc_synth_chain": (i32, [vp, u64, u64, u64, i64, i64, i32, i32, i32, vp, vp, vp]),
+    "hc_synth_uniform": (i32, [vp, u64, i64, i64, vp]),
+    "hc_flush_l2": (i32, [vp, vp, i64]),
+}
+
+_lib = None
+
+
+class HcError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[hc {code}] {msg}")
+        self.code = code
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2602_18741_b200.build` "
+                "(the B200 path has no CPU fallback)")
+        L = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype, fn.argtypes = res, args
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != HC_OK:
+        msg = lib().hc_last_error().decode(errors="replace")
+        if rc == HC_EINVAL:
+            raise ValueError(msg)
+        if rc == HC_EDOMAIN:
+            raise ArithmeticError(msg)  # std::domain_error analogue
+        raise HcError(rc, msg)

@@ -1,0 +1,58 @@
+"""Spectral grids and colour-matching data for the B200 path.
+
+Grids (spectrum.hpp:10-21): the reference's canonical 47-sample grid over
+368-830 nm and BASELINE.json's 81-sample grid over 380-780 nm (5 nm), both
+with wavelength_at(i) = lambda_min + step * i.
+
+CMF rows are the reference's CmfTable (colorimetry.cpp:45-61: CIE 1931 2-degree
+1 nm tables linearly resampled onto the grid, plus D65).  They are shipped as
+package data generated from the compiled reference by oracle/make_golden.py;
+at n = 81 every 5 nm sample falls exactly on a 1 nm table entry.  XYZ uses the
+radiance convention dlambda * sum cmf * s (colorimetry.cpp:75-87); sRGB the
+IEC 61966-2-1 matrix (colorimetry.cpp:22-26).
+"""
+from __future__ import annotations
+
+import json
+from functools import lru_cache
+from pathlib import Path
+
+import numpy as np
+
+DATA = Path(__file__).resolve().parent / "data"
+
+# (lambda_min, lambda_max) per supported sample count.
+GRIDS = {47: (368.0, 830.0), 81: (380.0, 780.0)}
+
+XYZ_TO_LINEAR_RGB = np.array(
+    [[3.2404542, -1.5371385, -0.4985314],
+     [-0.9692660, 1.8760108, 0.0415560],
+     [0.0556434, -0.2040259, 1.0572252]], dtype=np.float64)
+
+
+def grid(n: int) -> tuple[float, float]:
+    """(lambda_min, step) of the n-sample grid (spectrum.hpp:10-21)."""
+    lo, hi = GRIDS[n]
+    return lo, (hi - lo) / (n - 1)
+
+
+def wavelengths(n: int) -> np.ndarray:
+    lo, step = grid(n)
+    return np.array([lo + step * i for i in range(n)], dtype=np.float64)
+
+
+@lru_cache(maxsize=None)
+def cmf_table(n: int) -> dict:
+    """xbar, ybar, zbar, d65 on the n-grid as float64 arrays (+ 'cmf' 3 x n)."""
+    path = DATA / f"cmf_n{n}.json"
+    if not path.exists():
+        raise FileNotFoundError(f"{path} missing (generate with `python oracle/make_golden.py`)")
+    d = json.loads(path.read_text())
+    out = {k: np.array(d[k], dtype=np.float64) for k in ("xbar", "ybar", "zbar", "d65")}
+    out["cmf"] = np.stack([out["xbar"], out["ybar"], out["zbar"]])
+    out["lambda_min"], out["lambda_step"] = d["lambda_min"], d["lambda_step"]
+    return out
+
+
+def cmf_matrix(n: int) -> np.ndarray:
+    return np.ascontiguousarray(cmf_table(n)["cmf"])

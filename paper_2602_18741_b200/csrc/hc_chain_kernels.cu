@@ -1,0 +1,118 @@
+// hadacodec-b200: multi-bounce accumulation launchers (config 4).
+// Reference: evaluation.cpp:50-76, renderer.cpp:457-551 (see hc_chain.cuh).
+#include <algorithm>
+
+#include "hc_chain.cuh"
+#include "hc_launch.cuh"
+
+namespace hcb {
+
+template <class KernelFn>
+int chain_grid(hc_ctx ctx, KernelFn fn, int smem, int64_t P, int* grid) {
+  HC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int occ = 0;
+  HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+  if (occ < 1) return set_error(HC_EUNSUPPORTED, "chain kernel does not fit on an SM");
+  const int64_t blocks_needed = (P + 31) / 32;  // 32 pixels per 256-thread block iteration
+  *grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_needed, static_cast<int64_t>(occ) * ctx->sm_count)));
+  return HC_OK;
+}
+
+template <int K>
+int chain_latent_k(hc_codec c, const float* pal, int n_pal, const float* ill, int n_ill,
+                   const uint8_t* pidx, const uint8_t* iidx, const float* tw, int64_t P, int spp,
+                   float* latent, float* xyz, float* rgb) {
+  ChainLatentParams<K> p;
+  for (int i = 0; i < 3 * K; ++i) p.Mxyz[i] = c->Mxyz[i];
+  for (int i = 0; i < 9; ++i) p.Crgb[i] = c->Crgb[i];
+  p.pal = pal;
+  p.ill = ill;
+  p.n_pal = n_pal;
+  p.n_ill = n_ill;
+  p.pidx = reinterpret_cast<const uint32_t*>(pidx);
+  p.iidx = iidx;
+  p.tw = reinterpret_cast<const float4*>(tw);
+  p.P = P;
+  p.spp = spp;
+  p.latent = latent;
+  p.xyz = xyz;
+  p.rgb = rgb;
+  p.err = c->ctx->d_err;
+  const int smem = (n_pal + n_ill) * K * 4;
+  int grid = 0;
+  int rc = chain_grid(c->ctx, chain_latent_kernel<K>, smem, P, &grid);
+  if (rc != HC_OK) return rc;
+  chain_latent_kernel<K><<<grid, 256, smem, c->ctx->stream>>>(p);
+  HC_CHECK_LAUNCH(c->ctx, "chain_latent_kernel");
+  return HC_OK;
+}
+
+static bool chain_args_ok(int n_pal, int n_ill, const uint8_t* pidx, const float* tw, int spp) {
+  if (n_pal < 1 || n_pal > 256 || n_ill < 1 || n_ill > kMaxIllum) return false;
+  if (spp < 8 || spp % 8 != 0) return false;
+  if ((reinterpret_cast<uintptr_t>(pidx) & 3u) || (reinterpret_cast<uintptr_t>(tw) & 15u)) return false;
+  return true;
+}
+
+int chain_latent_launch(hc_codec c, const float* pal, int n_pal, const float* ill, int n_ill,
+                        const uint8_t* pidx, const uint8_t* iidx, const float* tw, int64_t P, int spp,
+                        float* latent, float* xyz, float* rgb) {
+  if (!chain_args_ok(n_pal, n_ill, pidx, tw, spp))
+    return set_error(HC_EINVAL, "multibounce: need 1 <= n_pal, n_ill <= 256, spp % 8 == 0, pidx 4-aligned, tw 16-aligned");
+  if (P <= 0) return HC_OK;
+  switch (c->k) {
+    case 3: return chain_latent_k<3>(c, pal, n_pal, ill, n_ill, pidx, iidx, tw, P, spp, latent, xyz, rgb);
+    case 6: return chain_latent_k<6>(c, pal, n_pal, ill, n_ill, pidx, iidx, tw, P, spp, latent, xyz, rgb);
+    case 9: return chain_latent_k<9>(c, pal, n_pal, ill, n_ill, pidx, iidx, tw, P, spp, latent, xyz, rgb);
+  }
+  return set_error(HC_EUNSUPPORTED, "multibounce_latent: k must be 3, 6 or 9");
+}
+
+template <int N, int SPL>
+int chain_spectral_ns(hc_codec c, const float* pal, int n_pal, const float* ill, int n_ill,
+                      const uint8_t* pidx, const uint8_t* iidx, const float* tw, int64_t P, int spp,
+                      float* xyz, float* rgb) {
+  ChainSpectralParams<N> p;
+  for (int i = 0; i < 3 * N; ++i) p.cmf[i] = c->cmf_dl[i];
+  for (int i = 0; i < 9; ++i) p.Crgb[i] = c->Crgb[i];
+  p.pal = pal;
+  p.ill = ill;
+  p.n_pal = n_pal;
+  p.n_ill = n_ill;
+  p.pidx = reinterpret_cast<const uint32_t*>(pidx);
+  p.iidx = iidx;
+  p.tw = reinterpret_cast<const float4*>(tw);
+  p.P = P;
+  p.spp = spp;
+  p.xyz = xyz;
+  p.rgb = rgb;
+  p.err = c->ctx->d_err;
+  const int smem = (n_pal + n_ill) * N * 4;
+  int grid = 0;
+  int rc = chain_grid(c->ctx, chain_spectral_kernel<N, SPL>, smem, P, &grid);
+  if (rc != HC_OK) return rc;
+  chain_spectral_kernel<N, SPL><<<grid, 256, smem, c->ctx->stream>>>(p);
+  HC_CHECK_LAUNCH(c->ctx, "chain_spectral_kernel");
+  return HC_OK;
+}
+
+int chain_spectral_launch(hc_codec c, const float* pal, int n_pal, const float* ill, int n_ill,
+                          const uint8_t* pidx, const uint8_t* iidx, const float* tw, int64_t P,
+                          int spp, float* xyz, float* rgb) {
+  if (!chain_args_ok(n_pal, n_ill, pidx, tw, spp))
+    return set_error(HC_EINVAL, "multibounce: need 1 <= n_pal, n_ill <= 256, spp % 8 == 0, pidx 4-aligned, tw 16-aligned");
+  if (P <= 0) return HC_OK;
+  const int spl = spp / 8;
+  if (c->n == 81) {
+    if (spl == 8) return chain_spectral_ns<81, 8>(c, pal, n_pal, ill, n_ill, pidx, iidx, tw, P, spp, xyz, rgb);
+    if (spl == 1) return chain_spectral_ns<81, 1>(c, pal, n_pal, ill, n_ill, pidx, iidx, tw, P, spp, xyz, rgb);
+    if (spl == 2) return chain_spectral_ns<81, 2>(c, pal, n_pal, ill, n_ill, pidx, iidx, tw, P, spp, xyz, rgb);
+    if (spl == 4) return chain_spectral_ns<81, 4>(c, pal, n_pal, ill, n_ill, pidx, iidx, tw, P, spp, xyz, rgb);
+  } else if (c->n == 47) {
+    if (spl == 8) return chain_spectral_ns<47, 8>(c, pal, n_pal, ill, n_ill, pidx, iidx, tw, P, spp, xyz, rgb);
+    if (spl == 1) return chain_spectral_ns<47, 1>(c, pal, n_pal, ill, n_ill, pidx, iidx, tw, P, spp, xyz, rgb);
+  }
+  return set_error(HC_EUNSUPPORTED, "multibounce_spectral: compiled for n=81 spp in {8,16,32,64}, n=47 spp in {8,64}");
+}
+
+}  // namespace hcb

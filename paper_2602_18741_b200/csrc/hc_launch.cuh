@@ -1,0 +1,102 @@
+// hadacodec-b200: host-side launch of the tile pipeline.
+#pragma once
+
+#include <algorithm>
+#include <atomic>
+
+#include "hc_internal.h"
+#include "hc_pipeline.cuh"
+
+namespace hcb {
+
+template <class Op>
+struct TileLaunchCache {
+  static std::atomic<int> configured;  // 0 = not yet, 1 = done
+  static int occ_pipeline, occ_generic;
+};
+template <class Op>
+std::atomic<int> TileLaunchCache<Op>::configured{0};
+template <class Op>
+int TileLaunchCache<Op>::occ_pipeline = 1;
+template <class Op>
+int TileLaunchCache<Op>::occ_generic = 1;
+
+template <class Op>
+int configure_tile_op() {
+  using Cache = TileLaunchCache<Op>;
+  if (Cache::configured.load(std::memory_order_acquire)) return HC_OK;
+  const int smem = TileLayout<Op>::smem_bytes();
+  HC_CUDA_TRY(cudaFuncSetAttribute(tile_pipeline<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  HC_CUDA_TRY(cudaFuncSetAttribute(tile_generic<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  int a = 0, b = 0;
+  HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, tile_pipeline<Op>, Op::THREADS, smem));
+  HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tile_generic<Op>, Op::THREADS, smem));
+  if (a < 1 || b < 1) return set_error(HC_EUNSUPPORTED, "tile kernel does not fit on an SM");
+  Cache::occ_pipeline = a;
+  Cache::occ_generic = b;
+  Cache::configured.store(1, std::memory_order_release);
+  return HC_OK;
+}
+
+inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// Launch Op over `items` items.  Full tiles of 16-byte-aligned streams go
+// through the TMA pipeline; the ragged tail (and everything, if any stream is
+// misaligned) through tile_generic.  `grid_out` (optional) receives the grid
+// sizes used: [pipeline, generic].
+template <class Op>
+int launch_tile_op(hc_ctx ctx, const typename Op::Params& p, int64_t items, int* grid_out = nullptr) {
+  if (items <= 0) {
+    if (grid_out) grid_out[0] = grid_out[1] = 0;
+    return HC_OK;
+  }
+  int rc = configure_tile_op<Op>();
+  if (rc != HC_OK) return rc;
+  using Cache = TileLaunchCache<Op>;
+  bool aligned = true;
+  for (int i = 0; i < Op::NIN; ++i) aligned &= al16(Op::in_ptr(p, i));
+  for (int i = 0; i < Op::NOUT; ++i) aligned &= al16(Op::out_ptr(p, i));
+  const int smem = TileLayout<Op>::smem_bytes();
+  const int64_t full = aligned ? items / Op::T : 0;
+  int g0 = 0, g1 = 0;
+  if (full > 0) {
+    g0 = static_cast<int>(std::min<int64_t>(full, static_cast<int64_t>(Cache::occ_pipeline) * ctx->sm_count));
+    tile_pipeline<Op><<<g0, Op::THREADS, smem, ctx->stream>>>(p, full);
+    HC_CHECK_LAUNCH(ctx, "tile_pipeline");
+  }
+  const int64_t begin = full * Op::T;
+  if (begin < items) {
+    const int64_t tiles = (items - begin + Op::T - 1) / Op::T;
+    g1 = static_cast<int>(std::min<int64_t>(tiles, static_cast<int64_t>(Cache::occ_generic) * ctx->sm_count));
+    tile_generic<Op><<<g1, Op::THREADS, smem, ctx->stream>>>(p, begin, items);
+    HC_CHECK_LAUNCH(ctx, "tile_generic");
+  }
+  if (grid_out) {
+    grid_out[0] = g0;
+    grid_out[1] = g1;
+  }
+  return HC_OK;
+}
+
+template <int N, int K>
+void fill_codec_const(const hc_codec_s* c, CodecConst<N, K>* cc) {
+  for (int i = 0; i < K * N; ++i) cc->E[i] = c->E[i];
+  for (int i = 0; i < N * K; ++i) cc->D[i] = c->D[i];
+  for (int i = 0; i < 3 * K; ++i) cc->Mxyz[i] = c->Mxyz[i];
+  for (int i = 0; i < 9; ++i) cc->Crgb[i] = c->Crgb[i];
+  for (int i = 0; i < 3 * N; ++i) cc->cmf[i] = c->cmf_dl[i];
+}
+
+}  // namespace hcb
+
+// (n, k) dispatch over the compiled instantiations.
+#define HC_DISPATCH_NK(n, k, FN, ...)                                                      \
+  do {                                                                                     \
+    if ((n) == 81 && (k) == 6) return FN<81, 6>(__VA_ARGS__);                              \
+    if ((n) == 81 && (k) == 9) return FN<81, 9>(__VA_ARGS__);                              \
+    if ((n) == 81 && (k) == 3) return FN<81, 3>(__VA_ARGS__);                              \
+    if ((n) == 47 && (k) == 6) return FN<47, 6>(__VA_ARGS__);                              \
+    if ((n) == 47 && (k) == 9) return FN<47, 9>(__VA_ARGS__);                              \
+    if ((n) == 47 && (k) == 3) return FN<47, 3>(__VA_ARGS__);                              \
+    return ::hcb::set_error(HC_EUNSUPPORTED, "unsupported (n, k); compiled: n in {47, 81}, k in {3, 6, 9}"); \
+  } while (0)

@@ -1,0 +1,403 @@
+// hadacodec-b200: per-item compute bodies plugged into the tile pipeline.
+//
+// Each Op is thread-per-item: the item's row sits in shared memory (odd row
+// strides n = 47 / 81 make the column walk bank-conflict free), the codec
+// coefficients are kernel parameters (constant-bank FFMA operands), and the
+// results are written to shared staging that the pipeline bulk-stores.
+//
+// Reference lines restated (fp32 arithmetic; parity within 1e-5 relative of
+// the fp64 reference):
+//   encode            codec.cpp:36-46
+//   decode / image    codec.cpp:52-71, renderer.cpp:661-690
+//   XYZ / sRGB        colorimetry.cpp:75-87, :103-105, renderer.cpp:692-719
+//   latent shading    renderer.cpp:462-471, :505-510 (NEE), slice_pass :274-283,
+//                     reassembly :645-657
+//   naive shading     the same loops at C = n (renderer.cpp:187-190, :203-205)
+//   loss residual     trainer.cpp:49-71
+#pragma once
+
+#include "hc_common.cuh"
+
+namespace hcb {
+
+enum : int {
+  kErrNegativeCode = 1,  // decode of a negative code (codec.cpp:56-62) -> HC_EDOMAIN
+  kErrIndexRange = 2,    // palette index >= palette size (renderer.cpp:166-181) -> HC_EINVAL
+};
+
+// ---------------------------------------------------------------- codec
+enum CodecMode : int { kRoundtrip = 0, kEncode = 1, kDecode = 2, kProject = 3 };
+
+template <int N, int K, int MODE, int T_, int THREADS_, int STAGES_>
+struct CodecOp {
+  static constexpr int T = T_, THREADS = THREADS_, STAGES = STAGES_;
+  static constexpr int NIN = 1;
+  __host__ __device__ static constexpr int in_bytes(int) { return (MODE == kDecode ? K : N) * 4; }
+  // out streams: 0 codes, 1 spectra, 2 XYZ, 3 sRGB
+  static constexpr int NOUT = MODE == kEncode ? 1 : (MODE == kProject ? 2 : (MODE == kDecode ? 3 : 4));
+  //   roundtrip: codes, spectra, XYZ, sRGB | encode: codes | decode: spectra, XYZ, sRGB
+  //   project: XYZ, sRGB
+  __host__ __device__ static constexpr int out_bytes(int i) {
+    return MODE == kRoundtrip ? (i == 0 ? K * 4 : (i == 1 ? N * 4 : 12))
+         : MODE == kEncode    ? K * 4
+         : MODE == kDecode    ? (i == 0 ? N * 4 : 12)
+                              : 12;
+  }
+  static constexpr int EXTRA_SMEM = 0;
+
+  struct Params {
+    CodecConst<N, K> cc;
+    const float* in;
+    float* out[4];
+    int* err;
+    int check_negative;
+  };
+  struct State {};
+  __device__ static void init_state(State&) {}
+  __host__ __device__ static const void* in_ptr(const Params& p, int) { return p.in; }
+  __host__ __device__ static void* out_ptr(const Params& p, int i) { return p.out[i]; }
+  __device__ static void setup(const Params&, unsigned char*) {}
+  __device__ static void finish(const Params&, State&, unsigned char*) {}
+
+  __device__ static void compute(const Params& p, State&, const unsigned char* const* ins,
+                                 unsigned char* const* outs, unsigned char*, int item, int64_t) {
+    if constexpr (MODE == kProject) {
+      const float* s = reinterpret_cast<const float*>(ins[0]) + item * N;
+      float xyz[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const float v = s[i];
+        xyz[0] = fmaf(p.cc.cmf[i], v, xyz[0]);
+        xyz[1] = fmaf(p.cc.cmf[N + i], v, xyz[1]);
+        xyz[2] = fmaf(p.cc.cmf[2 * N + i], v, xyz[2]);
+      }
+      float rgb[3];
+      xyz_to_rgb(p.cc.Crgb, xyz, rgb);
+      float* ox = reinterpret_cast<float*>(outs[0]) + item * 3;
+      float* orgb = reinterpret_cast<float*>(outs[1]) + item * 3;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        ox[c] = xyz[c];
+        orgb[c] = rgb[c];
+      }
+      return;
+    }
+    float z[K];
+    if constexpr (MODE == kDecode) {
+      const float* zi = reinterpret_cast<const float*>(ins[0]) + item * K;
+      bool neg = false;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        z[j] = zi[j];
+        neg |= !(z[j] >= 0.f);
+      }
+      if (neg && p.check_negative) atomicOr(p.err, kErrNegativeCode);
+    } else {
+      const float* s = reinterpret_cast<const float*>(ins[0]) + item * N;
+#pragma unroll
+      for (int j = 0; j < K; ++j) z[j] = 0.f;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const float v = s[i];
+#pragma unroll
+        for (int j = 0; j < K; ++j) z[j] = fmaf(p.cc.E[j * N + i], v, z[j]);
+      }
+      float* oz = reinterpret_cast<float*>(outs[0]) + item * K;
+#pragma unroll
+      for (int j = 0; j < K; ++j) oz[j] = z[j];
+      if constexpr (MODE == kEncode) return;
+    }
+    constexpr int kSpec = MODE == kRoundtrip ? 1 : 0;
+    constexpr int kXyz = kSpec + 1, kRgb = kSpec + 2;
+    if (p.out[MODE == kRoundtrip ? 1 : 0] != nullptr) {
+      float* os = reinterpret_cast<float*>(outs[kSpec]) + item * N;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        float acc = p.cc.D[i * K] * z[0];
+#pragma unroll
+        for (int j = 1; j < K; ++j) acc = fmaf(p.cc.D[i * K + j], z[j], acc);
+        os[i] = acc;
+      }
+    }
+    float xyz[3], rgb[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float acc = p.cc.Mxyz[c * K] * z[0];
+#pragma unroll
+      for (int j = 1; j < K; ++j) acc = fmaf(p.cc.Mxyz[c * K + j], z[j], acc);
+      xyz[c] = acc;
+    }
+    xyz_to_rgb(p.cc.Crgb, xyz, rgb);
+    float* ox = reinterpret_cast<float*>(outs[kXyz]) + item * 3;
+    float* orgb = reinterpret_cast<float*>(outs[kRgb]) + item * 3;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      ox[c] = xyz[c];
+      orgb[c] = rgb[c];
+    }
+  }
+};
+
+// ---------------------------------------------------------------- latent shading
+// G-buffer item: idx (u32, palette entry) + L fp32 Lambert weights c_{p,l}.
+// z = zR[idx] (.) sum_l c_l zL_l  (renderer.cpp:505-510 with thr = 1,
+// w = c_{p,l}), all k channels at once: the k/3 RGB passes of slice_pass are
+// channel-disjoint, so writing channel 3b+c of the HWC latent image IS the
+// reassembly of renderer.cpp:645-657.  Then XYZ = Mxyz z, sRGB, and optionally
+// the full decoded spectrum D z.
+constexpr int kMaxPalette = 256;
+
+template <int N, int K, int L, bool SPEC, int T_, int THREADS_, int STAGES_>
+struct ShadeLatentOp {
+  static constexpr int T = T_, THREADS = THREADS_, STAGES = STAGES_;
+  static constexpr int NIN = 2;
+  __host__ __device__ static constexpr int in_bytes(int i) { return i == 0 ? 4 : L * 4; }
+  static constexpr int NOUT = SPEC ? 4 : 3;  // XYZ, sRGB, latent, [spectra]
+  __host__ __device__ static constexpr int out_bytes(int i) { return i < 2 ? 12 : (i == 2 ? K * 4 : N * 4); }
+  static constexpr int EXTRA_SMEM = kMaxPalette * K * 4;
+
+  struct Params {
+    CodecConst<N, K> cc;
+    float light[L * K];
+    const uint32_t* idx;
+    const float* cosv;
+    const float* pal_codes;
+    int n_pal;
+    float* xyz;
+    float* rgb;
+    float* latent;
+    float* spectra;
+    int* err;
+  };
+  struct State {};
+  __device__ static void init_state(State&) {}
+  __host__ __device__ static const void* in_ptr(const Params& p, int i) {
+    return i == 0 ? static_cast<const void*>(p.idx) : static_cast<const void*>(p.cosv);
+  }
+  __host__ __device__ static void* out_ptr(const Params& p, int i) {
+    return i == 0 ? p.xyz : (i == 1 ? p.rgb : (i == 2 ? p.latent : p.spectra));
+  }
+  __device__ static void setup(const Params& p, unsigned char* extra) {
+    float* pal = reinterpret_cast<float*>(extra);
+    for (int i = threadIdx.x; i < p.n_pal * K; i += blockDim.x) pal[i] = p.pal_codes[i];
+  }
+  __device__ static void finish(const Params&, State&, unsigned char*) {}
+
+  __device__ static void compute(const Params& p, State&, const unsigned char* const* ins,
+                                 unsigned char* const* outs, unsigned char* extra, int item, int64_t) {
+    uint32_t id = reinterpret_cast<const uint32_t*>(ins[0])[item];
+    if (id >= static_cast<uint32_t>(p.n_pal)) {
+      atomicOr(p.err, kErrIndexRange);
+      id = 0;
+    }
+    const float* c = reinterpret_cast<const float*>(ins[1]) + item * L;
+    float acc[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[j] = 0.f;
+#pragma unroll
+    for (int l4 = 0; l4 < L; l4 += 4) {
+      const float4 w4 = *reinterpret_cast<const float4*>(c + l4);
+      const float w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int j = 0; j < K; ++j) acc[j] = fmaf(w[q], p.light[(l4 + q) * K + j], acc[j]);
+    }
+    const float* zr = reinterpret_cast<const float*>(extra) + id * K;
+    float z[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) z[j] = zr[j] * acc[j];
+    if (p.latent) {
+      float* ol = reinterpret_cast<float*>(outs[2]) + item * K;
+#pragma unroll
+      for (int j = 0; j < K; ++j) ol[j] = z[j];
+    }
+    if constexpr (SPEC) {
+      float* os = reinterpret_cast<float*>(outs[3]) + item * N;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        float a = p.cc.D[i * K] * z[0];
+#pragma unroll
+        for (int j = 1; j < K; ++j) a = fmaf(p.cc.D[i * K + j], z[j], a);
+        os[i] = a;
+      }
+    }
+    float xyz[3], rgb[3];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+      float a = p.cc.Mxyz[cc * K] * z[0];
+#pragma unroll
+      for (int j = 1; j < K; ++j) a = fmaf(p.cc.Mxyz[cc * K + j], z[j], a);
+      xyz[cc] = a;
+    }
+    xyz_to_rgb(p.cc.Crgb, xyz, rgb);
+    float* ox = reinterpret_cast<float*>(outs[0]) + item * 3;
+    float* orgb = reinterpret_cast<float*>(outs[1]) + item * 3;
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+      ox[cc] = xyz[cc];
+      orgb[cc] = rgb[cc];
+    }
+  }
+};
+
+// ---------------------------------------------------------------- naive spectral shading
+// S(lambda) = R_idx(lambda) * sum_l c_l L_l(lambda) per wavelength (the same
+// NEE loop at C = n, renderer.cpp:187-190 / :505-510), XYZ = dlambda * CMF . S
+// (colorimetry.cpp:75-87), sRGB.  Palette spectra live in shared memory; light
+// SPDs and CMF rows are constant-bank operands.
+template <int N, int L, bool SPEC, int T_, int THREADS_, int STAGES_>
+struct ShadeSpectralOp {
+  static constexpr int T = T_, THREADS = THREADS_, STAGES = STAGES_;
+  static constexpr int NIN = 2;
+  __host__ __device__ static constexpr int in_bytes(int i) { return i == 0 ? 4 : L * 4; }
+  static constexpr int NOUT = SPEC ? 3 : 2;  // XYZ, sRGB, [spectra]
+  __host__ __device__ static constexpr int out_bytes(int i) { return i < 2 ? 12 : N * 4; }
+  static constexpr int EXTRA_SMEM = kMaxPalette * N * 4;
+
+  struct Params {
+    float light[L * N];
+    float cmf[3 * N];
+    float Crgb[9];
+    const uint32_t* idx;
+    const float* cosv;
+    const float* pal_spectra;
+    int n_pal;
+    float* xyz;
+    float* rgb;
+    float* spectra;
+    int* err;
+  };
+  struct State {};
+  __device__ static void init_state(State&) {}
+  __host__ __device__ static const void* in_ptr(const Params& p, int i) {
+    return i == 0 ? static_cast<const void*>(p.idx) : static_cast<const void*>(p.cosv);
+  }
+  __host__ __device__ static void* out_ptr(const Params& p, int i) {
+    return i == 0 ? p.xyz : (i == 1 ? p.rgb : p.spectra);
+  }
+  __device__ static void setup(const Params& p, unsigned char* extra) {
+    float* pal = reinterpret_cast<float*>(extra);
+    for (int i = threadIdx.x; i < p.n_pal * N; i += blockDim.x) pal[i] = p.pal_spectra[i];
+  }
+  __device__ static void finish(const Params&, State&, unsigned char*) {}
+
+  __device__ static void compute(const Params& p, State&, const unsigned char* const* ins,
+                                 unsigned char* const* outs, unsigned char* extra, int item, int64_t) {
+    uint32_t id = reinterpret_cast<const uint32_t*>(ins[0])[item];
+    if (id >= static_cast<uint32_t>(p.n_pal)) {
+      atomicOr(p.err, kErrIndexRange);
+      id = 0;
+    }
+    const float* c = reinterpret_cast<const float*>(ins[1]) + item * L;
+    float w[L];
+#pragma unroll
+    for (int l4 = 0; l4 < L; l4 += 4) {
+      const float4 w4 = *reinterpret_cast<const float4*>(c + l4);
+      w[l4] = w4.x;
+      w[l4 + 1] = w4.y;
+      w[l4 + 2] = w4.z;
+      w[l4 + 3] = w4.w;
+    }
+    const float* R = reinterpret_cast<const float*>(extra) + id * N;
+    float* os = SPEC ? reinterpret_cast<float*>(outs[2]) + item * N : nullptr;
+    float xyz[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      float illum = w[0] * p.light[i];
+#pragma unroll
+      for (int l = 1; l < L; ++l) illum = fmaf(w[l], p.light[l * N + i], illum);
+      const float s = R[i] * illum;
+      if constexpr (SPEC) os[i] = s;
+      xyz[0] = fmaf(p.cmf[i], s, xyz[0]);
+      xyz[1] = fmaf(p.cmf[N + i], s, xyz[1]);
+      xyz[2] = fmaf(p.cmf[2 * N + i], s, xyz[2]);
+    }
+    float rgb[3];
+    xyz_to_rgb(p.Crgb, xyz, rgb);
+    float* ox = reinterpret_cast<float*>(outs[0]) + item * 3;
+    float* orgb = reinterpret_cast<float*>(outs[1]) + item * 3;
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+      ox[cc] = xyz[cc];
+      orgb[cc] = rgb[cc];
+    }
+  }
+};
+
+// ---------------------------------------------------------------- loss
+// sum over pairs and lambda of (D (E a (.) E b) - a (.) b)^2 (trainer.cpp:49-71).
+// Per pair the 81 squared residuals are summed in fp32 (all terms >= 0), pairs
+// are accumulated in fp64 per thread, then reduced per CTA into partials[].
+template <int N, int K, int T_, int THREADS_, int STAGES_>
+struct LossOp {
+  static constexpr int T = T_, THREADS = THREADS_, STAGES = STAGES_;
+  static constexpr int NIN = 2;
+  __host__ __device__ static constexpr int in_bytes(int) { return N * 4; }
+  static constexpr int NOUT = 0;
+  __host__ __device__ static constexpr int out_bytes(int) { return 0; }
+  static constexpr int EXTRA_SMEM = 32 * 8;
+
+  struct Params {
+    CodecConst<N, K> cc;
+    const float* a;
+    const float* b;
+    double* partials;  // one per CTA
+    int partial_offset;
+  };
+  struct State {
+    double acc;
+  };
+  __device__ static void init_state(State& s) { s.acc = 0.0; }
+  __host__ __device__ static const void* in_ptr(const Params& p, int i) {
+    return i == 0 ? static_cast<const void*>(p.a) : static_cast<const void*>(p.b);
+  }
+  __host__ __device__ static void* out_ptr(const Params&, int) { return nullptr; }
+  __device__ static void setup(const Params&, unsigned char*) {}
+
+  __device__ static void compute(const Params& p, State& st, const unsigned char* const* ins,
+                                 unsigned char* const*, unsigned char*, int item, int64_t) {
+    const float* a = reinterpret_cast<const float*>(ins[0]) + item * N;
+    const float* b = reinterpret_cast<const float*>(ins[1]) + item * N;
+    float za[K], zb[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) za[j] = zb[j] = 0.f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const float va = a[i], vb = b[i];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        za[j] = fmaf(p.cc.E[j * N + i], va, za[j]);
+        zb[j] = fmaf(p.cc.E[j * N + i], vb, zb[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < K; ++j) za[j] *= zb[j];
+    float r = 0.f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      float sh = p.cc.D[i * K] * za[0];
+#pragma unroll
+      for (int j = 1; j < K; ++j) sh = fmaf(p.cc.D[i * K + j], za[j], sh);
+      const float d = fmaf(-a[i], b[i], sh);
+      r = fmaf(d, d, r);
+    }
+    st.acc += static_cast<double>(r);
+  }
+  __device__ static void finish(const Params& p, State& st, unsigned char* extra) {
+    double v = st.acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    double* red = reinterpret_cast<double*>(extra);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < (THREADS + 31) / 32; ++w) t += red[w];
+      p.partials[p.partial_offset + blockIdx.x] = t;
+    }
+  }
+};
+
+}  // namespace hcb
