@@ -415,6 +415,21 @@ def run_ours(args) -> int:
     R = wl.R
     steps = max(R, (args.steps + R - 1) // R * R)
 
+    if args.plain:
+        # Profiling mode (ncu): plain stream launches, no graph, no extras, no JSON contract.
+        with torch.cuda.stream(stream):
+            for i in range(args.warmup + args.steps):
+                wl.step(i)
+        torch.cuda.synchronize()
+        if args.naive_plain:
+            with torch.cuda.stream(stream):
+                wn = Workload(api, ctx, args.config, rank, naive=True)
+                for i in range(args.steps):
+                    wn.step(i)
+            torch.cuda.synchronize()
+        print(json.dumps({"plain": True, "config": args.config, "steps": args.steps, "launches": ctx.launches}))
+        return 0
+
     g, per_step, n_in_graph = time_graph(torch, wl, steps, args.warmup, stream)
     reps = steps // n_in_graph
 
@@ -598,6 +613,8 @@ def main(argv=None) -> int:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-naive", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--plain", action="store_true", help="profiling mode: plain launches only")
+    ap.add_argument("--naive-plain", action="store_true", help="with --plain: also run the naive path")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3

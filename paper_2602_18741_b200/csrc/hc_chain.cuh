@@ -125,6 +125,133 @@ __global__ void __launch_bounds__(256) chain_latent_kernel(const __grid_constant
   }
 }
 
+// Replicated-table variant for small even-padded k (k = 3, 6): the code tables are
+// stored as float2 rows replicated 16x across bank pairs, lane l of each
+// half-warp reading replica l % 16, so every LDS.64 of the 5 random lookups per
+// sample is bank-conflict free whatever the indices.  Per sample the chain is
+// re-associated (SURVEY Appendix A #7 allows it):
+//   thr_d = thr_{d-1} (.) a_d ;  s = sum_d t_d thr_d ;  rad = le (.) s
+// and each lane sums its samples in fp32 before the fp64 cross-lane reduction.
+template <int K>
+__global__ void __launch_bounds__(256) chain_latent_rep_kernel(const __grid_constant__ ChainLatentParams<K> p) {
+  constexpr int KP = (K + 1) / 2;  // float2 per code
+  extern __shared__ __align__(16) float2 rep[];
+  const int n_ent = p.n_pal + p.n_ill;
+  for (int i = threadIdx.x; i < n_ent * KP * 16; i += blockDim.x) {
+    const int q = i >> 4;
+    const int e = q / KP, c2 = q - e * KP;
+    const float* src = e < p.n_pal ? p.pal + e * K : p.ill + (e - p.n_pal) * K;
+    const float lo = src[2 * c2];
+    const float hi = 2 * c2 + 1 < K ? src[2 * c2 + 1] : 0.f;
+    rep[i] = make_float2(lo, hi);
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int g = lane & (kChainLanes - 1);
+  const float2* mine = rep + (lane & 15);
+  constexpr int kPixPerWarp = 32 / kChainLanes;
+  const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t npal = static_cast<uint32_t>(p.n_pal), nill = static_cast<uint32_t>(p.n_ill);
+  for (int64_t qd = warp_id; qd * kPixPerWarp < p.P; qd += nwarps) {
+    const int64_t pix = qd * kPixPerWarp + lane / kChainLanes;
+    const bool valid = pix < p.P;
+    float part[2 * KP];
+#pragma unroll
+    for (int j = 0; j < 2 * KP; ++j) part[j] = 0.f;
+    const int64_t base = pix * p.spp;
+    bool bad = false;
+    const int per_lane = valid ? p.spp / kChainLanes : 0;
+    // Samples in groups of kGroup per lane with every load of the group issued
+    // before any use: ~170 B in flight per lane keeps HBM busy (the kernel was
+    // long-scoreboard bound issuing one sample's loads at a time).
+    constexpr int kGroup = 8;
+    for (int m0 = 0; m0 < per_lane; m0 += kGroup) {
+      uint32_t pkg[kGroup], lig[kGroup];
+      float4 t4g[kGroup];
+#pragma unroll
+      for (int m = 0; m < kGroup; ++m) {
+        const int64_t s = base + g + static_cast<int64_t>(m0 + m) * kChainLanes;
+        const bool in = m0 + m < per_lane;
+        pkg[m] = in ? __ldg(p.pidx + s) : 0u;
+        lig[m] = in ? static_cast<uint32_t>(__ldg(p.iidx + s)) : 0u;
+        t4g[m] = in ? ldg_stream(p.tw + s) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+    for (int m = 0; m < kGroup; ++m) {
+      if (m0 + m >= per_lane) break;
+      const uint32_t pk = pkg[m];
+      uint32_t li = lig[m];
+      const float4 t4 = t4g[m];
+      const float tw[4] = {t4.x, t4.y, t4.z, t4.w};
+      if (li >= nill) { bad = true; li = 0; }
+      float thr[2 * KP], acc[2 * KP];
+#pragma unroll
+      for (int d = 0; d < 4; ++d) {
+        uint32_t ai = (pk >> (8 * d)) & 0xffu;
+        if (ai >= npal) { bad = true; ai = 0; }
+        const float2* row = mine + ai * (KP * 16);
+#pragma unroll
+        for (int c2 = 0; c2 < KP; ++c2) {
+          const float2 a = row[c2 * 16];
+          if (d == 0) {
+            thr[2 * c2] = a.x;
+            thr[2 * c2 + 1] = a.y;
+            acc[2 * c2] = tw[0] * a.x;
+            acc[2 * c2 + 1] = tw[0] * a.y;
+          } else {
+            thr[2 * c2] *= a.x;
+            thr[2 * c2 + 1] *= a.y;
+            acc[2 * c2] = fmaf(tw[d], thr[2 * c2], acc[2 * c2]);
+            acc[2 * c2 + 1] = fmaf(tw[d], thr[2 * c2 + 1], acc[2 * c2 + 1]);
+          }
+        }
+      }
+      const float2* lrow = mine + (npal + li) * (KP * 16);
+#pragma unroll
+      for (int c2 = 0; c2 < KP; ++c2) {
+        const float2 le = lrow[c2 * 16];
+        part[2 * c2] = fmaf(le.x, acc[2 * c2], part[2 * c2]);
+        part[2 * c2 + 1] = fmaf(le.y, acc[2 * c2 + 1], part[2 * c2 + 1]);
+      }
+    }
+    }
+    if (bad) atomicOr(p.err, kErrIndexRange);
+    double acc[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[j] = static_cast<double>(part[j]);
+#pragma unroll
+    for (int o = kChainLanes / 2; o > 0; o >>= 1)
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc[j] += __shfl_xor_sync(0xffffffffu, acc[j], o);
+    if (valid && g == 0) {
+      const double inv = 1.0 / p.spp;
+      float z[K];
+#pragma unroll
+      for (int j = 0; j < K; ++j) z[j] = static_cast<float>(acc[j] * inv);
+      if (p.latent)
+#pragma unroll
+        for (int j = 0; j < K; ++j) p.latent[pix * K + j] = z[j];
+      float xyz[3], rgb[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float a = p.Mxyz[c * K] * z[0];
+#pragma unroll
+        for (int j = 1; j < K; ++j) a = fmaf(p.Mxyz[c * K + j], z[j], a);
+        xyz[c] = a;
+      }
+      xyz_to_rgb(p.Crgb, xyz, rgb);
+      if (p.xyz)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) p.xyz[pix * 3 + c] = xyz[c];
+      if (p.rgb)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) p.rgb[pix * 3 + c] = rgb[c];
+    }
+  }
+}
+
 // Naive n-sample chain: the same recursion per wavelength.  Loop order is
 // wavelength-outer so per-lane state stays in registers; the pixel spectrum
 // value float(acc/spp) is projected to XYZ on the fly (colorimetry.cpp:75-87).

@@ -1,17 +1,36 @@
 // hadacodec-b200: multi-bounce accumulation launchers (config 4).
 // Reference: evaluation.cpp:50-76, renderer.cpp:457-551 (see hc_chain.cuh).
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "hc_chain.cuh"
 #include "hc_launch.cuh"
 
 namespace hcb {
 
+// Occupancy per (kernel, dynamic smem) is cached: the launchers also run inside
+// CUDA-graph capture, where attribute / occupancy queries are best avoided.
 template <class KernelFn>
 int chain_grid(hc_ctx ctx, KernelFn fn, int smem, int64_t P, int* grid) {
-  HC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> cache;
   int occ = 0;
-  HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(reinterpret_cast<const void*>(fn), smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      occ = it->second;
+    } else {
+      HC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      HC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                       cudaSharedmemCarveoutMaxShared));
+      HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+      cache[key] = occ;
+    }
+  }
   if (occ < 1) return set_error(HC_EUNSUPPORTED, "chain kernel does not fit on an SM");
   const int64_t blocks_needed = (P + 31) / 32;  // 32 pixels per 256-thread block iteration
   *grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_needed, static_cast<int64_t>(occ) * ctx->sm_count)));
@@ -38,12 +57,20 @@ int chain_latent_k(hc_codec c, const float* pal, int n_pal, const float* ill, in
   p.xyz = xyz;
   p.rgb = rgb;
   p.err = c->ctx->d_err;
-  const int smem = (n_pal + n_ill) * K * 4;
   int grid = 0;
-  int rc = chain_grid(c->ctx, chain_latent_kernel<K>, smem, P, &grid);
-  if (rc != HC_OK) return rc;
-  chain_latent_kernel<K><<<grid, 256, smem, c->ctx->stream>>>(p);
-  HC_CHECK_LAUNCH(c->ctx, "chain_latent_kernel");
+  if constexpr (K <= 6) {
+    const int smem = (n_pal + n_ill) * ((K + 1) / 2) * 16 * 8;  // replicated float2 tables
+    int rc = chain_grid(c->ctx, chain_latent_rep_kernel<K>, smem, P, &grid);
+    if (rc != HC_OK) return rc;
+    chain_latent_rep_kernel<K><<<grid, 256, smem, c->ctx->stream>>>(p);
+    HC_CHECK_LAUNCH(c->ctx, "chain_latent_rep_kernel");
+  } else {
+    const int smem = (n_pal + n_ill) * K * 4;
+    int rc = chain_grid(c->ctx, chain_latent_kernel<K>, smem, P, &grid);
+    if (rc != HC_OK) return rc;
+    chain_latent_kernel<K><<<grid, 256, smem, c->ctx->stream>>>(p);
+    HC_CHECK_LAUNCH(c->ctx, "chain_latent_kernel");
+  }
   return HC_OK;
 }
 

@@ -28,6 +28,10 @@ int configure_tile_op() {
   const int smem = TileLayout<Op>::smem_bytes();
   HC_CUDA_TRY(cudaFuncSetAttribute(tile_pipeline<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   HC_CUDA_TRY(cudaFuncSetAttribute(tile_generic<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  HC_CUDA_TRY(cudaFuncSetAttribute(tile_pipeline<Op>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   cudaSharedmemCarveoutMaxShared));
+  HC_CUDA_TRY(cudaFuncSetAttribute(tile_generic<Op>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   cudaSharedmemCarveoutMaxShared));
   int a = 0, b = 0;
   HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, tile_pipeline<Op>, Op::THREADS, smem));
   HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tile_generic<Op>, Op::THREADS, smem));

@@ -23,7 +23,7 @@ __global__ void sum_partials_kernel(const double* partials, int count, double* o
 
 template <int N, int K>
 int loss_nk(hc_codec c, const float* A, const float* B, int64_t pairs, double* sum_dev) {
-  using Op = LossOp<N, K, 64, 64, 3>;
+  using Op = LossOp<N, K, 64, 64, 2>;  // 83 KB smem: 2 CTAs / SM, one tile computing + one loading each
   hc_ctx ctx = c->ctx;
   int rc = configure_tile_op<Op>();
   if (rc != HC_OK) return rc;
@@ -36,6 +36,12 @@ int loss_nk(hc_codec c, const float* A, const float* B, int64_t pairs, double* s
   }
   typename Op::Params p;
   fill_codec_const<N, K>(c, &p.cc);
+  for (int j = 0; j < K; ++j)
+    for (int l = 0; l < K; ++l) {
+      double g = 0.0;
+      for (int i = 0; i < N; ++i) g += static_cast<double>(c->D[i * K + j]) * static_cast<double>(c->D[i * K + l]);
+      p.G[j * K + l] = static_cast<float>(g);
+    }
   p.a = A;
   p.b = B;
   p.partials = ctx->d_partials;

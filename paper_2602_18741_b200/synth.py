@@ -130,10 +130,12 @@ def mlp_weights(seed: int, k: int = 6, hidden: int = 64) -> dict:
     b1 = np.array([rb.uniform(-0.1, 0.1) for _ in range(hidden)])
     b2 = np.array([rb.uniform(-0.1, 0.1) for _ in range(hidden)])
     b3 = np.array([rb.uniform(-0.1, 0.1) for _ in range(k)])
+    # Biases are drawn bf16-representable: layer 1's bias rides the tensor-core
+    # operand (constant-1 input column), so all three are kept on the bf16 grid.
     return {
-        "w1": bf16_round(w1), "b1": b1.astype(np.float32),
-        "w2": bf16_round(w2), "b2": b2.astype(np.float32),
-        "w3": bf16_round(w3), "b3": b3.astype(np.float32),
+        "w1": bf16_round(w1), "b1": bf16_round(b1),
+        "w2": bf16_round(w2), "b2": bf16_round(b2),
+        "w3": bf16_round(w3), "b3": bf16_round(b3),
         "w1_f64": w1, "w2_f64": w2, "w3_f64": w3,
     }
 
