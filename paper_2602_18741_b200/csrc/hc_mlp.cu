@@ -5,19 +5,26 @@
 // with ReLU, ReLU and a softplus(beta = 1) head (codec.cpp:8-12), bf16 operands,
 // fp32 accumulation.
 //
-// One 128-pixel tile = one M = 128 tcgen05 tile row block:
-//   L1  D[128 x 64]  = A1[128 x 16] . W1'^T   A1 = (r, g, b, 1, 0...) bf16, W1' = [W1 | b1 | 0]
-//   L2  D[128 x 64]  = A2[128 x 64] . W2^T    A2 = bf16(relu(L1)),   epilogue adds b2
-//   L3  D[128 x 16]  = A3[128 x 64] . W3'^T   A3 = bf16(relu(L2 + b2)), W3' = W3 padded to 16 rows
+// One 128-pixel tile = one M = 128 tcgen05 row block:
+//   L1  D[128 x 64] = A1[128 x 16] . W1'^T   (SS: A1 = (r, g, b, 1, 0...) bf16 in smem,
+//                                              W1' = [W1 | b1 | 0]: bias rides the MMA)
+//   L2  D[128 x 64] = A2[128 x 64] . W2^T    (TS: A2 = bf16(relu(L1)) in TMEM)
+//   L3  D[128 x 16] = A3[128 x 64] . W3'^T   (TS: A3 = bf16(relu(L2 + b2)) in TMEM)
 //   out = softplus(L3[:, :k] + b3)
-// Operands live in shared memory in the canonical no-swizzle K-major UMMA layout
-// (8-row x 16-byte core matrices; element (r, k) at (k/8)*LBO + r*16 + (k%8)*2),
-// accumulators in TMEM (one 64-column allocation per CTA, reused by the three
-// layers), the epilogue is TMEM -> registers (tcgen05.ld) -> cvt.rn.relu.bf16x2 ->
-// st.shared straight into the next layer's A tile.  One elected thread issues the
-// MMAs and commits them to an mbarrier.  Several CTAs per SM interleave their
-// MMA and epilogue phases on the shared tensor core.  RGB tiles stream in through
-// 1-D bulk copies (TMA); each thread stores its pixel's code row.
+// Hidden activations never touch shared memory: the epilogue reads the fp32
+// accumulator (tcgen05.ld), applies bias / ReLU, packs bf16x2 (cvt.rn.relu.bf16x2)
+// and writes the next layer's A operand back into TMEM (tcgen05.st), which the
+// next MMA reads directly ("A from TMEM").  With A in shared memory (SS) the
+// 128 x 16 A tile is re-read from smem by every N = 64 MMA and smem bandwidth,
+// not the tensor core, was the limit (profiles/README.md).
+//
+// One CTA per SM, 4 warpgroups = 4 independent tile streams.  Each stream owns
+// 128 TMEM columns of the CTA's 512 ([0,32) packed A2/A3, [32,96) the fp32
+// accumulator), a 4 KB A1 tile and a 2-deep ring of rgb tiles fetched by 1-D
+// bulk copies (TMA); its elected thread issues its MMAs and commits them to the
+// stream's mbarrier, so the streams' MMA and epilogue phases interleave on the
+// SM's tensor core.  Weights (12 KB, canonical no-swizzle K-major UMMA images,
+// element (n, k) at (k/8)*(N*16) + n*16 + (k%8)*2) are loaded once per CTA.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -37,28 +44,30 @@ constexpr int kHid = 64;      // hidden width
 constexpr int kK1 = 16;       // layer-1 K (3 inputs + bias column, padded)
 constexpr int kN3 = 16;       // layer-3 N (k padded)
 constexpr int kMaxK = 9;
-constexpr int kThreads = 128;
+constexpr int kStreams = 4;                 // warpgroups / tile streams per CTA
+constexpr int kThreads = 128 * kStreams;
+constexpr int kK2 = 80;                     // layers 2/3 K: 64 hidden + constant-1 bias column, padded
+constexpr int kColsPerStream = 128;         // TMEM columns per stream (512 total)
+constexpr int kColA = 0;                    // packed bf16 A2 / A3 (+ bias chunk): 40 columns
+constexpr int kColD = 48;                   // fp32 accumulator of layers 1 / 2: 64 columns
+constexpr int kColD3 = 112;                 // fp32 accumulator of layer 3: 16 columns
 
 // Shared-memory image offsets (bytes).
 constexpr int kW1Bytes = kHid * kK1 * 2;   // 2 KB
-constexpr int kW2Bytes = kHid * kHid * 2;  // 8 KB
-constexpr int kW3Bytes = kN3 * kHid * 2;   // 2 KB
+constexpr int kW2Bytes = kHid * kK2 * 2;   // 10 KB ([W2 | b2 | 0])
+constexpr int kW3Bytes = kN3 * kK2 * 2;    // 2.5 KB ([W3 | b3 | 0])
 constexpr int kWBytes = kW1Bytes + kW2Bytes + kW3Bytes;
 constexpr int kOffW1 = 0;
 constexpr int kOffW2 = kOffW1 + kW1Bytes;
 constexpr int kOffW3 = kOffW2 + kW2Bytes;
-// A1 (128 x 16) aliases the first 4 KB of the A2/A3 buffer: A1 is dead once layer 1
-// has completed, and the next tile's A1 is written after layer 3 has completed.
-constexpr int kOffA2 = kOffW3 + kW3Bytes;            // 128 x 64 bf16 = 16 KB (A1, A2, A3)
-constexpr int kOffA1 = kOffA2;
-constexpr int kOffIn = kOffA2 + kMlpM * kHid * 2;    // 2 x 128 x 3 f32
+constexpr int kA1Bytes = kMlpM * kK1 * 2;            // 4 KB
 constexpr int kInTile = kMlpM * 3 * 4;               // 1536 B
-constexpr int kOffBar = kOffIn + 2 * kInTile;
-constexpr int kSmemBytes = kOffBar + 64;              // ~31 KB: 7 CTAs / SM
+constexpr int kStreamBytes = kA1Bytes + 2 * kInTile;
+constexpr int kOffStreams = kWBytes;
+constexpr int kOffBar = kOffStreams + kStreams * kStreamBytes;
+constexpr int kSmemBytes = kOffBar + kStreams * 4 * 8 + 16;
 
 struct MlpParams {
-  float b2[kHid];
-  float b3[kN3];
   const uint8_t* wimg;  // kWBytes, canonical layouts
   const float* rgb;     // P x 3
   float* out;           // P x k
@@ -66,7 +75,9 @@ struct MlpParams {
   int64_t ntiles;
   int64_t P;
   int k;
-  int use_tma;          // 1: tiles are full and 16-byte aligned
+  int use_tma;          // 1: tiles are full and the rgb base is 16-byte aligned
+  long long* trace;     // debug (HC_MLP_TRACE): per-phase clock64 stamps of CTA 0
+  int exp_mode;         // debug (HC_MLP_EXP): bit0 skip softplus, bit1 skip stores
 };
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -84,12 +95,22 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
          (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
+// D[tmem] (+)= A[smem] . B[smem]
+__device__ __forceinline__ void mma_ss(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// D[tmem] (+)= A[tmem] . B[smem]
+__device__ __forceinline__ void mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -108,7 +129,14 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
                  "=r"(r[15])                                                                            \
                : "r"(taddr))
 
+#define HC_TMEM_ST16(taddr, r)                                                                          \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" \
+               ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), \
+                 "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])   \
+               : "memory")
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ uint32_t pack_relu_bf16(float lo, float hi) {
   uint32_t d;
@@ -121,173 +149,212 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return d;
 }
 
-// softplus(x) with the reference's identity branch (codec.cpp:8-12, beta = 1):
-// max(x, 0) + log1p(exp(-|x|)), log1p by series below 1e-3.
+// softplus(x) = max(x, 0) + log1p(exp(-|x|)) (codec.cpp:8-12, beta = 1), branch-free:
+// for x > 30 the log1p term is < 1e-13 and vanishes in fp32, which is exactly the
+// reference's identity branch; log1p uses its series below 2^-10 (lg2(1 + e) loses
+// relative precision there).
 __device__ __forceinline__ float softplus1(float x) {
-  if (x > 30.f) return x;
-  const float e = __expf(-fabsf(x));
-  const float l = e < 1e-3f ? e * (1.f - 0.5f * e) : __logf(1.f + e);
+  const float e = exp2f(-fabsf(x) * 1.4426950408889634f);
+  const float l = e < 0.0009765625f ? e * fmaf(-0.5f, e, 1.f) : __log2f(1.f + e) * 0.6931471805599453f;
   return fmaxf(x, 0.f) + l;
 }
 
-// Epilogue for a 64-column layer: TMEM lane (row) -> bf16 relu(acc [+ bias]) row of
-// the next A tile.  Thread r owns row r; chunk c of 8 bf16 goes to c*2048 + r*16.
-template <bool kBias>
-__device__ __forceinline__ void epilogue_hidden(uint32_t tmem_row, const float* bias, unsigned char* A, int r) {
+// Hidden-layer epilogue: fp32 accumulator row (64 TMEM columns of this thread's
+// lane; biases already accumulated by the MMA) -> bf16 relu(acc) packed in pairs
+// (element 2j in the low half) -> 32 TMEM columns of the next layer's A operand.
+__device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem_a) {
   uint32_t va[4][16];
-  HC_TMEM_LD16(tmem_row + 0, va[0]);
-  HC_TMEM_LD16(tmem_row + 16, va[1]);
-  HC_TMEM_LD16(tmem_row + 32, va[2]);
-  HC_TMEM_LD16(tmem_row + 48, va[3]);
+  HC_TMEM_LD16(tmem_acc + 0, va[0]);
+  HC_TMEM_LD16(tmem_acc + 16, va[1]);
+  HC_TMEM_LD16(tmem_acc + 32, va[2]);
+  HC_TMEM_LD16(tmem_acc + 48, va[3]);
   tmem_wait_ld();
+  uint32_t pk[2][16];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const uint32_t* v = va[q];
-    uint32_t pk[8];
+  for (int q = 0; q < 4; ++q)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      float lo = __uint_as_float(v[2 * j]), hi = __uint_as_float(v[2 * j + 1]);
-      if (kBias) {
-        lo += bias[q * 16 + 2 * j];
-        hi += bias[q * 16 + 2 * j + 1];
-      }
-      pk[j] = pack_relu_bf16(lo, hi);
-    }
-    // columns q*16 .. q*16+15 = chunks 2q, 2q+1
-    *reinterpret_cast<uint4*>(A + (2 * q) * (kMlpM * 16) + r * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-    *reinterpret_cast<uint4*>(A + (2 * q + 1) * (kMlpM * 16) + r * 16) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-  }
+    for (int j = 0; j < 8; ++j)
+      pk[q >> 1][(q & 1) * 8 + j] =
+          pack_relu_bf16(__uint_as_float(va[q][2 * j]), __uint_as_float(va[q][2 * j + 1]));
+  HC_TMEM_ST16(tmem_a + 0, pk[0]);
+  HC_TMEM_ST16(tmem_a + 16, pk[1]);
+  tmem_wait_st();
 }
 
-__global__ void __launch_bounds__(kThreads) mlp_kernel(const __grid_constant__ MlpParams p) {
+__device__ __forceinline__ void stream_barrier(int stream) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + stream), "n"(128) : "memory");
+}
+
+__global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant__ MlpParams p) {
   extern __shared__ __align__(1024) unsigned char sm[];
-  uint64_t* bar_in = reinterpret_cast<uint64_t*>(sm + kOffBar);  // [2]
-  uint64_t* bar_mma = bar_in + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_in + 3);
-  unsigned char* A1 = sm + kOffA1;
-  unsigned char* A2 = sm + kOffA2;
-  float* in_tiles = reinterpret_cast<float*>(sm + kOffIn);
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
+  const int st = warp >> 2;       // tile stream (warpgroup)
+  const int quarter = warp & 3;   // TMEM lane quarter of this warp
+  const int r = tid & 127;        // tile row = TMEM lane
+  const bool leader = r == 0;
+  unsigned char* A1 = sm + kOffStreams + st * kStreamBytes;
+  float* in_tiles = reinterpret_cast<float*>(A1 + kA1Bytes);
+  uint64_t* bar_in = reinterpret_cast<uint64_t*>(sm + kOffBar) + st * 4;  // [2]
+  uint64_t* bar_l1 = bar_in + 2;   // layer-1 MMA commits
+  uint64_t* bar_mma = bar_in + 3;  // layer-2 / layer-3 MMA commits
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kOffBar + kStreams * 4 * 8);
 
-  // Weights: canonical images prepared on the host.
   for (int i = tid; i < kWBytes / 16; i += kThreads)
     reinterpret_cast<uint4*>(sm)[i] = reinterpret_cast<const uint4*>(p.wimg)[i];
-  if (tid == 0) {
+  if (leader) {
     mbar_init(&bar_in[0], 1);
     mbar_init(&bar_in[1], 1);
+    mbar_init(bar_l1, 1);
     mbar_init(bar_mma, 1);
     fence_mbar_init();
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_row = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+  const uint32_t tcol = tmem + st * kColsPerStream;               // stream base, lane 0
+  const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+  const uint32_t tA = tcol + kColA, tD = tcol + kColD, tD3 = tcol + kColD3;
+  {
+    // Constant K chunk of the layer-2/3 A operand: element 64 = 1 (bias), 65..79 = 0.
+    uint32_t one[8] = {0x3F80u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(tA + 32 + lane_off),
+                 "r"(one[0]), "r"(one[1]), "r"(one[2]), "r"(one[3]), "r"(one[4]), "r"(one[5]), "r"(one[6]),
+                 "r"(one[7])
+                 : "memory");
+    tmem_wait_st();
+  }
 
   const uint32_t sW1 = smem_u32(sm + kOffW1), sW2 = smem_u32(sm + kOffW2), sW3 = smem_u32(sm + kOffW3);
-  const uint32_t sA1 = smem_u32(A1), sA2 = smem_u32(A2);
-  constexpr uint32_t kChunkA = kMlpM * 16;  // K-chunk stride of a 128-row A tile
-  const uint32_t id1 = idesc_bf16(kMlpM, kHid), id3 = idesc_bf16(kMlpM, kN3);
+  const uint32_t sA1 = smem_u32(A1);
+  constexpr uint32_t kChunkA = kMlpM * 16;  // K-chunk stride of the 128-row A1 tile
+  const uint32_t id64 = idesc_bf16(kMlpM, kHid), id16 = idesc_bf16(kMlpM, kN3);
 
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kStreams + st;
+  const int64_t tstride = static_cast<int64_t>(gridDim.x) * kStreams;
   auto load_tile = [&](int64_t t, int s) {
     mbar_arrive_expect_tx(&bar_in[s], kInTile);
     bulk_g2s(in_tiles + s * kMlpM * 3, p.rgb + (p.first_tile + t) * kMlpM * 3, kInTile, &bar_in[s]);
   };
-  if (p.use_tma && tid == 0) {
-    if (blockIdx.x < p.ntiles) load_tile(blockIdx.x, 0);
-    if (blockIdx.x + gridDim.x < p.ntiles) load_tile(blockIdx.x + gridDim.x, 1);
+  if (p.use_tma && leader) {
+    if (t0 < p.ntiles) load_tile(t0, 0);
+    if (t0 + tstride < p.ntiles) load_tile(t0 + tstride, 1);
   }
-
-  uint32_t mma_phase = 0;
-  int iter = 0;
-  for (int64_t t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++iter) {
-    const int s = iter & 1;
-    const int64_t tile = p.first_tile + t;
-    const int64_t row0 = tile * kMlpM;
+  // rgb of tile t -> (r, g, b, 1, 0 ...) bf16 row of A1 (smem), then layer 1 is issued.
+  auto prepare_input = [&](int64_t t, int it) {
+    const int s = it & 1;
+    const int64_t row0 = (p.first_tile + t) * kMlpM;
     const int64_t left = p.P - row0;
-    const int rows = left < kMlpM ? static_cast<int>(left) : kMlpM;
-    // ---- input: rgb -> (r, g, b, 1) bf16 into A1 chunk 0
     float x0 = 0.f, x1 = 0.f, x2 = 0.f;
     if (p.use_tma) {
-      mbar_wait(&bar_in[s], (iter >> 1) & 1);
-      const float* in = in_tiles + s * kMlpM * 3 + tid * 3;
+      mbar_wait(&bar_in[s], (it >> 1) & 1);
+      const float* in = in_tiles + s * kMlpM * 3 + r * 3;
       x0 = in[0];
       x1 = in[1];
       x2 = in[2];
-    } else if (tid < rows) {
-      const float* in = p.rgb + (row0 + tid) * 3;
+    } else if (r < left) {
+      const float* in = p.rgb + (row0 + r) * 3;
       x0 = in[0];
       x1 = in[1];
       x2 = in[2];
     }
-    *reinterpret_cast<uint4*>(A1 + tid * 16) = make_uint4(pack_bf16(x0, x1), pack_bf16(x2, 1.0f), 0u, 0u);
-    *reinterpret_cast<uint4*>(A1 + kMlpM * 16 + tid * 16) = make_uint4(0u, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(A1 + r * 16) = make_uint4(pack_bf16(x0, x1), pack_bf16(x2, 1.0f), 0u, 0u);
+    *reinterpret_cast<uint4*>(A1 + kChunkA + r * 16) = make_uint4(0u, 0u, 0u, 0u);
     fence_proxy_async_smem();
-    tc_fence_before();
-    __syncthreads();  // A1 complete; input slot s consumed
-    if (tid == 0) {
-      if (p.use_tma && t + 2 * gridDim.x < p.ntiles) load_tile(t + 2 * gridDim.x, s);
-      tc_fence_after();
-      mma_bf16(tmem, umma_desc(sA1, kChunkA, 128), umma_desc(sW1, kHid * 16, 128), id1, 0);
-      mma_commit(bar_mma);
-    }
-    // ---- layer 1 epilogue: relu -> A2 (bias folded into W1)
-    mbar_wait(bar_mma, mma_phase);
-    mma_phase ^= 1;
+  };
+  auto issue_l1 = [&](int64_t t, int it) {  // leader only, after the stream barrier
+    if (p.use_tma && t + 2 * tstride < p.ntiles) load_tile(t + 2 * tstride, it & 1);
     tc_fence_after();
-    epilogue_hidden<false>(tmem_row, nullptr, A2, tid);
-    fence_proxy_async_smem();
+    mma_ss(tD, umma_desc(sA1, kChunkA, 128), umma_desc(sW1, kHid * 16, 128), id64, 0);
+    mma_commit(bar_l1);
+  };
+
+  uint32_t l1_phase = 0, mma_phase = 0;
+  if (t0 < p.ntiles) {
+    prepare_input(t0, 0);
     tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
+    stream_barrier(st);
+    if (leader) issue_l1(t0, 0);
+  }
+  int iter = 0;
+  for (int64_t t = t0; t < p.ntiles; t += tstride, ++iter) {
+    const int64_t row0 = (p.first_tile + t) * kMlpM;
+    const int64_t left = p.P - row0;
+    const int rows = left < kMlpM ? static_cast<int>(left) : kMlpM;
+    long long* tr = (p.trace && blockIdx.x == 0 && r == 0 && iter < 32) ? p.trace + (st * 32 + iter) * 8 : nullptr;
+    if (tr) tr[0] = clock64();
+    // ---- layer 1 done -> relu -> A2 (TMEM)
+    mbar_wait(bar_l1, l1_phase);
+    l1_phase ^= 1;
+    if (tr) tr[1] = clock64();
+    tc_fence_after();
+    epilogue_hidden(tD + lane_off, tA + lane_off);
+    tc_fence_before();
+    stream_barrier(st);
+    if (tr) tr[2] = clock64();
+    if (leader) {
       tc_fence_after();
 #pragma unroll
-      for (int kk = 0; kk < kHid / 16; ++kk)
-        mma_bf16(tmem, umma_desc(sA2 + kk * 2 * kChunkA, kChunkA, 128),
-                 umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128), id1, kk > 0);
+      for (int kk = 0; kk < kK2 / 16; ++kk)
+        mma_ts(tD, tA + kk * 8, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128), id64, kk > 0);
       mma_commit(bar_mma);
     }
-    // ---- layer 2 epilogue: relu(acc + b2) -> A3 (reuses the A2 buffer: L2 has completed)
+    // ---- overlap: the next tile's A1 (smem is free: layer 1 of this tile is done)
+    const int64_t tn = t + tstride;
+    if (tn < p.ntiles) prepare_input(tn, iter + 1);
+    // ---- layer 2 done -> relu(acc + b2) -> A3 (TMEM, over A2)
     mbar_wait(bar_mma, mma_phase);
     mma_phase ^= 1;
+    if (tr) tr[3] = clock64();
     tc_fence_after();
-    epilogue_hidden<true>(tmem_row, p.b2, A2, tid);
-    fence_proxy_async_smem();
+    epilogue_hidden(tD + lane_off, tA + lane_off);
     tc_fence_before();
-    __syncthreads();
-    if (tid == 0) {
+    stream_barrier(st);
+    if (tr) tr[4] = clock64();
+    if (leader) {
       tc_fence_after();
 #pragma unroll
-      for (int kk = 0; kk < kHid / 16; ++kk)
-        mma_bf16(tmem, umma_desc(sA2 + kk * 2 * kChunkA, kChunkA, 128),
-                 umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id3, kk > 0);
+      for (int kk = 0; kk < kK2 / 16; ++kk)
+        mma_ts(tD3, tA + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
       mma_commit(bar_mma);
+      // next tile's layer 1 into the layer-1/2 accumulator, read out above (epi2)
+      if (tn < p.ntiles) issue_l1(tn, iter + 1);
     }
-    // ---- layer 3 epilogue: softplus(acc + b3) -> codes
+    // ---- layer 3 done -> softplus(acc + b3) -> codes
     mbar_wait(bar_mma, mma_phase);
     mma_phase ^= 1;
+    if (tr) tr[6] = clock64();
     tc_fence_after();
     uint32_t v[16];
-    HC_TMEM_LD16(tmem_row, v);
+    HC_TMEM_LD16(tD3 + lane_off, v);
     tmem_wait_ld();
     tc_fence_before();
     const int k = p.k;
-    if (tid < rows) {
-      float* o = p.out + (row0 + tid) * k;
+    if (r < rows && !(p.exp_mode & 2)) {
+      float* o = p.out + (row0 + r) * k;
+      if (k == 6) {
+        float y[6];
 #pragma unroll
-      for (int j = 0; j < kMaxK; ++j)
-        if (j < k) o[j] = softplus1(__uint_as_float(v[j]) + p.b3[j]);
+        for (int j = 0; j < 6; ++j) y[j] = (p.exp_mode & 1) ? __uint_as_float(v[j]) : softplus1(__uint_as_float(v[j]));
+        reinterpret_cast<float2*>(o)[0] = make_float2(y[0], y[1]);
+        reinterpret_cast<float2*>(o)[1] = make_float2(y[2], y[3]);
+        reinterpret_cast<float2*>(o)[2] = make_float2(y[4], y[5]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j)
+          if (j < k) o[j] = softplus1(__uint_as_float(v[j]));
+      }
     }
+    if (tr) tr[7] = clock64();
   }
-  if (tid == 0) bulk_wait_all<0>();
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 }  // namespace hcb
@@ -331,10 +398,13 @@ int hc_mlp_create(hc_ctx ctx, int hidden, int k, const float* w1, const float* b
   for (int n = 0; n < kHid; ++n) {
     for (int j = 0; j < 3; ++j) put_kmajor(img, kOffW1, kHid, kK1, n, j, w1[n * 3 + j]);
     put_kmajor(img, kOffW1, kHid, kK1, n, 3, b1[n]);  // bias via the constant-1 input column
-    for (int j = 0; j < kHid; ++j) put_kmajor(img, kOffW2, kHid, kHid, n, j, w2[n * kHid + j]);
+    for (int j = 0; j < kHid; ++j) put_kmajor(img, kOffW2, kHid, kK2, n, j, w2[n * kHid + j]);
+    put_kmajor(img, kOffW2, kHid, kK2, n, kHid, b2[n]);  // bias via the constant-1 A column
   }
-  for (int n = 0; n < k; ++n)
-    for (int j = 0; j < kHid; ++j) put_kmajor(img, kOffW3, kN3, kHid, n, j, w3[n * kHid + j]);
+  for (int n = 0; n < k; ++n) {
+    for (int j = 0; j < kHid; ++j) put_kmajor(img, kOffW3, kN3, kK2, n, j, w3[n * kHid + j]);
+    put_kmajor(img, kOffW3, kN3, kK2, n, kHid, b3[n]);
+  }
   hc_mlp m = new hc_mlp_s();
   m->ctx = ctx;
   m->hidden = hidden;
@@ -345,22 +415,14 @@ int hc_mlp_create(hc_ctx ctx, int hidden, int k, const float* w1, const float* b
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(mlp_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
-  // The occupancy API does not model TMEM (it reports 1 CTA / SM for tcgen05 kernels);
-  // the real limits are shared memory and the 512 TMEM columns (64 per CTA).
-  int smem_sm = 0, dev = 0;
-  if (e == cudaSuccess) e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  m->occ = smem_sm / (kSmemBytes + 1024);
+  // One CTA per SM: it allocates all 512 TMEM columns (4 streams x 128).
+  m->occ = 1;
   if (e != cudaSuccess) {
     if (m->d_wimg) cudaFree(m->d_wimg);
     delete m;
     return cuda_error(e, "hc_mlp_create");
   }
-  if (const char* o = std::getenv("HC_MLP_OCC")) m->occ = std::atoi(o);
-  m->occ = std::max(1, std::min(m->occ, 8));  // 8 x 64 TMEM columns = the full 512
   std::memset(&m->base, 0, sizeof(m->base));
-  for (int i = 0; i < kHid; ++i) m->base.b2[i] = b2[i];
-  for (int i = 0; i < k; ++i) m->base.b3[i] = b3[i];
   m->base.wimg = m->d_wimg;
   m->base.k = k;
   *out = m;
@@ -393,8 +455,36 @@ int hc_mlp_forward(hc_mlp m, const float* rgb, int64_t P, float* codes) {
     p.use_tma = 1;
     const int grid = static_cast<int>(std::min<int64_t>(full, static_cast<int64_t>(m->occ) * ctx->sm_count));
     if (std::getenv("HC_DEBUG")) std::fprintf(stderr, "[hc] mlp_kernel grid=%d occ=%d smem=%d\n", grid, m->occ, kSmemBytes);
+    long long* trace = nullptr;
+    if (const char* em = std::getenv("HC_MLP_EXP")) p.exp_mode = std::atoi(em);
+    if (std::getenv("HC_MLP_TRACE")) {
+      cudaMalloc(&trace, kStreams * 32 * 8 * sizeof(long long));
+      cudaMemset(trace, 0, kStreams * 32 * 8 * sizeof(long long));
+      p.trace = trace;
+    }
     mlp_kernel<<<grid, kThreads, kSmemBytes, ctx->stream>>>(p);
     HC_CHECK_LAUNCH(ctx, "mlp_kernel");
+    p.trace = nullptr;
+    if (trace) {
+      cudaStreamSynchronize(ctx->stream);
+      std::vector<long long> h(kStreams * 32 * 8);
+      cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost);
+      cudaFree(trace);
+      double acc[8] = {0};
+      int n = 0;
+      for (int st = 0; st < kStreams; ++st)
+        for (int it = 4; it < 31; ++it) {
+          const long long* a = &h[(st * 32 + it) * 8];
+          const long long* b = &h[(st * 32 + it + 1) * 8];
+          if (!a[0] || !b[0]) continue;
+          for (int k = 1; k < 8; ++k) acc[k - 1] += double(a[k] - a[k - 1]);
+          acc[7] += double(b[0] - a[7]);
+          ++n;
+        }
+      if (n)
+        std::fprintf(stderr, "[hc] mlp phase cycles (avg of %d tiles): L1wait %.0f epi1 %.0f L2wait %.0f epi2 %.0f nextin %.0f L3wait %.0f epi3 %.0f loop %.0f\n",
+                     n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n, acc[6] / n, acc[7] / n);
+    }
   }
   if (full * kMlpM < P) {
     p.first_tile = full;
