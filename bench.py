@@ -271,7 +271,8 @@ def run_reference_arm(args) -> int:
 class Workload:
     """Builds the per-rank inputs of one config and a step() closure over buffer set i."""
 
-    def __init__(self, api, ctx, cfg_key: str, rank: int, naive: bool = False):
+    def __init__(self, api, ctx, cfg_key: str, rank: int, naive: bool = False, world: int = 1,
+                 strong: bool = False):
         import torch
         from paper_2602_18741_b200 import synth
 
@@ -282,9 +283,18 @@ class Workload:
         self.codec = codec = api.Codec(ctx, E, D)
         self.sets = []
         R = cfg["rot"]
+        from paper_2602_18741_b200.sharding import row_band
+
+        def span(total_rows: int, width: int) -> tuple[int, int]:
+            # weak: rank r owns rows [r*H, (r+1)*H) of an N-frame-tall image;
+            # strong: one frame split into row bands (sharding.row_band).
+            if strong:
+                b = row_band(rank, world, total_rows, width)
+                return b.first_pixel, b.pixels
+            return rank * total_rows * width, total_rows * width
         if cfg_key in ("2", "3"):
             W, H, L = cfg["W"], cfg["H"], cfg["L"]
-            P = W * H
+            first, P = span(H, W)
             pal = synth.palette(SEED, 256, N_SPEC)
             lts = synth.lights(SEED, L, N_SPEC)
             self.pal_d = torch.from_numpy(pal).cuda()
@@ -293,7 +303,7 @@ class Workload:
             self.light_codes = codec.encode(torch.from_numpy(lts).cuda()).cpu().numpy()
             spec = cfg_key == "3"
             for r in range(R):
-                idx, cosv = api.synth_gbuffer(ctx, SEED + r, rank * P, P, L, 256)
+                idx, cosv = api.synth_gbuffer(ctx, SEED + r, first, P, L, 256)
                 outs = {"xyz": None if spec else ctx.empty(P, 3), "rgb": ctx.empty(P, 3),
                         "spectra": ctx.empty(P, N_SPEC) if spec else None, "latent": None}
                 self.sets.append((idx, cosv, outs))
@@ -307,9 +317,9 @@ class Workload:
                     codec.shade_latent(self.pal_codes, self.light_codes, idx, cosv, out=outs)
             self.step = step
         elif cfg_key == "1":
-            P = cfg["units"]
+            first, P = span(cfg["units"], 1)
             for r in range(R):
-                S = api.synth_gm_spectra(ctx, SEED + r, "codec.spectra", rank * P, P, N_SPEC)
+                S = api.synth_gm_spectra(ctx, SEED + r, "codec.spectra", first, P, N_SPEC)
                 outs = {"codes": ctx.empty(P, k), "spectra": ctx.empty(P, N_SPEC), "xyz": ctx.empty(P, 3),
                         "rgb": ctx.empty(P, 3)}
                 self.sets.append((S, outs))
@@ -321,7 +331,7 @@ class Workload:
             self.step = step
         elif cfg_key == "4":
             W, H, spp = cfg["W"], cfg["H"], cfg["spp"]
-            P = W * H
+            first, P = span(H, W)
             pal = synth.palette(SEED, 256, N_SPEC)
             ill = synth.lights(SEED, 16, N_SPEC, purpose="scene.illuminants")
             self.pal_d = torch.from_numpy(pal).cuda()
@@ -329,7 +339,7 @@ class Workload:
             self.pal_codes = codec.encode(self.pal_d)
             self.ill_codes = codec.encode(self.ill_d)
             for r in range(R):
-                pidx, iidx, tw = api.synth_chain(ctx, SEED + r, rank * P, P, spp, 256, 16)
+                pidx, iidx, tw = api.synth_chain(ctx, SEED + r, first, P, spp, 256, 16)
                 outs = {"xyz": ctx.empty(P, 3), "rgb": ctx.empty(P, 3), "latent": None}
                 self.sets.append((pidx, iidx, tw, outs))
             self.units = P
@@ -343,11 +353,11 @@ class Workload:
             self.step = step
         elif cfg_key == "5a":
             W, H = cfg["W"], cfg["H"]
-            P = W * H
+            first, P = span(H, W)
             w = synth.mlp_weights(SEED, 6, 64)
             self.mlp = api.Upsampler(ctx, w)
             for r in range(R):
-                rgb = api.synth_uniform(ctx, SEED + r, "mlp.input", rank * P * 3, P * 3).reshape(P, 3)
+                rgb = api.synth_uniform(ctx, SEED + r, "mlp.input", first * 3, P * 3).reshape(P, 3)
                 self.sets.append((rgb, ctx.empty(P, 6)))
             self.units = P
 
@@ -356,9 +366,9 @@ class Workload:
                 self.mlp.forward(rgb, out=out)
             self.step = step
         else:  # 5b
-            P = cfg["units"]
-            A = api.synth_gm_spectra(ctx, SEED, "loss.a", rank * P, P, N_SPEC)
-            B = api.synth_gm_spectra(ctx, SEED, "loss.b", rank * P, P, N_SPEC)
+            first, P = span(cfg["units"], 1)
+            A = api.synth_gm_spectra(ctx, SEED, "loss.a", first, P, N_SPEC)
+            B = api.synth_gm_spectra(ctx, SEED, "loss.b", first, P, N_SPEC)
             self.sum = ctx.empty(1, dtype=torch.float64)
             self.sets.append((A, B))
             self.units = P
@@ -410,7 +420,7 @@ def run_ours(args) -> int:
     stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
         ctx = api.Context(dev)
-        wl = Workload(api, ctx, args.config, rank)
+        wl = Workload(api, ctx, args.config, rank, world=world, strong=args.scaling == "strong")
     torch.cuda.synchronize()
     R = wl.R
     steps = max(R, (args.steps + R - 1) // R * R)
@@ -423,7 +433,8 @@ def run_ours(args) -> int:
         torch.cuda.synchronize()
         if args.naive_plain:
             with torch.cuda.stream(stream):
-                wn = Workload(api, ctx, args.config, rank, naive=True)
+                wn = Workload(api, ctx, args.config, rank, naive=True, world=world,
+                              strong=args.scaling == "strong")
                 for i in range(args.steps):
                     wn.step(i)
             torch.cuda.synchronize()
@@ -491,7 +502,7 @@ def run_ours(args) -> int:
         wn_step_ours = wl.step
         # rebuild the step closure with the naive path over the same buffers
         with torch.cuda.stream(stream):
-            wl2 = Workload(api, ctx, args.config, rank, naive=True)
+            wl2 = Workload(api, ctx, args.config, rank, naive=True, world=world, strong=args.scaling == "strong")
         gn, _, nn = time_graph(torch, wl2, steps if args.config != "4" else R, 1, stream)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -582,13 +593,13 @@ def run_ours(args) -> int:
         line = {
             "metric": METRIC if args.config == "2" else f"{cfg['unit']} config {args.config}",
             "value": value, "unit": cfg["unit"], "n_gpus": world, "steps": steps, "warmup": args.warmup,
-            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "bf16" if args.config == "5a" else "f32", "data": "synthetic (seeded, DESIGN.md Inputs)",
             "config": {"workload": cfg["name"], "config_id": args.config, "units_per_gpu": wl.units,
                        "l2": f"{R} rotating input/output buffer sets"
                              f" ({'each' if R == 1 else 'rotation'} > 2x 126 MB L2)",
                        "timing": "CUDA graph of the step replayed K times; CUDA events; max over ranks",
-                       "parallelism": f"row bands, weak scaling, {world} rank(s)"},
+                       "parallelism": f"row bands, {args.scaling} scaling, {world} rank(s), no data-path collective"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -610,6 +621,8 @@ def main(argv=None) -> int:
     ap.add_argument("--warmup", type=int, default=16)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="2")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="weak: one frame per GPU (default); strong: one frame split into row bands")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-naive", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

@@ -1,0 +1,173 @@
+// hadacodec-b200 — C++ drop-in host API for the reference's per-pixel codec /
+// latent-shading path, over the C ABI (include/hadacodec_b200.h).
+//
+// Mirrors the reference's public headers (/root/reference/proj/core/include/
+// hadacodec/{codec,colorimetry,renderer}.hpp): same type and function names,
+// argument meaning and exception types (std::invalid_argument, std::domain_error),
+// in namespace hadacodec::b200 so both libraries can be linked side by side.
+// Differences a caller should know:
+//   * the grid is a runtime property (n = 47 reference grid, or 81 = BASELINE grid)
+//     instead of the compile-time kSampleCount, so SpectralCurve is a vector;
+//   * arithmetic is fp32 on the GPU (reference: fp64), agreeing to ~1e-6 relative;
+//   * every call runs on a Device (one per GPU, one CUDA stream); the by-value
+//     calls copy in and out and synchronise, the *_batch / shade_* calls take
+//     whole images — the form the hot path should use.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hadacodec_b200.h"
+
+namespace hadacodec {
+namespace b200 {
+
+// spectrum.hpp:10-21 — runtime grid.
+struct Grid {
+  int n = 81;
+  double lambda_min = 380.0;
+  double lambda_step = 5.0;
+  double wavelength_at(int i) const { return lambda_min + lambda_step * i; }
+  static Grid reference47();  // 368..830 nm, 47 samples (the reference's kSampleCount)
+  static Grid baseline81();   // 380..780 nm, 81 samples (BASELINE.json)
+  static Grid for_samples(int n);
+};
+
+// spectrum.hpp:25-39
+struct SpectralCurve {
+  std::vector<double> v;
+  SpectralCurve() = default;
+  explicit SpectralCurve(int n, double value = 0.0) : v(static_cast<size_t>(n), value) {}
+  int size() const { return static_cast<int>(v.size()); }
+  double& operator[](int i) { return v[static_cast<size_t>(i)]; }
+  const double& operator[](int i) const { return v[static_cast<size_t>(i)]; }
+};
+
+// codec.hpp:14-22
+struct LatentCode {
+  std::vector<double> z;
+  int k() const { return static_cast<int>(z.size()); }
+  double& operator[](int i) { return z[static_cast<size_t>(i)]; }
+  const double& operator[](int i) const { return z[static_cast<size_t>(i)]; }
+};
+
+// codec.hpp:34-43
+struct CodecWeights {
+  int k = 6;
+  int n = 81;
+  double beta = 10.0;
+  std::vector<double> raw_enc;  // k x n
+  std::vector<double> raw_dec;  // n x k
+  int blocks() const { return k / 3; }
+};
+
+// codec.hpp:52-58
+struct EffectiveWeights {
+  int k = 0;
+  int n = 0;
+  std::vector<double> enc;  // k x n
+  std::vector<double> dec;  // n x k
+};
+
+// colorimetry.hpp:9-22
+enum class ColorSpace { XYZ, LinearRGB, Lab };
+struct ColorTriple {
+  ColorSpace space = ColorSpace::XYZ;
+  std::array<double, 3> c{};
+  double& operator[](int i) { return c[static_cast<size_t>(i)]; }
+  const double& operator[](int i) const { return c[static_cast<size_t>(i)]; }
+};
+
+// renderer.hpp:73-89 (row-major y, x, channel)
+struct ChannelImage {
+  int width = 0, height = 0, channels = 0;
+  std::vector<float> data;
+  float& at(int x, int y, int c) { return data[(static_cast<size_t>(y) * width + x) * channels + c]; }
+  float at(int x, int y, int c) const { return data[(static_cast<size_t>(y) * width + x) * channels + c]; }
+};
+
+// One GPU + one CUDA stream (hc_ctx).  Non-copyable; owns device scratch.
+class Device {
+ public:
+  explicit Device(int device = 0, void* stream = nullptr);
+  ~Device();
+  Device(const Device&) = delete;
+  Device& operator=(const Device&) = delete;
+  hc_ctx handle() const { return ctx_; }
+  void synchronize();  // throws the latched device-side violations
+  int64_t launches() const;
+
+ private:
+  hc_ctx ctx_ = nullptr;
+};
+
+// A codec resident on a Device: E, D and the folded 3 x k XYZ projection.
+class Codec {
+ public:
+  Codec(Device& dev, const EffectiveWeights& w, const Grid& grid);
+  Codec(Device& dev, const CodecWeights& w, const Grid& grid);  // softplus on the host
+  ~Codec();
+  Codec(const Codec&) = delete;
+  Codec& operator=(const Codec&) = delete;
+  hc_codec handle() const { return codec_; }
+  int k() const { return k_; }
+  int n() const { return n_; }
+  Device& device() const { return *dev_; }
+
+ private:
+  Device* dev_;
+  hc_codec codec_ = nullptr;
+  int k_ = 0, n_ = 0;
+};
+
+// ---- codec.hpp:46-82
+double softplus(double raw, double beta);
+double softplus_derivative(double raw, double beta);
+EffectiveWeights effective_weights(const CodecWeights& w);
+void validate(const CodecWeights& w, const Grid& grid);
+LatentCode encode(const Codec& c, const SpectralCurve& s);
+SpectralCurve decode(const Codec& c, const LatentCode& z);  // throws std::domain_error on negative codes
+LatentCode blockwise_hadamard(const LatentCode& a, const LatentCode& b);
+std::vector<std::array<double, 3>> split_blocks(const LatentCode& z);
+LatentCode join_blocks(const std::vector<std::array<double, 3>>& blocks);
+
+// ---- batched codec (row-major host buffers; rows x n spectra, rows x k codes)
+std::vector<float> encode_batch(const Codec& c, const std::vector<float>& spectra);
+struct RoundTrip {
+  std::vector<float> codes, spectra, xyz, rgb;
+};
+RoundTrip roundtrip_batch(const Codec& c, const std::vector<float>& spectra);
+
+// ---- colorimetry.hpp:45-56 (radiance convention, IEC sRGB), computed on the GPU
+ColorTriple spectrum_to_xyz(const Codec& c, const SpectralCurve& s);
+ColorTriple xyz_to_linear_rgb(const ColorTriple& xyz);
+
+// ---- renderer.hpp:109-115
+ChannelImage decode_image(const Codec& c, const ChannelImage& latent);   // k -> n channels
+ChannelImage image_to_linear_rgb(const Codec& c, const ChannelImage& img);  // n -> 3 channels
+
+// ---- G-buffer latent shading (configs 2/3): one frame, host buffers.
+struct GBuffer {
+  int width = 0, height = 0, lights = 0;
+  std::vector<uint32_t> palette_index;  // width * height
+  std::vector<float> cos_terms;         // width * height * lights
+};
+struct ShadedFrame {
+  ChannelImage latent;   // k channels (reassembled k/3 passes)
+  ChannelImage xyz;      // 3 channels
+  ChannelImage linear_rgb;
+};
+// palette_codes: n_pal x k, light_codes: L x k (e.g. from encode_batch on the assets,
+// as compile_scene does, renderer.cpp:201-225).
+ShadedFrame shade_latent(const Codec& c, const std::vector<float>& palette_codes,
+                         const std::vector<float>& light_codes, const GBuffer& g);
+// Naive n-sample path on the same G-buffer (palette_spectra n_pal x n, light_spectra L x n).
+ShadedFrame shade_spectral(const Codec& c, const std::vector<float>& palette_spectra,
+                           const std::vector<float>& light_spectra, const GBuffer& g);
+
+}  // namespace b200
+}  // namespace hadacodec

@@ -1,0 +1,223 @@
+// Drop-in API tests: the reference's own codec / colorimetry test cases
+// (proj/tests/test_codec.cpp, test_colorimetry.cpp) re-run through
+// include/hadacodec_b200.hpp on the GPU.  Exact checks stay exact; checks the
+// reference makes at 1e-14 against fp64 arithmetic are made at fp32 tolerance.
+#include <cmath>
+#include <cstdio>
+#include <limits>
+#include <stdexcept>
+#include <vector>
+
+#include "hadacodec_b200.hpp"
+
+using namespace hadacodec::b200;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(cond)                                                        \
+  do {                                                                     \
+    ++g_checks;                                                            \
+    if (!(cond)) {                                                         \
+      ++g_fail;                                                            \
+      std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+    }                                                                      \
+  } while (0)
+#define CHECK_THROWS_AS(expr, ex)      \
+  do {                                 \
+    bool _t = false;                   \
+    try {                              \
+      (void)(expr);                    \
+    } catch (const ex&) {              \
+      _t = true;                       \
+    } catch (...) {                    \
+    }                                  \
+    CHECK(_t && #ex);                  \
+  } while (0)
+
+static bool rel_close(double a, double b, double rel) { return std::fabs(a - b) <= rel * std::max(1.0, std::fabs(b)); }
+
+// xoshiro-free deterministic values (the reference's tests use Rng streams; any
+// seeded values exercise the same contracts).
+static double lcg(uint64_t& s) {
+  s = s * 6364136223846793005ull + 1442695040888963407ull;
+  return static_cast<double>(s >> 11) * 0x1.0p-53;
+}
+
+static CodecWeights random_weights(int k, int n, uint64_t seed) {  // test_codec.cpp:16-27
+  CodecWeights w;
+  w.k = k;
+  w.n = n;
+  w.raw_enc.resize(static_cast<size_t>(k) * n);
+  w.raw_dec.resize(static_cast<size_t>(n) * k);
+  for (double& v : w.raw_enc) v = -0.3 + 0.6 * lcg(seed);
+  for (double& v : w.raw_dec) v = -0.3 + 0.6 * lcg(seed);
+  return w;
+}
+
+int main() {
+  // softplus values and branches (test_codec.cpp:35-60): host arithmetic, exact contract
+  CHECK(rel_close(softplus(0.0, 10.0), 0.069314718055994526, 1e-14));
+  CHECK(rel_close(softplus(-1.0, 10.0), 4.5398899216864648e-06, 1e-12));
+  CHECK(rel_close(softplus(0.2, 10.0), 0.21269280110429728, 1e-14));
+  CHECK(softplus(3.1, 10.0) == 3.1);
+  CHECK(softplus(1000.0, 10.0) == 1000.0);
+  CHECK(softplus_derivative(3.1, 10.0) == 1.0);
+  CHECK(rel_close(softplus_derivative(0.2, 10.0), 0.88079707797788231, 1e-14));
+
+  Device dev(0);
+  const Grid g47 = Grid::reference47();
+
+  // effective weights strictly positive (test_codec.cpp:70-79)
+  const CodecWeights w = random_weights(6, 47, 17);
+  const EffectiveWeights e = effective_weights(w);
+  for (double v : e.enc) CHECK(v > 0.0);
+  for (double v : e.dec) CHECK(v > 0.0);
+
+  // encode / decode = explicit mat-vec (test_codec.cpp:81-111) at fp32 tolerance
+  Codec codec(dev, e, g47);
+  uint64_t s = 99;
+  SpectralCurve sc(47);
+  for (int i = 0; i < 47; ++i) sc[i] = lcg(s);
+  const LatentCode z = encode(codec, sc);
+  CHECK(z.k() == 6);
+  for (int j = 0; j < 6; ++j) {
+    double acc = 0.0;
+    for (int i = 0; i < 47; ++i) acc += static_cast<double>(static_cast<float>(e.enc[j * 47 + i])) *
+                                        static_cast<double>(static_cast<float>(sc[i]));
+    CHECK(rel_close(z[j], acc, 2e-6));
+    CHECK(z[j] >= 0.0);
+  }
+  const SpectralCurve d = decode(codec, z);
+  for (int i = 0; i < 47; ++i) {
+    double acc = 0.0;
+    for (int j = 0; j < 6; ++j) acc += static_cast<double>(static_cast<float>(e.dec[i * 6 + j])) * z[j];
+    CHECK(rel_close(d[i], acc, 2e-6));
+  }
+  // CodecWeights overload agrees with the EffectiveWeights path
+  Codec codec_raw(dev, w, g47);
+  const LatentCode z2 = encode(codec_raw, sc);
+  for (int j = 0; j < 6; ++j) CHECK(rel_close(z2[j], z[j], 1e-6));
+
+  // linearity (test_codec.cpp:113-137) at fp32 tolerance
+  for (int it = 0; it < 20; ++it) {
+    SpectralCurve a(47), b(47), ab(47), as(47);
+    const double alpha = 5.0 * lcg(s);
+    for (int i = 0; i < 47; ++i) {
+      a[i] = 2.0 * lcg(s);
+      b[i] = 2.0 * lcg(s);
+      ab[i] = static_cast<double>(static_cast<float>(a[i]) + static_cast<float>(b[i]));
+      as[i] = alpha * a[i];
+    }
+    const LatentCode za = encode(codec, a), zb = encode(codec, b), zs = encode(codec, ab), zc = encode(codec, as);
+    for (int j = 0; j < 6; ++j) {
+      CHECK(std::fabs(zs[j] - (za[j] + zb[j])) <= 2e-6 * std::max(1.0, std::fabs(za[j] + zb[j])));
+      CHECK(std::fabs(zc[j] - alpha * za[j]) <= 2e-6 * std::max(1.0, std::fabs(alpha * za[j])));
+    }
+  }
+
+  // decode rejects negative codes and wrong dimensions (test_codec.cpp:139-152)
+  LatentCode zz;
+  zz.z = {0.1, 0.2, 0.3, 0.4, 0.5, 0.6};
+  (void)decode(codec, zz);
+  zz[2] = -1e-9;
+  CHECK_THROWS_AS(decode(codec, zz), std::domain_error);
+  zz.z = {0.1, 0.2, 0.3};
+  CHECK_THROWS_AS(decode(codec, zz), std::invalid_argument);
+
+  // blockwise hadamard and block packing (test_codec.cpp:154-180): exact
+  LatentCode ha, hb;
+  ha.z = {1.0, 2.0, 3.0, 4.0, 5.0, 6.0};
+  hb.z = {0.5, 0.5, 2.0, 0.0, 1.0, 3.0};
+  const LatentCode h = blockwise_hadamard(ha, hb);
+  const double expect[6] = {0.5, 1.0, 6.0, 0.0, 5.0, 18.0};
+  for (int j = 0; j < 6; ++j) CHECK(h[j] == expect[j]);
+  LatentCode shortc;
+  shortc.z = {1.0, 2.0, 3.0};
+  CHECK_THROWS_AS(blockwise_hadamard(ha, shortc), std::invalid_argument);
+  const auto blocks = split_blocks(ha);
+  CHECK(blocks.size() == 2u && blocks[1][2] == 6.0);
+  const LatentCode joined = join_blocks(blocks);
+  for (int j = 0; j < 6; ++j) CHECK(joined[j] == ha[j]);
+  LatentCode bad;
+  bad.z = {1.0, 2.0, 3.0, 4.0};
+  CHECK_THROWS_AS(split_blocks(bad), std::invalid_argument);
+
+  // weight validation (test_codec.cpp:182-216)
+  CodecWeights v = w;
+  v.k = 0;
+  CHECK_THROWS_AS(validate(v, g47), std::invalid_argument);
+  v = w;
+  v.k = 5;
+  v.raw_enc.resize(5u * 47u);
+  v.raw_dec.resize(47u * 5u);
+  CHECK_THROWS_AS(validate(v, g47), std::invalid_argument);
+  v = w;
+  v.n = 46;
+  CHECK_THROWS_AS(validate(v, g47), std::invalid_argument);
+  v = w;
+  v.beta = 0.0;
+  CHECK_THROWS_AS(validate(v, g47), std::invalid_argument);
+  v = w;
+  v.raw_dec[3] = std::numeric_limits<double>::quiet_NaN();
+  CHECK_THROWS_AS(validate(v, g47), std::invalid_argument);
+
+  // radiance-convention XYZ of ones (test_colorimetry.cpp:66-70) at fp32 tolerance
+  const ColorTriple xyz = spectrum_to_xyz(codec, SpectralCurve(47, 1.0));
+  CHECK(rel_close(xyz[0], 106.852687015155, 1e-6));
+  CHECK(rel_close(xyz[1], 106.858452950433, 1e-6));
+  CHECK(rel_close(xyz[2], 106.836643798253, 1e-6));
+  // sRGB white (test_colorimetry.cpp:157-165)
+  ColorTriple wh;
+  wh.c = {0.95047, 1.0, 1.08883};
+  const ColorTriple rgbw = xyz_to_linear_rgb(wh);
+  for (int c = 0; c < 3; ++c) CHECK(std::fabs(rgbw[c] - 1.0) < 1e-6);
+
+  // decode_image / image_to_linear_rgb on a 7 x 5 latent image (renderer.cpp:661-719)
+  ChannelImage lat;
+  lat.width = 7;
+  lat.height = 5;
+  lat.channels = 6;
+  lat.data.resize(7 * 5 * 6);
+  for (float& x : lat.data) x = static_cast<float>(lcg(s));
+  const ChannelImage spec = decode_image(codec, lat);
+  CHECK(spec.channels == 47 && spec.data.size() == 7u * 5u * 47u);
+  for (int p = 0; p < 35; ++p)
+    for (int i = 0; i < 47; ++i) {
+      double acc = 0.0;
+      for (int j = 0; j < 6; ++j)
+        acc += static_cast<double>(static_cast<float>(e.dec[i * 6 + j])) * lat.data[p * 6 + j];
+      CHECK(rel_close(spec.data[p * 47 + i], acc, 2e-6));
+    }
+  const ChannelImage rgb = image_to_linear_rgb(codec, spec);
+  CHECK(rgb.channels == 3 && rgb.data.size() == 35u * 3u);
+  lat.channels = 5;
+  CHECK_THROWS_AS(decode_image(codec, lat), std::invalid_argument);
+
+  // G-buffer shading through the drop-in API: multipass/fused latent vs naive, finite
+  GBuffer gb;
+  gb.width = 16;
+  gb.height = 8;
+  gb.lights = 8;
+  for (int p = 0; p < 128; ++p) gb.palette_index.push_back(static_cast<uint32_t>(lcg(s) * 4));
+  for (int i = 0; i < 128 * 8; ++i) gb.cos_terms.push_back(static_cast<float>(lcg(s)));
+  std::vector<float> pal_spec(4 * 47), light_spec(8 * 47);
+  for (float& x : pal_spec) x = static_cast<float>(lcg(s));
+  for (float& x : light_spec) x = static_cast<float>(lcg(s));
+  const std::vector<float> pal_codes = encode_batch(codec, pal_spec), light_codes = encode_batch(codec, light_spec);
+  const ShadedFrame lf = shade_latent(codec, pal_codes, light_codes, gb);
+  const ShadedFrame nf = shade_spectral(codec, pal_spec, light_spec, gb);
+  for (int p = 0; p < 128; ++p) {
+    // latent channel c = zR[idx] * sum_l cos_l zL_l (renderer.cpp:505-510)
+    for (int c = 0; c < 6; ++c) {
+      double acc = 0.0;
+      for (int l = 0; l < 8; ++l) acc += gb.cos_terms[p * 8 + l] * light_codes[l * 6 + c];
+      CHECK(rel_close(lf.latent.data[p * 6 + c], pal_codes[gb.palette_index[p] * 6 + c] * acc, 2e-6));
+    }
+    CHECK(std::isfinite(nf.xyz.data[p * 3 + 1]) && nf.xyz.data[p * 3 + 1] >= 0.f);
+  }
+  gb.palette_index[3] = 77;  // out of range of the 4-entry palette
+  CHECK_THROWS_AS(shade_latent(codec, pal_codes, light_codes, gb), std::invalid_argument);
+
+  std::printf("drop-in: %d checks, %d failures, %lld kernel launches\n", g_checks, g_fail,
+              static_cast<long long>(dev.launches()));
+  return g_fail ? 1 : 0;
+}

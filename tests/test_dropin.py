@@ -1,0 +1,35 @@
+"""The C++ drop-in layer (include/hadacodec_b200.hpp): the header compiles against
+the C ABI on CPU; on a B200 the reference's codec / colorimetry test cases run
+through it (tests/cpp/test_dropin.cpp)."""
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+SRC = ROOT / "tests" / "cpp" / "test_dropin.cpp"
+
+
+def _compile(out):
+    from paper_2602_18741_b200 import build
+
+    lib = build.build()
+    cmd = ["g++", "-std=c++17", "-O1", f"-I{ROOT / 'include'}", str(SRC), f"-L{lib.parent}", "-lhadacodec_b200",
+           f"-Wl,-rpath,{lib.parent}", "-o", str(out)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return out
+
+
+def test_dropin_header_compiles_and_links(tmp_path):
+    exe = _compile(tmp_path / "test_dropin")
+    assert exe.exists()
+
+
+@pytest.mark.gpu
+def test_dropin_reference_cases_on_gpu(tmp_path):
+    exe = _compile(tmp_path / "test_dropin")
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stderr
+    assert "0 failures" in r.stdout
