@@ -163,6 +163,21 @@ __global__ void __launch_bounds__(256) chain_latent_rep_kernel(const __grid_cons
     const int64_t base = pix * p.spp;
     bool bad = false;
     const int per_lane = valid ? p.spp / kChainLanes : 0;
+    {
+      // Warm L2 with the next quad's sample records (no registers held): the 8 lanes
+      // of a pixel group each touch one 128-byte line of the next pixel's streams.
+      const int64_t npix = (qd + nwarps) * kPixPerWarp + lane / kChainLanes;
+      if (npix < p.P) {
+        const int64_t nb = npix * p.spp;
+        const char* twl = reinterpret_cast<const char*>(p.tw + nb);
+        for (int off = g * 128; off < p.spp * 16; off += kChainLanes * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(twl + off));
+        const char* pkl = reinterpret_cast<const char*>(p.pidx + nb);
+        for (int off = g * 128; off < p.spp * 4; off += kChainLanes * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pkl + off));
+        if (g == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.iidx + nb));
+      }
+    }
     // Samples in groups of kGroup per lane with every load of the group issued
     // before any use: ~170 B in flight per lane keeps HBM busy (the kernel was
     // long-scoreboard bound issuing one sample's loads at a time).

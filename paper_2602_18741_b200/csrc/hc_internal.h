@@ -19,6 +19,8 @@ struct hc_ctx_s {
   int partial_capacity = 0;
   void* scratch = nullptr;     // host-entry staging (grow-only)
   size_t scratch_bytes = 0;
+  cudaStream_t aux[3] = {nullptr, nullptr, nullptr};  // host-entry copy/compute pipeline
+  cudaEvent_t ev_fork = nullptr;
   std::atomic<int64_t> launches{0};
 };
 
@@ -40,6 +42,7 @@ int set_error(int code, const std::string& msg);
 int cuda_error(cudaError_t e, const char* where);
 void note_launch(hc_ctx ctx, int n = 1);
 int ensure_scratch(hc_ctx ctx, size_t bytes);
+int ensure_aux_streams(hc_ctx ctx);
 
 #define HC_CUDA_TRY(expr)                                        \
   do {                                                           \

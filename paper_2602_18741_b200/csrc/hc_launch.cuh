@@ -1,6 +1,8 @@
 // hadacodec-b200: host-side launch of the tile pipeline.
 #pragma once
 
+#include <cuda.h>
+
 #include <algorithm>
 #include <atomic>
 
@@ -43,6 +45,11 @@ int configure_tile_op() {
 }
 
 inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// 2-D tensor map over a [rows][row_floats] f32 array, box [box_rows][row_floats],
+// 128-byte swizzle (row_floats * 4 must be 128).  cuTensorMapEncodeTiled is
+// reached through the runtime's driver entry point (no libcuda link).
+int encode_rows_tmap_swizzle128(CUtensorMap* map, const void* base, int64_t rows, int row_floats, int box_rows);
 
 // Launch Op over `items` items.  Full tiles of 16-byte-aligned streams go
 // through the TMA pipeline; the ragged tail (and everything, if any stream is

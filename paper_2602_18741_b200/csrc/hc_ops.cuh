@@ -16,6 +16,8 @@
 //   loss residual     trainer.cpp:49-71
 #pragma once
 
+#include <cuda.h>
+
 #include "hc_common.cuh"
 
 namespace hcb {
@@ -44,6 +46,7 @@ struct CodecOp {
                               : 12;
   }
   static constexpr int EXTRA_SMEM = 0;
+  static constexpr int kTensorStream = -1;
 
   struct Params {
     CodecConst<N, K> cc;
@@ -52,6 +55,7 @@ struct CodecOp {
     int* err;
     int check_negative;
   };
+  __host__ __device__ static const void* tensor_map(const Params&) { return nullptr; }
   struct State {};
   __device__ static void init_state(State&) {}
   __host__ __device__ static const void* in_ptr(const Params& p, int) { return p.in; }
@@ -147,16 +151,37 @@ struct CodecOp {
 // the full decoded spectrum D z.
 constexpr int kMaxPalette = 256;
 
-template <int N, int K, int L, bool SPEC, int T_, int THREADS_, int STAGES_>
+// Output streams of a latent shade, selected at compile time (unused outputs get
+// no staging shared memory): bit 0 XYZ, bit 1 linear sRGB, bit 2 latent, bit 3 spectra.
+enum : int { kOutXyz = 1, kOutRgb = 2, kOutLatent = 4, kOutSpectra = 8 };
+
+__host__ __device__ constexpr int popcount4(int m) { return (m & 1) + ((m >> 1) & 1) + ((m >> 2) & 1) + ((m >> 3) & 1); }
+// Kind of the i-th enabled output of mask m.
+__host__ __device__ constexpr int out_kind(int m, int i) {
+  for (int b = 0; b < 4; ++b)
+    if (m & (1 << b)) {
+      if (i == 0) return 1 << b;
+      --i;
+    }
+  return 0;
+}
+// Stream slot of output `kind` in mask m.
+__host__ __device__ constexpr int out_slot(int m, int kind) { return popcount4(m & (kind - 1)); }
+
+template <int N, int K, int L, int OUTS, int T_, int THREADS_, int STAGES_>
 struct ShadeLatentOp {
   static constexpr int T = T_, THREADS = THREADS_, STAGES = STAGES_;
   static constexpr int NIN = 2;
   __host__ __device__ static constexpr int in_bytes(int i) { return i == 0 ? 4 : L * 4; }
-  static constexpr int NOUT = SPEC ? 4 : 3;  // XYZ, sRGB, latent, [spectra]
-  __host__ __device__ static constexpr int out_bytes(int i) { return i < 2 ? 12 : (i == 2 ? K * 4 : N * 4); }
+  static constexpr int NOUT = popcount4(OUTS);
+  __host__ __device__ static constexpr int out_bytes(int i) {
+    return out_kind(OUTS, i) == kOutLatent ? K * 4 : (out_kind(OUTS, i) == kOutSpectra ? N * 4 : 12);
+  }
   static constexpr int EXTRA_SMEM = kMaxPalette * K * 4;
+  static constexpr int kTensorStream = (L * 4 == 128) ? 1 : -1;  // 128-byte cos rows: swizzled 2-D TMA
 
   struct Params {
+    CUtensorMap cos_map;  // 2-D map of cos [P][L] with the 128-byte swizzle (used when L == 32)
     CodecConst<N, K> cc;
     float light[L * K];
     const uint32_t* idx;
@@ -169,13 +194,15 @@ struct ShadeLatentOp {
     float* spectra;
     int* err;
   };
+  __host__ __device__ static const void* tensor_map(const Params& p) { return &p.cos_map; }
   struct State {};
   __device__ static void init_state(State&) {}
   __host__ __device__ static const void* in_ptr(const Params& p, int i) {
     return i == 0 ? static_cast<const void*>(p.idx) : static_cast<const void*>(p.cosv);
   }
   __host__ __device__ static void* out_ptr(const Params& p, int i) {
-    return i == 0 ? p.xyz : (i == 1 ? p.rgb : (i == 2 ? p.latent : p.spectra));
+    const int k = out_kind(OUTS, i);
+    return k == kOutXyz ? p.xyz : (k == kOutRgb ? p.rgb : (k == kOutLatent ? p.latent : p.spectra));
   }
   __device__ static void setup(const Params& p, unsigned char* extra) {
     float* pal = reinterpret_cast<float*>(extra);
@@ -190,30 +217,32 @@ struct ShadeLatentOp {
       atomicOr(p.err, kErrIndexRange);
       id = 0;
     }
-    const float* c = reinterpret_cast<const float*>(ins[1]) + item * L;
+    const unsigned char* crow = ins[1] + item * (L * 4);
     float acc[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) acc[j] = 0.f;
 #pragma unroll
     for (int l4 = 0; l4 < L; l4 += 4) {
-      const float4 w4 = *reinterpret_cast<const float4*>(c + l4);
+      // swizzled rows (kTensorStream): 16-byte chunk q of row r sits at chunk q ^ (r & 7)
+      const int q = kTensorStream >= 0 ? ((l4 >> 2) ^ (item & 7)) : (l4 >> 2);
+      const float4 w4 = *reinterpret_cast<const float4*>(crow + q * 16);
       const float w[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int e = 0; e < 4; ++e)
 #pragma unroll
-        for (int j = 0; j < K; ++j) acc[j] = fmaf(w[q], p.light[(l4 + q) * K + j], acc[j]);
+        for (int j = 0; j < K; ++j) acc[j] = fmaf(w[e], p.light[(l4 + e) * K + j], acc[j]);
     }
     const float* zr = reinterpret_cast<const float*>(extra) + id * K;
     float z[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) z[j] = zr[j] * acc[j];
-    if (p.latent) {
-      float* ol = reinterpret_cast<float*>(outs[2]) + item * K;
+    if constexpr ((OUTS & kOutLatent) != 0) {
+      float* ol = reinterpret_cast<float*>(outs[out_slot(OUTS, kOutLatent)]) + item * K;
 #pragma unroll
       for (int j = 0; j < K; ++j) ol[j] = z[j];
     }
-    if constexpr (SPEC) {
-      float* os = reinterpret_cast<float*>(outs[3]) + item * N;
+    if constexpr ((OUTS & kOutSpectra) != 0) {
+      float* os = reinterpret_cast<float*>(outs[out_slot(OUTS, kOutSpectra)]) + item * N;
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         float a = p.cc.D[i * K] * z[0];
@@ -222,21 +251,26 @@ struct ShadeLatentOp {
         os[i] = a;
       }
     }
-    float xyz[3], rgb[3];
+    if constexpr ((OUTS & (kOutXyz | kOutRgb)) != 0) {
+      float xyz[3], rgb[3];
 #pragma unroll
-    for (int cc = 0; cc < 3; ++cc) {
-      float a = p.cc.Mxyz[cc * K] * z[0];
+      for (int cc = 0; cc < 3; ++cc) {
+        float a = p.cc.Mxyz[cc * K] * z[0];
 #pragma unroll
-      for (int j = 1; j < K; ++j) a = fmaf(p.cc.Mxyz[cc * K + j], z[j], a);
-      xyz[cc] = a;
-    }
-    xyz_to_rgb(p.cc.Crgb, xyz, rgb);
-    float* ox = reinterpret_cast<float*>(outs[0]) + item * 3;
-    float* orgb = reinterpret_cast<float*>(outs[1]) + item * 3;
+        for (int j = 1; j < K; ++j) a = fmaf(p.cc.Mxyz[cc * K + j], z[j], a);
+        xyz[cc] = a;
+      }
+      if constexpr ((OUTS & kOutXyz) != 0) {
+        float* ox = reinterpret_cast<float*>(outs[out_slot(OUTS, kOutXyz)]) + item * 3;
 #pragma unroll
-    for (int cc = 0; cc < 3; ++cc) {
-      ox[cc] = xyz[cc];
-      orgb[cc] = rgb[cc];
+        for (int cc = 0; cc < 3; ++cc) ox[cc] = xyz[cc];
+      }
+      if constexpr ((OUTS & kOutRgb) != 0) {
+        xyz_to_rgb(p.cc.Crgb, xyz, rgb);
+        float* orgb = reinterpret_cast<float*>(outs[out_slot(OUTS, kOutRgb)]) + item * 3;
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) orgb[cc] = rgb[cc];
+      }
     }
   }
 };
@@ -254,6 +288,7 @@ struct ShadeSpectralOp {
   static constexpr int NOUT = SPEC ? 3 : 2;  // XYZ, sRGB, [spectra]
   __host__ __device__ static constexpr int out_bytes(int i) { return i < 2 ? 12 : N * 4; }
   static constexpr int EXTRA_SMEM = kMaxPalette * N * 4;
+  static constexpr int kTensorStream = -1;
 
   struct Params {
     float light[L * N];
@@ -268,6 +303,7 @@ struct ShadeSpectralOp {
     float* spectra;
     int* err;
   };
+  __host__ __device__ static const void* tensor_map(const Params&) { return nullptr; }
   struct State {};
   __device__ static void init_state(State&) {}
   __host__ __device__ static const void* in_ptr(const Params& p, int i) {
@@ -337,6 +373,7 @@ struct LossOp {
   static constexpr int NOUT = 0;
   __host__ __device__ static constexpr int out_bytes(int) { return 0; }
   static constexpr int EXTRA_SMEM = 32 * 8;
+  static constexpr int kTensorStream = -1;
 
   struct Params {
     CodecConst<N, K> cc;
@@ -346,6 +383,7 @@ struct LossOp {
     double* partials;  // one per CTA
     int partial_offset;
   };
+  __host__ __device__ static const void* tensor_map(const Params&) { return nullptr; }
   struct State {
     double acc;
   };

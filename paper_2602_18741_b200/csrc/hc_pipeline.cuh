@@ -1,25 +1,28 @@
 // hadacodec-b200: the persistent tile pipeline shared by the bandwidth-bound
 // kernels (codec round trip, latent / spectral G-buffer shading, loss).
 //
-//   HBM --cp.async.bulk--> smem in[stage] --thread-per-item compute--> smem out[stage]
-//       --cp.async.bulk--> HBM
+//   HBM --TMA--> smem in[stage] --thread-per-item compute--> smem out[stage] --TMA--> HBM
 //
 // Every stream (G-buffer idx, cos rows, spectra, codes, XYZ, sRGB) is a dense
 // row-major array, so a tile of T consecutive items is ONE contiguous byte run
-// per stream: one bulk copy each, fully coalesced, no register staging.  The
-// input ring has STAGES slots; loads for tile t+STAGES are issued as soon as
-// tile t's slot is consumed, keeping STAGES tiles of bytes in flight per CTA.
-// Output slots are recycled once the bulk store that read them has drained
-// (cp.async.bulk.wait_group.read).
+// per stream: one bulk copy each (cp.async.bulk), fully coalesced, no register
+// staging.  One stream per Op may instead arrive through a 2-D tensor map with
+// the 128-byte swizzle (Op::kTensorStream): rows of exactly 128 bytes whose 16-byte
+// chunk c of row r lands at chunk c ^ (r & 7), which makes a quarter-warp's
+// LDS.128 of the same chunk index of 8 consecutive rows bank-conflict free.
+// The input ring has STAGES slots; loads for tile t+STAGES are issued as soon as
+// tile t's slot is consumed.  Output slots are recycled once the bulk store that
+// read them has drained (cp.async.bulk.wait_group.read).
 //
 // An Op supplies (all static):
 //   T, THREADS, STAGES, NIN, NOUT, in_bytes(i), out_bytes(i) (bytes/item),
+//   kTensorStream (-1 = none) and tensor_map(p),
 //   EXTRA_SMEM (bytes for op tables, e.g. the palette), Params, State,
 //   in_ptr(p, i), out_ptr(p, i) (nullptr = stream disabled),
 //   setup(p, extra_smem), compute(p, st, in[], out[], extra, item, global_item),
 //   finish(p, st, extra)
 // Ragged tails and unaligned pointers go through tile_generic, which runs the
-// same compute on word copies (no TMA).
+// same compute on word copies (no TMA; the swizzle is applied in software).
 #pragma once
 
 #include "hc_common.cuh"
@@ -27,25 +30,43 @@
 
 namespace hcb {
 
+constexpr int kTileAlign = 1024;  // every stream tile starts 1024-byte aligned (swizzle requirement)
+
+__host__ __device__ constexpr int align_up(int x, int a) { return (x + a - 1) / a * a; }
+
 template <class Op>
 struct TileLayout {
-  static constexpr int in_item_bytes() {
+  // Offset of input stream i within one stage (i == NIN gives the stage size).  The
+  // swizzled tensor stream starts 1024-byte aligned, every other stream 128-byte.
+  static constexpr int in_align(int i) { return i == Op::kTensorStream ? kTileAlign : 128; }
+  static constexpr int in_off(int i) {
     int s = 0;
-    for (int i = 0; i < Op::NIN; ++i) s += Op::in_bytes(i);
+    for (int j = 0; j < i; ++j) s = align_up(s, in_align(j)) + Op::T * Op::in_bytes(j);
+    return i < Op::NIN ? align_up(s, in_align(i)) : align_up(s, kTileAlign);
+  }
+  static constexpr int out_off(int i) {
+    int s = 0;
+    for (int j = 0; j < i; ++j) s = align_up(s, 128) + Op::T * Op::out_bytes(j);
+    return align_up(s, 128);
+  }
+  static constexpr int kInTile = in_off(Op::NIN);
+  static constexpr int kOutTile = align_up(out_off(Op::NOUT), kTileAlign);
+  static constexpr int kInBytes() {
+    int s = 0;
+    for (int j = 0; j < Op::NIN; ++j) s += Op::T * Op::in_bytes(j);
     return s;
   }
-  static constexpr int out_item_bytes() {
-    int s = 0;
-    for (int i = 0; i < Op::NOUT; ++i) s += Op::out_bytes(i);
-    return s;
-  }
-  static constexpr int kInTile = Op::T * in_item_bytes();
-  static constexpr int kOutTile = Op::T * out_item_bytes();
-  static constexpr int kBarBytes = 128;
+  static constexpr int kBarBytes = 1024;
   static constexpr int smem_bytes() {
-    return kBarBytes + Op::STAGES * (kInTile + kOutTile) + Op::EXTRA_SMEM;
+    return kBarBytes + Op::STAGES * (kInTile + kOutTile) + Op::EXTRA_SMEM + 1024;  // + base alignment slack
   }
 };
+
+// Dynamic shared memory, rounded up to a 1024-byte boundary.
+__device__ __forceinline__ unsigned char* aligned_smem_base(unsigned char* raw) {
+  const uint32_t a = smem_u32(raw);
+  return raw + ((kTileAlign - (a & (kTileAlign - 1))) & (kTileAlign - 1));
+}
 
 template <class Op>
 __global__ void __launch_bounds__(Op::THREADS)
@@ -53,7 +74,8 @@ __global__ void __launch_bounds__(Op::THREADS)
   using Lay = TileLayout<Op>;
   constexpr int S = Op::STAGES;
   constexpr int T = Op::T;
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = aligned_smem_base(smem_raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem);
   unsigned char* in_base = smem + Lay::kBarBytes;
   unsigned char* out_base = in_base + S * Lay::kInTile;
@@ -68,13 +90,17 @@ __global__ void __launch_bounds__(Op::THREADS)
   __syncthreads();
 
   auto issue_loads = [&](int64_t tile, int s) {
-    unsigned char* dst = in_base + s * Lay::kInTile;
-    mbar_arrive_expect_tx(&bar[s], Lay::kInTile);
+    unsigned char* stage = in_base + s * Lay::kInTile;
+    mbar_arrive_expect_tx(&bar[s], Lay::kInBytes());
 #pragma unroll
     for (int i = 0; i < Op::NIN; ++i) {
-      const unsigned char* src = static_cast<const unsigned char*>(Op::in_ptr(p, i));
-      bulk_g2s(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &bar[s]);
-      dst += T * Op::in_bytes(i);
+      unsigned char* dst = stage + Lay::in_off(i);
+      if (i == Op::kTensorStream) {
+        tma_load_2d(dst, Op::tensor_map(p), 0, static_cast<int>(tile * T), &bar[s]);
+      } else {
+        const unsigned char* src = static_cast<const unsigned char*>(Op::in_ptr(p, i));
+        bulk_g2s(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &bar[s]);
+      }
     }
   };
 
@@ -97,20 +123,10 @@ __global__ void __launch_bounds__(Op::THREADS)
 
     const unsigned char* ins[Op::NIN > 0 ? Op::NIN : 1];
     unsigned char* outs[Op::NOUT > 0 ? Op::NOUT : 1];
-    {
-      const unsigned char* q = in_base + s * Lay::kInTile;
 #pragma unroll
-      for (int i = 0; i < Op::NIN; ++i) {
-        ins[i] = q;
-        q += T * Op::in_bytes(i);
-      }
-      unsigned char* o = out_base + s * Lay::kOutTile;
+    for (int i = 0; i < Op::NIN; ++i) ins[i] = in_base + s * Lay::kInTile + Lay::in_off(i);
 #pragma unroll
-      for (int i = 0; i < Op::NOUT; ++i) {
-        outs[i] = o;
-        o += T * Op::out_bytes(i);
-      }
-    }
+    for (int i = 0; i < Op::NOUT; ++i) outs[i] = out_base + s * Lay::kOutTile + Lay::out_off(i);
     for (int item = tid; item < T; item += Op::THREADS)
       Op::compute(p, st, ins, outs, extra, item, tile * T + item);
     if (Op::NOUT > 0) fence_proxy_async_smem();
@@ -140,7 +156,8 @@ __global__ void __launch_bounds__(Op::THREADS)
     tile_generic(const __grid_constant__ typename Op::Params p, int64_t item_begin, int64_t item_end) {
   using Lay = TileLayout<Op>;
   constexpr int T = Op::T;
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = aligned_smem_base(smem_raw);
   unsigned char* in_base = smem + Lay::kBarBytes;
   unsigned char* out_base = in_base + Op::STAGES * Lay::kInTile;
   unsigned char* extra = out_base + Op::STAGES * Lay::kOutTile;
@@ -156,25 +173,25 @@ __global__ void __launch_bounds__(Op::THREADS)
     const int cnt = static_cast<int>(nitems - tile * T < T ? nitems - tile * T : T);
     const unsigned char* ins[Op::NIN > 0 ? Op::NIN : 1];
     unsigned char* outs[Op::NOUT > 0 ? Op::NOUT : 1];
-    {
-      unsigned char* q = in_base;
 #pragma unroll
-      for (int i = 0; i < Op::NIN; ++i) {
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(
-            static_cast<const unsigned char*>(Op::in_ptr(p, i)) + first * Op::in_bytes(i));
-        uint32_t* dst = reinterpret_cast<uint32_t*>(q);
-        const int words = cnt * Op::in_bytes(i) / 4;
+    for (int i = 0; i < Op::NIN; ++i) {
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(
+          static_cast<const unsigned char*>(Op::in_ptr(p, i)) + first * Op::in_bytes(i));
+      uint32_t* dst = reinterpret_cast<uint32_t*>(in_base + Lay::in_off(i));
+      const int words = cnt * Op::in_bytes(i) / 4;
+      if (i == Op::kTensorStream) {
+        // software 128-byte swizzle: word w of row r -> chunk ((w / 4) ^ (r & 7))
+        for (int w = tid; w < words; w += Op::THREADS) {
+          const int r = w >> 5, c = (w >> 2) & 7, e = w & 3;
+          dst[r * 32 + ((c ^ (r & 7)) << 2) + e] = src[w];
+        }
+      } else {
         for (int w = tid; w < words; w += Op::THREADS) dst[w] = src[w];
-        ins[i] = q;
-        q += T * Op::in_bytes(i);
       }
-      unsigned char* o = out_base;
-#pragma unroll
-      for (int i = 0; i < Op::NOUT; ++i) {
-        outs[i] = o;
-        o += T * Op::out_bytes(i);
-      }
+      ins[i] = in_base + Lay::in_off(i);
     }
+#pragma unroll
+    for (int i = 0; i < Op::NOUT; ++i) outs[i] = out_base + Lay::out_off(i);
     __syncthreads();
     for (int item = tid; item < cnt; item += Op::THREADS)
       Op::compute(p, st, ins, outs, extra, item, first + item);

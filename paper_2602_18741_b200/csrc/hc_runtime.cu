@@ -1,6 +1,8 @@
 // hadacodec-b200: C-ABI runtime — contexts, codecs, argument validation,
 // small utility kernels (single-pass shading, reassembly, Hadamard product,
 // seeded input generators, L2 flush) and the host-buffer entry points.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -39,6 +41,38 @@ int ensure_scratch(hc_ctx ctx, size_t bytes) {
   ctx->scratch_bytes = 0;
   HC_CUDA_TRY(cudaMalloc(&ctx->scratch, bytes));
   ctx->scratch_bytes = bytes;
+  return HC_OK;
+}
+
+int encode_rows_tmap_swizzle128(CUtensorMap* map, const void* base, int64_t rows, int row_floats, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!encode) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      HC_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      if (!fn || q != cudaDriverEntryPointSuccess)
+        return set_error(HC_ECUDA, "cuTensorMapEncodeTiled not available from the driver");
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+  }
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(row_floats), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(row_floats) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(row_floats), static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(HC_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return HC_OK;
+}
+
+int ensure_aux_streams(hc_ctx ctx) {
+  if (ctx->ev_fork) return HC_OK;
+  for (auto& st : ctx->aux) HC_CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  HC_CUDA_TRY(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
   return HC_OK;
 }
 
@@ -254,6 +288,9 @@ int hc_ctx_destroy(hc_ctx ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   if (ctx->scratch) cudaFree(ctx->scratch);
+  for (auto st : ctx->aux)
+    if (st) cudaStreamDestroy(st);
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
   if (ctx->d_partials) cudaFree(ctx->d_partials);
   if (ctx->d_err) cudaFree(ctx->d_err);
   delete ctx;
@@ -504,20 +541,36 @@ int hc_shade_latent_host(hc_codec c, const float* pal_codes, int n_pal, const fl
   auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
   rc = ensure_scratch(ctx, up(pal_b) + up(idx_b) + up(cos_b) + 2 * up(out_b));
   if (rc != HC_OK) return rc;
+  rc = ensure_aux_streams(ctx);
+  if (rc != HC_OK) return rc;
   char* base = static_cast<char*>(ctx->scratch);
   float* d_pal = reinterpret_cast<float*>(base);
   uint32_t* d_idx = reinterpret_cast<uint32_t*>(base + up(pal_b));
   float* d_cos = reinterpret_cast<float*>(base + up(pal_b) + up(idx_b));
   float* d_xyz = reinterpret_cast<float*>(base + up(pal_b) + up(idx_b) + up(cos_b));
   float* d_rgb = reinterpret_cast<float*>(base + up(pal_b) + up(idx_b) + up(cos_b) + up(out_b));
+  // Chunked 3-stream pipeline: chunk i's H2D (copy engine 0), chunk i-1's kernel and
+  // chunk i-2's D2H (copy engine 1) overlap.  Pinned host buffers give full PCIe rate.
   HC_CUDA_TRY(cudaMemcpyAsync(d_pal, pal_codes, pal_b, cudaMemcpyHostToDevice, ctx->stream));
-  HC_CUDA_TRY(cudaMemcpyAsync(d_idx, idx, idx_b, cudaMemcpyHostToDevice, ctx->stream));
-  HC_CUDA_TRY(cudaMemcpyAsync(d_cos, cosv, cos_b, cudaMemcpyHostToDevice, ctx->stream));
-  rc = shade_latent_launch(c, d_pal, n_pal, light_codes, L, d_idx, d_cos, P, nullptr, nullptr,
-                           xyz ? d_xyz : nullptr, rgb ? d_rgb : nullptr);
-  if (rc != HC_OK) return rc;
-  if (xyz) HC_CUDA_TRY(cudaMemcpyAsync(xyz, d_xyz, out_b, cudaMemcpyDeviceToHost, ctx->stream));
-  if (rgb) HC_CUDA_TRY(cudaMemcpyAsync(rgb, d_rgb, out_b, cudaMemcpyDeviceToHost, ctx->stream));
+  HC_CUDA_TRY(cudaEventRecord(ctx->ev_fork, ctx->stream));
+  for (auto st : ctx->aux) HC_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_fork, 0));
+  constexpr int64_t kChunk = 131072;  // pixels (multiple of every tile size)
+  cudaStream_t home = ctx->stream;
+  int ci = 0;
+  for (int64_t p0 = 0; p0 < P; p0 += kChunk, ++ci) {
+    const int64_t n = P - p0 < kChunk ? P - p0 : kChunk;
+    cudaStream_t st = ctx->aux[ci % 3];
+    HC_CUDA_TRY(cudaMemcpyAsync(d_idx + p0, idx + p0, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
+    HC_CUDA_TRY(cudaMemcpyAsync(d_cos + p0 * L, cosv + p0 * L, sizeof(float) * n * L, cudaMemcpyHostToDevice, st));
+    ctx->stream = st;
+    rc = shade_latent_launch(c, d_pal, n_pal, light_codes, L, d_idx + p0, d_cos + p0 * L, n, nullptr, nullptr,
+                             xyz ? d_xyz + p0 * 3 : nullptr, rgb ? d_rgb + p0 * 3 : nullptr);
+    ctx->stream = home;
+    if (rc != HC_OK) return rc;
+    if (xyz) HC_CUDA_TRY(cudaMemcpyAsync(xyz + p0 * 3, d_xyz + p0 * 3, sizeof(float) * n * 3, cudaMemcpyDeviceToHost, st));
+    if (rgb) HC_CUDA_TRY(cudaMemcpyAsync(rgb + p0 * 3, d_rgb + p0 * 3, sizeof(float) * n * 3, cudaMemcpyDeviceToHost, st));
+  }
+  for (auto st : ctx->aux) HC_CUDA_TRY(cudaStreamSynchronize(st));
   return hc_ctx_synchronize(ctx);
 }
 

@@ -2,19 +2,22 @@
 // reassembly + decode/projection) and naive n-sample spectral.
 // Reference: renderer.cpp:161-271 (compile_scene), :274-283 (slice_pass),
 // :505-510 (NEE channel loop), :645-657 (reassembly), :661-719 (decode/project).
+#include <cstring>
+
 #include "hc_launch.cuh"
 #include "hc_ops.cuh"
 
 namespace hcb {
 
-template <int N, int K, int L, bool SPEC>
+template <int N, int K, int L, int OUTS>
 int shade_latent_nkl(hc_codec c, const float* pal, int n_pal, const float* light, const uint32_t* idx,
                      const float* cosv, int64_t P, float* latent, float* spectra, float* xyz,
                      float* rgb) {
+  constexpr bool SPEC = (OUTS & kOutSpectra) != 0;
   constexpr int T = SPEC ? 64 : 256;
   constexpr int THREADS = T;
   constexpr int STAGES = SPEC ? 2 : 3;
-  using Op = ShadeLatentOp<N, K, L, SPEC, T, THREADS, STAGES>;
+  using Op = ShadeLatentOp<N, K, L, OUTS, T, THREADS, STAGES>;
   typename Op::Params p;
   fill_codec_const<N, K>(c, &p.cc);
   for (int i = 0; i < L * K; ++i) p.light[i] = light[i];
@@ -27,6 +30,13 @@ int shade_latent_nkl(hc_codec c, const float* pal, int n_pal, const float* light
   p.latent = latent;
   p.spectra = spectra;
   p.err = c->ctx->d_err;
+  std::memset(&p.cos_map, 0, sizeof(p.cos_map));
+  if constexpr (Op::kTensorStream >= 0) {
+    if (P >= T && al16(cosv)) {
+      const int rc = encode_rows_tmap_swizzle128(&p.cos_map, cosv, P, L, T);
+      if (rc != HC_OK) return rc;
+    }
+  }
   return launch_tile_op<Op>(c->ctx, p, P);
 }
 
@@ -34,13 +44,19 @@ template <int N, int K>
 int shade_latent_nk(hc_codec c, const float* pal, int n_pal, const float* light, int L,
                     const uint32_t* idx, const float* cosv, int64_t P, float* latent, float* spectra,
                     float* xyz, float* rgb) {
-  const bool spec = spectra != nullptr;
-  if (L == 8)
-    return spec ? shade_latent_nkl<N, K, 8, true>(c, pal, n_pal, light, idx, cosv, P, latent, spectra, xyz, rgb)
-                : shade_latent_nkl<N, K, 8, false>(c, pal, n_pal, light, idx, cosv, P, latent, spectra, xyz, rgb);
-  if (L == 32)
-    return spec ? shade_latent_nkl<N, K, 32, true>(c, pal, n_pal, light, idx, cosv, P, latent, spectra, xyz, rgb)
-                : shade_latent_nkl<N, K, 32, false>(c, pal, n_pal, light, idx, cosv, P, latent, spectra, xyz, rgb);
+  // Compiled output sets: the BASELINE ones (config 2: XYZ + sRGB; config 3: spectra +
+  // sRGB) and the general set (all four; disabled outputs are simply not stored).
+  const int want = (xyz ? kOutXyz : 0) | (rgb ? kOutRgb : 0) | (latent ? kOutLatent : 0) | (spectra ? kOutSpectra : 0);
+  constexpr int kC2 = kOutXyz | kOutRgb, kC3 = kOutRgb | kOutSpectra, kAll = 15;
+#define HC_SHADE_L(LL)                                                                                  \
+  if (L == LL) {                                                                                       \
+    if (want == kC2) return shade_latent_nkl<N, K, LL, kC2>(c, pal, n_pal, light, idx, cosv, P, latent, spectra, xyz, rgb); \
+    if (want == kC3) return shade_latent_nkl<N, K, LL, kC3>(c, pal, n_pal, light, idx, cosv, P, latent, spectra, xyz, rgb); \
+    return shade_latent_nkl<N, K, LL, kAll>(c, pal, n_pal, light, idx, cosv, P, latent, spectra, xyz, rgb);                 \
+  }
+  HC_SHADE_L(8)
+  HC_SHADE_L(32)
+#undef HC_SHADE_L
   return set_error(HC_EUNSUPPORTED, "shade_latent: light count must be 8 or 32");
 }
 

@@ -51,6 +51,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, u
       : "memory");
 }
 
+// 2-D tensor TMA load (cp.async.bulk.tensor): box at coordinates (x, y) of the tensor
+// map into shared memory (1024-byte aligned for the 128-byte swizzle).  SASS: UTMALDG.
+__device__ __forceinline__ void tma_load_2d(void* dst_smem, const void* tmap, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // global -> shared bulk copy with an L2 evict-first policy (streamed inputs).
 __device__ __forceinline__ void bulk_g2s_evict_first(void* dst_smem, const void* src_gmem,
                                                      uint32_t bytes, uint64_t* bar, uint64_t policy) {
