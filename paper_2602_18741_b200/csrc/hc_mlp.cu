@@ -46,16 +46,18 @@ constexpr int kN3 = 16;       // layer-3 N (k padded)
 constexpr int kMaxK = 9;
 constexpr int kStreams = 4;                 // warpgroups / tile streams per CTA
 constexpr int kThreads = 128 * kStreams;
-constexpr int kK2 = 80;                     // layers 2/3 K: 64 hidden + constant-1 bias column, padded
+constexpr int kK2 = 80;                     // layer 2 K: 64 hidden + constant-1 column (b2 rides the MMA)
+constexpr int kK3 = 64;                     // layer 3 K: b3 (6 values) is added in the epilogue instead of
+                                            // paying a fifth >= 45-cycle N = 16 MMA
 constexpr int kColsPerStream = 128;         // TMEM columns per stream (512 total)
-constexpr int kColA = 0;                    // packed bf16 A2 / A3 (+ bias chunk): 40 columns
+constexpr int kColA = 0;                    // packed bf16 A2 / A3 (+ constant chunk): 40 columns
 constexpr int kColD = 48;                   // fp32 accumulator of layers 1 / 2: 64 columns
 constexpr int kColD3 = 112;                 // fp32 accumulator of layer 3: 16 columns
 
 // Shared-memory image offsets (bytes).
 constexpr int kW1Bytes = kHid * kK1 * 2;   // 2 KB
 constexpr int kW2Bytes = kHid * kK2 * 2;   // 10 KB ([W2 | b2 | 0])
-constexpr int kW3Bytes = kN3 * kK2 * 2;    // 2.5 KB ([W3 | b3 | 0])
+constexpr int kW3Bytes = kN3 * kK3 * 2;    // 2 KB
 constexpr int kWBytes = kW1Bytes + kW2Bytes + kW3Bytes;
 constexpr int kOffW1 = 0;
 constexpr int kOffW2 = kOffW1 + kW1Bytes;
@@ -68,6 +70,8 @@ constexpr int kOffBar = kOffStreams + kStreams * kStreamBytes;
 constexpr int kSmemBytes = kOffBar + kStreams * 4 * 8 + 16;
 
 struct MlpParams {
+  float b2[kHid];
+  float b3[kN3];
   const uint8_t* wimg;  // kWBytes, canonical layouts
   const float* rgb;     // P x 3
   float* out;           // P x k
@@ -77,7 +81,6 @@ struct MlpParams {
   int k;
   int use_tma;          // 1: tiles are full and the rgb base is 16-byte aligned
   long long* trace;     // debug (HC_MLP_TRACE): per-phase clock64 stamps of CTA 0
-  int exp_mode;         // debug (HC_MLP_EXP): bit0 skip softplus, bit1 skip stores
 };
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -160,9 +163,10 @@ __device__ __forceinline__ float softplus1(float x) {
 }
 
 // Hidden-layer epilogue: fp32 accumulator row (64 TMEM columns of this thread's
-// lane; biases already accumulated by the MMA) -> bf16 relu(acc) packed in pairs
-// (element 2j in the low half) -> 32 TMEM columns of the next layer's A operand.
-__device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem_a) {
+// lane) -> bf16 relu(acc [+ bias]) packed in pairs (element 2j in the low half)
+// -> 32 TMEM columns of the next layer's A operand.
+template <bool kBias>
+__device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem_a, const float* bias) {
   uint32_t va[4][16];
   HC_TMEM_LD16(tmem_acc + 0, va[0]);
   HC_TMEM_LD16(tmem_acc + 16, va[1]);
@@ -173,9 +177,14 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem
 #pragma unroll
   for (int q = 0; q < 4; ++q)
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      pk[q >> 1][(q & 1) * 8 + j] =
-          pack_relu_bf16(__uint_as_float(va[q][2 * j]), __uint_as_float(va[q][2 * j + 1]));
+    for (int j = 0; j < 8; ++j) {
+      float lo = __uint_as_float(va[q][2 * j]), hi = __uint_as_float(va[q][2 * j + 1]);
+      if (kBias) {
+        lo += bias[q * 16 + 2 * j];
+        hi += bias[q * 16 + 2 * j + 1];
+      }
+      pk[q >> 1][(q & 1) * 8 + j] = pack_relu_bf16(lo, hi);
+    }
   HC_TMEM_ST16(tmem_a + 0, pk[0]);
   HC_TMEM_ST16(tmem_a + 16, pk[1]);
   tmem_wait_st();
@@ -221,7 +230,8 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
   const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
   const uint32_t tA = tcol + kColA, tD = tcol + kColD, tD3 = tcol + kColD3;
   {
-    // Constant K chunk of the layer-2/3 A operand: element 64 = 1 (bias), 65..79 = 0.
+    // Constant K chunk of the layer-2 A operand: element 64 = 1 (bias b2), 65..79 = 0.
+    // Written once; the epilogues only overwrite columns [0, 32).
     uint32_t one[8] = {0x3F80u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(tA + 32 + lane_off),
                  "r"(one[0]), "r"(one[1]), "r"(one[2]), "r"(one[3]), "r"(one[4]), "r"(one[5]), "r"(one[6]),
@@ -229,7 +239,6 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
                  : "memory");
     tmem_wait_st();
   }
-
   const uint32_t sW1 = smem_u32(sm + kOffW1), sW2 = smem_u32(sm + kOffW2), sW3 = smem_u32(sm + kOffW3);
   const uint32_t sA1 = smem_u32(A1);
   constexpr uint32_t kChunkA = kMlpM * 16;  // K-chunk stride of the 128-row A1 tile
@@ -274,6 +283,30 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
     mma_commit(bar_l1);
   };
 
+  // Codes of the previous tile: layer-3 accumulators are read right after layer 3
+  // completes (16 TMEM columns), but softplus + the global stores run later, under
+  // the next tile's layer-2 MMA, off the per-tile dependency chain.
+  uint32_t prev_v[kN3];
+  int64_t prev_row0 = -1;
+  int prev_rows = 0;
+  const int k = p.k;
+  auto store_codes = [&]() {
+    if (prev_row0 < 0 || r >= prev_rows) return;
+    float* o = p.out + (prev_row0 + r) * k;
+    if (k == 6) {
+      float y[6];
+#pragma unroll
+      for (int j = 0; j < 6; ++j) y[j] = softplus1(__uint_as_float(prev_v[j]) + p.b3[j]);
+      reinterpret_cast<float2*>(o)[0] = make_float2(y[0], y[1]);
+      reinterpret_cast<float2*>(o)[1] = make_float2(y[2], y[3]);
+      reinterpret_cast<float2*>(o)[2] = make_float2(y[4], y[5]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < kMaxK; ++j)
+        if (j < k) o[j] = softplus1(__uint_as_float(prev_v[j]) + p.b3[j]);
+    }
+  };
+
   uint32_t l1_phase = 0, mma_phase = 0;
   if (t0 < p.ntiles) {
     prepare_input(t0, 0);
@@ -293,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
     l1_phase ^= 1;
     if (tr) tr[1] = clock64();
     tc_fence_after();
-    epilogue_hidden(tD + lane_off, tA + lane_off);
+    epilogue_hidden<false>(tD + lane_off, tA + lane_off, nullptr);
     tc_fence_before();
     stream_barrier(st);
     if (tr) tr[2] = clock64();
@@ -304,54 +337,43 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
         mma_ts(tD, tA + kk * 8, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128), id64, kk > 0);
       mma_commit(bar_mma);
     }
-    // ---- overlap: the next tile's A1 (smem is free: layer 1 of this tile is done)
+    // ---- under layer 2: the next tile's A1 (smem is free: layer 1 of this tile is
+    // done) and the previous tile's codes
     const int64_t tn = t + tstride;
     if (tn < p.ntiles) prepare_input(tn, iter + 1);
+    store_codes();
+    if (tr) tr[3] = clock64();
     // ---- layer 2 done -> relu(acc + b2) -> A3 (TMEM, over A2)
     mbar_wait(bar_mma, mma_phase);
     mma_phase ^= 1;
-    if (tr) tr[3] = clock64();
+    if (tr) tr[4] = clock64();
     tc_fence_after();
-    epilogue_hidden(tD + lane_off, tA + lane_off);
+    epilogue_hidden<false>(tD + lane_off, tA + lane_off, nullptr);
     tc_fence_before();
     stream_barrier(st);
-    if (tr) tr[4] = clock64();
+    if (tr) tr[5] = clock64();
     if (leader) {
       tc_fence_after();
 #pragma unroll
-      for (int kk = 0; kk < kK2 / 16; ++kk)
+      for (int kk = 0; kk < kK3 / 16; ++kk)
         mma_ts(tD3, tA + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
       mma_commit(bar_mma);
       // next tile's layer 1 into the layer-1/2 accumulator, read out above (epi2)
       if (tn < p.ntiles) issue_l1(tn, iter + 1);
     }
-    // ---- layer 3 done -> softplus(acc + b3) -> codes
+    // ---- layer 3 done -> keep the 16 accumulator columns for store_codes()
     mbar_wait(bar_mma, mma_phase);
     mma_phase ^= 1;
     if (tr) tr[6] = clock64();
     tc_fence_after();
-    uint32_t v[16];
-    HC_TMEM_LD16(tD3 + lane_off, v);
+    HC_TMEM_LD16(tD3 + lane_off, prev_v);
     tmem_wait_ld();
     tc_fence_before();
-    const int k = p.k;
-    if (r < rows && !(p.exp_mode & 2)) {
-      float* o = p.out + (row0 + r) * k;
-      if (k == 6) {
-        float y[6];
-#pragma unroll
-        for (int j = 0; j < 6; ++j) y[j] = (p.exp_mode & 1) ? __uint_as_float(v[j]) : softplus1(__uint_as_float(v[j]));
-        reinterpret_cast<float2*>(o)[0] = make_float2(y[0], y[1]);
-        reinterpret_cast<float2*>(o)[1] = make_float2(y[2], y[3]);
-        reinterpret_cast<float2*>(o)[2] = make_float2(y[4], y[5]);
-      } else {
-#pragma unroll
-        for (int j = 0; j < kMaxK; ++j)
-          if (j < k) o[j] = softplus1(__uint_as_float(v[j]));
-      }
-    }
+    prev_row0 = row0;
+    prev_rows = rows;
     if (tr) tr[7] = clock64();
   }
+  store_codes();
   tc_fence_before();
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -402,8 +424,7 @@ int hc_mlp_create(hc_ctx ctx, int hidden, int k, const float* w1, const float* b
     put_kmajor(img, kOffW2, kHid, kK2, n, kHid, b2[n]);  // bias via the constant-1 A column
   }
   for (int n = 0; n < k; ++n) {
-    for (int j = 0; j < kHid; ++j) put_kmajor(img, kOffW3, kN3, kK2, n, j, w3[n * kHid + j]);
-    put_kmajor(img, kOffW3, kN3, kK2, n, kHid, b3[n]);
+    for (int j = 0; j < kHid; ++j) put_kmajor(img, kOffW3, kN3, kK3, n, j, w3[n * kHid + j]);
   }
   hc_mlp m = new hc_mlp_s();
   m->ctx = ctx;
@@ -423,6 +444,8 @@ int hc_mlp_create(hc_ctx ctx, int hidden, int k, const float* w1, const float* b
     return cuda_error(e, "hc_mlp_create");
   }
   std::memset(&m->base, 0, sizeof(m->base));
+  for (int i = 0; i < kHid; ++i) m->base.b2[i] = b2[i];
+  for (int i = 0; i < k; ++i) m->base.b3[i] = b3[i];
   m->base.wimg = m->d_wimg;
   m->base.k = k;
   *out = m;
@@ -456,7 +479,6 @@ int hc_mlp_forward(hc_mlp m, const float* rgb, int64_t P, float* codes) {
     const int grid = static_cast<int>(std::min<int64_t>(full, static_cast<int64_t>(m->occ) * ctx->sm_count));
     if (std::getenv("HC_DEBUG")) std::fprintf(stderr, "[hc] mlp_kernel grid=%d occ=%d smem=%d\n", grid, m->occ, kSmemBytes);
     long long* trace = nullptr;
-    if (const char* em = std::getenv("HC_MLP_EXP")) p.exp_mode = std::atoi(em);
     if (std::getenv("HC_MLP_TRACE")) {
       cudaMalloc(&trace, kStreams * 32 * 8 * sizeof(long long));
       cudaMemset(trace, 0, kStreams * 32 * 8 * sizeof(long long));
@@ -482,7 +504,7 @@ int hc_mlp_forward(hc_mlp m, const float* rgb, int64_t P, float* codes) {
           ++n;
         }
       if (n)
-        std::fprintf(stderr, "[hc] mlp phase cycles (avg of %d tiles): L1wait %.0f epi1 %.0f L2wait %.0f epi2 %.0f nextin %.0f L3wait %.0f epi3 %.0f loop %.0f\n",
+        std::fprintf(stderr, "[hc] mlp phase cycles (avg of %d tiles): L1wait %.0f epi1 %.0f L2issue %.0f in+store %.0f L2wait %.0f epi2 %.0f L3wait %.0f ldD3 %.0f\n",
                      n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n, acc[6] / n, acc[7] / n);
     }
   }
