@@ -105,7 +105,8 @@ int hc_blockwise_hadamard(hc_ctx ctx, const float* A, const float* B, int64_t ro
  * written as the reassembled HWC latent image (renderer.cpp:645-657), decoded
  * to spectra and/or projected to XYZ / linear sRGB.
  *   pal_codes  n_pal x k device codes (n_pal <= 256), light_codes L x k (host)
- *   L in {8, 32} (others -> HC_EUNSUPPORTED).  */
+ *   L in {8, 32}: fused TMA kernels; any other 1 <= L <= 64: generic kernel;
+ *   L > 64 -> HC_EUNSUPPORTED.  */
 int hc_shade_latent(hc_codec codec, const float* pal_codes, int n_pal, const float* light_codes,
                     int L, const uint32_t* idx, const float* cosv, int64_t P, float* latent,
                     float* spectra, float* xyz, float* rgb);
@@ -120,7 +121,7 @@ int hc_shade_latent_pass(hc_codec codec, int pass, const float* pal_codes, int n
 int hc_reassemble(hc_ctx ctx, const float* const* passes, int blocks, int64_t P, float* latent);
 /* Naive n-sample shading (config 2/3 ground truth): S_p = R_idx (.) sum_l cos_l L_l,
  * then XYZ / sRGB (renderer.cpp:187-190 at C = n, :692-719).
- *   pal_spectra n_pal x n device, light_spectra L x n host. */
+ *   pal_spectra n_pal x n device, light_spectra L x n host; L as for hc_shade_latent. */
 int hc_shade_spectral(hc_codec codec, const float* pal_spectra, int n_pal,
                       const float* light_spectra, int L, const uint32_t* idx, const float* cosv,
                       int64_t P, float* spectra, float* xyz, float* rgb);

@@ -2,12 +2,182 @@
 // reassembly + decode/projection) and naive n-sample spectral.
 // Reference: renderer.cpp:161-271 (compile_scene), :274-283 (slice_pass),
 // :505-510 (NEE channel loop), :645-657 (reassembly), :661-719 (decode/project).
+#include <algorithm>
 #include <cstring>
 
 #include "hc_launch.cuh"
 #include "hc_ops.cuh"
 
 namespace hcb {
+
+// ---------------------------------------------------------------- any light count
+// Runtime-L shading for light counts without a fused TMA instantiation (the
+// reference accepts any number of emitters): thread per pixel, G-buffer read with
+// plain loads, light codes / SPDs in the constant bank (L <= kMaxGenericLights).
+constexpr int kMaxGenericLights = 64;
+
+template <int N, int K>
+struct GenericLatentParams {
+  CodecConst<N, K> cc;
+  float light[kMaxGenericLights * K];
+  int L, n_pal;
+  const uint32_t* idx;
+  const float* cosv;
+  const float* pal;
+  int64_t P;
+  float *latent, *spectra, *xyz, *rgb;
+  int* err;
+};
+
+template <int N, int K>
+__global__ void __launch_bounds__(256) shade_latent_generic_kernel(const __grid_constant__ GenericLatentParams<N, K> p) {
+  __shared__ float pal[kMaxPalette * K];
+  for (int i = threadIdx.x; i < p.n_pal * K; i += blockDim.x) pal[i] = p.pal[i];
+  __syncthreads();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t px = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; px < p.P; px += stride) {
+    uint32_t id = p.idx[px];
+    if (id >= static_cast<uint32_t>(p.n_pal)) {
+      atomicOr(p.err, kErrIndexRange);
+      id = 0;
+    }
+    float acc[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) acc[j] = 0.f;
+    const float* c = p.cosv + px * p.L;
+    for (int l = 0; l < p.L; ++l) {
+      const float w = c[l];
+#pragma unroll
+      for (int j = 0; j < K; ++j) acc[j] = fmaf(w, p.light[l * K + j], acc[j]);
+    }
+    float z[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) z[j] = pal[id * K + j] * acc[j];
+    if (p.latent)
+#pragma unroll
+      for (int j = 0; j < K; ++j) p.latent[px * K + j] = z[j];
+    if (p.spectra)
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        float a = p.cc.D[i * K] * z[0];
+#pragma unroll
+        for (int j = 1; j < K; ++j) a = fmaf(p.cc.D[i * K + j], z[j], a);
+        p.spectra[px * N + i] = a;
+      }
+    float xyz[3], rgb[3];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+      float a = p.cc.Mxyz[cc * K] * z[0];
+#pragma unroll
+      for (int j = 1; j < K; ++j) a = fmaf(p.cc.Mxyz[cc * K + j], z[j], a);
+      xyz[cc] = a;
+    }
+    xyz_to_rgb(p.cc.Crgb, xyz, rgb);
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+      if (p.xyz) p.xyz[px * 3 + cc] = xyz[cc];
+      if (p.rgb) p.rgb[px * 3 + cc] = rgb[cc];
+    }
+  }
+}
+
+template <int N>
+struct GenericSpectralParams {
+  float light[kMaxGenericLights * N];
+  float cmf[3 * N];
+  float Crgb[9];
+  int L, n_pal;
+  const uint32_t* idx;
+  const float* cosv;
+  const float* pal;  // n_pal x N (read through L1: random rows)
+  int64_t P;
+  float *spectra, *xyz, *rgb;
+  int* err;
+};
+
+template <int N>
+__global__ void __launch_bounds__(256) shade_spectral_generic_kernel(const __grid_constant__ GenericSpectralParams<N> p) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t px = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; px < p.P; px += stride) {
+    uint32_t id = p.idx[px];
+    if (id >= static_cast<uint32_t>(p.n_pal)) {
+      atomicOr(p.err, kErrIndexRange);
+      id = 0;
+    }
+    const float* c = p.cosv + px * p.L;
+    const float* R = p.pal + static_cast<int64_t>(id) * N;
+    float xyz[3] = {0.f, 0.f, 0.f};
+    for (int i = 0; i < N; ++i) {
+      float illum = 0.f;
+      for (int l = 0; l < p.L; ++l) illum = fmaf(c[l], p.light[l * N + i], illum);
+      const float s = __ldg(R + i) * illum;
+      if (p.spectra) p.spectra[px * N + i] = s;
+      xyz[0] = fmaf(p.cmf[i], s, xyz[0]);
+      xyz[1] = fmaf(p.cmf[N + i], s, xyz[1]);
+      xyz[2] = fmaf(p.cmf[2 * N + i], s, xyz[2]);
+    }
+    float rgb[3];
+    xyz_to_rgb(p.Crgb, xyz, rgb);
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+      if (p.xyz) p.xyz[px * 3 + cc] = xyz[cc];
+      if (p.rgb) p.rgb[px * 3 + cc] = rgb[cc];
+    }
+  }
+}
+
+static int generic_grid(hc_ctx ctx, int64_t P) {
+  const int64_t g = (P + 255) / 256;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, static_cast<int64_t>(ctx->sm_count) * 8)));
+}
+
+template <int N, int K>
+int shade_latent_generic(hc_codec c, const float* pal, int n_pal, const float* light, int L, const uint32_t* idx,
+                         const float* cosv, int64_t P, float* latent, float* spectra, float* xyz, float* rgb) {
+  if (L > kMaxGenericLights) return set_error(HC_EUNSUPPORTED, "shade_latent: at most 64 lights");
+  if (P <= 0) return HC_OK;
+  GenericLatentParams<N, K> p;
+  fill_codec_const<N, K>(c, &p.cc);
+  for (int i = 0; i < L * K; ++i) p.light[i] = light[i];
+  p.L = L;
+  p.n_pal = n_pal;
+  p.idx = idx;
+  p.cosv = cosv;
+  p.pal = pal;
+  p.P = P;
+  p.latent = latent;
+  p.spectra = spectra;
+  p.xyz = xyz;
+  p.rgb = rgb;
+  p.err = c->ctx->d_err;
+  shade_latent_generic_kernel<N, K><<<generic_grid(c->ctx, P), 256, 0, c->ctx->stream>>>(p);
+  HC_CHECK_LAUNCH(c->ctx, "shade_latent_generic_kernel");
+  return HC_OK;
+}
+
+template <int N>
+int shade_spectral_generic(hc_codec c, const float* pal, int n_pal, const float* light, int L, const uint32_t* idx,
+                           const float* cosv, int64_t P, float* spectra, float* xyz, float* rgb) {
+  if (L > kMaxGenericLights) return set_error(HC_EUNSUPPORTED, "shade_spectral: at most 64 lights");
+  if (P <= 0) return HC_OK;
+  GenericSpectralParams<N> p;
+  for (int i = 0; i < L * N; ++i) p.light[i] = light[i];
+  for (int i = 0; i < 3 * N; ++i) p.cmf[i] = c->cmf_dl[i];
+  for (int i = 0; i < 9; ++i) p.Crgb[i] = c->Crgb[i];
+  p.L = L;
+  p.n_pal = n_pal;
+  p.idx = idx;
+  p.cosv = cosv;
+  p.pal = pal;
+  p.P = P;
+  p.spectra = spectra;
+  p.xyz = xyz;
+  p.rgb = rgb;
+  p.err = c->ctx->d_err;
+  shade_spectral_generic_kernel<N><<<generic_grid(c->ctx, P), 256, 0, c->ctx->stream>>>(p);
+  HC_CHECK_LAUNCH(c->ctx, "shade_spectral_generic_kernel");
+  return HC_OK;
+}
 
 template <int N, int K, int L, int OUTS>
 int shade_latent_nkl(hc_codec c, const float* pal, int n_pal, const float* light, const uint32_t* idx,
@@ -57,7 +227,7 @@ int shade_latent_nk(hc_codec c, const float* pal, int n_pal, const float* light,
   HC_SHADE_L(8)
   HC_SHADE_L(32)
 #undef HC_SHADE_L
-  return set_error(HC_EUNSUPPORTED, "shade_latent: light count must be 8 or 32");
+  return shade_latent_generic<N, K>(c, pal, n_pal, light, L, idx, cosv, P, latent, spectra, xyz, rgb);
 }
 
 int shade_latent_launch(hc_codec c, const float* pal, int n_pal, const float* light, int L,
@@ -98,7 +268,7 @@ int shade_spectral_n(hc_codec c, const float* pal, int n_pal, const float* light
   if (L == 32)
     return spec ? shade_spectral_nl<N, 32, true>(c, pal, n_pal, light, idx, cosv, P, spectra, xyz, rgb)
                 : shade_spectral_nl<N, 32, false>(c, pal, n_pal, light, idx, cosv, P, spectra, xyz, rgb);
-  return set_error(HC_EUNSUPPORTED, "shade_spectral: light count must be 8 or 32");
+  return shade_spectral_generic<N>(c, pal, n_pal, light, L, idx, cosv, P, spectra, xyz, rgb);
 }
 
 int shade_spectral_launch(hc_codec c, const float* pal, int n_pal, const float* light, int L,

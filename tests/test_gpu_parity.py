@@ -201,7 +201,8 @@ def _scene(api, ctx, k, L, n=81):
 
 
 @pytest.mark.parametrize("k,L,P,spec", [(6, 8, 50_003, False), (6, 8, 4096, True), (9, 32, 20_011, True),
-                                        (9, 32, 777, False), (3, 8, 1000, True)])
+                                        (9, 32, 777, False), (3, 8, 1000, True), (6, 5, 3001, True),
+                                        (9, 1, 1000, False), (6, 64, 513, True)])
 def test_shade_latent_vs_oracle(api, ctx, orc, k, L, P, spec):
     codec, E, D, pal, lts, pal_d, pal_codes, light_codes = _scene(api, ctx, k, L)
     idx, cosv = api.synth_gbuffer(ctx, SEED, 0, P, L, 256)
@@ -245,7 +246,8 @@ def test_multipass_equals_fused(api, ctx, k, L):
     assert np.array_equal(host(multi), host(fused))
 
 
-@pytest.mark.parametrize("L,P,spec", [(8, 30_001, False), (32, 5000, True), (8, 2048, True)])
+@pytest.mark.parametrize("L,P,spec", [(8, 30_001, False), (32, 5000, True), (8, 2048, True), (3, 1001, True),
+                                      (17, 999, False)])
 def test_shade_spectral_vs_oracle(api, ctx, orc, L, P, spec):
     codec, E, D, pal, lts, pal_d, _, _ = _scene(api, ctx, 6, L)
     idx, cosv = api.synth_gbuffer(ctx, SEED, 3, P, L, 256)
