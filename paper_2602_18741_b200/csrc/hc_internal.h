@@ -19,7 +19,8 @@ struct hc_ctx_s {
   int partial_capacity = 0;
   void* scratch = nullptr;     // host-entry staging (grow-only)
   size_t scratch_bytes = 0;
-  cudaStream_t aux[3] = {nullptr, nullptr, nullptr};  // host-entry copy/compute pipeline
+  static constexpr int kAux = 4;
+  cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr, nullptr};  // host-entry copy/compute pipeline
   cudaEvent_t ev_fork = nullptr;
   std::atomic<int64_t> launches{0};
 };

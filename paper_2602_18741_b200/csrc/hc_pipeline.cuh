@@ -82,13 +82,6 @@ __global__ void __launch_bounds__(Op::THREADS)
   unsigned char* extra = out_base + S * Lay::kOutTile;
   const int tid = threadIdx.x;
 
-  Op::setup(p, extra);
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
-    fence_mbar_init();
-  }
-  __syncthreads();
-
   auto issue_loads = [&](int64_t tile, int s) {
     unsigned char* stage = in_base + s * Lay::kInTile;
     mbar_arrive_expect_tx(&bar[s], Lay::kInBytes());
@@ -104,12 +97,18 @@ __global__ void __launch_bounds__(Op::THREADS)
     }
   };
 
+  // The first STAGES tiles are requested before the op's table setup (e.g. the
+  // palette copy) so the two latencies overlap at kernel start.
   if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
     for (int s = 0; s < S; ++s) {
       const int64_t tile = blockIdx.x + static_cast<int64_t>(s) * gridDim.x;
       if (tile < ntiles) issue_loads(tile, s);
     }
   }
+  Op::setup(p, extra);
+  __syncthreads();
 
   typename Op::State st;
   Op::init_state(st);

@@ -554,12 +554,13 @@ int hc_shade_latent_host(hc_codec c, const float* pal_codes, int n_pal, const fl
   HC_CUDA_TRY(cudaMemcpyAsync(d_pal, pal_codes, pal_b, cudaMemcpyHostToDevice, ctx->stream));
   HC_CUDA_TRY(cudaEventRecord(ctx->ev_fork, ctx->stream));
   for (auto st : ctx->aux) HC_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_fork, 0));
-  constexpr int64_t kChunk = 131072;  // pixels (multiple of every tile size)
+  constexpr int64_t kChunk = 131072;  // pixels (multiple of every tile size); finer chunks measured slower
+  constexpr int kAuxStreams = hc_ctx_s::kAux;
   cudaStream_t home = ctx->stream;
   int ci = 0;
   for (int64_t p0 = 0; p0 < P; p0 += kChunk, ++ci) {
     const int64_t n = P - p0 < kChunk ? P - p0 : kChunk;
-    cudaStream_t st = ctx->aux[ci % 3];
+    cudaStream_t st = ctx->aux[ci % kAuxStreams];
     HC_CUDA_TRY(cudaMemcpyAsync(d_idx + p0, idx + p0, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
     HC_CUDA_TRY(cudaMemcpyAsync(d_cos + p0 * L, cosv + p0 * L, sizeof(float) * n * L, cudaMemcpyHostToDevice, st));
     ctx->stream = st;
