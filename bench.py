@@ -97,7 +97,7 @@ class ClockSampler:
                 self.samples.append((mhz, rs))
             except Exception:  # noqa: BLE001
                 pass
-            time.sleep(0.002)
+            time.sleep(0.0005)
 
     def __enter__(self):
         if self.nv:

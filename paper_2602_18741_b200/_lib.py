@@ -8,7 +8,10 @@ from __future__ import annotations
 import ctypes as C
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libhadacodec_b200.so"
+import os
+
+# HC_LIB overrides the library path (tuning sweeps load variant builds from tools/bin/).
+LIB_PATH = Path(os.environ.get("HC_LIB") or Path(__file__).resolve().parent / "libhadacodec_b200.so")
 
 HC_OK, HC_EINVAL, HC_EDOMAIN, HC_ECUDA, HC_ENOMEM, HC_EUNSUPPORTED = range(6)
 

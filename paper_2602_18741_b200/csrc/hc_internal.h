@@ -23,6 +23,7 @@ struct hc_ctx_s {
   cudaStream_t aux[kAux] = {nullptr, nullptr, nullptr, nullptr};  // host-entry copy/compute pipeline
   cudaEvent_t ev_fork = nullptr;
   std::atomic<int64_t> launches{0};
+  int pdl = 1;  // programmatic dependent launch for tile kernels (HC_PDL=0 disables)
 };
 
 struct hc_codec_s {

@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <utility>
 
 #include "hc_internal.h"
 #include "hc_pipeline.cuh"
@@ -14,7 +15,7 @@ namespace hcb {
 template <class Op>
 struct TileLaunchCache {
   static std::atomic<int> configured;  // 0 = not yet, 1 = done
-  static int occ_pipeline, occ_generic;
+  static int occ_pipeline, occ_generic;  // occ_pipeline: of tile_pipeline_ws for warp-specialised ops
 };
 template <class Op>
 std::atomic<int> TileLaunchCache<Op>::configured{0};
@@ -22,6 +23,7 @@ template <class Op>
 int TileLaunchCache<Op>::occ_pipeline = 1;
 template <class Op>
 int TileLaunchCache<Op>::occ_generic = 1;
+
 
 template <class Op>
 int configure_tile_op() {
@@ -34,14 +36,43 @@ int configure_tile_op() {
                                    cudaSharedmemCarveoutMaxShared));
   HC_CUDA_TRY(cudaFuncSetAttribute(tile_generic<Op>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                    cudaSharedmemCarveoutMaxShared));
-  int a = 0, b = 0;
-  HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, tile_pipeline<Op>, Op::THREADS, smem));
+  int a = 0, b = 0, w = 1;
+  if constexpr (Op::kWarpSpecialized) {
+    const int smem_ws = WsLayout<Op>::smem_bytes();
+    HC_CUDA_TRY(cudaFuncSetAttribute(tile_pipeline_ws<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_ws));
+    HC_CUDA_TRY(cudaFuncSetAttribute(tile_pipeline_ws<Op>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared));
+    HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&w, tile_pipeline_ws<Op>,
+                                                              Op::THREADS + kProducerWarp, smem_ws));
+    a = w;
+  } else {
+    HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, tile_pipeline<Op>, Op::THREADS, smem));
+  }
   HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, tile_generic<Op>, Op::THREADS, smem));
-  if (a < 1 || b < 1) return set_error(HC_EUNSUPPORTED, "tile kernel does not fit on an SM");
+  if (a < 1 || b < 1 || w < 1) return set_error(HC_EUNSUPPORTED, "tile kernel does not fit on an SM");
   Cache::occ_pipeline = a;
   Cache::occ_generic = b;
   Cache::configured.store(1, std::memory_order_release);
   return HC_OK;
+}
+
+// Launch with the programmatic-stream-serialization attribute (PDL) when the
+// context allows it: the kernel may begin while the previous kernel on the
+// stream drains; kernels using this must call pdl_wait_prior_grids() before
+// their first global access (tile_pipeline / tile_generic do).
+template <class... KArgs, class... Args>
+cudaError_t launch_k(hc_ctx ctx, void (*kern)(KArgs...), int grid, int block, int smem, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx->pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 inline bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
@@ -72,14 +103,19 @@ int launch_tile_op(hc_ctx ctx, const typename Op::Params& p, int64_t items, int*
   int g0 = 0, g1 = 0;
   if (full > 0) {
     g0 = static_cast<int>(std::min<int64_t>(full, static_cast<int64_t>(Cache::occ_pipeline) * ctx->sm_count));
-    tile_pipeline<Op><<<g0, Op::THREADS, smem, ctx->stream>>>(p, full);
+    if constexpr (Op::kWarpSpecialized) {
+      HC_CUDA_TRY(launch_k(ctx, tile_pipeline_ws<Op>, g0, Op::THREADS + kProducerWarp,
+                           WsLayout<Op>::smem_bytes(), p, full));
+    } else {
+      HC_CUDA_TRY(launch_k(ctx, tile_pipeline<Op>, g0, Op::THREADS, smem, p, full));
+    }
     HC_CHECK_LAUNCH(ctx, "tile_pipeline");
   }
   const int64_t begin = full * Op::T;
   if (begin < items) {
     const int64_t tiles = (items - begin + Op::T - 1) / Op::T;
     g1 = static_cast<int>(std::min<int64_t>(tiles, static_cast<int64_t>(Cache::occ_generic) * ctx->sm_count));
-    tile_generic<Op><<<g1, Op::THREADS, smem, ctx->stream>>>(p, begin, items);
+    HC_CUDA_TRY(launch_k(ctx, tile_generic<Op>, g1, Op::THREADS, smem, p, begin, items));
     HC_CHECK_LAUNCH(ctx, "tile_generic");
   }
   if (grid_out) {

@@ -47,6 +47,8 @@ struct CodecOp {
   }
   static constexpr int EXTRA_SMEM = 0;
   static constexpr int kTensorStream = -1;
+  static constexpr bool kWarpSpecialized = false;
+  static constexpr bool kEvictFirstLoads = false;
 
   struct Params {
     CodecConst<N, K> cc;
@@ -179,6 +181,11 @@ struct ShadeLatentOp {
   }
   static constexpr int EXTRA_SMEM = kMaxPalette * K * 4;
   static constexpr int kTensorStream = (L * 4 == 128) ? 1 : -1;  // 128-byte cos rows: swizzled 2-D TMA
+  // Pipeline choice (measured, profiles/README.md): the spectra-writing variant runs the
+  // warp-specialised pipeline (78 -> 85 % HBM); the small-output variant streams its
+  // inputs with an L2 evict-first policy (80 -> 81 %).
+  static constexpr bool kWarpSpecialized = (OUTS & kOutSpectra) != 0;
+  static constexpr bool kEvictFirstLoads = (OUTS & kOutSpectra) == 0;
 
   struct Params {
     CUtensorMap cos_map;  // 2-D map of cos [P][L] with the 128-byte swizzle (used when L == 32)
@@ -289,6 +296,8 @@ struct ShadeSpectralOp {
   __host__ __device__ static constexpr int out_bytes(int i) { return i < 2 ? 12 : N * 4; }
   static constexpr int EXTRA_SMEM = kMaxPalette * N * 4;
   static constexpr int kTensorStream = -1;
+  static constexpr bool kWarpSpecialized = false;
+  static constexpr bool kEvictFirstLoads = false;
 
   struct Params {
     float light[L * N];
@@ -374,6 +383,8 @@ struct LossOp {
   __host__ __device__ static constexpr int out_bytes(int) { return 0; }
   static constexpr int EXTRA_SMEM = 32 * 8;
   static constexpr int kTensorStream = -1;
+  static constexpr bool kWarpSpecialized = false;
+  static constexpr bool kEvictFirstLoads = false;
 
   struct Params {
     CodecConst<N, K> cc;

@@ -20,7 +20,9 @@
 //   EXTRA_SMEM (bytes for op tables, e.g. the palette), Params, State,
 //   in_ptr(p, i), out_ptr(p, i) (nullptr = stream disabled),
 //   setup(p, extra_smem), compute(p, st, in[], out[], extra, item, global_item),
-//   finish(p, st, extra)
+//   finish(p, st, extra),
+//   kWarpSpecialized (run tile_pipeline_ws instead of tile_pipeline),
+//   kEvictFirstLoads (stream the inputs through L2 with an evict-first policy)
 // Ragged tails and unaligned pointers go through tile_generic, which runs the
 // same compute on word copies (no TMA; the swizzle is applied in software).
 #pragma once
@@ -92,16 +94,28 @@ __global__ void __launch_bounds__(Op::THREADS)
         tma_load_2d(dst, Op::tensor_map(p), 0, static_cast<int>(tile * T), &bar[s]);
       } else {
         const unsigned char* src = static_cast<const unsigned char*>(Op::in_ptr(p, i));
-        bulk_g2s(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &bar[s]);
+        if constexpr (Op::kEvictFirstLoads)
+          bulk_g2s_evict_first(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &bar[s],
+                               policy_evict_first());
+        else
+          bulk_g2s(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &bar[s]);
       }
     }
   };
 
-  // The first STAGES tiles are requested before the op's table setup (e.g. the
-  // palette copy) so the two latencies overlap at kernel start.
+  // The grid is persistent (<= one wave), so the next kernel may be scheduled
+  // right away: its CTAs take SM slots as ours exit and do their setup while
+  // our tail drains.  Global memory is touched only after every prior grid is
+  // complete (pdl_wait_prior_grids), so any aliasing between launches is safe.
+  pdl_launch_dependents();
   if (tid == 0) {
     for (int s = 0; s < S; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
+  }
+  pdl_wait_prior_grids();
+  // The first STAGES tiles are requested before the op's table setup (e.g. the
+  // palette copy) so the two latencies overlap at kernel start.
+  if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       const int64_t tile = blockIdx.x + static_cast<int64_t>(s) * gridDim.x;
       if (tile < ntiles) issue_loads(tile, s);
@@ -148,6 +162,131 @@ __global__ void __launch_bounds__(Op::THREADS)
   Op::finish(p, st, extra);
 }
 
+// Warp-specialised variant: THREADS consumer threads + one producer warp, no
+// CTA-wide barrier inside the loop.  Per input slot s: full[s] (TMA bytes
+// landed) and empty[s] (one arrival per consumer warp once it has read in[s]
+// and written its outputs).  Outputs use their own ring of OUT_STAGES slots;
+// ofree[o] is re-armed by the producer once the bulk store that read out[o] has
+// drained, so a warp that finishes tile t early moves on to tile t+1 without
+// waiting for the slowest warp.
+constexpr int kOutStages = 2;
+constexpr int kProducerWarp = 32;
+
+template <class Op>
+struct WsLayout {
+  using Lay = TileLayout<Op>;
+  static constexpr int kOutSlots = Op::NOUT > 0 ? kOutStages : 0;
+  static constexpr int smem_bytes() {
+    return Lay::kBarBytes + Op::STAGES * Lay::kInTile + kOutSlots * Lay::kOutTile + Op::EXTRA_SMEM + 1024;
+  }
+};
+
+template <class Op>
+__global__ void __launch_bounds__(Op::THREADS + kProducerWarp)
+    tile_pipeline_ws(const __grid_constant__ typename Op::Params p, int64_t ntiles) {
+  using Lay = TileLayout<Op>;
+  constexpr int S = Op::STAGES;
+  constexpr int SO = kOutStages;
+  constexpr int T = Op::T;
+  constexpr int NCW = Op::THREADS / 32;  // consumer warps
+  static_assert(Op::THREADS % 32 == 0, "consumer threads must be whole warps");
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = aligned_smem_base(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + S;
+  uint64_t* ofree = empty + S;
+  unsigned char* in_base = smem + Lay::kBarBytes;
+  unsigned char* out_base = in_base + S * Lay::kInTile;
+  unsigned char* extra = out_base + WsLayout<Op>::kOutSlots * Lay::kOutTile;
+  const int tid = threadIdx.x;
+  const bool producer = tid == Op::THREADS;
+
+  auto issue_loads = [&](int64_t tile, int s) {
+    unsigned char* stage = in_base + s * Lay::kInTile;
+    mbar_arrive_expect_tx(&full[s], Lay::kInBytes());
+#pragma unroll
+    for (int i = 0; i < Op::NIN; ++i) {
+      unsigned char* dst = stage + Lay::in_off(i);
+      if (i == Op::kTensorStream) {
+        tma_load_2d(dst, Op::tensor_map(p), 0, static_cast<int>(tile * T), &full[s]);
+      } else {
+        const unsigned char* src = static_cast<const unsigned char*>(Op::in_ptr(p, i));
+        if constexpr (Op::kEvictFirstLoads)
+          bulk_g2s_evict_first(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &full[s],
+                               policy_evict_first());
+        else
+          bulk_g2s(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &full[s]);
+      }
+    }
+  };
+
+  pdl_launch_dependents();
+  if (producer) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+    for (int o = 0; o < SO; ++o) mbar_init(&ofree[o], 1);
+    fence_mbar_init();
+  }
+  pdl_wait_prior_grids();
+  if (producer) {
+    for (int s = 0; s < S; ++s) {
+      const int64_t tile = blockIdx.x + static_cast<int64_t>(s) * gridDim.x;
+      if (tile < ntiles) issue_loads(tile, s);
+    }
+    for (int o = 0; o < SO; ++o) mbar_arrive(&ofree[o]);  // every output slot starts free
+  }
+  Op::setup(p, extra);
+  __syncthreads();
+
+  typename Op::State st;
+  Op::init_state(st);
+  if (tid < Op::THREADS) {
+    int iter = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
+      const int s = iter % S;
+      const int o = iter % SO;
+      mbar_wait(&full[s], (iter / S) & 1);
+      if (Op::NOUT > 0) mbar_wait(&ofree[o], (iter / SO) & 1);
+      const unsigned char* ins[Op::NIN > 0 ? Op::NIN : 1];
+      unsigned char* outs[Op::NOUT > 0 ? Op::NOUT : 1];
+#pragma unroll
+      for (int i = 0; i < Op::NIN; ++i) ins[i] = in_base + s * Lay::kInTile + Lay::in_off(i);
+#pragma unroll
+      for (int i = 0; i < Op::NOUT; ++i) outs[i] = out_base + o * Lay::kOutTile + Lay::out_off(i);
+      for (int item = tid; item < T; item += Op::THREADS)
+        Op::compute(p, st, ins, outs, extra, item, tile * T + item);
+      if (Op::NOUT > 0) fence_proxy_async_smem();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    }
+  } else if (producer) {
+    int iter = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
+      const int s = iter % S;
+      mbar_wait(&empty[s], (iter / S) & 1);
+      if (Op::NOUT > 0) {
+        unsigned char* ob = out_base + (iter % SO) * Lay::kOutTile;
+#pragma unroll
+        for (int i = 0; i < Op::NOUT; ++i) {
+          unsigned char* dst = static_cast<unsigned char*>(Op::out_ptr(p, i));
+          if (dst) bulk_s2g(dst + tile * T * Op::out_bytes(i), ob + Lay::out_off(i), T * Op::out_bytes(i));
+        }
+        bulk_commit();
+      }
+      const int64_t next = tile + static_cast<int64_t>(S) * gridDim.x;
+      if (next < ntiles) issue_loads(next, s);
+      if (Op::NOUT > 0 && iter + 1 >= SO) {
+        bulk_wait_read<SO - 1>();  // the store of tile iter + 1 - SO has read its slot
+        mbar_arrive(&ofree[(iter + 1) % SO]);
+      }
+    }
+    bulk_wait_all<0>();
+  }
+  Op::finish(p, st, extra);
+}
+
 // Same computation without TMA: word-granular copies, any alignment, any item
 // range [item_begin, item_end).  Used for ragged tails and unaligned buffers.
 template <class Op>
@@ -161,6 +300,7 @@ __global__ void __launch_bounds__(Op::THREADS)
   unsigned char* out_base = in_base + Op::STAGES * Lay::kInTile;
   unsigned char* extra = out_base + Op::STAGES * Lay::kOutTile;
   const int tid = threadIdx.x;
+  pdl_wait_prior_grids();
   Op::setup(p, extra);
   __syncthreads();
   typename Op::State st;

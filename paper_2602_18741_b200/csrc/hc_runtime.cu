@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -268,6 +269,7 @@ int hc_ctx_create(int device, void* stream, hc_ctx* out) {
   c->stream = static_cast<cudaStream_t>(stream);
   c->sm_count = prop.multiProcessorCount;
   c->max_smem_optin = prop.sharedMemPerBlockOptin;
+  if (const char* pdl = std::getenv("HC_PDL")) c->pdl = pdl[0] != '0';
   cudaError_t e = cudaMalloc(&c->d_err, sizeof(int));
   if (e != cudaSuccess) {
     delete c;

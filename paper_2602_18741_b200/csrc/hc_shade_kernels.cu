@@ -8,6 +8,16 @@
 #include "hc_launch.cuh"
 #include "hc_ops.cuh"
 
+#ifndef HC_C2_T
+#define HC_C2_T 256
+#endif
+#ifndef HC_C2_THREADS
+#define HC_C2_THREADS 256
+#endif
+#ifndef HC_C2_STAGES
+#define HC_C2_STAGES 3
+#endif
+
 namespace hcb {
 
 // ---------------------------------------------------------------- any light count
@@ -184,9 +194,10 @@ int shade_latent_nkl(hc_codec c, const float* pal, int n_pal, const float* light
                      const float* cosv, int64_t P, float* latent, float* spectra, float* xyz,
                      float* rgb) {
   constexpr bool SPEC = (OUTS & kOutSpectra) != 0;
-  constexpr int T = SPEC ? 64 : 256;
-  constexpr int THREADS = T;
-  constexpr int STAGES = SPEC ? 2 : 3;
+  constexpr bool C2 = L == 8 && OUTS == (kOutXyz | kOutRgb);
+  constexpr int T = SPEC ? 64 : (C2 ? HC_C2_T : 256);
+  constexpr int THREADS = C2 ? HC_C2_THREADS : T;
+  constexpr int STAGES = SPEC ? 2 : (C2 ? HC_C2_STAGES : 3);
   using Op = ShadeLatentOp<N, K, L, OUTS, T, THREADS, STAGES>;
   typename Op::Params p;
   fill_codec_const<N, K>(c, &p.cc);
