@@ -271,6 +271,15 @@ class Codec:
                                                lc.shape[0], _np_ptr(idx), _np_ptr(cosv), idx.size, _np_ptr(xyz),
                                                _np_ptr(rgb)))
 
+    def roundtrip_host(self, S: np.ndarray, Z: Optional[np.ndarray] = None, S2: Optional[np.ndarray] = None,
+                       xyz: Optional[np.ndarray] = None, rgb: Optional[np.ndarray] = None) -> None:
+        """Host-buffer round trip (encode -> decode_image -> image_to_linear_rgb); outputs may be None."""
+        S = np.ascontiguousarray(S, dtype=np.float32)
+        rows = S.size // self.n
+        self.ctx.bind_stream()
+        _check(_lib.lib().hc_roundtrip_host(self.h, _np_ptr(S), rows, *[None if a is None else _np_ptr(a)
+                                                                        for a in (Z, S2, xyz, rgb)]))
+
 
 def blockwise_hadamard(ctx: Context, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
     """codec.cpp:77-85, batched over rows."""

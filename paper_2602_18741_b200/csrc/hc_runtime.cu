@@ -293,6 +293,7 @@ int hc_ctx_destroy(hc_ctx ctx) {
   for (auto st : ctx->aux)
     if (st) cudaStreamDestroy(st);
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+
   if (ctx->d_partials) cudaFree(ctx->d_partials);
   if (ctx->d_err) cudaFree(ctx->d_err);
   delete ctx;
@@ -532,6 +533,12 @@ int hc_hadamard_loss(hc_codec c, const float* A, const float* B, int64_t pairs, 
 }
 
 // ------------------------------------------------------------------ host-buffer entry points
+// Pipelined host-buffer call: chunk i's H2D copies, chunk i-1's kernel and chunk
+// i-2's D2H copies overlap on hc_ctx_s::kAux streams (round robin).  Measured on the
+// B200 host (tools/e2e_sweep.sh): 256K-pixel chunks (8 per 1080p
+// frame) balance the ~4 us per-copy cost against pipeline fill / drain; role streams
+// (all H2D on one stream, all D2H on another), a ramped chunk schedule, and letting
+// the kernel write pinned outputs over PCIe (zero copy) all measured slower.
 int hc_shade_latent_host(hc_codec c, const float* pal_codes, int n_pal, const float* light_codes, int L,
                          const uint32_t* idx, const float* cosv, int64_t P, float* xyz, float* rgb) {
   int rc = check_shade_args(c, pal_codes, n_pal, light_codes, L, idx, cosv, P);
@@ -551,18 +558,15 @@ int hc_shade_latent_host(hc_codec c, const float* pal_codes, int n_pal, const fl
   float* d_cos = reinterpret_cast<float*>(base + up(pal_b) + up(idx_b));
   float* d_xyz = reinterpret_cast<float*>(base + up(pal_b) + up(idx_b) + up(cos_b));
   float* d_rgb = reinterpret_cast<float*>(base + up(pal_b) + up(idx_b) + up(cos_b) + up(out_b));
-  // Chunked 3-stream pipeline: chunk i's H2D (copy engine 0), chunk i-1's kernel and
-  // chunk i-2's D2H (copy engine 1) overlap.  Pinned host buffers give full PCIe rate.
   HC_CUDA_TRY(cudaMemcpyAsync(d_pal, pal_codes, pal_b, cudaMemcpyHostToDevice, ctx->stream));
   HC_CUDA_TRY(cudaEventRecord(ctx->ev_fork, ctx->stream));
   for (auto st : ctx->aux) HC_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_fork, 0));
-  constexpr int64_t kChunk = 131072;  // pixels (multiple of every tile size); finer chunks measured slower
-  constexpr int kAuxStreams = hc_ctx_s::kAux;
+  constexpr int64_t kChunk = 262144;  // pixels (multiple of every tile size)
   cudaStream_t home = ctx->stream;
   int ci = 0;
   for (int64_t p0 = 0; p0 < P; p0 += kChunk, ++ci) {
     const int64_t n = P - p0 < kChunk ? P - p0 : kChunk;
-    cudaStream_t st = ctx->aux[ci % kAuxStreams];
+    cudaStream_t st = ctx->aux[ci % hc_ctx_s::kAux];
     HC_CUDA_TRY(cudaMemcpyAsync(d_idx + p0, idx + p0, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
     HC_CUDA_TRY(cudaMemcpyAsync(d_cos + p0 * L, cosv + p0 * L, sizeof(float) * n * L, cudaMemcpyHostToDevice, st));
     ctx->stream = st;

@@ -217,6 +217,34 @@ def test_shade_latent_vs_oracle(api, ctx, orc, k, L, P, spec):
     _check(f"rgb k={k} L={L}", host(out["rgb"]), ref[3])
 
 
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("k,L,P", [(6, 8, 300_007), (9, 32, 131_072), (3, 5, 1001)])
+def test_shade_latent_host_buffers(api, ctx, k, L, P, pinned):
+    """hc_shade_latent_host (chunked H2D -> kernel -> D2H pipeline over the aux streams,
+    ragged last chunk, pinned or pageable host buffers) == the device-resident call."""
+    codec, E, D, pal, lts, pal_d, pal_codes, light_codes = _scene(api, ctx, k, L)
+    idx, cosv = api.synth_gbuffer(ctx, SEED, 11, P, L, 256)
+    dev = codec.shade_latent(pal_codes, light_codes, idx, cosv)
+    if pinned:
+        xyz_t, rgb_t = torch.zeros(P, 3).pin_memory(), torch.zeros(P, 3).pin_memory()
+        xyz, rgb = xyz_t.numpy(), rgb_t.numpy()
+    else:
+        xyz, rgb = np.zeros((P, 3), np.float32), np.zeros((P, 3), np.float32)
+    codec.shade_latent_host(host(pal_codes), light_codes, host(idx), host(cosv), xyz, rgb)
+    assert np.array_equal(xyz, host(dev["xyz"])) and np.array_equal(rgb, host(dev["rgb"]))
+
+
+def test_roundtrip_host_buffers(api, ctx, orc):
+    codec, E, D = _codec(api, ctx, 6)
+    rows = 20_001
+    S = host(api.synth_gm_spectra(ctx, SEED, "host.rt", 0, rows, 81))
+    dev = codec.roundtrip(torch.from_numpy(S).cuda())
+    Z, S2, xyz, rgb = (np.zeros((rows, d), np.float32) for d in (6, 81, 3, 3))
+    codec.roundtrip_host(S, Z, S2, xyz, rgb)
+    for key, got in (("codes", Z), ("spectra", S2), ("xyz", xyz), ("rgb", rgb)):
+        assert np.array_equal(got, host(dev[key])), key
+
+
 def test_shade_golden(api, ctx, golden):
     for tag, k, L in (("c2", 6, 8), ("c3", 9, 32)):
         codec = api.Codec(ctx, golden[f"E{k}"], golden[f"D{k}"])
