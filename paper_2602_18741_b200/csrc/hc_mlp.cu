@@ -8,23 +8,30 @@
 // One 128-pixel tile = one M = 128 tcgen05 row block:
 //   L1  D[128 x 64] = A1[128 x 16] . W1'^T   (SS: A1 = (r, g, b, 1, 0...) bf16 in smem,
 //                                              W1' = [W1 | b1 | 0]: bias rides the MMA)
-//   L2  D[128 x 64] = A2[128 x 64] . W2^T    (TS: A2 = bf16(relu(L1)) in TMEM)
-//   L3  D[128 x 16] = A3[128 x 64] . W3'^T   (TS: A3 = bf16(relu(L2 + b2)) in TMEM)
+//   L2  D[128 x 64] = A2[128 x 80] . W2'^T   (TS: A2 = [bf16(relu(L1)) | 1 | 0] in TMEM,
+//                                              W2' = [W2 | b2 | 0])
+//   L3  D[128 x 16] = A3[128 x 64] . W3^T    (TS: A3 = bf16(relu(L2)) in TMEM)
 //   out = softplus(L3[:, :k] + b3)
 // Hidden activations never touch shared memory: the epilogue reads the fp32
-// accumulator (tcgen05.ld), applies bias / ReLU, packs bf16x2 (cvt.rn.relu.bf16x2)
-// and writes the next layer's A operand back into TMEM (tcgen05.st), which the
-// next MMA reads directly ("A from TMEM").  With A in shared memory (SS) the
-// 128 x 16 A tile is re-read from smem by every N = 64 MMA and smem bandwidth,
-// not the tensor core, was the limit (profiles/README.md).
+// accumulator (tcgen05.ld), applies ReLU, packs bf16x2 (cvt.rn.relu.bf16x2) and
+// writes the next layer's A operand back into TMEM (tcgen05.st), which the next
+// MMA reads directly ("A from TMEM").  With A in shared memory (SS) the 128 x 16 A
+// tile is re-read from smem by every MMA and smem bandwidth was the limit.
 //
-// One CTA per SM, 4 warpgroups = 4 independent tile streams.  Each stream owns
-// 128 TMEM columns of the CTA's 512 ([0,32) packed A2/A3, [32,96) the fp32
-// accumulator), a 4 KB A1 tile and a 2-deep ring of rgb tiles fetched by 1-D
-// bulk copies (TMA); its elected thread issues its MMAs and commits them to the
-// stream's mbarrier, so the streams' MMA and epilogue phases interleave on the
-// SM's tensor core.  Weights (12 KB, canonical no-swizzle K-major UMMA images,
-// element (n, k) at (k/8)*(N*16) + n*16 + (k%8)*2) are loaded once per CTA.
+// One CTA per SM, 4 tile streams.  Each stream owns 128 TMEM columns of the CTA's
+// 512 ([0,40) packed A2/A3 + the constant-1 chunk, [48,112) the fp32 layer-1/2
+// accumulator, [112,128) the layer-3 accumulator), a 4 KB A1 tile and a 2-deep
+// ring of rgb tiles fetched by 1-D bulk copies (TMA).  A stream is 4 epilogue
+// warps (one per TMEM lane quarter) plus one MMA-issuer warp: tools/mma_probe3.cu
+// measured that one thread can issue a tcgen05.mma only every ~45 cycles while
+// several issuing warps overlap up to the tensor pipe's rate, so issuing from the
+// epilogue warps put 10 x 45 cycles per tile on their critical path (the old
+// layout's phase trace).  The warps hand off through mbarriers only:
+//   issuer:   wait a1 -> L1 -> commit l1 | wait a2 -> L2 -> commit l2 | wait a3 -> L3 -> commit l3
+//   epilogue: wait l1 -> relu(D) -> A2, arrive a2 | next A1, arrive a1 | codes of the previous tile
+//             | wait l2 -> relu(D) -> A3, arrive a3 | wait l3 -> keep D3 for the codes
+// Weights (12 KB, canonical no-swizzle K-major UMMA images, element (n, k) at
+// (k/8)*(N*16) + n*16 + (k%8)*2) are loaded once per CTA.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -44,8 +51,9 @@ constexpr int kHid = 64;      // hidden width
 constexpr int kK1 = 16;       // layer-1 K (3 inputs + bias column, padded)
 constexpr int kN3 = 16;       // layer-3 N (k padded)
 constexpr int kMaxK = 9;
-constexpr int kStreams = 4;                 // warpgroups / tile streams per CTA
-constexpr int kThreads = 128 * kStreams;
+constexpr int kStreams = 4;                 // tile streams per CTA
+constexpr int kEpiThreads = 128 * kStreams; // epilogue warps: warp w -> stream w / 4, lane quarter w % 4
+constexpr int kThreads = kEpiThreads + 32 * kStreams;  // + one MMA-issuer warp per stream
 constexpr int kK2 = 80;                     // layer 2 K: 64 hidden + constant-1 column (b2 rides the MMA)
 constexpr int kK3 = 64;                     // layer 3 K: b3 (6 values) is added in the epilogue instead of
                                             // paying a fifth >= 45-cycle N = 16 MMA
@@ -67,7 +75,8 @@ constexpr int kInTile = kMlpM * 3 * 4;               // 1536 B
 constexpr int kStreamBytes = kA1Bytes + 2 * kInTile;
 constexpr int kOffStreams = kWBytes;
 constexpr int kOffBar = kOffStreams + kStreams * kStreamBytes;
-constexpr int kSmemBytes = kOffBar + kStreams * 4 * 8 + 16;
+constexpr int kBarsPerStream = 8;  // in[2], l1, l2, l3, a1, a2, a3
+constexpr int kSmemBytes = kOffBar + kStreams * kBarsPerStream * 8 + 16;
 
 struct MlpParams {
   float b2[kHid];
@@ -190,190 +199,186 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem
   tmem_wait_st();
 }
 
-__device__ __forceinline__ void stream_barrier(int stream) {
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + stream), "n"(128) : "memory");
-}
-
 __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant__ MlpParams p) {
   extern __shared__ __align__(1024) unsigned char sm[];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
-  const int st = warp >> 2;       // tile stream (warpgroup)
-  const int quarter = warp & 3;   // TMEM lane quarter of this warp
-  const int r = tid & 127;        // tile row = TMEM lane
-  const bool leader = r == 0;
+  const bool issuer = tid >= kEpiThreads;
+  const int st = issuer ? (tid - kEpiThreads) >> 5 : warp >> 2;  // tile stream
+  const int quarter = warp & 3;                                    // TMEM lane quarter (epilogue warps)
+  const int r = tid & 127;                                         // tile row = TMEM lane (epilogue)
   unsigned char* A1 = sm + kOffStreams + st * kStreamBytes;
   float* in_tiles = reinterpret_cast<float*>(A1 + kA1Bytes);
-  uint64_t* bar_in = reinterpret_cast<uint64_t*>(sm + kOffBar) + st * 4;  // [2]
-  uint64_t* bar_l1 = bar_in + 2;   // layer-1 MMA commits
-  uint64_t* bar_mma = bar_in + 3;  // layer-2 / layer-3 MMA commits
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kOffBar + kStreams * 4 * 8);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kOffBar) + st * kBarsPerStream;
+  uint64_t* bar_in = bars;         // [2] rgb tile landed (TMA transaction count)
+  uint64_t* bar_l1 = bars + 2;     // layer-1 MMAs complete (tcgen05.commit)
+  uint64_t* bar_l2 = bars + 3;     // layer-2 MMAs complete
+  uint64_t* bar_l3 = bars + 4;     // layer-3 MMAs complete
+  uint64_t* bar_a1 = bars + 5;     // A1 tile written to smem (4 epilogue warps)
+  uint64_t* bar_a2 = bars + 6;     // A2 written to TMEM (4 epilogue warps)
+  uint64_t* bar_a3 = bars + 7;     // A3 written to TMEM (4 epilogue warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kOffBar + kStreams * kBarsPerStream * 8);
 
   for (int i = tid; i < kWBytes / 16; i += kThreads)
     reinterpret_cast<uint4*>(sm)[i] = reinterpret_cast<const uint4*>(p.wimg)[i];
-  if (leader) {
-    mbar_init(&bar_in[0], 1);
-    mbar_init(&bar_in[1], 1);
-    mbar_init(bar_l1, 1);
-    mbar_init(bar_mma, 1);
+  if (issuer && (tid & 31) == 0) {
+    for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
+    for (int i = 5; i < 8; ++i) mbar_init(&bars[i], 4);
     fence_mbar_init();
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  fence_proxy_async_smem();  // weight images are read by the tensor core (async proxy)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tcol = tmem + st * kColsPerStream;               // stream base, lane 0
-  const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+  const uint32_t tcol = tmem + st * kColsPerStream;  // stream base, lane 0
   const uint32_t tA = tcol + kColA, tD = tcol + kColD, tD3 = tcol + kColD3;
-  {
-    // Constant K chunk of the layer-2 A operand: element 64 = 1 (bias b2), 65..79 = 0.
-    // Written once; the epilogues only overwrite columns [0, 32).
-    uint32_t one[8] = {0x3F80u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(tA + 32 + lane_off),
-                 "r"(one[0]), "r"(one[1]), "r"(one[2]), "r"(one[3]), "r"(one[4]), "r"(one[5]), "r"(one[6]),
-                 "r"(one[7])
-                 : "memory");
-    tmem_wait_st();
-  }
-  const uint32_t sW1 = smem_u32(sm + kOffW1), sW2 = smem_u32(sm + kOffW2), sW3 = smem_u32(sm + kOffW3);
-  const uint32_t sA1 = smem_u32(A1);
-  constexpr uint32_t kChunkA = kMlpM * 16;  // K-chunk stride of the 128-row A1 tile
-  const uint32_t id64 = idesc_bf16(kMlpM, kHid), id16 = idesc_bf16(kMlpM, kN3);
-
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kStreams + st;
   const int64_t tstride = static_cast<int64_t>(gridDim.x) * kStreams;
-  auto load_tile = [&](int64_t t, int s) {
-    mbar_arrive_expect_tx(&bar_in[s], kInTile);
-    bulk_g2s(in_tiles + s * kMlpM * 3, p.rgb + (p.first_tile + t) * kMlpM * 3, kInTile, &bar_in[s]);
-  };
-  if (p.use_tma && leader) {
-    if (t0 < p.ntiles) load_tile(t0, 0);
-    if (t0 + tstride < p.ntiles) load_tile(t0 + tstride, 1);
-  }
-  // rgb of tile t -> (r, g, b, 1, 0 ...) bf16 row of A1 (smem), then layer 1 is issued.
-  auto prepare_input = [&](int64_t t, int it) {
-    const int s = it & 1;
-    const int64_t row0 = (p.first_tile + t) * kMlpM;
-    const int64_t left = p.P - row0;
-    float x0 = 0.f, x1 = 0.f, x2 = 0.f;
-    if (p.use_tma) {
-      mbar_wait(&bar_in[s], (it >> 1) & 1);
-      const float* in = in_tiles + s * kMlpM * 3 + r * 3;
-      x0 = in[0];
-      x1 = in[1];
-      x2 = in[2];
-    } else if (r < left) {
-      const float* in = p.rgb + (row0 + r) * 3;
-      x0 = in[0];
-      x1 = in[1];
-      x2 = in[2];
-    }
-    *reinterpret_cast<uint4*>(A1 + r * 16) = make_uint4(pack_bf16(x0, x1), pack_bf16(x2, 1.0f), 0u, 0u);
-    *reinterpret_cast<uint4*>(A1 + kChunkA + r * 16) = make_uint4(0u, 0u, 0u, 0u);
-    fence_proxy_async_smem();
-  };
-  auto issue_l1 = [&](int64_t t, int it) {  // leader only, after the stream barrier
-    if (p.use_tma && t + 2 * tstride < p.ntiles) load_tile(t + 2 * tstride, it & 1);
-    tc_fence_after();
-    mma_ss(tD, umma_desc(sA1, kChunkA, 128), umma_desc(sW1, kHid * 16, 128), id64, 0);
-    mma_commit(bar_l1);
-  };
+  constexpr uint32_t kChunkA = kMlpM * 16;  // K-chunk stride of the 128-row A1 tile
 
-  // Codes of the previous tile: layer-3 accumulators are read right after layer 3
-  // completes (16 TMEM columns), but softplus + the global stores run later, under
-  // the next tile's layer-2 MMA, off the per-tile dependency chain.
-  uint32_t prev_v[kN3];
-  int64_t prev_row0 = -1;
-  int prev_rows = 0;
-  const int k = p.k;
-  auto store_codes = [&]() {
-    if (prev_row0 < 0 || r >= prev_rows) return;
-    float* o = p.out + (prev_row0 + r) * k;
-    if (k == 6) {
-      float y[6];
+  if (issuer) {
+    // ------------------------------------------------------------ MMA-issuer warp
+    if ((tid & 31) == 0) {
+      const uint32_t sW1 = smem_u32(sm + kOffW1), sW2 = smem_u32(sm + kOffW2), sW3 = smem_u32(sm + kOffW3);
+      const uint32_t sA1 = smem_u32(A1);
+      const uint32_t id64 = idesc_bf16(kMlpM, kHid), id16 = idesc_bf16(kMlpM, kN3);
+      auto load_tile = [&](int64_t t, int s) {
+        mbar_arrive_expect_tx(&bar_in[s], kInTile);
+        bulk_g2s(in_tiles + s * kMlpM * 3, p.rgb + (p.first_tile + t) * kMlpM * 3, kInTile, &bar_in[s]);
+      };
+      if (p.use_tma) {
+        if (t0 < p.ntiles) load_tile(t0, 0);
+        if (t0 + tstride < p.ntiles) load_tile(t0 + tstride, 1);
+      }
+      int iter = 0;
+      for (int64_t t = t0; t < p.ntiles; t += tstride, ++iter) {
+        const uint32_t ph = iter & 1;
+        mbar_wait(bar_a1, ph);  // A1(t) in smem; rgb slot (iter & 1) consumed
+        tc_fence_after();
+        if (p.use_tma && t + 2 * tstride < p.ntiles) load_tile(t + 2 * tstride, iter & 1);
+        mma_ss(tD, umma_desc(sA1, kChunkA, 128), umma_desc(sW1, kHid * 16, 128), id64, 0);
+        mma_commit(bar_l1);
+        mbar_wait(bar_a2, ph);  // A2(t) in TMEM, D read out
+        tc_fence_after();
 #pragma unroll
-      for (int j = 0; j < 6; ++j) y[j] = softplus1(__uint_as_float(prev_v[j]) + p.b3[j]);
-      reinterpret_cast<float2*>(o)[0] = make_float2(y[0], y[1]);
-      reinterpret_cast<float2*>(o)[1] = make_float2(y[2], y[3]);
-      reinterpret_cast<float2*>(o)[2] = make_float2(y[4], y[5]);
-    } else {
+        for (int kk = 0; kk < kK2 / 16; ++kk)
+          mma_ts(tD, tA + kk * 8, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128), id64, kk > 0);
+        mma_commit(bar_l2);
+        mbar_wait(bar_a3, ph);  // A3(t) in TMEM, D read out; D3(t - 1) read out
+        tc_fence_after();
 #pragma unroll
-      for (int j = 0; j < kMaxK; ++j)
-        if (j < k) o[j] = softplus1(__uint_as_float(prev_v[j]) + p.b3[j]);
+        for (int kk = 0; kk < kK3 / 16; ++kk)
+          mma_ts(tD3, tA + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
+        mma_commit(bar_l3);
+      }
     }
-  };
+  } else {
+    // ------------------------------------------------------------ epilogue warps
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    {
+      // Constant K chunk of the layer-2 A operand: element 64 = 1 (bias b2), 65..79 = 0.
+      // Written once; the epilogues only overwrite columns [0, 32).
+      uint32_t one[8] = {0x3F80u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(tA + 32 + lane_off),
+                   "r"(one[0]), "r"(one[1]), "r"(one[2]), "r"(one[3]), "r"(one[4]), "r"(one[5]), "r"(one[6]),
+                   "r"(one[7])
+                   : "memory");
+      tmem_wait_st();
+    }
+    // rgb of tile t -> (r, g, b, 1, 0 ...) bf16 row of A1 (smem), then one arrival per warp on a1.
+    auto prepare_input = [&](int64_t t, int it) {
+      const int s = it & 1;
+      const int64_t row0 = (p.first_tile + t) * kMlpM;
+      const int64_t left = p.P - row0;
+      float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+      if (p.use_tma) {
+        mbar_wait(&bar_in[s], (it >> 1) & 1);
+        const float* in = in_tiles + s * kMlpM * 3 + r * 3;
+        x0 = in[0];
+        x1 = in[1];
+        x2 = in[2];
+      } else if (r < left) {
+        const float* in = p.rgb + (row0 + r) * 3;
+        x0 = in[0];
+        x1 = in[1];
+        x2 = in[2];
+      }
+      *reinterpret_cast<uint4*>(A1 + r * 16) = make_uint4(pack_bf16(x0, x1), pack_bf16(x2, 1.0f), 0u, 0u);
+      *reinterpret_cast<uint4*>(A1 + kChunkA + r * 16) = make_uint4(0u, 0u, 0u, 0u);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(bar_a1);
+    };
+    // Codes of the previous tile: the layer-3 accumulator is read right after layer 3
+    // completes, softplus + the global stores run later, under the next tile's MMAs.
+    uint32_t prev_v[kN3];
+    int64_t prev_row0 = -1;
+    int prev_rows = 0;
+    const int k = p.k;
+    auto store_codes = [&]() {
+      if (prev_row0 < 0 || r >= prev_rows) return;
+      float* o = p.out + (prev_row0 + r) * k;
+      if (k == 6) {
+        float y[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) y[j] = softplus1(__uint_as_float(prev_v[j]) + p.b3[j]);
+        reinterpret_cast<float2*>(o)[0] = make_float2(y[0], y[1]);
+        reinterpret_cast<float2*>(o)[1] = make_float2(y[2], y[3]);
+        reinterpret_cast<float2*>(o)[2] = make_float2(y[4], y[5]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j)
+          if (j < k) o[j] = softplus1(__uint_as_float(prev_v[j]) + p.b3[j]);
+      }
+    };
+    auto handoff = [&](uint64_t* bar) {  // TMEM stores of this warp done -> issuer
+      tc_fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(bar);
+    };
 
-  uint32_t l1_phase = 0, mma_phase = 0;
-  if (t0 < p.ntiles) {
-    prepare_input(t0, 0);
-    tc_fence_before();
-    stream_barrier(st);
-    if (leader) issue_l1(t0, 0);
-  }
-  int iter = 0;
-  for (int64_t t = t0; t < p.ntiles; t += tstride, ++iter) {
-    const int64_t row0 = (p.first_tile + t) * kMlpM;
-    const int64_t left = p.P - row0;
-    const int rows = left < kMlpM ? static_cast<int>(left) : kMlpM;
-    long long* tr = (p.trace && blockIdx.x == 0 && r == 0 && iter < 32) ? p.trace + (st * 32 + iter) * 8 : nullptr;
-    if (tr) tr[0] = clock64();
-    // ---- layer 1 done -> relu -> A2 (TMEM)
-    mbar_wait(bar_l1, l1_phase);
-    l1_phase ^= 1;
-    if (tr) tr[1] = clock64();
-    tc_fence_after();
-    epilogue_hidden<false>(tD + lane_off, tA + lane_off, nullptr);
-    tc_fence_before();
-    stream_barrier(st);
-    if (tr) tr[2] = clock64();
-    if (leader) {
+    if (t0 < p.ntiles) prepare_input(t0, 0);
+    int iter = 0;
+    for (int64_t t = t0; t < p.ntiles; t += tstride, ++iter) {
+      const uint32_t ph = iter & 1;
+      const int64_t row0 = (p.first_tile + t) * kMlpM;
+      const int64_t left = p.P - row0;
+      const int rows = left < kMlpM ? static_cast<int>(left) : kMlpM;
+      long long* tr = (p.trace && blockIdx.x == 0 && r == 0 && iter < 32) ? p.trace + (st * 32 + iter) * 8 : nullptr;
+      if (tr) tr[0] = clock64();
+      mbar_wait(bar_l1, ph);
+      if (tr) tr[1] = clock64();
       tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < kK2 / 16; ++kk)
-        mma_ts(tD, tA + kk * 8, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128), id64, kk > 0);
-      mma_commit(bar_mma);
+      epilogue_hidden<false>(tD + lane_off, tA + lane_off, nullptr);
+      handoff(bar_a2);
+      if (tr) tr[2] = clock64();
+      const int64_t tn = t + tstride;
+      if (tn < p.ntiles) prepare_input(tn, iter + 1);  // A1 is free: layer 1 of tile t is done
+      store_codes();  // previous tile's softplus + stores, under this tile's layer-2 MMAs
+      if (tr) tr[3] = clock64();
+      mbar_wait(bar_l2, ph);
+      if (tr) tr[4] = clock64();
+      tc_fence_after();
+      epilogue_hidden<false>(tD + lane_off, tA + lane_off, nullptr);
+      handoff(bar_a3);
+      if (tr) tr[5] = clock64();
+      mbar_wait(bar_l3, ph);
+      if (tr) tr[6] = clock64();
+      tc_fence_after();
+      HC_TMEM_LD16(tD3 + lane_off, prev_v);
+      tmem_wait_ld();
+      prev_row0 = row0;
+      prev_rows = rows;
+      if (tr) tr[7] = clock64();
     }
-    // ---- under layer 2: the next tile's A1 (smem is free: layer 1 of this tile is
-    // done) and the previous tile's codes
-    const int64_t tn = t + tstride;
-    if (tn < p.ntiles) prepare_input(tn, iter + 1);
     store_codes();
-    if (tr) tr[3] = clock64();
-    // ---- layer 2 done -> relu(acc + b2) -> A3 (TMEM, over A2)
-    mbar_wait(bar_mma, mma_phase);
-    mma_phase ^= 1;
-    if (tr) tr[4] = clock64();
-    tc_fence_after();
-    epilogue_hidden<false>(tD + lane_off, tA + lane_off, nullptr);
-    tc_fence_before();
-    stream_barrier(st);
-    if (tr) tr[5] = clock64();
-    if (leader) {
-      tc_fence_after();
-#pragma unroll
-      for (int kk = 0; kk < kK3 / 16; ++kk)
-        mma_ts(tD3, tA + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
-      mma_commit(bar_mma);
-      // next tile's layer 1 into the layer-1/2 accumulator, read out above (epi2)
-      if (tn < p.ntiles) issue_l1(tn, iter + 1);
-    }
-    // ---- layer 3 done -> keep the 16 accumulator columns for store_codes()
-    mbar_wait(bar_mma, mma_phase);
-    mma_phase ^= 1;
-    if (tr) tr[6] = clock64();
-    tc_fence_after();
-    HC_TMEM_LD16(tD3 + lane_off, prev_v);
-    tmem_wait_ld();
-    tc_fence_before();
-    prev_row0 = row0;
-    prev_rows = rows;
-    if (tr) tr[7] = clock64();
   }
-  store_codes();
   tc_fence_before();
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
@@ -504,7 +509,7 @@ int hc_mlp_forward(hc_mlp m, const float* rgb, int64_t P, float* codes) {
           ++n;
         }
       if (n)
-        std::fprintf(stderr, "[hc] mlp phase cycles (avg of %d tiles): L1wait %.0f epi1 %.0f L2issue %.0f in+store %.0f L2wait %.0f epi2 %.0f L3wait %.0f ldD3 %.0f\n",
+        std::fprintf(stderr, "[hc] mlp phase cycles (avg of %d tiles): L1wait %.0f epi1 %.0f nextA1+codes %.0f L2wait %.0f epi2 %.0f L3wait %.0f ldD3 %.0f loop %.0f\n",
                      n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n, acc[6] / n, acc[7] / n);
     }
   }

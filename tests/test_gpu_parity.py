@@ -384,29 +384,41 @@ def test_hadamard_loss_golden(api, ctx, golden):
 
 
 # ----------------------------------------------------------------- MLP (config 5a)
-def _mlp_or_skip(api, ctx, w):
-    from paper_2602_18741_b200._lib import HcError
-
-    try:
-        return api.Upsampler(ctx, w)
-    except HcError as e:
-        pytest.skip(f"MLP kernel not available: {e}")
-
-
-@pytest.mark.parametrize("P", [40, 128 * 148 + 77])
-def test_mlp_vs_oracle(api, ctx, orc, P):
-    w = synth.mlp_weights(SEED, 6, 64)
-    mlp = _mlp_or_skip(api, ctx, w)
+@pytest.mark.parametrize("k,P", [(6, 40), (6, 128 * 148 + 77), (6, 128 * 148 * 4 * 3 + 5), (9, 128 * 600),
+                                 (3, 1), (9, 1000)])
+def test_mlp_vs_oracle(api, ctx, orc, k, P):
+    """Multiple tiles per stream, ragged tails (generic path), k in {3, 6, 9}."""
+    w = synth.mlp_weights(SEED, k, 64)
+    mlp = api.Upsampler(ctx, w)
     rgb = api.synth_uniform(ctx, SEED, "mlp.input", 0, P * 3).reshape(P, 3)
+    got = host(mlp.forward(rgb))
+    ref = np.zeros((P, k), np.float32)
+    orc.orc_mlp_forward(host(rgb), P, 64, k, w["w1"], w["b1"], w["w2"], w["b2"], w["w3"], w["b3"], ref)
+    _check(f"mlp k={k} P={P}", got, ref, MLP_TOL)
+    assert np.all(got >= 0)
+
+
+def test_mlp_unaligned_input_and_repeat(api, ctx, orc):
+    """rgb base not 16-byte aligned (no bulk copies), and two calls give identical codes."""
+    w = synth.mlp_weights(SEED, 6, 64)
+    mlp = api.Upsampler(ctx, w)
+    P = 128 * 300 + 3
+    buf = api.synth_uniform(ctx, SEED, "mlp.input", 0, P * 3 + 1)
+    rgb = buf[1:].reshape(P, 3)
+    assert rgb.data_ptr() % 16 != 0
     got = host(mlp.forward(rgb))
     ref = np.zeros((P, 6), np.float32)
     orc.orc_mlp_forward(host(rgb), P, 64, 6, w["w1"], w["b1"], w["w2"], w["b2"], w["w3"], w["b3"], ref)
-    _check(f"mlp P={P}", got, ref, MLP_TOL)
-    assert np.all(got >= 0)
+    _check("mlp unaligned", got, ref, MLP_TOL)
+    rgb2 = torch.empty(P, 3, device="cuda")
+    rgb2.copy_(rgb)
+    a, b = host(mlp.forward(rgb2)), host(mlp.forward(rgb2))
+    assert np.array_equal(a, b)
+    assert np.array_equal(a, got)
 
 
 def test_mlp_golden(api, ctx, golden):
     w = {k: golden[f"c5_{k}"] for k in ("w1", "b1", "w2", "b2", "w3", "b3")}
-    mlp = _mlp_or_skip(api, ctx, w)
+    mlp = api.Upsampler(ctx, w)
     got = host(mlp.forward(torch.from_numpy(np.ascontiguousarray(golden["c5_rgb"])).cuda()))
     _check("golden mlp", got, golden["c5_codes"], MLP_TOL)
