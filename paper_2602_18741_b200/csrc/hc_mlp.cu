@@ -161,14 +161,16 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return d;
 }
 
-// softplus(x) = max(x, 0) + log1p(exp(-|x|)) (codec.cpp:8-12, beta = 1), branch-free:
-// for x > 30 the log1p term is < 1e-13 and vanishes in fp32, which is exactly the
-// reference's identity branch; log1p uses its series below 2^-10 (lg2(1 + e) loses
-// relative precision there).
+// softplus(x) = max(x, 0) + ln2 * log2(1 + 2^(-|x| log2 e)) (codec.cpp:8-12, beta = 1) in
+// six instructions (two MUFU): for x > 30 the log term is < 1e-13 and vanishes in fp32,
+// which is the reference's identity branch; for very negative x the result is the tiny
+// e = exp(x) with an absolute error ~1e-7 (ex2 / lg2.approx: 2^-22), far inside the bf16
+// MLP tolerance, which is relative to the row's largest code.
 __device__ __forceinline__ float softplus1(float x) {
-  const float e = exp2f(-fabsf(x) * 1.4426950408889634f);
-  const float l = e < 0.0009765625f ? e * fmaf(-0.5f, e, 1.f) : __log2f(1.f + e) * 0.6931471805599453f;
-  return fmaxf(x, 0.f) + l;
+  float e, l;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-fabsf(x) * 1.4426950408889634f));
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(1.f + e));
+  return fmaf(l, 0.6931471805599453f, fmaxf(x, 0.f));
 }
 
 // Hidden-layer epilogue: fp32 accumulator row (64 TMEM columns of this thread's
