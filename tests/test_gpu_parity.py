@@ -200,15 +200,17 @@ def _scene(api, ctx, k, L, n=81):
     return codec, E, D, pal, lts, pal_d, pal_codes, light_codes
 
 
-@pytest.mark.parametrize("k,L,P,spec", [(6, 8, 50_003, False), (6, 8, 4096, True), (9, 32, 20_011, True),
-                                        (9, 32, 777, False), (3, 8, 1000, True), (6, 5, 3001, True),
-                                        (9, 1, 1000, False), (6, 64, 513, True)])
-def test_shade_latent_vs_oracle(api, ctx, orc, k, L, P, spec):
-    codec, E, D, pal, lts, pal_d, pal_codes, light_codes = _scene(api, ctx, k, L)
+@pytest.mark.parametrize("k,L,P,spec,n", [(6, 8, 50_003, False, 81), (6, 8, 4096, True, 81),
+                                          (9, 32, 20_011, True, 81), (9, 32, 777, False, 81), (3, 8, 1000, True, 81),
+                                          (6, 5, 3001, True, 81), (9, 1, 1000, False, 81), (6, 64, 513, True, 81),
+                                          (6, 8, 5000, True, 47), (9, 32, 3001, False, 47), (3, 8, 777, True, 47),
+                                          (9, 13, 2000, True, 47)])
+def test_shade_latent_vs_oracle(api, ctx, orc, k, L, P, spec, n):
+    codec, E, D, pal, lts, pal_d, pal_codes, light_codes = _scene(api, ctx, k, L, n)
     idx, cosv = api.synth_gbuffer(ctx, SEED, 0, P, L, 256)
     out = codec.shade_latent(pal_codes, light_codes, idx, cosv, latent=True, spectra=spec)
-    ref = [np.zeros((P, d), np.float32) for d in (k, 81, 3, 3)]
-    orc.orc_shade_latent(D, k, 81, cmf_matrix(81), grid(81)[1], host(pal_codes), light_codes, L,
+    ref = [np.zeros((P, d), np.float32) for d in (k, n, 3, 3)]
+    orc.orc_shade_latent(D, k, n, cmf_matrix(n), grid(n)[1], host(pal_codes), light_codes, L,
                          host(idx).view(np.uint32), host(cosv), P, *ref)
     _check(f"latent k={k} L={L}", host(out["latent"]), ref[0])
     if spec:
@@ -274,14 +276,15 @@ def test_multipass_equals_fused(api, ctx, k, L):
     assert np.array_equal(host(multi), host(fused))
 
 
-@pytest.mark.parametrize("L,P,spec", [(8, 30_001, False), (32, 5000, True), (8, 2048, True), (3, 1001, True),
-                                      (17, 999, False)])
-def test_shade_spectral_vs_oracle(api, ctx, orc, L, P, spec):
-    codec, E, D, pal, lts, pal_d, _, _ = _scene(api, ctx, 6, L)
+@pytest.mark.parametrize("L,P,spec,n", [(8, 30_001, False, 81), (32, 5000, True, 81), (8, 2048, True, 81),
+                                        (3, 1001, True, 81), (17, 999, False, 81), (8, 4099, True, 47),
+                                        (32, 1000, False, 47)])
+def test_shade_spectral_vs_oracle(api, ctx, orc, L, P, spec, n):
+    codec, E, D, pal, lts, pal_d, _, _ = _scene(api, ctx, 6, L, n)
     idx, cosv = api.synth_gbuffer(ctx, SEED, 3, P, L, 256)
     out = codec.shade_spectral(pal_d, lts, idx, cosv, spectra=spec)
-    ref = [np.zeros((P, d), np.float32) for d in (81, 3, 3)]
-    orc.orc_shade_spectral(81, cmf_matrix(81), grid(81)[1], pal, lts, L, host(idx).view(np.uint32), host(cosv), P,
+    ref = [np.zeros((P, d), np.float32) for d in (n, 3, 3)]
+    orc.orc_shade_spectral(n, cmf_matrix(n), grid(n)[1], pal, lts, L, host(idx).view(np.uint32), host(cosv), P,
                            *ref)
     if spec:
         _check(f"naive spectra L={L}", host(out["spectra"]), ref[0])
@@ -322,29 +325,29 @@ def test_empty_inputs(api, ctx):
 
 
 # ----------------------------------------------------------------- multi-bounce (config 4)
-@pytest.mark.parametrize("spp", [64, 8])
-def test_multibounce_vs_oracle(api, ctx, orc, spp):
-    codec, E, D, pal, _, pal_d, pal_codes, _ = _scene(api, ctx, 6, 8)
-    ill = synth.lights(SEED, 16, 81, purpose="scene.illuminants")
+@pytest.mark.parametrize("spp,k,n", [(64, 6, 81), (8, 6, 81), (16, 9, 81), (32, 3, 81), (8, 3, 47), (64, 6, 47)])
+def test_multibounce_vs_oracle(api, ctx, orc, spp, k, n):
+    codec, E, D, pal, _, pal_d, pal_codes, _ = _scene(api, ctx, k, 8, n)
+    ill = synth.lights(SEED, 16, n, purpose="scene.illuminants")
     ill_d = torch.from_numpy(ill).cuda()
     ill_codes = codec.encode(ill_d)
     P = 1237
     pidx, iidx, tw = api.synth_chain(ctx, SEED, 0, P, spp, 256, 16)
     out = codec.multibounce_latent(pal_codes, ill_codes, pidx, iidx, tw, latent=True)
     ph, ih, th = host(pidx), host(iidx), host(tw)
-    lat = np.zeros((P, 6), np.float32)
-    orc.orc_chain(6, host(pal_codes), host(ill_codes), ph, ih, th, P, spp, 4, lat)
+    lat = np.zeros((P, k), np.float32)
+    orc.orc_chain(k, host(pal_codes), host(ill_codes), ph, ih, th, P, spp, 4, lat)
     _check("chain latent", host(out["latent"]), lat)
-    S2 = np.zeros((P, 81), np.float32)
+    S2 = np.zeros((P, n), np.float32)
     X, R = np.zeros((P, 3), np.float32), np.zeros((P, 3), np.float32)
-    orc.orc_decode(D, 6, 81, lat, P, S2)
-    orc.orc_spectra_to_outputs(cmf_matrix(81), grid(81)[1], 81, S2, P, X, R)
+    orc.orc_decode(D, k, n, lat, P, S2)
+    orc.orc_spectra_to_outputs(cmf_matrix(n), grid(n)[1], n, S2, P, X, R)
     _check("chain xyz", host(out["xyz"]), X)
     _check("chain rgb", host(out["rgb"]), R)
     nv = codec.multibounce_spectral(pal_d, ill_d, pidx, iidx, tw)
-    spec = np.zeros((P, 81), np.float32)
-    orc.orc_chain(81, pal, ill, ph, ih, th, P, spp, 4, spec)
-    orc.orc_spectra_to_outputs(cmf_matrix(81), grid(81)[1], 81, spec, P, X, R)
+    spec = np.zeros((P, n), np.float32)
+    orc.orc_chain(n, pal, ill, ph, ih, th, P, spp, 4, spec)
+    orc.orc_spectra_to_outputs(cmf_matrix(n), grid(n)[1], n, spec, P, X, R)
     _check("chain naive xyz", host(nv["xyz"]), X)
     _check("chain naive rgb", host(nv["rgb"]), R)
 
@@ -365,13 +368,14 @@ def test_multibounce_golden(api, ctx, golden):
 
 
 # ----------------------------------------------------------------- loss (config 5b)
-@pytest.mark.parametrize("pairs", [29, 100_003])
-def test_hadamard_loss_vs_oracle(api, ctx, orc, pairs):
-    codec, E, D = _codec(api, ctx, 6)
-    A = api.synth_gm_spectra(ctx, SEED, "loss.a", 0, pairs, 81)
-    B = api.synth_gm_spectra(ctx, SEED, "loss.b", 0, pairs, 81)
+@pytest.mark.parametrize("pairs,k,n", [(29, 6, 81), (100_003, 6, 81), (70_001, 9, 81), (5000, 3, 81),
+                                       (64 * 296 * 3, 6, 47), (1001, 9, 47)])
+def test_hadamard_loss_vs_oracle(api, ctx, orc, pairs, k, n):
+    codec, E, D = _codec(api, ctx, k, n)
+    A = api.synth_gm_spectra(ctx, SEED, "loss.a", 0, pairs, n)
+    B = api.synth_gm_spectra(ctx, SEED, "loss.b", 0, pairs, n)
     got = float(host(codec.hadamard_loss(A, B))[0])
-    want = orc.orc_hadamard_loss(E, D, 6, 81, host(A), host(B), pairs)
+    want = orc.orc_hadamard_loss(E, D, k, n, host(A), host(B), pairs)
     print(f"loss pairs={pairs}: got={got!r} want={want!r} rel={abs(got - want) / abs(want):.2e}")
     assert got == pytest.approx(want, rel=TOL)
 
