@@ -152,6 +152,41 @@ int hc_mlp_forward(hc_mlp mlp, const float* rgb, int64_t P, float* codes);
  * of (D (E a (.) E b) - a (.) b)^2 into *sum_dev (one f64 on the device). */
 int hc_hadamard_loss(hc_codec codec, const float* A, const float* B, int64_t pairs, double* sum_dev);
 
+/* ------------------------------------------------------------------ colour-metric tail
+ * Consumers of the shading output.  Images are P pixels x
+ * `channels` floats on the device, channels = 3 (linear sRGB) or the codec's n
+ * (spectra, converted with image_to_linear_rgb in fp64).  Percentiles are exact
+ * nearest-rank order statistics (evaluation.cpp:14-21).  Calls returning values
+ * through host pointers synchronise the context stream. */
+
+/* exposure_for (renderer.cpp:721-752; renderer.hpp:119, default percentile 99.5):
+ * 1 / (percentile of per-pixel luminance), 1 when that is <= 1e-12.  Luminance =
+ * Rec.709 luma of linear RGB, or dlambda * ybar . s of spectra. */
+int hc_exposure_for(hc_codec codec, const float* img, int64_t P, int channels, double percentile,
+                    double* exposure);
+/* tonemap_srgb8 (renderer.cpp:754-773): out[3P] = uchar(srgb_encode(clamp(rgb * exposure, 0, 1))
+ * * 255 + 0.5).  Asynchronous. */
+int hc_tonemap_srgb8(hc_ctx ctx, const float* rgb, int64_t P, double exposure, uint8_t* out);
+/* error_map (renderer.cpp:775-802): mse[P] (may be NULL) = mean over channels of the squared
+ * linear-RGB difference, *mean_mse (host) = its mean. */
+int hc_error_map(hc_codec codec, const float* a, int channels_a, const float* b, int channels_b, int64_t P,
+                 float* mse, double* mean_mse);
+/* scene_color_report (evaluation.cpp:122-154): out4 (host) = {mean_de76, p95_de76, mse, exposure},
+ * Delta E76 in Lab under the sRGB white with the ground truth's exposure applied to both. */
+int hc_scene_color_report(hc_codec codec, const float* gt, int channels_gt, const float* test,
+                          int channels_test, int64_t P, double* out4);
+/* Stream-ordered form (no synchronisation, capturable in a CUDA graph): out4_dev is device
+ * memory; test_srgb8 (may be NULL) additionally receives tonemap_srgb8(test, exposure_for(gt))
+ * from the same pass, as run_report writes next to the report (tools/main.cpp:604-623). */
+int hc_scene_color_report_dev(hc_codec codec, const float* gt, int channels_gt, const float* test,
+                              int channels_test, int64_t P, double* out4_dev, uint8_t* test_srgb8);
+/* Per-pixel Delta E94 of multibounce_eval (evaluation.cpp:59-86): Lab of both XYZ images under
+ * white_xyz (host, 3 doubles; CmfTable::white_xyz) scaled to the ground truth's max(Y, 1e-6).
+ * out3 (host) = {mean, median, p95}; de[P] (may be NULL) per pixel.  HC_EDOMAIN for a
+ * non-positive white (xyz_to_lab, colorimetry.cpp:119-123). */
+int hc_delta_e94_report(hc_ctx ctx, const float* xyz_gt, const float* xyz_test, int64_t P,
+                        const double* white_xyz, float* de, double* out3);
+
 /* ------------------------------------------------------------------ host-buffer entry points
  * Reference-facing value calls: inputs and outputs in HOST memory (pinned for
  * full copy speed), copies and compute on the context stream, synchronised on

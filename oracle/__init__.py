@@ -88,6 +88,19 @@ _ORACLE_SIGS = {
     "orc_mlp_forward": (None, [_f32p, C.c_int64, C.c_int, C.c_int, _f32p, _f32p, _f32p, _f32p, _f32p,
                                _f32p, _f32p]),
     "orc_hadamard_loss": (C.c_double, [_f32p, _f32p, C.c_int, C.c_int, _f32p, _f32p, C.c_int64]),
+    # colour-metric tail
+    "orc_percentile_nearest_rank": (C.c_double, [_f64p, C.c_int64, C.c_double]),
+    "orc_luminance": (None, [_f32p, C.c_int64, C.c_int, _f64n, C.c_double, _f64p]),
+    "orc_exposure_for": (C.c_double, [_f32p, C.c_int64, C.c_int, _f64n, C.c_double, C.c_double]),
+    "orc_srgb_encode": (C.c_double, [C.c_double]),
+    "orc_tonemap_srgb8": (None, [_f32p, C.c_int64, C.c_double, _u8p]),
+    "orc_image_to_linear_rgb": (None, [_f32p, C.c_int64, C.c_int, _f64p, C.c_double, _f32p]),
+    "orc_error_map": (C.c_double, [_f32p, C.c_int, _f32p, C.c_int, C.c_int64, _f64p, C.c_double, _f32n]),
+    "orc_xyz_to_lab": (None, [_f64p, _f64p, _f64p]),
+    "orc_delta_e76": (C.c_double, [_f64p, _f64p]),
+    "orc_delta_e94": (C.c_double, [_f64p, _f64p]),
+    "orc_scene_color_report": (None, [_f32p, C.c_int, _f32p, C.c_int, C.c_int64, _f64p, C.c_double, _f64p]),
+    "orc_delta_e94_report": (None, [_f32p, _f32p, C.c_int64, _f64p, _f32n, _f64p]),
 }
 
 _REF_SIGS = {
@@ -124,6 +137,16 @@ _REF_SIGS = {
                                _f32p, C.c_int]),
     "ref_hadamard_loss": (C.c_double, [_f32p, _f32p, C.c_int, _f32p, _f32p, C.c_int64, C.c_int]),
     "ref_thread_count": (C.c_int, []),
+    # colour-metric tail
+    "ref_exposure_for": (C.c_double, [_f32p, C.c_int64, C.c_int, C.c_double]),
+    "ref_tonemap_srgb8": (None, [_f32p, C.c_int64, C.c_double, _u8p]),
+    "ref_error_map": (C.c_double, [_f32p, C.c_int, _f32p, C.c_int, C.c_int64, _f32n]),
+    "ref_scene_color_report": (None, [_f32p, C.c_int, _f32p, C.c_int, C.c_int64, _f64p]),
+    "ref_xyz_to_lab": (None, [_f64p, _f64p, _f64p]),
+    "ref_delta_e76": (C.c_double, [_f64p, _f64p]),
+    "ref_delta_e94": (C.c_double, [_f64p, _f64p]),
+    "ref_srgb_encode": (C.c_double, [C.c_double]),
+    "ref_delta_e94_report": (None, [_f32p, _f32p, C.c_int64, _f32n, _f64p]),
 }
 
 _oracle = None

@@ -279,3 +279,232 @@ void orc_spectrum_to_xyz_d(const double* cmf, double dlambda, int n, const doubl
   xyz[1] = y * dlambda;
   xyz[2] = z * dlambda;
 }
+
+/* ===================================================================== colour-metric tail
+ * the reference's consumers of the hot path's output —
+ * exposure_for / tonemap_srgb8 / error_map (renderer.cpp:721-802),
+ * scene_color_report (evaluation.cpp:122-154) and the per-chain Delta E94 of
+ * multibounce_eval (evaluation.cpp:59-86) — over pixel arrays instead of
+ * ChannelImage (P = width * height pixels, HWC). */
+
+/* IEC 61966-2-1 linear sRGB -> XYZ (colorimetry.cpp:27-31). */
+static const double kRgbToXyz[9] = {
+    0.4124564, 0.3575761, 0.1804375,
+    0.2126729, 0.7151522, 0.0721750,
+    0.0193339, 0.1191920, 0.9503041,
+};
+
+static int cmp_double(const void* a, const void* b) {
+  const double x = *(const double*)a, y = *(const double*)b;
+  return (x > y) - (x < y);
+}
+
+/* percentile_nearest_rank (evaluation.cpp:14-21); the same index rule as exposure_for
+ * (renderer.cpp:744-747).  Sorts a copy. */
+double orc_percentile_nearest_rank(const double* v, int64_t count, double p) {
+  if (count <= 0) return 0.0;
+  double* s = (double*)malloc(sizeof(double) * (size_t)count);
+  if (!s) abort();
+  memcpy(s, v, sizeof(double) * (size_t)count);
+  qsort(s, (size_t)count, sizeof(double), cmp_double);
+  const double rank = p / 100.0 * (double)count;
+  int64_t idx = (int64_t)ceil(rank);
+  idx = idx == 0 ? 0 : idx - 1;
+  if (idx > count - 1) idx = count - 1;
+  const double r = s[idx];
+  free(s);
+  return r;
+}
+
+/* Per-pixel luminance of exposure_for (renderer.cpp:730-742): Rec.709 luma of linear RGB
+ * (3 channels) or dlambda * sum_i ybar_i s_i (n channels). */
+void orc_luminance(const float* img, int64_t P, int channels, const double* ybar, double dlambda,
+                   double* lum) {
+  for (int64_t p = 0; p < P; ++p) {
+    const float* px = img + p * channels;
+    double v = 0.0;
+    if (channels == 3) {
+      v = 0.2126 * (double)px[0] + 0.7152 * (double)px[1] + 0.0722 * (double)px[2];
+    } else {
+      for (int i = 0; i < channels; ++i) v += ybar[i] * (double)px[i];
+      v *= dlambda;
+    }
+    lum[p] = v;
+  }
+}
+
+/* exposure_for (renderer.cpp:721-752): 1 / nearest-rank percentile of the luminance. */
+double orc_exposure_for(const float* img, int64_t P, int channels, const double* ybar, double dlambda,
+                        double percentile) {
+  double* lum = (double*)malloc(sizeof(double) * (size_t)(P > 0 ? P : 1));
+  if (!lum) abort();
+  orc_luminance(img, P, channels, ybar, dlambda, lum);
+  const double ref = orc_percentile_nearest_rank(lum, P, percentile);
+  free(lum);
+  return ref > 1e-12 ? 1.0 / ref : 1.0;
+}
+
+/* srgb_encode (colorimetry.cpp:159-162). */
+double orc_srgb_encode(double linear) {
+  if (linear <= 0.0031308) return 12.92 * linear;
+  return 1.055 * pow(linear, 1.0 / 2.4) - 0.055;
+}
+
+/* tonemap_srgb8 (renderer.cpp:754-773). */
+void orc_tonemap_srgb8(const float* rgb, int64_t P, double exposure, uint8_t* out) {
+  for (int64_t i = 0; i < P * 3; ++i) {
+    double v = (double)rgb[i] * exposure;
+    v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
+    out[i] = (uint8_t)(orc_srgb_encode(v) * 255.0 + 0.5);
+  }
+}
+
+/* image_to_linear_rgb (renderer.cpp:692-719): identity for 3 channels, else
+ * spectrum_to_xyz (colorimetry.cpp:75-87) + xyz_to_linear_rgb (:103-105) in double. */
+void orc_image_to_linear_rgb(const float* img, int64_t P, int channels, const double* cmf, double dlambda,
+                             float* rgb) {
+  for (int64_t p = 0; p < P; ++p) {
+    const float* px = img + p * channels;
+    if (channels == 3) {
+      rgb[p * 3] = px[0];
+      rgb[p * 3 + 1] = px[1];
+      rgb[p * 3 + 2] = px[2];
+      continue;
+    }
+    double x = 0, y = 0, z = 0;
+    for (int i = 0; i < channels; ++i) {
+      x += cmf[i] * (double)px[i];
+      y += cmf[channels + i] * (double)px[i];
+      z += cmf[2 * channels + i] * (double)px[i];
+    }
+    const double xyz[3] = {x * dlambda, y * dlambda, z * dlambda};
+    for (int r = 0; r < 3; ++r)
+      rgb[p * 3 + r] = (float)(kXyzToRgb[3 * r] * xyz[0] + kXyzToRgb[3 * r + 1] * xyz[1] +
+                               kXyzToRgb[3 * r + 2] * xyz[2]);
+  }
+}
+
+/* error_map (renderer.cpp:775-802): per-pixel mean of squared linear-RGB differences
+ * (float), returns the mean over pixels (double).  mse may be NULL. */
+double orc_error_map(const float* a, int ca, const float* b, int cb, int64_t P, const double* cmf,
+                     double dlambda, float* mse) {
+  float* ra = (float*)malloc(sizeof(float) * (size_t)(P > 0 ? P : 1) * 3);
+  float* rb = (float*)malloc(sizeof(float) * (size_t)(P > 0 ? P : 1) * 3);
+  if (!ra || !rb) abort();
+  orc_image_to_linear_rgb(a, P, ca, cmf, dlambda, ra);
+  orc_image_to_linear_rgb(b, P, cb, cmf, dlambda, rb);
+  double total = 0.0;
+  for (int64_t p = 0; p < P; ++p) {
+    double acc = 0.0;
+    for (int c = 0; c < 3; ++c) {
+      const double d = (double)ra[p * 3 + c] - (double)rb[p * 3 + c];
+      acc += d * d;
+    }
+    acc /= 3.0;
+    if (mse) mse[p] = (float)acc;
+    total += acc;
+  }
+  free(ra);
+  free(rb);
+  return total / (double)P;
+}
+
+/* xyz_to_lab (colorimetry.cpp:118-135). */
+void orc_xyz_to_lab(const double* xyz, const double* white, double* lab) {
+  const double delta = 6.0 / 29.0;
+  const double delta3 = delta * delta * delta;
+  double f[3];
+  for (int i = 0; i < 3; ++i) {
+    const double t = xyz[i] / white[i];
+    f[i] = t > delta3 ? cbrt(t) : t / (3.0 * delta * delta) + 4.0 / 29.0;
+  }
+  lab[0] = 116.0 * f[1] - 16.0;
+  lab[1] = 500.0 * (f[0] - f[1]);
+  lab[2] = 200.0 * (f[1] - f[2]);
+}
+
+/* delta_e76 / delta_e94 (colorimetry.cpp:137-157; graphic-arts constants). */
+double orc_delta_e76(const double* a, const double* b) {
+  const double dl = a[0] - b[0], da = a[1] - b[1], db = a[2] - b[2];
+  return sqrt(dl * dl + da * da + db * db);
+}
+double orc_delta_e94(const double* ref, const double* sample) {
+  const double dl = ref[0] - sample[0];
+  const double c1 = hypot(ref[1], ref[2]);
+  const double c2 = hypot(sample[1], sample[2]);
+  const double dc = c1 - c2;
+  const double da = ref[1] - sample[1];
+  const double db = ref[2] - sample[2];
+  double dh2 = da * da + db * db - dc * dc;
+  dh2 = dh2 > 0.0 ? dh2 : 0.0;
+  const double sc = 1.0 + 0.045 * c1;
+  const double sh = 1.0 + 0.015 * c1;
+  return sqrt(dl * dl + (dc / sc) * (dc / sc) + dh2 / (sh * sh));
+}
+
+/* scene_color_report (evaluation.cpp:122-154): out = {mean_de76, p95_de76, mse, exposure}.
+ * ybar = cmf + n (row 1) when the ground truth is spectral. */
+void orc_scene_color_report(const float* gt, int cgt, const float* test, int ctest, int64_t P,
+                            const double* cmf, double dlambda, double* out) {
+  const double exposure = orc_exposure_for(gt, P, cgt, cgt == 3 ? NULL : cmf + cgt, dlambda, 99.5);
+  float* ga = (float*)malloc(sizeof(float) * (size_t)(P > 0 ? P : 1) * 3);
+  float* ta = (float*)malloc(sizeof(float) * (size_t)(P > 0 ? P : 1) * 3);
+  double* des = (double*)malloc(sizeof(double) * (size_t)(P > 0 ? P : 1));
+  if (!ga || !ta || !des) abort();
+  orc_image_to_linear_rgb(gt, P, cgt, cmf, dlambda, ga);
+  orc_image_to_linear_rgb(test, P, ctest, cmf, dlambda, ta);
+  const double white[3] = {0.95047, 1.0, 1.08883}; /* srgb_reference_white, colorimetry.cpp:111-116 */
+  double sum = 0.0;
+  for (int64_t p = 0; p < P; ++p) {
+    double a[3], b[3], xa[3], xb[3], la[3], lb[3];
+    for (int c = 0; c < 3; ++c) {
+      a[c] = (double)ga[p * 3 + c] * exposure;
+      b[c] = (double)ta[p * 3 + c] * exposure;
+    }
+    for (int r = 0; r < 3; ++r) {
+      xa[r] = kRgbToXyz[3 * r] * a[0] + kRgbToXyz[3 * r + 1] * a[1] + kRgbToXyz[3 * r + 2] * a[2];
+      xb[r] = kRgbToXyz[3 * r] * b[0] + kRgbToXyz[3 * r + 1] * b[1] + kRgbToXyz[3 * r + 2] * b[2];
+    }
+    orc_xyz_to_lab(xa, white, la);
+    orc_xyz_to_lab(xb, white, lb);
+    des[p] = orc_delta_e76(la, lb);
+    sum += des[p];
+  }
+  out[0] = P > 0 ? sum / (double)P : 0.0; /* mean_of (evaluation.cpp:23-28) */
+  out[1] = orc_percentile_nearest_rank(des, P, 95.0);
+  out[2] = orc_error_map(gt, cgt, test, ctest, P, cmf, dlambda, NULL);
+  out[3] = exposure;
+  free(ga);
+  free(ta);
+  free(des);
+}
+
+/* R5: the Delta E94 of multibounce_eval (evaluation.cpp:59-86) per
+ * pixel of a ground-truth and a test XYZ image: white = D65 white scaled to the ground
+ * truth's luminance (max(Y_gt, 1e-6) / Y_white), Lab of both, delta_e94(gt, test).
+ * out = {mean, median, p95}; de (may be NULL) per pixel. */
+void orc_delta_e94_report(const float* xyz_gt, const float* xyz_test, int64_t P, const double* white_d65,
+                          float* de, double* out) {
+  double* v = (double*)malloc(sizeof(double) * (size_t)(P > 0 ? P : 1));
+  if (!v) abort();
+  double sum = 0.0;
+  for (int64_t p = 0; p < P; ++p) {
+    double g[3], t[3], w[3], lg[3], lt[3];
+    for (int c = 0; c < 3; ++c) {
+      g[c] = (double)xyz_gt[p * 3 + c];
+      t[c] = (double)xyz_test[p * 3 + c];
+    }
+    const double y_white = g[1] > 1e-6 ? g[1] : 1e-6;
+    const double scale = y_white / white_d65[1];
+    for (int c = 0; c < 3; ++c) w[c] = white_d65[c] * scale;
+    orc_xyz_to_lab(g, w, lg);
+    orc_xyz_to_lab(t, w, lt);
+    v[p] = orc_delta_e94(lg, lt);
+    if (de) de[p] = (float)v[p];
+    sum += v[p];
+  }
+  out[0] = P > 0 ? sum / (double)P : 0.0;
+  out[1] = orc_percentile_nearest_rank(v, P, 50.0);
+  out[2] = orc_percentile_nearest_rank(v, P, 95.0);
+  free(v);
+}

@@ -67,6 +67,27 @@ void orc_mlp_forward(const float* rgb, int64_t P, int hidden, int k, const float
 double orc_hadamard_loss(const float* E, const float* D, int k, int n, const float* A,
                          const float* B, int64_t pairs);
 
+/* Colour-metric tail (SURVEY §8f row 1; renderer.cpp:721-802, evaluation.cpp:14-28, :59-86,
+ * :122-154, colorimetry.cpp:111-162).  Images are P pixels x channels (3 = linear RGB, n =
+ * spectra); cmf = [3][n] rows (xbar, ybar, zbar) of the grid. */
+double orc_percentile_nearest_rank(const double* v, int64_t count, double p);
+void orc_luminance(const float* img, int64_t P, int channels, const double* ybar, double dlambda, double* lum);
+double orc_exposure_for(const float* img, int64_t P, int channels, const double* ybar, double dlambda,
+                        double percentile);
+double orc_srgb_encode(double linear);
+void orc_tonemap_srgb8(const float* rgb, int64_t P, double exposure, uint8_t* out);
+void orc_image_to_linear_rgb(const float* img, int64_t P, int channels, const double* cmf, double dlambda,
+                             float* rgb);
+double orc_error_map(const float* a, int ca, const float* b, int cb, int64_t P, const double* cmf,
+                     double dlambda, float* mse);
+void orc_xyz_to_lab(const double* xyz, const double* white, double* lab);
+double orc_delta_e76(const double* a, const double* b);
+double orc_delta_e94(const double* ref, const double* sample);
+void orc_scene_color_report(const float* gt, int cgt, const float* test, int ctest, int64_t P,
+                            const double* cmf, double dlambda, double* out);
+void orc_delta_e94_report(const float* xyz_gt, const float* xyz_test, int64_t P, const double* white_d65,
+                          float* de, double* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,6 +33,7 @@
 #include "hadacodec/codec.hpp"
 #include "hadacodec/colorimetry.hpp"
 #include "hadacodec/dataset.hpp"
+#include "hadacodec/evaluation.hpp"
 #include "hadacodec/renderer.hpp"
 #include "hadacodec/rng.hpp"
 #include "hadacodec/spectrum.hpp"
@@ -484,6 +485,97 @@ double ref_hadamard_loss(const float* E, const float* D, int k, const float* A, 
   double total = 0.0;
   for (double v : part) total += v;
   return total;
+}
+
+// ---------------------------------------------------------------- colour-metric tail
+// the reference's own exposure_for / tonemap_srgb8 / error_map
+// (renderer.cpp:721-802) and scene_color_report (evaluation.cpp:122-154) on a P x 1
+// image; and R5, the per-chain Delta E94 of multibounce_eval (evaluation.cpp:59-86)
+// applied per pixel, built from xyz_to_lab / delta_e94 / CmfTable::white_xyz.
+
+double ref_exposure_for(const float* img, int64_t P, int channels, double percentile) {
+  return exposure_for(band_image(P, channels, img), percentile);
+}
+
+void ref_tonemap_srgb8(const float* rgb, int64_t P, double exposure, uint8_t* out) {
+  const std::vector<unsigned char> v = tonemap_srgb8(band_image(P, 3, rgb), exposure);
+  std::memcpy(out, v.data(), v.size());
+}
+
+double ref_error_map(const float* a, int ca, const float* b, int cb, int64_t P, float* mse) {
+  const ErrorMap em = error_map(band_image(P, ca, a), band_image(P, cb, b));
+  if (mse) std::memcpy(mse, em.mse.data(), sizeof(float) * em.mse.size());
+  return em.mean_mse;
+}
+
+void ref_scene_color_report(const float* gt, int cgt, const float* test, int ctest, int64_t P, double* out4) {
+  const SceneColorReport r = scene_color_report(band_image(P, cgt, gt), band_image(P, ctest, test));
+  out4[0] = r.mean_de76;
+  out4[1] = r.p95_de76;
+  out4[2] = r.mse;
+  out4[3] = r.exposure;
+}
+
+void ref_xyz_to_lab(const double* xyz, const double* white, double* lab) {
+  ColorTriple x, w;
+  x.space = w.space = ColorSpace::XYZ;
+  x.c = {xyz[0], xyz[1], xyz[2]};
+  w.c = {white[0], white[1], white[2]};
+  const ColorTriple l = xyz_to_lab(x, w);
+  for (int i = 0; i < 3; ++i) lab[i] = l[i];
+}
+
+double ref_delta_e76(const double* a, const double* b) {
+  ColorTriple x, y;
+  x.space = y.space = ColorSpace::Lab;
+  x.c = {a[0], a[1], a[2]};
+  y.c = {b[0], b[1], b[2]};
+  return delta_e76(x, y);
+}
+
+double ref_delta_e94(const double* a, const double* b) {
+  ColorTriple x, y;
+  x.space = y.space = ColorSpace::Lab;
+  x.c = {a[0], a[1], a[2]};
+  y.c = {b[0], b[1], b[2]};
+  return delta_e94(x, y);
+}
+
+double ref_srgb_encode(double v) { return srgb_encode(v); }
+
+// R5: out3 = {mean, median, p95} of per-pixel delta_e94(lab(gt), lab(test)) with the
+// white scaled to the ground truth's Y (evaluation.cpp:63-74), mean_of / nearest rank
+// as evaluation.cpp:14-28.
+void ref_delta_e94_report(const float* xyz_gt, const float* xyz_test, int64_t P, float* de, double* out3) {
+  const ColorTriple white_d65 = CmfTable::instance().white_xyz();
+  std::vector<double> v(static_cast<size_t>(P));
+  for (int64_t p = 0; p < P; ++p) {
+    ColorTriple g, t;
+    g.space = t.space = ColorSpace::XYZ;
+    for (int c = 0; c < 3; ++c) {
+      g.c[c] = static_cast<double>(xyz_gt[p * 3 + c]);
+      t.c[c] = static_cast<double>(xyz_test[p * 3 + c]);
+    }
+    const double y_white = std::max(g[1], 1e-6);
+    ColorTriple white = white_d65;
+    const double scale = y_white / white_d65[1];
+    for (int c = 0; c < 3; ++c) white[c] *= scale;
+    v[static_cast<size_t>(p)] = delta_e94(xyz_to_lab(g, white), xyz_to_lab(t, white));
+    if (de) de[p] = static_cast<float>(v[static_cast<size_t>(p)]);
+  }
+  double acc = 0.0;
+  for (double x : v) acc += x;
+  out3[0] = P > 0 ? acc / static_cast<double>(P) : 0.0;
+  auto rank = [&](double pct) {
+    std::vector<double> s = v;
+    std::sort(s.begin(), s.end());
+    const double r = pct / 100.0 * static_cast<double>(s.size());
+    size_t idx = static_cast<size_t>(std::ceil(r));
+    idx = idx == 0 ? 0 : idx - 1;
+    return s[std::min(idx, s.size() - 1)];
+  };
+  out3[1] = P > 0 ? rank(50.0) : 0.0;
+  out3[2] = P > 0 ? rank(95.0) : 0.0;
 }
 
 int ref_thread_count() { return render_thread_count(); }

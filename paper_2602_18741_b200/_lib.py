@@ -46,6 +46,12 @@ SIGNATURES: dict[str, tuple] = {
     "hc_mlp_destroy": (i32, [vp]),
     "hc_mlp_forward": (i32, [vp, vp, i64, vp]),
     "hc_hadamard_loss": (i32, [vp, vp, vp, i64, vp]),
+    "hc_exposure_for": (i32, [vp, vp, i64, i32, f64, C.POINTER(f64)]),
+    "hc_tonemap_srgb8": (i32, [vp, vp, i64, f64, vp]),
+    "hc_error_map": (i32, [vp, vp, i32, vp, i32, i64, vp, C.POINTER(f64)]),
+    "hc_scene_color_report": (i32, [vp, vp, i32, vp, i32, i64, vp]),
+    "hc_scene_color_report_dev": (i32, [vp, vp, i32, vp, i32, i64, vp, vp]),
+    "hc_delta_e94_report": (i32, [vp, vp, vp, i64, vp, vp, vp]),
     "hc_shade_latent_host": (i32, [vp, vp, i32, vp, i32, vp, vp, i64, vp, vp]),
     "hc_roundtrip_host": (i32, [vp, vp, i64, vp, vp, vp, vp]),
     "hc_stream_key": (u64, [u64, C.c_char_p]),

@@ -17,6 +17,8 @@ of ``libhadacodec_b200.so``.  Calls are enqueued on torch's current stream.
   multibounce chain (evaluation.cpp:50-76)   Codec.multibounce_latent / _spectral
   upsample(UpsamplerWeights, rgb)            Upsampler.forward(rgb[P, 3]) -> codes[P, k]
   loss residual (trainer.cpp:49-71)          Codec.hadamard_loss(A, B)
+  exposure_for / tonemap_srgb8 / error_map   exposure_for / tonemap_srgb8 / error_map
+  scene_color_report (evaluation.cpp)        scene_color_report; delta_e94_report (per pixel)
 """
 from __future__ import annotations
 
@@ -302,6 +304,98 @@ def reassemble(ctx: Context, passes: Sequence[torch.Tensor]) -> torch.Tensor:
     ctx.bind_stream()
     _check(_lib.lib().hc_reassemble(ctx.h, C.cast(arr, C.c_void_p), len(passes), P, _p(latent)))
     return latent
+
+
+# ------------------------------------------------------------ colour-metric tail
+def _image(t: torch.Tensor, codec: "Codec", name: str) -> tuple[torch.Tensor, int, int]:
+    t = _cuda(t, torch.float32, name)
+    ch = t.shape[-1] if t.dim() > 1 else 1
+    if ch not in (3, codec.n):
+        raise ValueError(f"{name}: expected 3 or {codec.n} channels (decode latent images first)")
+    return t, ch, t.numel() // ch
+
+
+def exposure_for(codec: "Codec", img: torch.Tensor, percentile: float = 99.5) -> float:
+    """renderer.cpp:721-752: 1 / nearest-rank luminance percentile (1 if <= 1e-12)."""
+    img, ch, P = _image(img, codec, "img")
+    out = C.c_double()
+    codec.ctx.bind_stream()
+    _check(_lib.lib().hc_exposure_for(codec.h, _p(img), P, ch, float(percentile), C.byref(out)))
+    return out.value
+
+
+def tonemap_srgb8(ctx: Context, rgb: torch.Tensor, exposure: float, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """renderer.cpp:754-773: uint8 [P, 3] sRGB of exposure-scaled linear RGB."""
+    rgb = _cuda(rgb, torch.float32, "rgb")
+    P = rgb.numel() // 3
+    if out is None:
+        out = torch.empty(P, 3, dtype=torch.uint8, device=rgb.device)
+    ctx.bind_stream()
+    _check(_lib.lib().hc_tonemap_srgb8(ctx.h, _p(rgb), P, float(exposure), _p(out)))
+    return out
+
+
+def error_map(codec: "Codec", a: torch.Tensor, b: torch.Tensor) -> tuple[torch.Tensor, float]:
+    """renderer.cpp:775-802: (per-pixel linear-RGB MSE [P] f32, mean MSE)."""
+    a, ca, P = _image(a, codec, "a")
+    b, cb, Pb = _image(b, codec, "b")
+    if P != Pb:
+        raise ValueError("error_map: image sizes differ")
+    mse = codec.ctx.empty(P)
+    mean = C.c_double()
+    codec.ctx.bind_stream()
+    _check(_lib.lib().hc_error_map(codec.h, _p(a), ca, _p(b), cb, P, _p(mse), C.byref(mean)))
+    return mse, mean.value
+
+
+def scene_color_report(codec: "Codec", gt: torch.Tensor, test: torch.Tensor) -> dict:
+    """evaluation.cpp:122-154: mean / p95 Delta E76, linear-RGB MSE, exposure of the ground truth."""
+    gt, cg, P = _image(gt, codec, "gt")
+    test, ct, Pt = _image(test, codec, "test")
+    if P != Pt:
+        raise ValueError("scene_color_report: image sizes differ")
+    out = (C.c_double * 4)()
+    codec.ctx.bind_stream()
+    _check(_lib.lib().hc_scene_color_report(codec.h, _p(gt), cg, _p(test), ct, P, C.cast(out, C.c_void_p)))
+    return {"mean_de76": out[0], "p95_de76": out[1], "mse": out[2], "exposure": out[3]}
+
+
+def scene_color_report_dev(codec: "Codec", gt: torch.Tensor, test: torch.Tensor, out: Optional[torch.Tensor] = None,
+                           preview: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """Stream-ordered scene_color_report: f64 [4] device tensor {mean_de76, p95_de76, mse, exposure};
+    `preview` (uint8 [P, 3], optional) receives tonemap_srgb8(test, exposure) from the same pass."""
+    gt, cg, P = _image(gt, codec, "gt")
+    test, ct, Pt = _image(test, codec, "test")
+    if P != Pt:
+        raise ValueError("scene_color_report: image sizes differ")
+    if out is None:
+        out = codec.ctx.empty(4, dtype=torch.float64)
+    codec.ctx.bind_stream()
+    _check(_lib.lib().hc_scene_color_report_dev(codec.h, _p(gt), cg, _p(test), ct, P, _p(out), _p(preview)))
+    return out
+
+
+def delta_e94_report(ctx: Context, xyz_gt: torch.Tensor, xyz_test: torch.Tensor, n: int = 81,
+                     white: Optional[Sequence[float]] = None, per_pixel: bool = False) -> dict:
+    """multibounce_eval's metric (evaluation.cpp:59-86) per pixel: mean / median / p95 Delta E94
+    with the D65 white (CmfTable::white_xyz of grid n unless given) scaled to the truth's Y."""
+    from .colorimetry import white_xyz
+
+    xyz_gt = _cuda(xyz_gt, torch.float32, "xyz_gt")
+    xyz_test = _cuda(xyz_test, torch.float32, "xyz_test")
+    P = xyz_gt.numel() // 3
+    if xyz_test.numel() != xyz_gt.numel():
+        raise ValueError("delta_e94_report: image sizes differ")
+    w = (C.c_double * 3)(*(white if white is not None else white_xyz(n)))
+    out = (C.c_double * 3)()
+    de = ctx.empty(P) if per_pixel else None
+    ctx.bind_stream()
+    _check(_lib.lib().hc_delta_e94_report(ctx.h, _p(xyz_gt), _p(xyz_test), P, C.cast(w, C.c_void_p), _p(de),
+                                          C.cast(out, C.c_void_p)))
+    res = {"mean_de94": out[0], "median_de94": out[1], "p95_de94": out[2]}
+    if per_pixel:
+        res["de94"] = de
+    return res
 
 
 def split_blocks(z: np.ndarray) -> list:

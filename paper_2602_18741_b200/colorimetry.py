@@ -56,3 +56,22 @@ def cmf_table(n: int) -> dict:
 
 def cmf_matrix(n: int) -> np.ndarray:
     return np.ascontiguousarray(cmf_table(n)["cmf"])
+
+
+@lru_cache(maxsize=None)
+def white_xyz(n: int) -> tuple[float, float, float]:
+    """CmfTable::white_xyz (colorimetry.cpp:45-73): D65-weighted rows normalised so a unit
+    reflectance has Y = 100, summed — in the reference's sequential fp64 order."""
+    t = cmf_table(n)
+    x, y, z, d = (t[r].tolist() for r in ("xbar", "ybar", "zbar", "d65"))
+    norm = 0.0
+    for i in range(n):
+        norm += y[i] * d[i]
+    scale = 100.0 / norm
+    out = []
+    for row in (x, y, z):
+        acc = 0.0
+        for i in range(n):
+            acc += scale * row[i] * d[i]
+        out.append(acc)
+    return tuple(out)

@@ -52,6 +52,11 @@ int ensure_aux_streams(hc_ctx ctx);
     if (_e != cudaSuccess) return ::hcb::cuda_error(_e, #expr);  \
   } while (0)
 
+#define HC_REQUIRE(cond, code, msg)               \
+  do {                                            \
+    if (!(cond)) return ::hcb::set_error((code), (msg)); \
+  } while (0)
+
 #define HC_CHECK_LAUNCH(ctx, what)                                   \
   do {                                                               \
     cudaError_t _e = cudaGetLastError();                             \

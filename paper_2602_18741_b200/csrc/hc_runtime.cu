@@ -244,11 +244,6 @@ static uint64_t fnv1a64(const char* s) {
 
 using namespace hcb;
 
-#define HC_REQUIRE(cond, code, msg) \
-  do {                              \
-    if (!(cond)) return set_error((code), (msg)); \
-  } while (0)
-
 extern "C" {
 
 const char* hc_last_error(void) { return g_last_error.c_str(); }

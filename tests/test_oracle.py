@@ -225,3 +225,79 @@ def test_decode_rejects_negative_in_reference(ref81):
     assert ref81.ref_decode_rows_d(D, 6, Z, 1, S) == 0
     Z[0, 2] = -1e-9
     assert ref81.ref_decode_rows_d(D, 6, Z, 1, S) == 1
+
+
+# ----------------------------------------------------------------- colour-metric tail
+def test_colour_difference_kats(orc, kats):
+    c = kats["colour_differences"]
+    a, b = np.array(c["a"]), np.array(c["b"])
+    assert orc.orc_delta_e76(a, b) == pytest.approx(c["de76_ab"], rel=c["eps"])
+    assert orc.orc_delta_e94(a, b) == pytest.approx(c["de94_ab"], rel=c["eps"])
+    assert orc.orc_delta_e94(b, a) == pytest.approx(c["de94_ba"], rel=c["eps"])
+    assert orc.orc_delta_e76(a, a) == 0.0 and orc.orc_delta_e94(a, a) == 0.0
+    assert orc.orc_delta_e94(np.array(c["c"]), np.array(c["d"])) == pytest.approx(c["de94_cd"], rel=c["eps"])
+
+
+def test_lab_and_srgb_encode_kats(orc, kats):
+    k = kats["lab_near_black"]
+    lab = np.zeros(3)
+    orc.orc_xyz_to_lab(np.array(k["xyz"]), np.array(k["white"]), lab)
+    for got, want, eps in zip(lab, k["lab"], k["eps"]):
+        assert got == pytest.approx(want, rel=eps)
+    t = cmf_table(47)
+    norm = float(np.sum(t["ybar"] * t["d65"]))
+    white = np.array([float(np.sum(100.0 / norm * t[r] * t["d65"])) for r in ("xbar", "ybar", "zbar")])
+    orc.orc_xyz_to_lab(white, white, lab)
+    assert lab[0] == pytest.approx(kats["lab_white47"]["L"], rel=kats["lab_white47"]["eps"])
+    assert abs(lab[1]) < kats["lab_white47"]["ab_abs"] and abs(lab[2]) < kats["lab_white47"]["ab_abs"]
+    for x, want, eps in kats["srgb_encode"]["cases"]:
+        assert orc.orc_srgb_encode(x) == pytest.approx(want, rel=eps, abs=0.0)
+
+
+def _metric_images(seed, P, n):
+    """Linear-RGB-like and spectral images with negatives, zeros and a wide dynamic range."""
+    rng = np.random.default_rng(seed)
+    rgb_a = (rng.lognormal(-1.0, 1.5, (P, 3)) * (rng.random((P, 3)) > 0.02)).astype(np.float32)
+    rgb_a[:7] = [[0, 0, 0], [1e-9, 0, 0], [-0.01, 0.02, 0.0], [5, 5, 5], [0.5, 0.5, 0.5], [0.5, 0.5, 0.5], [2, 0, 1]]
+    rgb_b = (rgb_a * rng.normal(1.0, 0.05, (P, 3))).astype(np.float32)
+    spec = rng.random((P, n)).astype(np.float32) * rng.lognormal(0.0, 1.0, (P, 1)).astype(np.float32)
+    spec2 = (spec * rng.normal(1.0, 0.03, (P, n))).astype(np.float32)
+    return rgb_a, rgb_b, spec, spec2
+
+
+@pytest.mark.parametrize("n", [47, 81])
+def test_metric_tail_oracle_matches_compiled_reference(orc, n):
+    """exposure_for / tonemap_srgb8 / error_map / scene_color_report / Delta E94 report:
+    the C restatement against the reference's own functions (oracle/_ref)."""
+    ref = oracle.reference(n)
+    if ref is None:
+        pytest.skip("compiled reference not built")
+    P = 3001
+    cmf, dl = cmf_matrix(n), grid(n)[1]
+    a, b, s, s2 = _metric_images(5 + n, P, n)
+    for img, ch in ((a, 3), (s, n)):
+        for pct in (99.5, 50.0, 0.0, 100.0):
+            got = orc.orc_exposure_for(img, P, ch, None if ch == 3 else np.ascontiguousarray(cmf[1]), dl, pct)
+            assert got == ref.ref_exposure_for(img, P, ch, pct)
+    e = ref.ref_exposure_for(a, P, 3, 99.5)
+    u1, u2 = np.zeros(P * 3, np.uint8), np.zeros(P * 3, np.uint8)
+    orc.orc_tonemap_srgb8(a, P, e, u1)
+    ref.ref_tonemap_srgb8(a, P, e, u2)
+    assert np.array_equal(u1, u2)
+    for x, cx, y, cy in ((a, 3, b, 3), (s, n, s2, n), (s, n, b, 3)):
+        m1, m2 = np.zeros(P, np.float32), np.zeros(P, np.float32)
+        assert orc.orc_error_map(x, cx, y, cy, P, cmf, dl, m1) == ref.ref_error_map(x, cx, y, cy, P, m2)
+        assert np.array_equal(m1, m2)
+        r1, r2 = np.zeros(4), np.zeros(4)
+        orc.orc_scene_color_report(x, cx, y, cy, P, cmf, dl, r1)
+        ref.ref_scene_color_report(x, cx, y, cy, P, r2)
+        assert np.array_equal(r1, r2), (r1, r2)
+    white = np.zeros(3)
+    ref.ref_white_xyz(white)
+    xg = (a * 40).astype(np.float32)
+    xt = (b * 40).astype(np.float32)
+    d1, d2 = np.zeros(P, np.float32), np.zeros(P, np.float32)
+    o1, o2 = np.zeros(3), np.zeros(3)
+    orc.orc_delta_e94_report(xg, xt, P, white, d1, o1)
+    ref.ref_delta_e94_report(xg, xt, P, d2, o2)
+    assert np.array_equal(d1, d2) and np.array_equal(o1, o2)
