@@ -56,6 +56,10 @@ CONFIGS = {
                unit="Mpixel/s", bytes_per_unit=36, flops_per_unit=9344, rot=2),
     "5b": dict(name="Hadamard near-multiplicativity loss, 2^24 pairs, n=81, k=6", units=1 << 24, k=6,
                unit="M pairs/s", bytes_per_unit=648, rot=1),
+    # SURVEY §8f row 1 (the next row): the colour-metric tail of a config-2 frame.
+    "6": dict(name="1920x1080 colour-metric tail: scene_color_report(naive n=81 sRGB, latent k=6 sRGB) "
+                   "+ tonemap_srgb8 preview of the latent frame", W=1920, H=1080, k=6, L=8, unit="Mpixel/s",
+              bytes_per_unit=27, rot=8),
 }
 
 
@@ -207,6 +211,29 @@ def cpu_reference_run(cfg_key: str, budget_s: float, threads: int = 0, rank: int
             ref.ref_mlp_forward(rgb, P, 64, 6, w["w1"], w["b1"], w["w2"], w["b2"], w["w3"], w["b3"], out, nthreads)
 
         sample = f"{P} texels (8 rows)"
+    elif cfg_key == "6":
+        # the reference's own scene_color_report + tonemap_srgb8 (single-threaded as written)
+        L, W = cfg["L"], cfg["W"]
+        pal = synth.palette(SEED, 256, N_SPEC)
+        lts = synth.lights(SEED, L, N_SPEC)
+        pc = np.zeros((256, k), np.float32)
+        lc = np.zeros((L, k), np.float32)
+        ref.ref_asset_codes(E, k, pal, 256, pc)
+        ref.ref_asset_codes(E, k, lts, L, lc)
+        P = 64 * W
+        idx, cosv = synth.gbuffer_np(SEED, rank * cfg["H"] * W, P, L, 256)
+        cosv = np.ascontiguousarray(cosv)
+        gt, test = np.zeros((P, 3), np.float32), np.zeros((P, 3), np.float32)
+        ref.ref_shade_spectral(pal, lts, L, idx, cosv, P, None, None, gt, nthreads)
+        ref.ref_shade_latent(E, D, k, pc, lc, L, idx, cosv, P, None, None, None, test, nthreads)
+        rep, u8 = np.zeros(4), np.zeros(P * 3, np.uint8)
+        nthreads = 1
+
+        def run():
+            ref.ref_scene_color_report(gt, 3, test, 3, P, rep)
+            ref.ref_tonemap_srgb8(test, P, rep[3], u8)
+
+        sample = f"{P} px (64 rows): scene_color_report + tonemap_srgb8 of the reference (single-threaded)"
     else:  # 5b
         P = 1 << 15
         A = synth.gm_spectra_ctr(SEED, "loss.a", 0, 1024, N_SPEC)
@@ -315,6 +342,27 @@ class Workload:
                     codec.shade_spectral(self.pal_d, self.lts, idx, cosv, out=outs)
                 else:
                     codec.shade_latent(self.pal_codes, self.light_codes, idx, cosv, out=outs)
+            self.step = step
+        elif cfg_key == "6":
+            W, H, L = cfg["W"], cfg["H"], cfg["L"]
+            first, P = span(H, W)
+            pal = synth.palette(SEED, 256, N_SPEC)
+            lts = synth.lights(SEED, L, N_SPEC)
+            pal_d = torch.from_numpy(pal).cuda()
+            pal_codes = codec.encode(pal_d)
+            light_codes = codec.encode(torch.from_numpy(lts).cuda()).cpu().numpy()
+            for r in range(R):  # ground truth = naive n = 81 render, test = latent render of the same frame
+                idx, cosv = api.synth_gbuffer(ctx, SEED + r, first, P, L, 256)
+                gt = codec.shade_spectral(pal_d, lts, idx, cosv)["rgb"]
+                test = codec.shade_latent(pal_codes, light_codes, idx, cosv, xyz=False)["rgb"]
+                self.sets.append((gt, test, ctx.empty(4, dtype=torch.float64),
+                                  torch.empty(P, 3, dtype=torch.uint8, device="cuda")))
+                del idx, cosv
+            self.units = P
+
+            def step(i):
+                gt, test, out, prev = self.sets[i % R]
+                api.scene_color_report_dev(codec, gt, test, out=out, preview=prev)
             self.step = step
         elif cfg_key == "1":
             first, P = span(cfg["units"], 1)

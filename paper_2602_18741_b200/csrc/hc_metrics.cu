@@ -13,20 +13,25 @@
 //
 // Percentiles are exact order statistics from a radix select over order-preserving
 // 64-bit keys of the doubles, with no sort and no host round trip:
-//   1. the kernel that produces the values also writes their keys and a histogram of
-//      the top 15 key bits (sign, exponent, 3 mantissa bits; per-CTA 128 KB shared-
-//      memory histogram with warp-aggregated increments, non-zero bins flushed);
-//   2. one CTA scans the 32768 bins and fixes the bucket holding the wanted rank;
-//   3. keys of that bucket are compacted (warp-aggregated appends) — typically a few
-//      percent of the pixels;
-//   4. four 12/13-bit digit passes over the candidates fix the remaining 49 bits.
+//   1. the kernel that produces the values also writes their keys and histograms of
+//      the top 15 and top 9 key bits (per-CTA 130 KB shared-memory histograms with
+//      warp-aggregated increments, non-zero bins flushed);
+//   2. the bucket holding the wanted rank is found from a 512-bin coarse histogram and
+//      the 64 top bins under it;
+//   3. keys of that bucket are compacted (per-CTA reserved ranges);
+//   4. a 12-bit digit pass over the candidates, a second compaction, and three more
+//      digit passes — on one CTA once few candidates remain — fix the other 49 bits.
+// Steps 2-4 are one cooperative launch (grid syncs between the phases).
 // Traffic per select is one extra read of the keys.  Means are per-CTA fp64 partial
 // sums reduced in a fixed order (deterministic run to run).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "hadacodec_b200.h"
@@ -40,10 +45,15 @@ constexpr int kThreads = 256;
 constexpr int kProdThreads = 1024;                 // producer kernels: 1 CTA/SM (128 KB histogram)
 constexpr int kTopShift = 49;                      // top digit = key bits [49, 64)
 constexpr int kTopBins = 1 << (64 - kTopShift);    // 32768
-constexpr int kTopSmem = kTopBins * 4;
+constexpr int kCoarseShift = 55;                   // coarse digit = key bits [55, 64): 512 bins
+constexpr int kCoarseBins = 1 << (64 - kCoarseShift);
+constexpr int kSubBins = kTopBins / kCoarseBins;    // 64 top bins per coarse bin
+constexpr int kTopSmem = (kTopBins + kCoarseBins) * 4;
+constexpr unsigned int kSmallCand = 32768;         // finish on one CTA below this many keys
 constexpr int kFineBins = 8192;                    // <= 13-bit digits over the candidates
-constexpr int kFineShift[4] = {37, 25, 13, 0};
-constexpr int kFineBits[4] = {12, 12, 12, 13};
+// fine digit passes: shift 37, 25, 13, 0; widths 12, 12, 12, 13
+__host__ __device__ constexpr int fine_shift(int pass) { return pass == 3 ? 0 : 37 - 12 * pass; }
+__host__ __device__ constexpr int fine_bits(int pass) { return pass == 3 ? 13 : 12; }
 
 struct CmfRows {
   double row[3][kMaxN];  // xbar, ybar, zbar (unscaled, the grid's CmfTable rows)
@@ -62,13 +72,13 @@ struct SelectState {
   unsigned long long rank;    // 0-based rank still to find inside the prefix
   unsigned int count;         // candidates (keys of the selected top bucket)
   unsigned int pad;
-  unsigned int hist[kFineBins];
 };
 
-// Top-digit histogram in dynamic shared memory: zero, add (warp-aggregated: lanes
-// with the same bucket add once), flush the non-zero bins to the global histogram.
+// Top-digit histogram in dynamic shared memory (kTopBins fine + kCoarseBins coarse
+// counters): zero, add (warp-aggregated: lanes with the same bucket add once), flush the
+// non-zero bins to the global histogram (same layout).
 __device__ __forceinline__ void top_hist_zero(unsigned int* h) {
-  for (int i = threadIdx.x; i < kTopBins; i += blockDim.x) h[i] = 0;
+  for (int i = threadIdx.x; i < kTopBins + kCoarseBins; i += blockDim.x) h[i] = 0;
   __syncthreads();
 }
 __device__ __forceinline__ void top_hist_add(unsigned int* h, unsigned long long key, bool valid) {
@@ -77,10 +87,13 @@ __device__ __forceinline__ void top_hist_add(unsigned int* h, unsigned long long
   const unsigned int bin = static_cast<unsigned int>(key >> kTopShift);
   const unsigned int peers = __match_any_sync(active, bin);
   if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&h[bin], __popc(peers));
+  const unsigned int cbin = bin / kSubBins;
+  const unsigned int cpeers = __match_any_sync(active, cbin);
+  if ((threadIdx.x & 31) == __ffs(cpeers) - 1) atomicAdd(&h[kTopBins + cbin], __popc(cpeers));
 }
 __device__ __forceinline__ void top_hist_flush(const unsigned int* h, unsigned int* g) {
   __syncthreads();
-  for (int i = threadIdx.x; i < kTopBins; i += blockDim.x)
+  for (int i = threadIdx.x; i < kTopBins + kCoarseBins; i += blockDim.x)
     if (h[i]) atomicAdd(&g[i], h[i]);
 }
 
@@ -107,15 +120,18 @@ __device__ __forceinline__ double block_sum(double v) {
   return t;  // valid in thread 0
 }
 
-// xyz_to_lab (colorimetry.cpp:118-135).
-__device__ __forceinline__ void xyz_to_lab(const double* xyz, const double* white, double* lab) {
+// xyz_to_lab (colorimetry.cpp:118-135), with the white point given as its reciprocal:
+// xyz / white -> xyz * (1 / white) and the linear branch's / (3 delta^2) -> * constant,
+// <= 1 ulp apart from the reference's quotients (the Delta E bars are 1e-12 relative).
+__device__ __forceinline__ void xyz_to_lab(const double* xyz, const double* inv_white, double* lab) {
   const double delta = 6.0 / 29.0;
   const double delta3 = delta * delta * delta;
+  const double inv_lin = 1.0 / (3.0 * delta * delta);
   double f[3];
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    const double t = xyz[i] / white[i];
-    f[i] = t > delta3 ? cbrt(t) : t / (3.0 * delta * delta) + 4.0 / 29.0;
+    const double t = xyz[i] * inv_white[i];
+    f[i] = t > delta3 ? cbrt(t) : t * inv_lin + 4.0 / 29.0;
   }
   lab[0] = 116.0 * f[1] - 16.0;
   lab[1] = 500.0 * (f[0] - f[1]);
@@ -129,31 +145,54 @@ __device__ __forceinline__ void xyz_to_lab(const double* xyz, const double* whit
   for (int64_t base = int64_t(blockIdx.x) * kProdThreads + (threadIdx.x & ~31); base < (P);       \
        base += int64_t(gridDim.x) * kProdThreads)
 
-// exposure_for's luminance (renderer.cpp:730-742) -> keys + top histogram.
+// exposure_for's luminance (renderer.cpp:730-742) -> keys + top histogram.  Four pixels
+// per lane per iteration keep four independent loads in flight.
 __global__ void __launch_bounds__(kProdThreads) lum_keys_kernel(const float* __restrict__ img, int64_t P,
                                                                 int channels, const __grid_constant__ CmfRows c,
                                                                 unsigned long long* __restrict__ keys,
                                                                 unsigned int* __restrict__ top_hist) {
   extern __shared__ unsigned int th[];
   top_hist_zero(th);
-  HC_WARP_LOOP(P) {
-    const int64_t p = base + (threadIdx.x & 31);
-    const bool valid = p < P;
-    unsigned long long key = 0;
-    if (valid) {
-      const float* px = img + p * channels;
-      double v = 0.0;
-      if (channels == 3) {
-        v = 0.2126 * static_cast<double>(px[0]) + 0.7152 * static_cast<double>(px[1]) +
-            0.0722 * static_cast<double>(px[2]);
-      } else {
-        for (int i = 0; i < channels; ++i) v += c.row[1][i] * static_cast<double>(px[i]);
-        v *= c.dlambda;
+  constexpr int U = 4;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t(blockIdx.x) * kProdThreads + (threadIdx.x & ~31)) * U; base < P;
+       base += int64_t(gridDim.x) * kProdThreads * U) {
+    unsigned long long key[U];
+    bool valid[U];
+    if (channels == 3) {
+      float r[U][3];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t p = base + u * 32 + lane;
+        valid[u] = p < P;
+        const float* px = img + (valid[u] ? p : 0) * 3;
+        r[u][0] = __ldg(px);
+        r[u][1] = __ldg(px + 1);
+        r[u][2] = __ldg(px + 2);
       }
-      key = dkey(v);
-      keys[p] = key;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double v = 0.2126 * static_cast<double>(r[u][0]) + 0.7152 * static_cast<double>(r[u][1]) +
+                         0.0722 * static_cast<double>(r[u][2]);
+        key[u] = dkey(v);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t p = base + u * 32 + lane;
+        valid[u] = p < P;
+        const float* px = img + (valid[u] ? p : 0) * channels;
+        double v = 0.0;
+        for (int i = 0; i < channels; ++i) v += c.row[1][i] * static_cast<double>(__ldg(px + i));
+        v *= c.dlambda;
+        key[u] = dkey(v);
+      }
     }
-    top_hist_add(th, key, valid);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (valid[u]) keys[base + u * 32 + lane] = key[u];
+      top_hist_add(th, key[u], valid[u]);
+    }
   }
   top_hist_flush(th, top_hist);
 }
@@ -191,10 +230,17 @@ __device__ __forceinline__ double pixel_mse(const float* a, const float* b) {
 }
 
 // tonemap_srgb8's per-channel byte (renderer.cpp:764-768, srgb_encode colorimetry.cpp:159-162).
+// The fp64 pow is only needed when the scaled value lands within 0.01 of a rounding
+// boundary: a float pow (relative error ~1e-6, i.e. ~3e-4 of a code value) decides all
+// other cases identically, so the bytes equal the fp64 reference's.
 __device__ __forceinline__ uint8_t srgb8(float x, double exposure) {
   double v = static_cast<double>(x) * exposure;
   v = v < 0.0 ? 0.0 : (v > 1.0 ? 1.0 : v);
-  const double enc = v <= 0.0031308 ? 12.92 * v : 1.055 * pow(v, 1.0 / 2.4) - 0.055;
+  if (v <= 0.0031308) return static_cast<uint8_t>(12.92 * v * 255.0 + 0.5);
+  const float t = (1.055f * __powf(static_cast<float>(v), 1.0f / 2.4f) - 0.055f) * 255.0f + 0.5f;
+  const float frac = t - floorf(t);
+  if (frac > 0.01f && frac < 0.99f) return static_cast<uint8_t>(t);
+  const double enc = 1.055 * pow(v, 1.0 / 2.4) - 0.055;
   return static_cast<uint8_t>(enc * 255.0 + 0.5);
 }
 
@@ -225,7 +271,8 @@ __global__ void __launch_bounds__(kProdThreads) de76_kernel(const float* __restr
   extern __shared__ unsigned int th[];
   top_hist_zero(th);
   const double e = *exposure;
-  const double white[3] = {0.95047, 1.0, 1.08883};  // srgb_reference_white (colorimetry.cpp:111-116)
+  // 1 / srgb_reference_white (colorimetry.cpp:111-116)
+  const double white[3] = {1.0 / 0.95047, 1.0, 1.0 / 1.08883};
   double acc_de = 0.0, acc_mse = 0.0;
   HC_WARP_LOOP(P) {
     const int64_t p = base + (threadIdx.x & 31);
@@ -274,7 +321,7 @@ __global__ void __launch_bounds__(kProdThreads) de76_kernel(const float* __restr
 // the ground truth's luminance; delta_e94 with graphic-arts constants (colorimetry.cpp:145-157).
 __global__ void __launch_bounds__(kProdThreads) de94_kernel(const float* __restrict__ xyz_gt,
                                                             const float* __restrict__ xyz_test, int64_t P,
-                                                            double wx, double wy, double wz,
+                                                            double wx, double wy, double wz,  // 1/wx, wy, 1/wz
                                                             float* __restrict__ de_out,
                                                             unsigned long long* __restrict__ keys,
                                                             unsigned int* __restrict__ top_hist, double* partials) {
@@ -293,10 +340,10 @@ __global__ void __launch_bounds__(kProdThreads) de94_kernel(const float* __restr
         t[c] = static_cast<double>(xyz_test[p * 3 + c]);
       }
       const double y_white = g[1] > 1e-6 ? g[1] : 1e-6;
-      const double scale = y_white / wy;
-      w[0] = wx * scale;
-      w[1] = wy * scale;
-      w[2] = wz * scale;
+      const double inv_scale = wy / y_white;  // 1 / (y_white / wy); wx, wz passed as reciprocals
+      w[0] = inv_scale * wx;
+      w[1] = 1.0 / y_white;
+      w[2] = inv_scale * wz;
       xyz_to_lab(g, w, lg);
       xyz_to_lab(t, w, lt);
       const double dl = lg[0] - lt[0];
@@ -333,120 +380,268 @@ __global__ void __launch_bounds__(kThreads) tonemap_kernel(const float* __restri
 }
 
 // ---------------------------------------------------------------- radix select
-// Top bucket: one CTA, 32 bins per thread.  Fixes prefix = bucket << 49 and the rank
-// inside it, resets the candidate count and the fine histogram.
-__global__ void __launch_bounds__(1024) top_scan_kernel(const unsigned int* __restrict__ top_hist, SelectState* st,
-                                                        unsigned long long rank) {
-  __shared__ unsigned long long s[1024];
-  constexpr int kPer = kTopBins / 1024;
-  const int t = threadIdx.x;
+// Block-wide search of a shared-memory histogram hs[nbins]: the digit whose cumulative
+// count passes `rank` and the count below it.  Each thread owns nbins / blockDim
+// contiguous bins (read with a per-lane skew: conflict-free), the per-thread sums are
+// scanned with warp shuffles.  Every thread returns the same (digit, below).
+template <int NT, int NBINS>
+__device__ __forceinline__ void find_digit(const unsigned int* hs, unsigned long long rank, int* digit,
+                                           unsigned long long* below) {
+  constexpr int kPer = NBINS / NT;
+  static_assert(kPer >= 1 && (kPer & (kPer - 1)) == 0, "find_digit: power-of-two bins per thread");
+  __shared__ unsigned long long warp_tot[NT / 32];
+  __shared__ int s_digit;
+  __shared__ unsigned long long s_below;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   unsigned long long local = 0;
-  for (int j = 0; j < kPer; ++j) local += top_hist[t * kPer + j];
-  s[t] = local;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
-    const unsigned long long v = t >= o ? s[t - o] : 0ull;
-    __syncthreads();
-    s[t] += v;
-    __syncthreads();
+#pragma unroll 8
+  for (int j = 0; j < kPer; ++j) local += hs[t * kPer + ((j + lane) & (kPer - 1))];
+  unsigned long long incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
   }
-  unsigned long long cum = s[t] - local;
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  unsigned long long warp_base = 0;
+  for (int w = 0; w < warp; ++w) warp_base += warp_tot[w];
+  unsigned long long cum = warp_base + incl - local;
   if (cum <= rank && rank < cum + local) {
     for (int j = 0; j < kPer; ++j) {
-      const unsigned long long c = top_hist[t * kPer + j];
-      if (rank < cum + c) {
-        st->prefix = static_cast<unsigned long long>(t * kPer + j) << kTopShift;
-        st->rank = rank - cum;
+      const unsigned long long cnt = hs[t * kPer + j];
+      if (rank < cum + cnt) {
+        s_digit = t * kPer + j;
+        s_below = cum;
         break;
       }
-      cum += c;
+      cum += cnt;
     }
   }
-  if (t == 0) st->count = 0;
-  for (int i = t; i < kFineBins; i += 1024) st->hist[i] = 0;
+  __syncthreads();
+  *digit = s_digit;
+  *below = s_below;
+  __syncthreads();
 }
 
-// Keys of the selected top bucket -> cand[] (warp-aggregated appends).
-__global__ void __launch_bounds__(kThreads) compact_kernel(const unsigned long long* __restrict__ keys, int64_t P,
-                                                           SelectState* st, unsigned long long* __restrict__ cand) {
-  const unsigned long long want = st->prefix >> kTopShift;
+// Warp 0 finds, among nb <= 64 bins in shared memory, the one holding `rank`; result in
+// (*digit, *below) for the whole block.
+__device__ __forceinline__ void find_small(const unsigned int* bins, int nb, unsigned long long rank, int* digit,
+                                           unsigned long long* below) {
+  __shared__ int s_d;
+  __shared__ unsigned long long s_b;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const unsigned long long c0 = 2 * lane < nb ? bins[2 * lane] : 0ull;
+    const unsigned long long c1 = 2 * lane + 1 < nb ? bins[2 * lane + 1] : 0ull;
+    unsigned long long incl = c0 + c1;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const unsigned long long cum = incl - c0 - c1;
+    if (cum <= rank && rank < cum + c0) {
+      s_d = 2 * lane;
+      s_b = cum;
+    } else if (cum + c0 <= rank && rank < cum + c0 + c1) {
+      s_d = 2 * lane + 1;
+      s_b = cum + c0;
+    }
+  }
+  __syncthreads();
+  *digit = s_d;
+  *below = s_b;
+  __syncthreads();
+}
+
+// Candidates matching `want` (the key bits above `shift`) -> out[] with warp-aggregated
+// appends (one global atomic per warp with a match; the buckets are narrow, so matches
+// are a few percent of the keys at most).
+template <int U>
+__device__ __forceinline__ void compact_range(const unsigned long long* __restrict__ src, int64_t n, int shift,
+                                              unsigned long long want, unsigned int* counter,
+                                              unsigned long long* __restrict__ out) {
   const int lane = threadIdx.x & 31;
-  for (int64_t base = int64_t(blockIdx.x) * kThreads + (threadIdx.x & ~31); base < P;
-       base += int64_t(gridDim.x) * kThreads) {
-    const int64_t p = base + lane;
-    const unsigned long long k = p < P ? keys[p] : 0ull;
-    const bool match = p < P && (k >> kTopShift) == want;
-    const unsigned int ball = __ballot_sync(0xffffffffu, match);
-    if (!ball) continue;
-    const int leader = __ffs(ball) - 1;
-    unsigned int pos = 0;
-    if (lane == leader) pos = atomicAdd(&st->count, static_cast<unsigned int>(__popc(ball)));
-    pos = __shfl_sync(0xffffffffu, pos, leader);
-    if (match) cand[pos + __popc(ball & ((1u << lane) - 1u))] = k;
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) fine_hist_kernel(const unsigned long long* __restrict__ cand,
-                                                             SelectState* st, int shift, int bits,
-                                                             unsigned long long hi_mask) {
-  __shared__ unsigned int h[kFineBins];
-  for (int i = threadIdx.x; i < kFineBins; i += kThreads) h[i] = 0;
-  __syncthreads();
-  const unsigned int count = st->count;
-  const unsigned long long prefix = st->prefix;
-  const unsigned int dmask = (1u << bits) - 1u;
-  for (unsigned int i = blockIdx.x * kThreads + threadIdx.x; i < count; i += gridDim.x * kThreads) {
-    const unsigned long long k = cand[i];
-    if ((k & hi_mask) == prefix) atomicAdd(&h[(k >> shift) & dmask], 1u);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < kFineBins; i += kThreads)
-    if (h[i]) atomicAdd(&st->hist[i], h[i]);
-}
-
-// One CTA, 8 bins per thread: fix the digit holding the rank, clear the histogram.
-__global__ void __launch_bounds__(1024) fine_scan_kernel(SelectState* st, int shift, int bits) {
-  __shared__ unsigned long long s[1024];
-  constexpr int kPer = kFineBins / 1024;
-  const int t = threadIdx.x;
-  const int nb = 1 << bits;
-  unsigned int c[kPer];
-  unsigned long long local = 0;
+  const int64_t step = int64_t(gridDim.x) * blockDim.x * U;
+  for (int64_t base = (int64_t(blockIdx.x) * blockDim.x + (threadIdx.x & ~31)) * U; base < n; base += step) {
+    unsigned long long k[U];
 #pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    c[j] = t * kPer + j < nb ? st->hist[t * kPer + j] : 0u;
-    local += c[j];
-  }
-  s[t] = local;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    const unsigned long long v = t >= o ? s[t - o] : 0ull;
-    __syncthreads();
-    s[t] += v;
-    __syncthreads();
-  }
-  unsigned long long cum = s[t] - local;
-  const unsigned long long rank = st->rank;
-  __syncthreads();
-  if (cum <= rank && rank < cum + local) {
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = base + u * 32 + lane;
+      k[u] = p < n ? __ldcg(src + p) : ~0ull;
+    }
 #pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      if (rank < cum + c[j]) {
-        st->prefix |= static_cast<unsigned long long>(t * kPer + j) << shift;
-        st->rank = rank - cum;
-        break;
-      }
-      cum += c[j];
+    for (int u = 0; u < U; ++u) {
+      const bool match = base + u * 32 + lane < n && (k[u] >> shift) == want;
+      const unsigned int ball = __ballot_sync(0xffffffffu, match);
+      if (!ball) continue;
+      const int leader = __ffs(ball) - 1;
+      unsigned int pos = 0;
+      if (lane == leader) pos = atomicAdd(counter, static_cast<unsigned int>(__popc(ball)));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (match) out[pos + __popc(ball & ((1u << lane) - 1u))] = k[u];
     }
   }
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) st->hist[t * kPer + j] = 0;
 }
 
-// result = the selected double (mode 0) or exposure_for's 1 / value (mode 1).
-__global__ void select_value_kernel(const SelectState* st, int mode, double* out) {
-  if (threadIdx.x == 0) {
-    const double v = dval(st->prefix);
+// Block-synchronous compaction through a shared-memory staging buffer: per iteration the
+// CTA's matches (at most kSelThreads * U) are appended with shared atomics, then one
+// global atomic reserves their range and the block copies them out coalesced.  Used for
+// the top-bucket pass, where thousands of matches would otherwise serialise on one
+// global counter.
+template <int U>
+__device__ __forceinline__ void compact_staged(const unsigned long long* __restrict__ src, int64_t n, int shift,
+                                               unsigned long long want, unsigned int* counter,
+                                               unsigned long long* __restrict__ out, unsigned long long* stage) {
+  __shared__ unsigned int s_fill, s_base;
+  const int lane = threadIdx.x & 31;
+  const int64_t step = int64_t(gridDim.x) * blockDim.x * U;
+  const int64_t first = int64_t(blockIdx.x) * blockDim.x * U;
+  if (threadIdx.x == 0) s_fill = 0;
+  __syncthreads();
+  for (int64_t chunk = first; chunk < n; chunk += step) {  // block-uniform
+    const int64_t base = chunk + (threadIdx.x & ~31) * U;
+    unsigned long long k[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t p = base + u * 32 + lane;
+      k[u] = p < n ? __ldcs(src + p) : ~0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool match = base + u * 32 + lane < n && (k[u] >> shift) == want;
+      const unsigned int ball = __ballot_sync(0xffffffffu, match);
+      if (!ball) continue;
+      const int leader = __ffs(ball) - 1;
+      unsigned int pos = 0;
+      if (lane == leader) pos = atomicAdd(&s_fill, static_cast<unsigned int>(__popc(ball)));
+      pos = __shfl_sync(0xffffffffu, pos, leader);
+      if (match) stage[pos + __popc(ball & ((1u << lane) - 1u))] = k[u];
+    }
+    __syncthreads();
+    const unsigned int fill = s_fill;
+    if (fill) {
+      if (threadIdx.x == 0) s_base = atomicAdd(counter, fill);
+      __syncthreads();
+      for (unsigned int i = threadIdx.x; i < fill; i += blockDim.x) out[s_base + i] = stage[i];
+      __syncthreads();
+      if (threadIdx.x == 0) s_fill = 0;
+      __syncthreads();
+    }
+  }
+}
+
+// One digit pass over `count` candidates: shared histogram of the digit at `shift` for keys
+// matching `prefix` above it.
+__device__ __forceinline__ void digit_hist(unsigned int* hs, const unsigned long long* __restrict__ cand,
+                                           unsigned int count, unsigned long long prefix, int shift, int bits,
+                                           unsigned int first, unsigned int stride) {
+  const unsigned long long hi_mask = ~0ull << (shift + bits);
+  const unsigned int dmask = (1u << bits) - 1u;
+  for (int i = threadIdx.x; i < (1 << bits); i += blockDim.x) hs[i] = 0;
+  __syncthreads();
+  for (unsigned int i = first; i < count; i += stride) {
+    const unsigned long long k = __ldcg(cand + i);
+    if ((k & hi_mask) == prefix) atomicAdd(&hs[(k >> shift) & dmask], 1u);
+  }
+  __syncthreads();
+}
+
+// The whole select in one cooperative launch (co-resident grid, one CTA per SM):
+//   A. every CTA reads the 512-bin coarse histogram and the 64 top bins under the selected
+//      coarse bin (L2-resident) and finds the top bucket holding `rank`;
+//   B. the keys of that bucket are compacted into cand[];
+//   C. digit pass 0 (bits 37-48) over the candidates on the whole grid (shared histograms
+//      flushed to a global one, grid sync, every CTA scans it identically), then the
+//      candidates matching the 27 fixed bits are compacted again into cand2[] — typically
+//      a handful — and, below kSmallCand of them, CTA 0 alone runs passes 1-3.
+// work = [count, count2, 2 x pad, 4 x kFineBins histograms] (16-byte aligned), zeroed
+// before the launch.
+constexpr int kSelThreads = 512;
+__global__ void __launch_bounds__(kSelThreads) select_kernel(const unsigned long long* __restrict__ keys, int64_t P,
+                                                             const unsigned int* __restrict__ top_hist,
+                                                             unsigned long long rank, unsigned long long* cand,
+                                                             unsigned long long* cand2, unsigned int* work, int mode,
+                                                             double* out, long long* trace) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ unsigned int hs[];  // kFineBins histogram (+ staging)
+  const bool tr = trace && blockIdx.x == 0 && threadIdx.x == 0;
+  if (tr) trace[0] = clock64();
+  // ---- A
+  for (int i = threadIdx.x; i < kCoarseBins; i += kSelThreads) hs[i] = __ldcg(top_hist + kTopBins + i);
+  __syncthreads();
+  int d;
+  unsigned long long below;
+  find_digit<kSelThreads, kCoarseBins>(hs, rank, &d, &below);
+  rank -= below;
+  const int coarse = d;
+  for (int i = threadIdx.x; i < kSubBins; i += kSelThreads) hs[kCoarseBins + i] = __ldcg(top_hist + coarse * kSubBins + i);
+  __syncthreads();
+  find_small(hs + kCoarseBins, kSubBins, rank, &d, &below);
+  rank -= below;
+  const unsigned long long bucket = static_cast<unsigned long long>(coarse * kSubBins + d);
+  unsigned long long prefix = bucket << kTopShift;
+  if (tr) trace[1] = clock64();
+  // ---- B
+  static_assert(kSelThreads * 8 * 8 <= kFineBins * 4, "staging buffer fits the shared histogram");
+  compact_staged<8>(keys, P, kTopShift, bucket, &work[0], cand, reinterpret_cast<unsigned long long*>(hs));
+  if (tr) trace[2] = clock64();
+  grid.sync();
+  const unsigned int count = __ldcg(&work[0]);
+  if (tr) trace[3] = clock64();
+  // ---- C, pass 0 on the grid
+  {
+    const int shift = fine_shift(0), bits = fine_bits(0);
+    digit_hist(hs, cand, count, prefix, shift, bits, blockIdx.x * kSelThreads + threadIdx.x, gridDim.x * kSelThreads);
+    constexpr int kBins0 = 1 << 12;  // fine_bits(0)
+    unsigned int* g = work + 4;
+    for (int i = threadIdx.x; i < kBins0; i += kSelThreads)
+      if (hs[i]) atomicAdd(&g[i], hs[i]);
+    grid.sync();
+    for (int i = threadIdx.x * 4; i < kBins0; i += kSelThreads * 4)
+      *reinterpret_cast<uint4*>(hs + i) = __ldcg(reinterpret_cast<const uint4*>(g + i));
+    __syncthreads();
+    find_digit<kSelThreads, kBins0>(hs, rank, &d, &below);
+    prefix |= static_cast<unsigned long long>(d) << shift;
+    rank -= below;
+  }
+  if (tr) trace[4] = clock64();
+  compact_range<2>(cand, count, fine_shift(0), prefix >> fine_shift(0), &work[1], cand2);
+  grid.sync();
+  const unsigned int count2 = __ldcg(&work[1]);
+  if (tr) {
+    trace[5] = clock64();
+    trace[20] = count;
+    trace[21] = count2;
+  }
+  const bool small = count2 <= kSmallCand;
+  if (small && blockIdx.x != 0) return;
+  // ---- C, passes 1-3 (CTA 0 alone when few candidates remain, else the grid)
+  for (int pass = 1; pass < 4; ++pass) {
+    const int shift = fine_shift(pass), bits = fine_bits(pass);
+    for (int i = (1 << bits) + threadIdx.x; i < kFineBins; i += kSelThreads) hs[i] = 0;  // unused digits
+    if (small) {
+      digit_hist(hs, cand2, count2, prefix, shift, bits, threadIdx.x, kSelThreads);
+    } else {
+      digit_hist(hs, cand2, count2, prefix, shift, bits, blockIdx.x * kSelThreads + threadIdx.x,
+                 gridDim.x * kSelThreads);
+      unsigned int* g = work + 4 + pass * kFineBins;
+      for (int i = threadIdx.x; i < kFineBins; i += kSelThreads)
+        if (hs[i]) atomicAdd(&g[i], hs[i]);
+      grid.sync();
+      for (int i = threadIdx.x * 4; i < kFineBins; i += kSelThreads * 4)
+        *reinterpret_cast<uint4*>(hs + i) = __ldcg(reinterpret_cast<const uint4*>(g + i));
+      __syncthreads();
+    }
+    find_digit<kSelThreads, kFineBins>(hs, rank, &d, &below);
+    prefix |= static_cast<unsigned long long>(d) << shift;
+    rank -= below;
+    if (tr) trace[5 + pass] = clock64();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const double v = dval(prefix);
     *out = mode == 0 ? v : (v > 1e-12 ? 1.0 / v : 1.0);
   }
 }
@@ -465,7 +660,9 @@ __global__ void __launch_bounds__(kThreads) mean_kernel(const double* partials, 
 struct Scratch {
   unsigned long long* keys;  // P
   unsigned long long* cand;  // P (worst case)
+  unsigned long long* cand2; // P (worst case)
   unsigned int* top_hist;    // kTopBins
+  unsigned int* fine;        // select work area: count, 3 x pad, 4 x kFineBins histograms
   SelectState* st;
   double* partials;  // 2 x grid_max
   double* results;   // [8]
@@ -473,6 +670,7 @@ struct Scratch {
   float* rgb_b;
   int grid;       // 256-thread kernels
   int prod_grid;  // producer kernels (1 CTA / SM)
+  int sel_grid;   // cooperative select (co-resident)
 };
 
 int value_grid(hc_ctx ctx, int64_t P) {
@@ -490,6 +688,16 @@ int configure_producers() {
   return HC_OK;
 }
 
+// Co-resident grid of the cooperative select: one CTA per SM.
+int sel_grid_size(hc_ctx ctx) {
+  static int blocks_per_sm = -1;
+  if (blocks_per_sm < 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, select_kernel, kSelThreads, kFineBins * 4) !=
+          cudaSuccess)
+    blocks_per_sm = 0;
+  return std::min(blocks_per_sm, 1) * ctx->sm_count;
+}
+
 int get_scratch(hc_ctx ctx, int64_t P, bool rgb_a, bool rgb_b, Scratch* s) {
   int rc = configure_producers();
   if (rc != HC_OK) return rc;
@@ -498,19 +706,24 @@ int get_scratch(hc_ctx ctx, int64_t P, bool rgb_a, bool rgb_b, Scratch* s) {
   s->prod_grid = static_cast<int>(std::max<int64_t>(
       1, std::min<int64_t>((P + kProdThreads - 1) / kProdThreads, int64_t(ctx->sm_count))));
   const int pmax = std::max(s->grid, s->prod_grid);
-  const size_t kb = up(sizeof(unsigned long long) * P), hb = up(sizeof(unsigned int) * kTopBins),
-               sb = up(sizeof(SelectState)), pb = up(sizeof(double) * 2 * pmax), rb = up(sizeof(double) * 8),
-               cb = up(sizeof(float) * 3 * P);
-  rc = ensure_scratch(ctx, 2 * kb + hb + sb + pb + rb + (rgb_a ? cb : 0) + (rgb_b ? cb : 0));
+  s->sel_grid = sel_grid_size(ctx);
+  if (s->sel_grid < 1) return set_error(HC_EUNSUPPORTED, "select: cooperative grid does not fit");
+  const size_t kb = up(sizeof(unsigned long long) * P), hb = up(sizeof(unsigned int) * (kTopBins + kCoarseBins)),
+               fb = up(sizeof(unsigned int) * (4 + 4 * kFineBins)), sb = up(sizeof(SelectState)),
+               pb = up(sizeof(double) * 2 * pmax), rb = up(sizeof(double) * 8), cb = up(sizeof(float) * 3 * P);
+  rc = ensure_scratch(ctx, 3 * kb + hb + fb + sb + pb + rb + (rgb_a ? cb : 0) + (rgb_b ? cb : 0));
   if (rc != HC_OK) return rc;
-  char* b = static_cast<char*>(ctx->scratch);
+  char* b0 = static_cast<char*>(ctx->scratch);
+  s->cand2 = reinterpret_cast<unsigned long long*>(b0);
+  char* b = b0 + kb;
   s->keys = reinterpret_cast<unsigned long long*>(b);
   s->cand = reinterpret_cast<unsigned long long*>(b + kb);
   s->top_hist = reinterpret_cast<unsigned int*>(b + 2 * kb);
-  s->st = reinterpret_cast<SelectState*>(b + 2 * kb + hb);
-  s->partials = reinterpret_cast<double*>(b + 2 * kb + hb + sb);
-  s->results = reinterpret_cast<double*>(b + 2 * kb + hb + sb + pb);
-  char* rest = b + 2 * kb + hb + sb + pb + rb;
+  s->fine = reinterpret_cast<unsigned int*>(b + 2 * kb + hb);
+  s->st = reinterpret_cast<SelectState*>(b + 2 * kb + hb + fb);
+  s->partials = reinterpret_cast<double*>(b + 2 * kb + hb + fb + sb);
+  s->results = reinterpret_cast<double*>(b + 2 * kb + hb + fb + sb + pb);
+  char* rest = b + 2 * kb + hb + fb + sb + pb + rb;
   s->rgb_a = rgb_a ? reinterpret_cast<float*>(rest) : nullptr;
   s->rgb_b = rgb_b ? reinterpret_cast<float*>(rest + (rgb_a ? cb : 0)) : nullptr;
   return HC_OK;
@@ -528,27 +741,37 @@ int64_t nearest_rank_index(int64_t count, double p) {
 }
 
 int clear_top_hist(hc_ctx ctx, const Scratch& s) {
-  HC_CUDA_TRY(cudaMemsetAsync(s.top_hist, 0, sizeof(unsigned int) * kTopBins, ctx->stream));
+  HC_CUDA_TRY(cudaMemsetAsync(s.top_hist, 0, sizeof(unsigned int) * (kTopBins + kCoarseBins), ctx->stream));
   return HC_OK;
 }
 
 // Exact order statistic `rank` of keys[0, P) whose top histogram is built -> out (mode 0
 // value, 1 exposure).  The top histogram is left intact (several ranks of one key set).
 int select_rank(hc_ctx ctx, const Scratch& s, int64_t P, int64_t rank, int mode, double* out) {
-  top_scan_kernel<<<1, 1024, 0, ctx->stream>>>(s.top_hist, s.st, static_cast<unsigned long long>(rank));
-  HC_CHECK_LAUNCH(ctx, "top_scan_kernel");
-  compact_kernel<<<s.grid, kThreads, 0, ctx->stream>>>(s.keys, P, s.st, s.cand);
-  HC_CHECK_LAUNCH(ctx, "compact_kernel");
-  const int fg = std::min(s.grid, ctx->sm_count * 2);
-  for (int pass = 0; pass < 4; ++pass) {
-    const int shift = kFineShift[pass], bits = kFineBits[pass];
-    fine_hist_kernel<<<fg, kThreads, 0, ctx->stream>>>(s.cand, s.st, shift, bits, ~0ull << (shift + bits));
-    HC_CHECK_LAUNCH(ctx, "fine_hist_kernel");
-    fine_scan_kernel<<<1, 1024, 0, ctx->stream>>>(s.st, shift, bits);
-    HC_CHECK_LAUNCH(ctx, "fine_scan_kernel");
+  static long long* sel_trace = nullptr;  // HC_SELECT_TRACE=1: per-phase clock64 of CTA 0 (debug)
+  if (!sel_trace && std::getenv("HC_SELECT_TRACE")) cudaMalloc(&sel_trace, 24 * sizeof(long long));
+  HC_CUDA_TRY(cudaMemsetAsync(s.fine, 0, sizeof(unsigned int) * (4 + 4 * kFineBins), ctx->stream));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(s.sel_grid);
+  cfg.blockDim = dim3(kSelThreads);
+  cfg.dynamicSmemBytes = kFineBins * 4;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  HC_CUDA_TRY(cudaLaunchKernelEx(&cfg, select_kernel, static_cast<const unsigned long long*>(s.keys), P,
+                                 static_cast<const unsigned int*>(s.top_hist), static_cast<unsigned long long>(rank),
+                                 s.cand, s.cand2, s.fine, mode, out, sel_trace));
+  HC_CHECK_LAUNCH(ctx, "select_kernel");
+  if (sel_trace) {
+    long long h[24];
+    cudaMemcpy(h, sel_trace, sizeof(h), cudaMemcpyDeviceToHost);
+    std::fprintf(stderr, "[hc] select: P=%lld cand=%lld cand2=%lld A=%lld B=%lld sync=%lld pass0=%lld compact2=%lld "
+                 "p1=%lld p2=%lld p3=%lld\n", static_cast<long long>(P), h[20], h[21], h[1] - h[0], h[2] - h[1],
+                 h[3] - h[2], h[4] - h[3], h[5] - h[4], h[6] - h[5], h[7] - h[6], h[8] - h[7]);
   }
-  select_value_kernel<<<1, 32, 0, ctx->stream>>>(s.st, mode, out);
-  HC_CHECK_LAUNCH(ctx, "select_value_kernel");
   return HC_OK;
 }
 
@@ -711,8 +934,9 @@ int hc_delta_e94_report(hc_ctx ctx, const float* xyz_gt, const float* xyz_test, 
   int rc = get_scratch(ctx, P, false, false, &s);
   if (rc != HC_OK) return rc;
   if ((rc = clear_top_hist(ctx, s)) != HC_OK) return rc;
-  de94_kernel<<<s.prod_grid, kProdThreads, kTopSmem, ctx->stream>>>(xyz_gt, xyz_test, P, white_xyz[0], white_xyz[1],
-                                                                     white_xyz[2], de, s.keys, s.top_hist, s.partials);
+  de94_kernel<<<s.prod_grid, kProdThreads, kTopSmem, ctx->stream>>>(xyz_gt, xyz_test, P, 1.0 / white_xyz[0],
+                                                                     white_xyz[1], 1.0 / white_xyz[2], de, s.keys,
+                                                                     s.top_hist, s.partials);
   HC_CHECK_LAUNCH(ctx, "de94_kernel");
   mean_kernel<<<1, kThreads, 0, ctx->stream>>>(s.partials, s.prod_grid, static_cast<double>(P), s.results);
   HC_CHECK_LAUNCH(ctx, "mean_kernel");
