@@ -150,6 +150,24 @@ ColorTriple xyz_to_linear_rgb(const ColorTriple& xyz);
 ChannelImage decode_image(const Codec& c, const ChannelImage& latent);   // k -> n channels
 ChannelImage image_to_linear_rgb(const Codec& c, const ChannelImage& img);  // n -> 3 channels
 
+// ---- colour-metric tail (renderer.hpp:117-133, evaluation.hpp:48-59), computed on the GPU.
+// Images are linear RGB (3 channels) or spectra (n channels), as in the reference.
+double exposure_for(const Codec& c, const ChannelImage& img, double percentile = 99.5);
+std::vector<unsigned char> tonemap_srgb8(Device& dev, const ChannelImage& linear_rgb, double exposure);
+struct ErrorMap {  // renderer.hpp:127-131
+  int width = 0, height = 0;
+  std::vector<float> mse;
+  double mean_mse = 0;
+};
+ErrorMap error_map(const Codec& c, const ChannelImage& a, const ChannelImage& b);
+struct SceneColorReport {  // evaluation.hpp:50-55
+  double mean_de76 = 0;
+  double p95_de76 = 0;
+  double mse = 0;
+  double exposure = 0;
+};
+SceneColorReport scene_color_report(const Codec& c, const ChannelImage& ground_truth, const ChannelImage& test);
+
 // ---- G-buffer latent shading (configs 2/3): one frame, host buffers.
 struct GBuffer {
   int width = 0, height = 0, lights = 0;

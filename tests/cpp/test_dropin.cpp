@@ -217,6 +217,42 @@ int main() {
   gb.palette_index[3] = 77;  // out of range of the 4-entry palette
   CHECK_THROWS_AS(shade_latent(codec, pal_codes, light_codes, gb), std::invalid_argument);
 
+  // colour-metric tail (renderer.cpp:721-802, evaluation.cpp:122-154, colorimetry.cpp:159-162)
+  {
+    ChannelImage grey;
+    grey.width = 4;
+    grey.height = 2;
+    grey.channels = 3;
+    grey.data.assign(24, 0.25f);
+    const double e = exposure_for(codec, grey);
+    const double lum = 0.2126 * 0.25 + 0.7152 * 0.25 + 0.0722 * 0.25;
+    CHECK(e == 1.0 / lum);
+    ChannelImage half = grey;
+    half.data.assign(24, 0.5f);
+    const std::vector<unsigned char> b = tonemap_srgb8(dev, half, 1.0);
+    CHECK(b.size() == 24u && b[0] == 188 && b[23] == 188);  // srgb_encode(0.5) = 0.73535698 -> 188
+    CHECK(tonemap_srgb8(dev, half, 10.0)[5] == 255);
+    ChannelImage dark = grey;
+    dark.data.assign(24, 0.0f);
+    CHECK(exposure_for(codec, dark) == 1.0);
+    const ErrorMap em = error_map(codec, grey, half);
+    CHECK(em.mse.size() == 8u && rel_close(em.mse[0], 0.0625, 1e-7) && rel_close(em.mean_mse, 0.0625, 1e-12));
+    const SceneColorReport same = scene_color_report(codec, half, half);
+    CHECK(same.mean_de76 == 0.0 && same.p95_de76 == 0.0 && same.mse == 0.0);
+    const SceneColorReport diff = scene_color_report(codec, half, grey);
+    CHECK(diff.mean_de76 > 0.0 && diff.p95_de76 == diff.mean_de76 && rel_close(diff.mse, 0.0625, 1e-12));
+    ChannelImage five = grey;
+    five.channels = 5;
+    five.data.assign(40, 0.1f);
+    CHECK_THROWS_AS(exposure_for(codec, five), std::invalid_argument);
+    CHECK_THROWS_AS(tonemap_srgb8(dev, five, 1.0), std::invalid_argument);
+    ChannelImage wide = grey;
+    wide.width = 8;
+    wide.height = 1;
+    CHECK_THROWS_AS(error_map(codec, grey, ChannelImage{3, 1, 3, std::vector<float>(9, 0.f)}), std::invalid_argument);
+    (void)wide;
+  }
+
   std::printf("drop-in: %d checks, %d failures, %lld kernel launches\n", g_checks, g_fail,
               static_cast<long long>(dev.launches()));
   return g_fail ? 1 : 0;
