@@ -187,6 +187,59 @@ int hc_scene_color_report_dev(hc_codec codec, const float* gt, int channels_gt, 
 int hc_delta_e94_report(hc_ctx ctx, const float* xyz_gt, const float* xyz_test, int64_t P,
                         const double* white_xyz, float* de, double* out3);
 
+/* ------------------------------------------------------------------ path tracer
+ * The reference's unidirectional path tracer with next-event estimation
+ * (renderer.hpp:93-107, renderer.cpp:437-659) on a Cornell-style scene: an axis-
+ * aligned box shell with per-wall Lambertian materials, spheres / blocks and
+ * parallelogram area lights (renderer.hpp:16-53).  Spectral curves are given on the
+ * codec's grid (n samples).  Deterministic and identical to the reference's per-sample
+ * streams (Rng::pixel_stream); see DESIGN.md for the parity statement. */
+enum { HC_RENDER_SPECTRAL = 0, HC_RENDER_LATENT = 1, HC_RENDER_RGB = 2 };
+
+typedef struct hc_scene_object {  /* SceneObject (renderer.hpp:32-39) */
+  int kind;                       /* 0 sphere, 1 block */
+  double center[3];
+  double radius;
+  double box_min[3], box_max[3];
+  int material;
+} hc_scene_object;
+
+typedef struct hc_scene_light {   /* SceneLight (renderer.hpp:24-30) */
+  double corner[3], edge_u[3], edge_v[3];
+  const double* spd;              /* n samples, emitted radiance */
+  double scale;
+} hc_scene_light;
+
+typedef struct hc_scene {         /* Scene + Camera (renderer.hpp:16-53) */
+  double cam_position[3], cam_look_at[3], cam_up[3];
+  double cam_vfov_degrees;
+  double box_min[3], box_max[3];
+  int wall_material[6];           /* left, right, floor, ceiling, back, front; -1 = absent */
+  int n_materials;
+  const double* materials;        /* n_materials x n reflectances in [0, 1] */
+  int n_objects;
+  const hc_scene_object* objects;
+  int n_lights;
+  const hc_scene_light* lights;
+} hc_scene;
+
+typedef struct hc_render_job {    /* RenderJob (renderer.hpp:57-72) */
+  int mode;                       /* HC_RENDER_* */
+  int width, height, spp;
+  int max_depth;                  /* -1 = unbounded with Russian roulette from depth 5 */
+  uint64_t seed;
+} hc_render_job;
+
+/* render (renderer.hpp:100-101): image (device, height x width x C floats; C = n spectral,
+ * k latent, 3 rgb), path_hashes (device, width x height, may be NULL), *shading_evals (host,
+ * may be NULL).  The codec supplies the grid (and the codes in latent mode); rgb mode needs
+ * the grid's D65 row `d65` (n doubles, CmfTable).  Synchronous. */
+int hc_render(hc_codec codec, const hc_scene* scene, const hc_render_job* job, const double* d65, float* image,
+              uint64_t* path_hashes, uint64_t* shading_evals);
+/* render_latent_multipass (renderer.hpp:106-107): k/3 three-channel passes, concatenated. */
+int hc_render_latent_multipass(hc_codec codec, const hc_scene* scene, const hc_render_job* job, float* image,
+                               uint64_t* path_hashes, uint64_t* shading_evals);
+
 /* ------------------------------------------------------------------ host-buffer entry points
  * Reference-facing value calls: inputs and outputs in HOST memory (pinned for
  * full copy speed), copies and compute on the context stream, synchronised on

@@ -38,6 +38,7 @@
 #include "hadacodec/rng.hpp"
 #include "hadacodec/spectrum.hpp"
 #include "hadacodec/upsampler.hpp"
+#include "hadacodec_b200.h"  // POD scene / job structs only (ref_render)
 
 using namespace hadacodec;
 
@@ -576,6 +577,82 @@ void ref_delta_e94_report(const float* xyz_gt, const float* xyz_test, int64_t P,
   };
   out3[1] = P > 0 ? rank(50.0) : 0.0;
   out3[2] = P > 0 ? rank(95.0) : 0.0;
+}
+
+// ---------------------------------------------------------------- path tracer
+// the reference's own render / render_latent_multipass
+// (renderer.cpp:437-659) on a scene given as the C ABI's POD structs; latent mode
+// uses the identity-softplus codec (effective weights = E, D exactly).
+namespace {
+Scene to_scene(const hc_scene* sc) {
+  Scene s;
+  s.camera.position = {sc->cam_position[0], sc->cam_position[1], sc->cam_position[2]};
+  s.camera.look_at = {sc->cam_look_at[0], sc->cam_look_at[1], sc->cam_look_at[2]};
+  s.camera.up = {sc->cam_up[0], sc->cam_up[1], sc->cam_up[2]};
+  s.camera.vfov_degrees = sc->cam_vfov_degrees;
+  s.box_min = {sc->box_min[0], sc->box_min[1], sc->box_min[2]};
+  s.box_max = {sc->box_max[0], sc->box_max[1], sc->box_max[2]};
+  for (int w = 0; w < 6; ++w) s.wall_material[w] = sc->wall_material[w];
+  for (int m = 0; m < sc->n_materials; ++m) {
+    SpectralCurve c;
+    for (int i = 0; i < N; ++i) c[i] = sc->materials[m * N + i];
+    s.materials.push_back(c);
+  }
+  for (int o = 0; o < sc->n_objects; ++o) {
+    const hc_scene_object& x = sc->objects[o];
+    SceneObject obj;
+    obj.kind = x.kind == 0 ? SceneObject::Kind::sphere : SceneObject::Kind::block;
+    obj.center = {x.center[0], x.center[1], x.center[2]};
+    obj.radius = x.radius;
+    obj.box_min = {x.box_min[0], x.box_min[1], x.box_min[2]};
+    obj.box_max = {x.box_max[0], x.box_max[1], x.box_max[2]};
+    obj.material = x.material;
+    s.objects.push_back(obj);
+  }
+  for (int l = 0; l < sc->n_lights; ++l) {
+    const hc_scene_light& x = sc->lights[l];
+    SceneLight li;
+    li.corner = {x.corner[0], x.corner[1], x.corner[2]};
+    li.edge_u = {x.edge_u[0], x.edge_u[1], x.edge_u[2]};
+    li.edge_v = {x.edge_v[0], x.edge_v[1], x.edge_v[2]};
+    for (int i = 0; i < N; ++i) li.spd[i] = x.spd[i];
+    li.scale = x.scale;
+    s.lights.push_back(li);
+  }
+  return s;
+}
+}  // namespace
+
+// Returns 0, or 1 when the reference threw std::invalid_argument.
+int ref_render(const hc_scene* sc, const hc_render_job* job, int k, const float* E, const float* D, int multipass,
+               float* image, uint64_t* hashes, uint64_t* evals) {
+  try {
+    const Scene scene = to_scene(sc);
+    RenderJob j;
+    j.mode = job->mode == HC_RENDER_SPECTRAL ? RenderMode::spectral
+                                             : (job->mode == HC_RENDER_LATENT ? RenderMode::latent : RenderMode::rgb);
+    j.width = job->width;
+    j.height = job->height;
+    j.spp = job->spp;
+    j.max_depth = job->max_depth;
+    j.seed = job->seed;
+    j.collect_path_hashes = hashes != nullptr;
+    ChannelImage img;
+    if (multipass) {
+      img = render_latent_multipass(scene, j, identity_codec(E, D, k));
+    } else if (j.mode == RenderMode::latent) {
+      const CodecWeights cw = identity_codec(E, D, k);
+      img = render(scene, j, &cw);
+    } else {
+      img = render(scene, j);
+    }
+    std::memcpy(image, img.data.data(), sizeof(float) * img.data.size());
+    if (hashes) std::memcpy(hashes, img.path_hashes.data(), sizeof(uint64_t) * img.path_hashes.size());
+    if (evals) *evals = img.shading_evals;
+    return 0;
+  } catch (const std::invalid_argument&) {
+    return 1;
+  }
 }
 
 int ref_thread_count() { return render_thread_count(); }

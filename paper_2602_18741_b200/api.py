@@ -19,6 +19,7 @@ of ``libhadacodec_b200.so``.  Calls are enqueued on torch's current stream.
   loss residual (trainer.cpp:49-71)          Codec.hadamard_loss(A, B)
   exposure_for / tonemap_srgb8 / error_map   exposure_for / tonemap_srgb8 / error_map
   scene_color_report (evaluation.cpp)        scene_color_report; delta_e94_report (per pixel)
+  render / render_latent_multipass           render(codec, scene, mode, ..., multipass)
 """
 from __future__ import annotations
 
@@ -304,6 +305,104 @@ def reassemble(ctx: Context, passes: Sequence[torch.Tensor]) -> torch.Tensor:
     ctx.bind_stream()
     _check(_lib.lib().hc_reassemble(ctx.h, C.cast(arr, C.c_void_p), len(passes), P, _p(latent)))
     return latent
+
+
+# ------------------------------------------------------------ path tracer
+class HcSceneObject(C.Structure):
+    _fields_ = [("kind", C.c_int), ("center", C.c_double * 3), ("radius", C.c_double),
+                ("box_min", C.c_double * 3), ("box_max", C.c_double * 3), ("material", C.c_int)]
+
+
+class HcSceneLight(C.Structure):
+    _fields_ = [("corner", C.c_double * 3), ("edge_u", C.c_double * 3), ("edge_v", C.c_double * 3),
+                ("spd", C.POINTER(C.c_double)), ("scale", C.c_double)]
+
+
+class HcScene(C.Structure):
+    _fields_ = [("cam_position", C.c_double * 3), ("cam_look_at", C.c_double * 3), ("cam_up", C.c_double * 3),
+                ("cam_vfov_degrees", C.c_double), ("box_min", C.c_double * 3), ("box_max", C.c_double * 3),
+                ("wall_material", C.c_int * 6), ("n_materials", C.c_int), ("materials", C.POINTER(C.c_double)),
+                ("n_objects", C.c_int), ("objects", C.POINTER(HcSceneObject)), ("n_lights", C.c_int),
+                ("lights", C.POINTER(HcSceneLight))]
+
+
+class HcRenderJob(C.Structure):
+    _fields_ = [("mode", C.c_int), ("width", C.c_int), ("height", C.c_int), ("spp", C.c_int),
+                ("max_depth", C.c_int), ("seed", C.c_uint64)]
+
+
+RENDER_MODES = {"spectral": 0, "latent": 1, "rgb": 2}
+
+
+def scene_struct(scene: dict, n: int):
+    """(HcScene, keep-alive list) from a scene dict with the reference's field names
+    (renderer.hpp:16-53): camera{position, look_at, up, vfov_degrees}, box_min, box_max,
+    wall_material[6], materials [m][n], objects [{kind: 'sphere'|'block', center, radius,
+    box_min, box_max, material}], lights [{corner, edge_u, edge_v, spd [n], scale}]."""
+    keep = []
+    cam = {"position": (0, 1, 3.25), "look_at": (0, 1, 0), "up": (0, 1, 0), "vfov_degrees": 40.0}
+    cam.update(scene.get("camera", {}))
+    mats = np.ascontiguousarray(np.asarray(scene.get("materials", []), dtype=np.float64).reshape(-1, n))
+    keep.append(mats)
+    objs = (HcSceneObject * max(1, len(scene.get("objects", []))))()
+    for i, o in enumerate(scene.get("objects", [])):
+        objs[i].kind = 0 if o.get("kind", "sphere") == "sphere" else 1
+        objs[i].center[:] = o.get("center", (0, 0, 0))
+        objs[i].radius = o.get("radius", 0.0)
+        objs[i].box_min[:] = o.get("box_min", (0, 0, 0))
+        objs[i].box_max[:] = o.get("box_max", (0, 0, 0))
+        objs[i].material = o["material"]
+    lts = (HcSceneLight * max(1, len(scene.get("lights", []))))()
+    for i, l in enumerate(scene.get("lights", [])):
+        spd = np.ascontiguousarray(np.asarray(l["spd"], dtype=np.float64))
+        if spd.size != n:
+            raise ValueError("scene light spd must have n samples")
+        keep.append(spd)
+        lts[i].corner[:] = l["corner"]
+        lts[i].edge_u[:] = l["edge_u"]
+        lts[i].edge_v[:] = l["edge_v"]
+        lts[i].spd = spd.ctypes.data_as(C.POINTER(C.c_double))
+        lts[i].scale = l.get("scale", 1.0)
+    keep += [objs, lts]
+    sc = HcScene()
+    sc.cam_position[:] = cam["position"]
+    sc.cam_look_at[:] = cam["look_at"]
+    sc.cam_up[:] = cam["up"]
+    sc.cam_vfov_degrees = cam["vfov_degrees"]
+    sc.box_min[:] = scene.get("box_min", (-1, 0, -1))
+    sc.box_max[:] = scene.get("box_max", (1, 2, 1))
+    sc.wall_material[:] = scene.get("wall_material", (-1,) * 6)
+    sc.n_materials = mats.shape[0]
+    sc.materials = mats.ctypes.data_as(C.POINTER(C.c_double))
+    sc.n_objects = len(scene.get("objects", []))
+    sc.objects = C.cast(objs, C.POINTER(HcSceneObject))
+    sc.n_lights = len(scene.get("lights", []))
+    sc.lights = C.cast(lts, C.POINTER(HcSceneLight))
+    return sc, keep
+
+
+def render(codec: "Codec", scene: dict, mode: str = "spectral", width: int = 128, height: int = 128, spp: int = 64,
+           max_depth: int = 3, seed: int = 0, path_hashes: bool = False, multipass: bool = False) -> dict:
+    """render / render_latent_multipass (renderer.hpp:100-107): image [H, W, C] f32 on the device
+    (C = n spectral, k latent, 3 rgb), shading_evals, optional per-pixel path hashes."""
+    from .colorimetry import cmf_table
+
+    sc, keep = scene_struct(scene, codec.n)
+    job = HcRenderJob(RENDER_MODES["latent" if multipass else mode], width, height, spp, max_depth, seed)
+    C_ = {"spectral": codec.n, "latent": codec.k, "rgb": 3}["latent" if multipass else mode]
+    img = codec.ctx.empty(height, width, C_)
+    hashes = torch.empty(height, width, dtype=torch.int64, device=img.device) if path_hashes else None
+    evals = C.c_uint64()
+    codec.ctx.bind_stream()
+    if multipass:
+        _check(_lib.lib().hc_render_latent_multipass(codec.h, C.addressof(sc), C.addressof(job), _p(img), _p(hashes),
+                                                     C.addressof(evals)))
+    else:
+        d65 = np.ascontiguousarray(cmf_table(codec.n)["d65"])
+        _check(_lib.lib().hc_render(codec.h, C.addressof(sc), C.addressof(job), _np_ptr(d65), _p(img), _p(hashes),
+                                    C.addressof(evals)))
+    del keep
+    return {"image": img, "path_hashes": hashes, "shading_evals": evals.value}
 
 
 # ------------------------------------------------------------ colour-metric tail (SURVEY §8f row 1)

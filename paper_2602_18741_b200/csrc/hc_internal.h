@@ -32,6 +32,8 @@ struct hc_codec_s {
   double dlambda = 0.0;
   std::vector<float> E;       // k x n
   std::vector<float> D;       // n x k
+  std::vector<double> Ed;     // k x n effective weights in fp64 (renderer compile_scene)
+  std::vector<double> Dd;     // n x k
   std::vector<double> cmf;    // 3 x n (unscaled)
   std::vector<float> Mxyz;    // 3 x k = dlambda * CMF * D (computed in f64)
   std::vector<float> cmf_dl;  // 3 x n = dlambda * CMF

@@ -319,15 +319,17 @@ int hc_ctx_synchronize(hc_ctx ctx) {
 int64_t hc_ctx_launch_count(hc_ctx ctx) { return ctx ? ctx->launches.load() : -1; }
 
 // ------------------------------------------------------------------ codec
-static int codec_finish(hc_ctx ctx, int k, int n, std::vector<float> E, std::vector<float> D,
+static int codec_finish(hc_ctx ctx, int k, int n, std::vector<double> Ed, std::vector<double> Dd,
                         const double* cmf, double dlambda, hc_codec* out) {
   hc_codec c = new hc_codec_s();
   c->ctx = ctx;
   c->k = k;
   c->n = n;
   c->dlambda = dlambda;
-  c->E = std::move(E);
-  c->D = std::move(D);
+  c->E.assign(Ed.begin(), Ed.end());
+  c->D.assign(Dd.begin(), Dd.end());
+  c->Ed = std::move(Ed);
+  c->Dd = std::move(Dd);
   c->cmf.assign(cmf, cmf + 3 * n);
   c->Mxyz.resize(3 * k);
   c->cmf_dl.resize(3 * n);
@@ -360,9 +362,9 @@ int hc_codec_create(hc_ctx ctx, int k, int n, const float* E, const float* D, co
                     double dlambda, hc_codec* out) {
   int rc = validate_dims(ctx, k, n, E, D, cmf, dlambda, out);
   if (rc != HC_OK) return rc;
-  std::vector<float> e(E, E + k * n), d(D, D + n * k);
-  for (float v : e) HC_REQUIRE(std::isfinite(v), HC_EINVAL, "codec weights: non-finite encoder entry");
-  for (float v : d) HC_REQUIRE(std::isfinite(v), HC_EINVAL, "codec weights: non-finite decoder entry");
+  std::vector<double> e(E, E + k * n), d(D, D + n * k);
+  for (double v : e) HC_REQUIRE(std::isfinite(v), HC_EINVAL, "codec weights: non-finite encoder entry");
+  for (double v : d) HC_REQUIRE(std::isfinite(v), HC_EINVAL, "codec weights: non-finite decoder entry");
   return codec_finish(ctx, k, n, std::move(e), std::move(d), cmf, dlambda, out);
 }
 
@@ -371,12 +373,12 @@ int hc_codec_create_raw(hc_ctx ctx, int k, int n, double beta, const double* raw
   int rc = validate_dims(ctx, k, n, raw_enc, raw_dec, cmf, dlambda, out);
   if (rc != HC_OK) return rc;
   HC_REQUIRE(beta > 0.0, HC_EINVAL, "codec weights: beta must be positive");
-  std::vector<float> e(k * n), d(n * k);
+  std::vector<double> e(k * n), d(n * k);
   for (int i = 0; i < k * n; ++i) {
     HC_REQUIRE(std::isfinite(raw_enc[i]), HC_EINVAL, "codec weights: non-finite encoder entry");
     HC_REQUIRE(std::isfinite(raw_dec[i]), HC_EINVAL, "codec weights: non-finite decoder entry");
-    e[i] = static_cast<float>(softplus(raw_enc[i], beta));
-    d[i] = static_cast<float>(softplus(raw_dec[i], beta));
+    e[i] = softplus(raw_enc[i], beta);  // effective_weights (codec.cpp:21-34), kept in fp64
+    d[i] = softplus(raw_dec[i], beta);
   }
   return codec_finish(ctx, k, n, std::move(e), std::move(d), cmf, dlambda, out);
 }

@@ -160,3 +160,25 @@ def chain_np(seed: int, first: int, P: int, spp: int, n_pal: int, n_ill: int):
 
 def uniform_np(seed: int, purpose: str, first: int, count: int) -> np.ndarray:
     return ctr_u24(stream_key(seed, purpose), np.arange(first, first + count, dtype=np.uint64))
+
+
+def cornell_scene(n: int, block: bool = False) -> dict:
+    """The reference render benchmark's enclosed test scene (benchmarks/bm_render.cpp:14-36):
+    grey / red / green walls, open front, a grey sphere and a ceiling area light; with
+    `block`, a second (axis-aligned box) object exercises hit_block (renderer.cpp:342-381)."""
+    grey = [0.7] * n
+    red = gaussian_curve(620.0, 60.0, 0.6, n)
+    green = gaussian_curve(540.0, 60.0, 0.6, n)
+    scene = {
+        "materials": [grey, red, green],
+        "wall_material": [1, 2, 0, 0, 0, -1],
+        "objects": [{"kind": "sphere", "center": (0.35, 0.4, -0.3), "radius": 0.4, "material": 0}],
+        "lights": [{"corner": (-0.25, 1.999, -0.25), "edge_u": (0.5, 0.0, 0.0), "edge_v": (0.0, 0.0, 0.5),
+                    "spd": [1.0] * n, "scale": 12.0}],
+    }
+    if block:
+        scene["objects"].append({"kind": "block", "box_min": (-0.7, 0.0, -0.6), "box_max": (-0.2, 0.9, -0.1),
+                                 "material": 1})
+        scene["lights"].append({"corner": (0.9, 1.2, 0.5), "edge_u": (0.0, 0.0, -0.3), "edge_v": (0.0, -0.3, 0.0),
+                                "spd": gaussian_curve(580.0, 80.0, 1.0, n), "scale": 3.0})
+    return scene
