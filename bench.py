@@ -60,6 +60,12 @@ CONFIGS = {
     "6": dict(name="1920x1080 colour-metric tail: scene_color_report(naive n=81 sRGB, latent k=6 sRGB) "
                    "+ tonemap_srgb8 preview of the latent frame", W=1920, H=1080, k=6, L=8, unit="Mpixel/s",
               bytes_per_unit=27, rot=8),
+    # the reference's path tracer, latent k = 6 (naive: spectral n = 81).
+    # Units are pixel-samples; the algorithmic bytes are the image writes (k floats per pixel
+    # over spp samples), so the HBM fraction is ~0: the tracer is fp64 / latency bound.
+    "7": dict(name="Cornell box path trace (bm_render scene + block + 2nd light), 256x256, 64 spp, depth 3, "
+                   "latent k=6 (naive: spectral n=81)", W=256, H=256, spp=64, depth=3, k=6,
+              unit="M samples/s", bytes_per_unit=6 * 4 / 64, rot=1, graph=False),
 }
 
 
@@ -211,6 +217,24 @@ def cpu_reference_run(cfg_key: str, budget_s: float, threads: int = 0, rank: int
             ref.ref_mlp_forward(rgb, P, 64, 6, w["w1"], w["b1"], w["w2"], w["b2"], w["w3"], w["b3"], out, nthreads)
 
         sample = f"{P} texels (8 rows)"
+    elif cfg_key == "7":
+        import ctypes as C
+
+        from paper_2602_18741_b200 import api as _api
+
+        scene = synth.cornell_scene(N_SPEC, block=True)
+        sc, keep = _api.scene_struct(scene, N_SPEC)
+        W = H = 64
+        spp = 16
+        job = _api.HcRenderJob(1, W, H, spp, cfg["depth"], SEED + rank)
+        img = np.zeros(W * H * k, np.float32)
+        ev = C.c_uint64()
+        P = W * H * spp
+
+        def run():
+            ref.ref_render(C.addressof(sc), C.addressof(job), k, E, D, 0, img, None, C.byref(ev))
+
+        sample = f"{W}x{H} px x {spp} spp latent render of the reference (render_compiled's thread pool)"
     elif cfg_key == "6":
         # the reference's own scene_color_report + tonemap_srgb8 (single-threaded as written)
         L, W = cfg["L"], cfg["W"]
@@ -364,6 +388,16 @@ class Workload:
                 gt, test, out, prev = self.sets[i % R]
                 api.scene_color_report_dev(codec, gt, test, out=out, preview=prev)
             self.step = step
+        elif cfg_key == "7":
+            W, H, spp, depth = cfg["W"], cfg["H"], cfg["spp"], cfg["depth"]
+            scene = synth.cornell_scene(N_SPEC, block=True)
+            mode = "spectral" if naive else "latent"
+            self.units = W * H * spp
+            self.sets.append({"rgb": None})
+
+            def step(i):  # weak scaling: every rank renders its own frame (seed per rank)
+                api.render(codec, scene, mode, W, H, spp, depth, seed=SEED + rank)
+            self.step = step
         elif cfg_key == "1":
             first, P = span(cfg["units"], 1)
             for r in range(R):
@@ -427,10 +461,31 @@ class Workload:
         self.R = R
 
 
+class _PlainReplay:
+    """Stand-in for a CUDA graph for configs whose step cannot be captured (the path
+    tracer compiles the scene on the host and synchronises): replay() runs the steps."""
+
+    def __init__(self, wl, n: int):
+        self.wl, self.n = wl, n
+
+    def replay(self):
+        for i in range(self.n):
+            self.wl.step(i)
+
+
 def time_graph(torch, wl, steps: int, warmup: int, stream) -> tuple[float, int]:
     """Capture R steps (one per buffer set) in a CUDA graph; replay to cover `steps`.
     Returns (elapsed ms over exactly `steps` steps, launches per step)."""
     R = wl.R
+    if not wl.cfg.get("graph", True):
+        with torch.cuda.stream(stream):
+            for i in range(max(warmup, 1)):
+                wl.step(i)
+            torch.cuda.synchronize()
+            l0 = wl.codec.ctx.launches
+            wl.step(0)
+            torch.cuda.synchronize()
+        return _PlainReplay(wl, min(R, steps)), wl.codec.ctx.launches - l0, min(R, steps)
     reps = max(1, steps // R)
     assert reps * R == steps or steps < R, "steps must be a multiple of the rotation"
     ctx = wl.codec.ctx
@@ -544,17 +599,17 @@ def run_ours(args) -> int:
 
     extra = {}
     # ---- naive n = 81 comparison on the same inputs (configs 2 / 4)
-    if args.config in ("2", "3", "4") and not args.no_naive:
+    if args.config in ("2", "3", "4", "7") and not args.no_naive:
         wn = Workload.__new__(Workload)
         wn.__dict__.update(wl.__dict__)
         wn_step_ours = wl.step
         # rebuild the step closure with the naive path over the same buffers
         with torch.cuda.stream(stream):
             wl2 = Workload(api, ctx, args.config, rank, naive=True, world=world, strong=args.scaling == "strong")
-        gn, _, nn = time_graph(torch, wl2, steps if args.config != "4" else R, 1, stream)
+        gn, _, nn = time_graph(torch, wl2, steps if args.config not in ("4", "7") else R, 1, stream)
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        nreps = max(1, (steps if args.config != "4" else R) // nn)
+        nreps = max(1, (steps if args.config not in ("4", "7") else R) // nn)
         with torch.cuda.stream(stream):
             e0.record(stream)
             for _ in range(nreps):
@@ -644,9 +699,13 @@ def run_ours(args) -> int:
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "bf16" if args.config == "5a" else "f32", "data": "synthetic (seeded, DESIGN.md Inputs)",
             "config": {"workload": cfg["name"], "config_id": args.config, "units_per_gpu": wl.units,
-                       "l2": f"{R} rotating input/output buffer sets"
-                             f" ({'each' if R == 1 else 'rotation'} > 2x 126 MB L2)",
-                       "timing": "CUDA graph of the step replayed K times; CUDA events; max over ranks",
+                       "l2": (f"{R} rotating input/output buffer sets"
+                              f" ({'each' if R == 1 else 'rotation'} > 2x 126 MB L2)") if cfg.get("graph", True)
+                             else "compute-bound step; scene tables are KB-sized (no L2 rotation needed)",
+                       "timing": ("CUDA graph of the step replayed K times; CUDA events; max over ranks"
+                                  if cfg.get("graph", True) else
+                                  "K synchronous render calls (host scene compile included); CUDA events; "
+                                  "max over ranks"),
                        "parallelism": f"row bands, {args.scaling} scaling, {world} rank(s), no data-path collective"},
             "roofline": roof,
             "cpu_baseline": cpu,

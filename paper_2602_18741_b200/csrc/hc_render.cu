@@ -18,6 +18,7 @@
 // the read-only path.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -360,106 +361,117 @@ __device__ inline bool intersect(const RenderParams& p, const Ray& ray, double t
 }
 
 // ---------------------------------------------------------------- path kernel (renderer.cpp:448-563)
+// One sample of one pixel (renderer.cpp:456-559): radiance rad[C]; shading units added to
+// *evals; the hit sequence folded into *hash when hash != nullptr.
+template <int C>
+__device__ __forceinline__ void trace_sample(const RenderParams& p, int x, int y, int s, float* rad,
+                                             unsigned long long* evals, uint64_t* hash) {
+  float thr[C];
+  const int nl = p.n_lights;
+  Rng geo = Rng::pixel(p.seed, x, y, s, 0);
+  Rng rr = Rng::pixel(p.seed, x, y, s, 1);
+  const double jx = geo.uniform();
+  const double jy = geo.uniform();
+  Ray ray;
+  {  // camera_ray (renderer.cpp:63-68)
+    const double px = x + jx, py = y + jy;
+    const double u = (2.0 * px / p.width - 1.0) * p.cam.tan_half * p.cam.aspect;
+    const double v = (1.0 - 2.0 * py / p.height) * p.cam.tan_half;
+    ray = {p.cam.origin, normalize(add(add(p.cam.forward, mul(p.cam.right, u)), mul(p.cam.up, v)))};
+  }
+  for (int c = 0; c < C; ++c) {
+    thr[c] = 1.0f;
+    rad[c] = 0.0f;
+  }
+  for (int depth = 0;; ++depth) {
+    Hit hit;
+    if (!intersect(p, ray, kRayEpsilon, INFINITY, &hit)) break;
+    if (hash) {  // hash_hit (renderer.cpp:436-442)
+      *hash = fnv_bytes(*hash, &hit.p.x, 8);
+      *hash = fnv_bytes(*hash, &hit.p.y, 8);
+      *hash = fnv_bytes(*hash, &hit.p.z, 8);
+      const uint32_t prim = static_cast<uint32_t>(hit.prim);
+      *hash = fnv_bytes(*hash, &prim, 4);
+    }
+    if (hit.light >= 0) {  // emitters seen directly by the camera only
+      if (depth == 0 && dot(ray.d, hit.n) < 0.0) {
+        const float* le = p.emission + hit.light * C;
+        for (int c = 0; c < C; ++c) rad[c] += thr[c] * __ldg(le + c);
+      }
+      break;
+    }
+    if (p.max_depth >= 0 && depth >= p.max_depth) break;
+    *evals += p.eval_unit;
+    const V3 n_sh = dot(hit.n, ray.d) < 0.0 ? hit.n : mul(hit.n, -1.0);
+    const float* albedo = p.albedo + hit.material * C;
+
+    if (nl > 0) {  // next-event estimation: one area sample on one light
+      const uint32_t li = geo.index(static_cast<uint32_t>(nl));
+      const double lu = geo.uniform();
+      const double lv = geo.uniform();
+      const LightG lg = p.lights[li];
+      const V3 lp = add(add(lg.corner, mul(lg.eu, lu)), mul(lg.ev, lv));
+      const V3 d = sub(lp, hit.p);
+      const double dist2 = dot(d, d);
+      const double dist = sqrt(dist2);
+      if (dist > kRayEpsilon) {
+        const V3 wi = mul(d, 1.0 / dist);
+        const double cos_s = dot(n_sh, wi);
+        const double cos_l = -dot(lg.n, wi);
+        if (cos_s > 0.0 && cos_l > 0.0) {
+          Hit occ;
+          if (!intersect(p, {hit.p, wi}, kRayEpsilon, dist - kRayEpsilon, &occ)) {
+            const double geom = cos_s * cos_l / dist2 * lg.area * static_cast<double>(nl) / kPi;
+            const float w = static_cast<float>(geom);
+            const float* le = p.emission + li * C;
+            for (int c = 0; c < C; ++c) rad[c] += thr[c] * __ldg(albedo + c) * __ldg(le + c) * w;
+          }
+        }
+      }
+    }
+    if (p.max_depth >= 0 && depth + 1 >= p.max_depth) break;
+
+    // cosine-weighted continuation; throughput picks up the bare albedo
+    const double u1 = geo.uniform();
+    const double u2 = geo.uniform();
+    const double r = sqrt(u1);
+    const double phi = 2.0 * kPi * u2;
+    const V3 tangent = fabs(n_sh.x) > 0.9 ? normalize(cross({0, 1, 0}, n_sh)) : normalize(cross({1, 0, 0}, n_sh));
+    const V3 bitangent = cross(n_sh, tangent);
+    const double om = 1.0 - u1;
+    double sin_phi, cos_phi;
+    sincos_cr(phi, &sin_phi, &cos_phi);
+    const V3 dir = normalize(add(add(mul(tangent, r * cos_phi), mul(bitangent, r * sin_phi)),
+                                 mul(n_sh, sqrt(om > 0.0 ? om : 0.0))));
+    for (int c = 0; c < C; ++c) thr[c] *= __ldg(albedo + c);
+
+    if (p.max_depth < 0 && depth >= 5) {  // Russian roulette on throughput luminance
+      float acc = 0.0f;
+      for (int c = 0; c < C; ++c) acc += __ldg(p.luma + c) * thr[c];
+      const float q = acc < 0.05f ? 0.05f : (acc > 1.0f ? 1.0f : acc);
+      if (rr.uniform() >= static_cast<double>(q)) break;
+      const float inv_q = 1.0f / q;
+      for (int c = 0; c < C; ++c) thr[c] *= inv_q;
+    }
+    ray = {hit.p, dir};
+  }
+}
+
+// Pixel-serial form: one thread per pixel loops over its samples, like a reference
+// worker (needed when path hashes are collected: the hash chains the hits of all samples
+// in order).
 template <int C>
 __global__ void __launch_bounds__(128) render_kernel(const __grid_constant__ RenderParams p) {
   const int64_t pix = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (pix >= static_cast<int64_t>(p.width) * p.height) return;
   const int x = static_cast<int>(pix % p.width), y = static_cast<int>(pix / p.width);
-  float thr[C], rad[C];
+  float rad[C];
   double accum[C];
   for (int c = 0; c < C; ++c) accum[c] = 0.0;
   uint64_t pixel_hash = 0xcbf29ce484222325ull;
   unsigned long long evals = 0;
-  const int nl = p.n_lights;
-
   for (int s = 0; s < p.spp; ++s) {
-    Rng geo = Rng::pixel(p.seed, x, y, s, 0);
-    Rng rr = Rng::pixel(p.seed, x, y, s, 1);
-    const double jx = geo.uniform();
-    const double jy = geo.uniform();
-    Ray ray;
-    {  // camera_ray (renderer.cpp:63-68)
-      const double px = x + jx, py = y + jy;
-      const double u = (2.0 * px / p.width - 1.0) * p.cam.tan_half * p.cam.aspect;
-      const double v = (1.0 - 2.0 * py / p.height) * p.cam.tan_half;
-      ray = {p.cam.origin, normalize(add(add(p.cam.forward, mul(p.cam.right, u)), mul(p.cam.up, v)))};
-    }
-    for (int c = 0; c < C; ++c) {
-      thr[c] = 1.0f;
-      rad[c] = 0.0f;
-    }
-    for (int depth = 0;; ++depth) {
-      Hit hit;
-      if (!intersect(p, ray, kRayEpsilon, INFINITY, &hit)) break;
-      if (p.hashes) {  // hash_hit (renderer.cpp:436-442)
-        pixel_hash = fnv_bytes(pixel_hash, &hit.p.x, 8);
-        pixel_hash = fnv_bytes(pixel_hash, &hit.p.y, 8);
-        pixel_hash = fnv_bytes(pixel_hash, &hit.p.z, 8);
-        const uint32_t prim = static_cast<uint32_t>(hit.prim);
-        pixel_hash = fnv_bytes(pixel_hash, &prim, 4);
-      }
-      if (hit.light >= 0) {  // emitters seen directly by the camera only
-        if (depth == 0 && dot(ray.d, hit.n) < 0.0) {
-          const float* le = p.emission + hit.light * C;
-          for (int c = 0; c < C; ++c) rad[c] += thr[c] * __ldg(le + c);
-        }
-        break;
-      }
-      if (p.max_depth >= 0 && depth >= p.max_depth) break;
-      evals += p.eval_unit;
-      const V3 n_sh = dot(hit.n, ray.d) < 0.0 ? hit.n : mul(hit.n, -1.0);
-      const float* albedo = p.albedo + hit.material * C;
-
-      if (nl > 0) {  // next-event estimation: one area sample on one light
-        const uint32_t li = geo.index(static_cast<uint32_t>(nl));
-        const double lu = geo.uniform();
-        const double lv = geo.uniform();
-        const LightG lg = p.lights[li];
-        const V3 lp = add(add(lg.corner, mul(lg.eu, lu)), mul(lg.ev, lv));
-        const V3 d = sub(lp, hit.p);
-        const double dist2 = dot(d, d);
-        const double dist = sqrt(dist2);
-        if (dist > kRayEpsilon) {
-          const V3 wi = mul(d, 1.0 / dist);
-          const double cos_s = dot(n_sh, wi);
-          const double cos_l = -dot(lg.n, wi);
-          if (cos_s > 0.0 && cos_l > 0.0) {
-            Hit occ;
-            if (!intersect(p, {hit.p, wi}, kRayEpsilon, dist - kRayEpsilon, &occ)) {
-              const double geom = cos_s * cos_l / dist2 * lg.area * static_cast<double>(nl) / kPi;
-              const float w = static_cast<float>(geom);
-              const float* le = p.emission + li * C;
-              for (int c = 0; c < C; ++c) rad[c] += thr[c] * __ldg(albedo + c) * __ldg(le + c) * w;
-            }
-          }
-        }
-      }
-      if (p.max_depth >= 0 && depth + 1 >= p.max_depth) break;
-
-      // cosine-weighted continuation; throughput picks up the bare albedo
-      const double u1 = geo.uniform();
-      const double u2 = geo.uniform();
-      const double r = sqrt(u1);
-      const double phi = 2.0 * kPi * u2;
-      const V3 tangent = fabs(n_sh.x) > 0.9 ? normalize(cross({0, 1, 0}, n_sh)) : normalize(cross({1, 0, 0}, n_sh));
-      const V3 bitangent = cross(n_sh, tangent);
-      const double om = 1.0 - u1;
-      double sin_phi, cos_phi;
-      sincos_cr(phi, &sin_phi, &cos_phi);
-      const V3 dir = normalize(add(add(mul(tangent, r * cos_phi), mul(bitangent, r * sin_phi)),
-                                   mul(n_sh, sqrt(om > 0.0 ? om : 0.0))));
-      for (int c = 0; c < C; ++c) thr[c] *= __ldg(albedo + c);
-
-      if (p.max_depth < 0 && depth >= 5) {  // Russian roulette on throughput luminance
-        float acc = 0.0f;
-        for (int c = 0; c < C; ++c) acc += __ldg(p.luma + c) * thr[c];
-        const float q = acc < 0.05f ? 0.05f : (acc > 1.0f ? 1.0f : acc);
-        if (rr.uniform() >= static_cast<double>(q)) break;
-        const float inv_q = 1.0f / q;
-        for (int c = 0; c < C; ++c) thr[c] *= inv_q;
-      }
-      ray = {hit.p, dir};
-    }
+    trace_sample<C>(p, x, y, s, rad, &evals, p.hashes ? &pixel_hash : nullptr);
     for (int c = 0; c < C; ++c) accum[c] += static_cast<double>(rad[c]);
   }
   const double inv_spp = 1.0 / p.spp;
@@ -467,6 +479,45 @@ __global__ void __launch_bounds__(128) render_kernel(const __grid_constant__ Ren
   for (int c = 0; c < C; ++c) out[c] = static_cast<float>(accum[c] * inv_spp);
   if (p.hashes) p.hashes[pix] = pixel_hash;
   if (evals) atomicAdd(p.evals, evals);
+}
+
+// Sample-parallel form: one thread per (sample, pixel) of a chunk of samples writes its
+// radiance; accumulate_kernel then adds the chunk's samples to the per-pixel fp64 sums in
+// sample order, so the image is bit-identical to the pixel-serial form with spp x the
+// parallelism.
+template <int C>
+__global__ void __launch_bounds__(128) render_samples_kernel(const __grid_constant__ RenderParams p, int s0, int ns,
+                                                             float* __restrict__ samples) {
+  const int64_t P = static_cast<int64_t>(p.width) * p.height;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long evals = 0;
+  if (t < P * ns) {
+    const int64_t pix = t % P;
+    const int j = static_cast<int>(t / P);
+    const int x = static_cast<int>(pix % p.width), y = static_cast<int>(pix / p.width);
+    float rad[C];
+    trace_sample<C>(p, x, y, s0 + j, rad, &evals, nullptr);
+    float* out = samples + (static_cast<int64_t>(j) * P + pix) * C;
+    for (int c = 0; c < C; ++c) out[c] = rad[c];
+  }
+  // one atomic per warp
+  for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
+  if ((threadIdx.x & 31) == 0 && evals) atomicAdd(p.evals, evals);
+}
+
+template <int C>
+__global__ void accumulate_kernel(const float* __restrict__ samples, int64_t P, int ns, double* __restrict__ accum) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P * C; i += int64_t(gridDim.x) * blockDim.x) {
+    double a = accum[i];
+    for (int j = 0; j < ns; ++j) a += static_cast<double>(samples[j * P * C + i]);
+    accum[i] = a;
+  }
+}
+
+__global__ void finalize_kernel(const double* __restrict__ accum, int64_t count, double inv_spp,
+                                float* __restrict__ image) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < count; i += int64_t(gridDim.x) * blockDim.x)
+    image[i] = static_cast<float>(accum[i] * inv_spp);
 }
 
 // ---------------------------------------------------------------- compile_scene (renderer.cpp:201-272)
@@ -647,6 +698,36 @@ struct DevVec {
   }
 };
 
+// Pixel-serial launch when path hashes are collected, else sample-parallel in chunks of
+// samples whose radiance buffers stay under ~256 MB.
+template <int C>
+int launch_render(hc_ctx ctx, const RenderParams& p) {
+  const int64_t P = static_cast<int64_t>(p.width) * p.height;
+  if (p.hashes) {
+    render_kernel<C><<<static_cast<int>((P + 127) / 128), 128, 0, ctx->stream>>>(p);
+    HC_CHECK_LAUNCH(ctx, "render_kernel");
+    return HC_OK;
+  }
+  const int64_t per_sample = P * C * static_cast<int64_t>(sizeof(float));
+  const int ns = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(p.spp, (int64_t(256) << 20) / per_sample)));
+  int rc = ensure_scratch(ctx, static_cast<size_t>(P) * C * sizeof(double) + static_cast<size_t>(ns) * per_sample + 256);
+  if (rc != HC_OK) return rc;
+  double* accum = static_cast<double*>(ctx->scratch);
+  float* samples = reinterpret_cast<float*>(static_cast<char*>(ctx->scratch) + ((P * C * sizeof(double) + 255) & ~size_t(255)));
+  HC_CUDA_TRY(cudaMemsetAsync(accum, 0, sizeof(double) * P * C, ctx->stream));
+  const int agrid = static_cast<int>(std::min<int64_t>((P * C + 255) / 256, int64_t(ctx->sm_count) * 16));
+  for (int s0 = 0; s0 < p.spp; s0 += ns) {
+    const int n = std::min(ns, p.spp - s0);
+    render_samples_kernel<C><<<static_cast<int>((P * n + 127) / 128), 128, 0, ctx->stream>>>(p, s0, n, samples);
+    HC_CHECK_LAUNCH(ctx, "render_samples_kernel");
+    accumulate_kernel<C><<<agrid, 256, 0, ctx->stream>>>(samples, P, n, accum);
+    HC_CHECK_LAUNCH(ctx, "accumulate_kernel");
+  }
+  finalize_kernel<<<agrid, 256, 0, ctx->stream>>>(accum, P * C, 1.0 / p.spp, p.image);
+  HC_CHECK_LAUNCH(ctx, "finalize_kernel");
+  return HC_OK;
+}
+
 // Render one compiled scene into image (H x W x cs.channels, device).
 int render_compiled(hc_ctx ctx, const Compiled& cs, const hc_render_job* job, float* image, uint64_t* hashes,
                     unsigned long long* evals_dev) {
@@ -679,17 +760,15 @@ int render_compiled(hc_ctx ctx, const Compiled& cs, const hc_render_job* job, fl
   p.image = image;
   p.hashes = hashes;
   p.evals = evals_dev;
-  const int64_t P = static_cast<int64_t>(job->width) * job->height;
-  const int grid = static_cast<int>((P + 127) / 128);
   switch (cs.channels) {
-    case 3: render_kernel<3><<<grid, 128, 0, ctx->stream>>>(p); break;
-    case 6: render_kernel<6><<<grid, 128, 0, ctx->stream>>>(p); break;
-    case 9: render_kernel<9><<<grid, 128, 0, ctx->stream>>>(p); break;
-    case 47: render_kernel<47><<<grid, 128, 0, ctx->stream>>>(p); break;
-    case 81: render_kernel<81><<<grid, 128, 0, ctx->stream>>>(p); break;
+    case 3: rc = launch_render<3>(ctx, p); break;
+    case 6: rc = launch_render<6>(ctx, p); break;
+    case 9: rc = launch_render<9>(ctx, p); break;
+    case 47: rc = launch_render<47>(ctx, p); break;
+    case 81: rc = launch_render<81>(ctx, p); break;
     default: return set_error(HC_EUNSUPPORTED, "renderer: compiled for 3, 6, 9, 47 or 81 channels");
   }
-  HC_CHECK_LAUNCH(ctx, "render_kernel");
+  if (rc != HC_OK) return rc;
   HC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // the scene tables are freed on return
   return HC_OK;
 }
@@ -722,13 +801,11 @@ int hc_render(hc_codec codec, const hc_scene* scene, const hc_render_job* job, c
   try {
     Compiled cs = compile_scene(codec, scene, job->mode, d65);
     cs.frame = camera_frame(scene, job->width, job->height);
-    rc = ensure_scratch(ctx, sizeof(unsigned long long));
+    DevVec<unsigned long long> evals;  // own buffer: render_compiled uses ctx->scratch
+    if ((rc = evals.put(std::vector<unsigned long long>(1, 0ull), ctx->stream)) != HC_OK) return rc;
+    rc = render_compiled(ctx, cs, job, image, path_hashes, evals.p);
     if (rc != HC_OK) return rc;
-    auto* evals = static_cast<unsigned long long*>(ctx->scratch);
-    HC_CUDA_TRY(cudaMemsetAsync(evals, 0, sizeof(unsigned long long), ctx->stream));
-    rc = render_compiled(ctx, cs, job, image, path_hashes, evals);
-    if (rc != HC_OK) return rc;
-    if (shading_evals) HC_CUDA_TRY(cudaMemcpy(shading_evals, evals, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    if (shading_evals) HC_CUDA_TRY(cudaMemcpy(shading_evals, evals.p, sizeof(uint64_t), cudaMemcpyDeviceToHost));
   } catch (const std::invalid_argument& e) {
     return set_error(HC_EINVAL, e.what());
   }
@@ -746,21 +823,20 @@ int hc_render_latent_multipass(hc_codec codec, const hc_scene* scene, const hc_r
   try {
     Compiled full = compile_scene(codec, scene, HC_RENDER_LATENT, nullptr);
     full.frame = camera_frame(scene, job->width, job->height);
-    rc = ensure_scratch(ctx, sizeof(unsigned long long) * 2 + sizeof(float) * 3 * P);
-    if (rc != HC_OK) return rc;
-    auto* evals = static_cast<unsigned long long*>(ctx->scratch);
-    float* pass_img = reinterpret_cast<float*>(static_cast<char*>(ctx->scratch) + 2 * sizeof(unsigned long long));
-    HC_CUDA_TRY(cudaMemsetAsync(evals, 0, sizeof(unsigned long long), ctx->stream));
+    DevVec<unsigned long long> evals;  // own buffers: render_compiled uses ctx->scratch
+    DevVec<float> pass_img;
+    if ((rc = evals.put(std::vector<unsigned long long>(1, 0ull), ctx->stream)) != HC_OK) return rc;
+    if ((rc = pass_img.put(std::vector<float>(static_cast<size_t>(3 * P), 0.0f), ctx->stream)) != HC_OK) return rc;
     for (int b = 0; b < k / 3; ++b) {  // renderer.cpp:641-657
       const Compiled pass = slice_pass(full, b);
-      rc = render_compiled(ctx, pass, job, pass_img, b == 0 ? path_hashes : nullptr, evals);
+      rc = render_compiled(ctx, pass, job, pass_img.p, b == 0 ? path_hashes : nullptr, evals.p);
       if (rc != HC_OK) return rc;
       interleave_pass_kernel<<<static_cast<int>(std::min<int64_t>((3 * P + 255) / 256, 4096)), 256, 0, ctx->stream>>>(
-          pass_img, P, k, b, image);
+          pass_img.p, P, k, b, image);
       HC_CHECK_LAUNCH(ctx, "interleave_pass_kernel");
     }
     HC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
-    if (shading_evals) HC_CUDA_TRY(cudaMemcpy(shading_evals, evals, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    if (shading_evals) HC_CUDA_TRY(cudaMemcpy(shading_evals, evals.p, sizeof(uint64_t), cudaMemcpyDeviceToHost));
   } catch (const std::invalid_argument& e) {
     return set_error(HC_EINVAL, e.what());
   }

@@ -58,11 +58,13 @@ def test_render_bit_exact_vs_reference(api, ctx, mode, n, k, depth, block, multi
     scene = synth.cornell_scene(n, block)
     W, H, spp, seed = 40, 24, 8, 5
     got = api.render(codec, scene, mode, W, H, spp, depth, seed, path_hashes=True, multipass=multipass)
+    fast = api.render(codec, scene, mode, W, H, spp, depth, seed, multipass=multipass)  # sample-parallel path
     img, hashes, evals = _reference(api, scene, n, k, E, D, mode, W, H, spp, depth, seed, multipass)
-    g = got["image"].cpu().numpy()
-    assert g.shape == img.shape
-    assert np.array_equal(g, img), f"{int(np.sum(g != img))} values differ"
-    assert got["shading_evals"] == evals
+    for r in (got, fast):
+        g = r["image"].cpu().numpy()
+        assert g.shape == img.shape
+        assert np.array_equal(g, img), f"{int(np.sum(g != img))} values differ"
+        assert r["shading_evals"] == evals
     eq = np.mean(got["path_hashes"].cpu().numpy().view(np.uint64).reshape(-1) == hashes)
     print(f"{mode} n={n} k={k} depth={depth}: path-hash agreement {eq:.4f}")
     assert eq >= 0.9
