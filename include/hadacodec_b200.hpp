@@ -86,6 +86,8 @@ struct ColorTriple {
 struct ChannelImage {
   int width = 0, height = 0, channels = 0;
   std::vector<float> data;
+  std::uint64_t shading_evals = 0;          // render: shading units (renderer.hpp:78-81)
+  std::vector<std::uint64_t> path_hashes;   // render with collect_path_hashes
   float& at(int x, int y, int c) { return data[(static_cast<size_t>(y) * width + x) * channels + c]; }
   float at(int x, int y, int c) const { return data[(static_cast<size_t>(y) * width + x) * channels + c]; }
 };
@@ -149,6 +151,48 @@ ColorTriple xyz_to_linear_rgb(const ColorTriple& xyz);
 // ---- renderer.hpp:109-115
 ChannelImage decode_image(const Codec& c, const ChannelImage& latent);   // k -> n channels
 ChannelImage image_to_linear_rgb(const Codec& c, const ChannelImage& img);  // n -> 3 channels
+
+// ---- path tracer (renderer.hpp:12-107), computed on the GPU
+struct Vec3 {
+  double x = 0, y = 0, z = 0;
+};
+struct Camera {
+  Vec3 position{0, 1, 3.25};
+  Vec3 look_at{0, 1, 0};
+  Vec3 up{0, 1, 0};
+  double vfov_degrees = 40.0;
+};
+struct SceneLight {
+  Vec3 corner, edge_u, edge_v;
+  SpectralCurve spd;
+  double scale = 1.0;
+};
+struct SceneObject {
+  enum class Kind { sphere, block };
+  Kind kind = Kind::sphere;
+  Vec3 center;
+  double radius = 0;
+  Vec3 box_min, box_max;
+  int material = 0;
+};
+struct Scene {
+  Camera camera;
+  Vec3 box_min{-1, 0, -1}, box_max{1, 2, 1};
+  std::array<int, 6> wall_material{-1, -1, -1, -1, -1, -1};
+  std::vector<SpectralCurve> materials;
+  std::vector<SceneObject> objects;
+  std::vector<SceneLight> lights;
+};
+enum class RenderMode { spectral, latent, rgb };
+struct RenderJob {
+  RenderMode mode = RenderMode::spectral;
+  int width = 128, height = 128, spp = 64, max_depth = 3;
+  std::uint64_t seed = 0;
+  bool collect_path_hashes = false;
+};
+// The codec supplies the grid (and, in latent mode, the codes).
+ChannelImage render(const Codec& c, const Scene& scene, const RenderJob& job);
+ChannelImage render_latent_multipass(const Codec& c, const Scene& scene, const RenderJob& job);
 
 // ---- colour-metric tail (renderer.hpp:117-133, evaluation.hpp:48-59), computed on the GPU.
 // Images are linear RGB (3 channels) or spectra (n channels), as in the reference.

@@ -253,6 +253,50 @@ int main() {
     (void)wide;
   }
 
+  // path tracer (renderer.hpp:93-107): multipass == single latent render at fixed depth,
+  // path hashes identical across modes, counters in native units, invalid jobs rejected.
+  {
+    const int n = codec.n();
+    Scene sc;
+    sc.materials.push_back(SpectralCurve(n, 0.7));
+    SpectralCurve red(n, 0.0);
+    for (int i = 0; i < n; ++i) red[i] = 0.1 + 0.5 * i / n;
+    sc.materials.push_back(red);
+    sc.wall_material = {1, 0, 0, 0, 0, -1};
+    SceneObject sphere;
+    sphere.center = {0.3, 0.4, -0.2};
+    sphere.radius = 0.35;
+    sc.objects.push_back(sphere);
+    SceneLight light;
+    light.corner = {-0.25, 1.999, -0.25};
+    light.edge_u = {0.5, 0.0, 0.0};
+    light.edge_v = {0.0, 0.0, 0.5};
+    light.spd = SpectralCurve(n, 1.0);
+    light.scale = 12.0;
+    sc.lights.push_back(light);
+    RenderJob job;
+    job.width = 24;
+    job.height = 16;
+    job.spp = 4;
+    job.collect_path_hashes = true;
+    job.mode = RenderMode::latent;
+    const ChannelImage lat = render(codec, sc, job);
+    const ChannelImage mp = render_latent_multipass(codec, sc, job);
+    CHECK(lat.channels == codec.k() && lat.data == mp.data && lat.path_hashes == mp.path_hashes);
+    job.mode = RenderMode::spectral;
+    const ChannelImage spec = render(codec, sc, job);
+    job.mode = RenderMode::rgb;
+    const ChannelImage rgb = render(codec, sc, job);
+    CHECK(spec.channels == n && rgb.channels == 3);
+    CHECK(spec.path_hashes == lat.path_hashes && rgb.path_hashes == lat.path_hashes);
+    CHECK(spec.shading_evals == rgb.shading_evals * static_cast<uint64_t>(n) && lat.shading_evals == rgb.shading_evals * 2);
+    job.spp = 0;
+    CHECK_THROWS_AS(render(codec, sc, job), std::invalid_argument);
+    job.spp = 2;
+    sc.wall_material[4] = 9;
+    CHECK_THROWS_AS(render(codec, sc, job), std::invalid_argument);
+  }
+
   std::printf("drop-in: %d checks, %d failures, %lld kernel launches\n", g_checks, g_fail,
               static_cast<long long>(dev.launches()));
   return g_fail ? 1 : 0;
