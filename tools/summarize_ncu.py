@@ -20,7 +20,7 @@ from collections import defaultdict
 from pathlib import Path
 
 ALGO_BYTES = {"1": 696 * (1 << 20), "2": 60 * 1920 * 1080, "3": 468 * 3840 * 2160, "4": 1368 * 2048 * 2048,
-              "5a": 36 * 4096 * 4096, "5b": 648 * (1 << 24), "6": 27 * 1920 * 1080}
+              "5a": 36 * 4096 * 4096, "5b": 648 * (1 << 24), "6": 27 * 1920 * 1080, "7": 6 * 4 * 256 * 256}
 METRICS = [
     ("gpu__time_duration.sum", "duration (us)"),
     ("dram__bytes_read.sum", "DRAM read (bytes)"),
