@@ -51,16 +51,18 @@ constexpr int kHid = 64;      // hidden width
 constexpr int kK1 = 16;       // layer-1 K (3 inputs + bias column, padded)
 constexpr int kN3 = 16;       // layer-3 N (k padded)
 constexpr int kMaxK = 9;
-constexpr int kStreams = 4;                 // tile streams per CTA
+constexpr int kStreams = 3;                 // tile streams per CTA
 constexpr int kEpiThreads = 128 * kStreams; // epilogue warps: warp w -> stream w / 4, lane quarter w % 4
 constexpr int kThreads = kEpiThreads + 32 * kStreams;  // + one MMA-issuer warp per stream
 constexpr int kK2 = 80;                     // layer 2 K: 64 hidden + constant-1 column (b2 rides the MMA)
 constexpr int kK3 = 64;                     // layer 3 K: b3 (6 values) is added in the epilogue instead of
                                             // paying a fifth >= 45-cycle N = 16 MMA
-constexpr int kColsPerStream = 128;         // TMEM columns per stream (512 total)
-constexpr int kColA = 0;                    // packed bf16 A2 / A3 (+ constant chunk): 40 columns
-constexpr int kColD = 48;                   // fp32 accumulator of layers 1 / 2: 64 columns
-constexpr int kColD3 = 112;                 // fp32 accumulator of layer 3: 16 columns
+constexpr int kColsPerStream = 160;         // TMEM columns per stream (3 x 160 of the 512 allocated)
+constexpr int kColA = 0;                    // packed bf16 A2 (+ constant chunk): 40 columns
+constexpr int kColA3 = 40;                  // packed bf16 A3: 32 columns (separate, so layer 1 of the
+                                            // next tile can run while layer 3 still reads A3)
+constexpr int kColD = 80;                   // fp32 accumulator of layers 1 / 2: 64 columns
+constexpr int kColD3 = 144;                 // fp32 accumulator of layer 3: 16 columns
 
 // Shared-memory image offsets (bytes).
 constexpr int kW1Bytes = kHid * kK1 * 2;   // 2 KB
@@ -238,46 +240,98 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t tcol = tmem + st * kColsPerStream;  // stream base, lane 0
-  const uint32_t tA = tcol + kColA, tD = tcol + kColD, tD3 = tcol + kColD3;
+  const uint32_t tA = tcol + kColA, tA3 = tcol + kColA3, tD = tcol + kColD, tD3 = tcol + kColD3;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kStreams + st;
   const int64_t tstride = static_cast<int64_t>(gridDim.x) * kStreams;
   constexpr uint32_t kChunkA = kMlpM * 16;  // K-chunk stride of the 128-row A1 tile
 
   if (issuer) {
     // ------------------------------------------------------------ MMA-issuer warp
-    if ((tid & 31) == 0) {
-      const uint32_t sW1 = smem_u32(sm + kOffW1), sW2 = smem_u32(sm + kOffW2), sW3 = smem_u32(sm + kOffW3);
-      const uint32_t sA1 = smem_u32(A1);
-      const uint32_t id64 = idesc_bf16(kMlpM, kHid), id16 = idesc_bf16(kMlpM, kN3);
-      auto load_tile = [&](int64_t t, int s) {
-        mbar_arrive_expect_tx(&bar_in[s], kInTile);
-        bulk_g2s(in_tiles + s * kMlpM * 3, p.rgb + (p.first_tile + t) * kMlpM * 3, kInTile, &bar_in[s]);
-      };
-      if (p.use_tma) {
-        if (t0 < p.ntiles) load_tile(t0, 0);
-        if (t0 + tstride < p.ntiles) load_tile(t0 + tstride, 1);
+    // Lane 0 issues the MMAs and the rgb bulk copies; the whole warp builds each tile's
+    // A1 (r, g, b, 1) rows in shared memory, so the epilogue warps never do.
+    const int lane = tid & 31;
+    const bool elect = lane == 0;
+    const uint32_t sW1 = smem_u32(sm + kOffW1), sW2 = smem_u32(sm + kOffW2), sW3 = smem_u32(sm + kOffW3);
+    const uint32_t sA1 = smem_u32(A1);
+    const uint32_t id64 = idesc_bf16(kMlpM, kHid), id16 = idesc_bf16(kMlpM, kN3);
+    auto load_tile = [&](int64_t t, int s) {
+      mbar_arrive_expect_tx(&bar_in[s], kInTile);
+      bulk_g2s(in_tiles + s * kMlpM * 3, p.rgb + (p.first_tile + t) * kMlpM * 3, kInTile, &bar_in[s]);
+    };
+    if (p.use_tma && elect) {
+      if (t0 < p.ntiles) load_tile(t0, 0);
+      if (t0 + tstride < p.ntiles) load_tile(t0 + tstride, 1);
+    }
+    // rgb of tile t -> (r, g, b, 1, 0 ...) bf16 rows of A1; frees rgb slot it & 1 for the
+    // tile two strides on.
+    auto prepare_a1 = [&](int64_t t, int it) {
+      const int s = it & 1;
+      const int64_t row0 = (p.first_tile + t) * kMlpM;
+      const int64_t left = p.P - row0;
+      if (p.use_tma) mbar_wait(&bar_in[s], (it >> 1) & 1);
+#pragma unroll
+      for (int q = 0; q < kMlpM / 32; ++q) {
+        const int row = q * 32 + lane;
+        float x0 = 0.f, x1 = 0.f, x2 = 0.f;
+        if (p.use_tma) {
+          const float* in = in_tiles + s * kMlpM * 3 + row * 3;
+          x0 = in[0];
+          x1 = in[1];
+          x2 = in[2];
+        } else if (row < left) {
+          const float* in = p.rgb + (row0 + row) * 3;
+          x0 = in[0];
+          x1 = in[1];
+          x2 = in[2];
+        }
+        *reinterpret_cast<uint4*>(A1 + row * 16) = make_uint4(pack_bf16(x0, x1), pack_bf16(x2, 1.0f), 0u, 0u);
+        *reinterpret_cast<uint4*>(A1 + kChunkA + row * 16) = make_uint4(0u, 0u, 0u, 0u);
       }
-      int iter = 0;
-      for (int64_t t = t0; t < p.ntiles; t += tstride, ++iter) {
-        const uint32_t ph = iter & 1;
-        mbar_wait(bar_a1, ph);  // A1(t) in smem; rgb slot (iter & 1) consumed
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (elect && p.use_tma && t + 2 * tstride < p.ntiles) load_tile(t + 2 * tstride, s);
+    };
+    auto issue_l1 = [&]() {
+      if (elect) {
         tc_fence_after();
-        if (p.use_tma && t + 2 * tstride < p.ntiles) load_tile(t + 2 * tstride, iter & 1);
         mma_ss(tD, umma_desc(sA1, kChunkA, 128), umma_desc(sW1, kHid * 16, 128), id64, 0);
         mma_commit(bar_l1);
-        mbar_wait(bar_a2, ph);  // A2(t) in TMEM, D read out
+      }
+      __syncwarp();
+    };
+    if (t0 < p.ntiles) {
+      prepare_a1(t0, 0);
+      issue_l1();
+    }
+    int iter = 0;
+    for (int64_t t = t0; t < p.ntiles; t += tstride, ++iter) {
+      const uint32_t ph = iter & 1;
+      const int64_t tn = t + tstride;
+      mbar_wait(bar_a2, ph);  // A2(t) in TMEM, D read out
+      if (elect) {
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kK2 / 16; ++kk)
           mma_ts(tD, tA + kk * 8, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128), id64, kk > 0);
         mma_commit(bar_l2);
-        mbar_wait(bar_a3, ph);  // A3(t) in TMEM, D read out; D3(t - 1) read out
+      }
+      __syncwarp();
+      if (tn < p.ntiles) {
+        mbar_wait(bar_l1, ph);  // layer 1 of tile t has read A1
+        prepare_a1(tn, iter + 1);
+      }
+      mbar_wait(bar_a3, ph);  // A3(t) in TMEM, D read out, D3(t - 1) read out
+      // Layer 1 of the next tile first: D is free and A1 is ready, and A2 / A3 are separate
+      // TMEM regions, so its epilogue never waits for this tile's layer 3.
+      if (tn < p.ntiles) issue_l1();
+      if (elect) {
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < kK3 / 16; ++kk)
-          mma_ts(tD3, tA + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
+          mma_ts(tD3, tA3 + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
         mma_commit(bar_l3);
       }
+      __syncwarp();
     }
   } else {
     // ------------------------------------------------------------ epilogue warps
@@ -292,31 +346,6 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
                    : "memory");
       tmem_wait_st();
     }
-    // rgb of tile t -> (r, g, b, 1, 0 ...) bf16 row of A1 (smem), then one arrival per warp on a1.
-    auto prepare_input = [&](int64_t t, int it) {
-      const int s = it & 1;
-      const int64_t row0 = (p.first_tile + t) * kMlpM;
-      const int64_t left = p.P - row0;
-      float x0 = 0.f, x1 = 0.f, x2 = 0.f;
-      if (p.use_tma) {
-        mbar_wait(&bar_in[s], (it >> 1) & 1);
-        const float* in = in_tiles + s * kMlpM * 3 + r * 3;
-        x0 = in[0];
-        x1 = in[1];
-        x2 = in[2];
-      } else if (r < left) {
-        const float* in = p.rgb + (row0 + r) * 3;
-        x0 = in[0];
-        x1 = in[1];
-        x2 = in[2];
-      }
-      *reinterpret_cast<uint4*>(A1 + r * 16) = make_uint4(pack_bf16(x0, x1), pack_bf16(x2, 1.0f), 0u, 0u);
-      *reinterpret_cast<uint4*>(A1 + kChunkA + r * 16) = make_uint4(0u, 0u, 0u, 0u);
-      fence_proxy_async_smem();
-      tc_fence_before();
-      __syncwarp();
-      if ((tid & 31) == 0) mbar_arrive(bar_a1);
-    };
     // Codes of the previous tile: the layer-3 accumulator is read right after layer 3
     // completes, softplus + the global stores run later, under the next tile's MMAs.
     uint32_t prev_v[kN3];
@@ -345,7 +374,6 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       if ((tid & 31) == 0) mbar_arrive(bar);
     };
 
-    if (t0 < p.ntiles) prepare_input(t0, 0);
     int iter = 0;
     for (int64_t t = t0; t < p.ntiles; t += tstride, ++iter) {
       const uint32_t ph = iter & 1;
@@ -357,29 +385,35 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       mbar_wait(bar_l1, ph);
       if (tr) tr[1] = clock64();
       tc_fence_after();
-      epilogue_hidden<false>(tD + lane_off, tA + lane_off, nullptr);
+      epilogue_hidden<false>(tD + lane_off, tA + lane_off, nullptr);  // A2 (layer 2 of t-1 is done)
       handoff(bar_a2);
       if (tr) tr[2] = clock64();
-      const int64_t tn = t + tstride;
-      if (tn < p.ntiles) prepare_input(tn, iter + 1);  // A1 is free: layer 1 of tile t is done
-      store_codes();  // previous tile's softplus + stores, under this tile's layer-2 MMAs
       if (tr) tr[3] = clock64();
-      mbar_wait(bar_l2, ph);
+      if (iter > 0) {  // layer 3 of the previous tile: its codes, under this tile's layer 2
+        mbar_wait(bar_l3, ph ^ 1);
+        tc_fence_after();
+        HC_TMEM_LD16(tD3 + lane_off, prev_v);
+        tmem_wait_ld();
+        store_codes();
+      }
       if (tr) tr[4] = clock64();
-      tc_fence_after();
-      epilogue_hidden<false>(tD + lane_off, tA + lane_off, nullptr);
-      handoff(bar_a3);
+      mbar_wait(bar_l2, ph);
       if (tr) tr[5] = clock64();
-      mbar_wait(bar_l3, ph);
+      tc_fence_after();
+      epilogue_hidden<false>(tD + lane_off, tA3 + lane_off, nullptr);  // A3 (layer 3 of t-1 read out above)
+      handoff(bar_a3);
+      prev_row0 = row0;
+      prev_rows = rows;
       if (tr) tr[6] = clock64();
+      if (tr) tr[7] = clock64();
+    }
+    if (iter > 0) {  // the last tile's codes
+      mbar_wait(bar_l3, (iter - 1) & 1);
       tc_fence_after();
       HC_TMEM_LD16(tD3 + lane_off, prev_v);
       tmem_wait_ld();
-      prev_row0 = row0;
-      prev_rows = rows;
-      if (tr) tr[7] = clock64();
+      store_codes();
     }
-    store_codes();
   }
   tc_fence_before();
   __syncthreads();
@@ -511,7 +545,7 @@ int hc_mlp_forward(hc_mlp m, const float* rgb, int64_t P, float* codes) {
           ++n;
         }
       if (n)
-        std::fprintf(stderr, "[hc] mlp phase cycles (avg of %d tiles): L1wait %.0f epi1 %.0f nextA1+codes %.0f L2wait %.0f epi2 %.0f L3wait %.0f ldD3 %.0f loop %.0f\n",
+        std::fprintf(stderr, "[hc] mlp phase cycles (avg of %d tiles): L1wait %.0f epi1 %.0f nextA1 %.0f prevD3+codes %.0f L2wait %.0f epi2 %.0f - %.0f loop %.0f\n",
                      n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n, acc[6] / n, acc[7] / n);
     }
   }
