@@ -684,7 +684,7 @@ def run_ours(args) -> int:
         extra["e2e_matches_device"] = bool(np.array_equal(dev_rgb, nr))
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the contract: rank 0 at N = 1 only
         try:
             cpu = cpu_reference_run(args.config, budget_s=args.cpu_seconds)
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "seconds", "cpu")}
@@ -717,6 +717,7 @@ def run_ours(args) -> int:
         line.update(extra)
         emit(line)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 
