@@ -240,6 +240,18 @@ int hc_render(hc_codec codec, const hc_scene* scene, const hc_render_job* job, c
 int hc_render_latent_multipass(hc_codec codec, const hc_scene* scene, const hc_render_job* job, float* image,
                                uint64_t* path_hashes, uint64_t* shading_evals);
 
+/* ------------------------------------------------------------------ formats
+ * print_g17 ("%.17g", io.cpp:108-112) on the device: slots (n x 32 bytes, not NUL-
+ * terminated) receive the text of v[i], lens[i] its length; bit-identical to glibc's
+ * snprintf("%.17g") (exact digits, round half to even). */
+int hc_format_g17(hc_ctx ctx, const double* v, int64_t n, char* slots, uint8_t* lens);
+/* write_codes_csv (io.cpp:312-330) of device codes [rows][k] (float, printed as the double
+ * they widen to) with ids first_id + row: header "id,c0,...\n", rows "id,v0,...\n".  With
+ * out == NULL only *length (host) is returned (size query); else out (device, capacity
+ * bytes) receives the file.  Synchronous. */
+int hc_codes_csv_write(hc_ctx ctx, const float* codes, int64_t rows, int k, uint64_t first_id, char* out,
+                       int64_t capacity, int64_t* length);
+
 /* ------------------------------------------------------------------ host-buffer entry points
  * Reference-facing value calls: inputs and outputs in HOST memory (pinned for
  * full copy speed), copies and compute on the context stream, synchronised on

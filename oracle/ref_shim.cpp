@@ -34,6 +34,7 @@
 #include "hadacodec/colorimetry.hpp"
 #include "hadacodec/dataset.hpp"
 #include "hadacodec/evaluation.hpp"
+#include "hadacodec/io.hpp"
 #include "hadacodec/renderer.hpp"
 #include "hadacodec/rng.hpp"
 #include "hadacodec/spectrum.hpp"
@@ -651,6 +652,26 @@ int ref_render(const hc_scene* sc, const hc_render_job* job, int k, const float*
     if (evals) *evals = img.shading_evals;
     return 0;
   } catch (const std::invalid_argument&) {
+    return 1;
+  }
+}
+
+// ---------------------------------------------------------------- formats
+// the reference's own write_codes_csv (io.cpp:312-330, print_g17
+// :108-112) for float codes widened to double, ids first_id + row.
+int ref_write_codes_csv(const char* path, const float* Z, int64_t rows, int k, uint64_t first_id) {
+  try {
+    std::vector<std::string> ids;
+    std::vector<LatentCode> codes;
+    for (int64_t r = 0; r < rows; ++r) {
+      ids.push_back(std::to_string(first_id + static_cast<uint64_t>(r)));
+      LatentCode z;
+      for (int j = 0; j < k; ++j) z.z.push_back(static_cast<double>(Z[r * k + j]));
+      codes.push_back(z);
+    }
+    write_codes_csv(path, ids, codes);
+    return 0;
+  } catch (const std::exception&) {
     return 1;
   }
 }

@@ -405,6 +405,32 @@ def render(codec: "Codec", scene: dict, mode: str = "spectral", width: int = 128
     return {"image": img, "path_hashes": hashes, "shading_evals": evals.value}
 
 
+# ------------------------------------------------------------ formats
+def format_g17(ctx: Context, v: torch.Tensor) -> list:
+    """print_g17 (io.cpp:108-112) of every value of a float64 CUDA tensor, on the device."""
+    v = _cuda(v, torch.float64, "v").reshape(-1)
+    n = v.numel()
+    slots = torch.empty(n, 32, dtype=torch.uint8, device=v.device)
+    lens = torch.empty(n, dtype=torch.uint8, device=v.device)
+    ctx.bind_stream()
+    _check(_lib.lib().hc_format_g17(ctx.h, _p(v), n, _p(slots), _p(lens)))
+    s, ln = slots.cpu().numpy(), lens.cpu().numpy()
+    return [bytes(s[i, :ln[i]]).decode() for i in range(n)]
+
+
+def codes_csv(ctx: Context, codes: torch.Tensor, first_id: int = 0) -> bytes:
+    """write_codes_csv (io.cpp:312-330) of codes [rows, k] (float32, device), ids first_id + row."""
+    codes = _cuda(codes, torch.float32, "codes")
+    rows, k = codes.shape
+    length = C.c_int64()
+    ctx.bind_stream()
+    _check(_lib.lib().hc_codes_csv_write(ctx.h, _p(codes), rows, k, first_id, None, 0, C.byref(length)))
+    out = torch.empty(length.value, dtype=torch.uint8, device=codes.device)
+    _check(_lib.lib().hc_codes_csv_write(ctx.h, _p(codes), rows, k, first_id, _p(out), length.value,
+                                         C.byref(length)))
+    return bytes(out.cpu().numpy())
+
+
 # ------------------------------------------------------------ colour-metric tail (SURVEY §8f row 1)
 def _image(t: torch.Tensor, codec: "Codec", name: str) -> tuple[torch.Tensor, int, int]:
     t = _cuda(t, torch.float32, name)

