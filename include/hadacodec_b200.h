@@ -251,6 +251,11 @@ int hc_format_g17(hc_ctx ctx, const double* v, int64_t n, char* slots, uint8_t* 
  * bytes) receives the file.  Synchronous. */
 int hc_codes_csv_write(hc_ctx ctx, const float* codes, int64_t rows, int k, uint64_t first_id, char* out,
                        int64_t capacity, int64_t* length);
+/* parse_double (io.cpp:78-88: std::stod of a trimmed cell, fully consumed) of n cells held
+ * in fixed slots (stride bytes, lens[i] used): out[i] the correctly rounded double,
+ * status[i] 0 ok, 1 not a number / trailing junk, 2 out of range (ERANGE: std::stod throws). */
+int hc_parse_doubles(hc_ctx ctx, const char* slots, const uint8_t* lens, int64_t n, int stride, double* out,
+                     int8_t* status);
 
 /* ------------------------------------------------------------------ host-buffer entry points
  * Reference-facing value calls: inputs and outputs in HOST memory (pinned for

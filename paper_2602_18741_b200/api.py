@@ -418,6 +418,25 @@ def format_g17(ctx: Context, v: torch.Tensor) -> list:
     return [bytes(s[i, :ln[i]]).decode() for i in range(n)]
 
 
+def parse_doubles(ctx: Context, cells: Sequence[bytes]) -> tuple[np.ndarray, np.ndarray]:
+    """parse_double (io.cpp:78-88) of trimmed cells on the device: (values, status 0/1/2)."""
+    n = len(cells)
+    stride = max([len(c) for c in cells] + [1])
+    buf = np.zeros((n, stride), np.uint8)
+    lens = np.zeros(n, np.uint8 if stride < 256 else np.int64)
+    if stride >= 256:
+        raise ValueError("parse_doubles: cells longer than 255 bytes")
+    for i, c in enumerate(cells):
+        buf[i, :len(c)] = np.frombuffer(c, np.uint8)
+        lens[i] = len(c)
+    d_buf, d_len = torch.from_numpy(buf).cuda(), torch.from_numpy(lens).cuda()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    st = torch.empty(n, dtype=torch.int8, device="cuda")
+    ctx.bind_stream()
+    _check(_lib.lib().hc_parse_doubles(ctx.h, _p(d_buf), _p(d_len), n, stride, _p(out), _p(st)))
+    return out.cpu().numpy(), st.cpu().numpy()
+
+
 def codes_csv(ctx: Context, codes: torch.Tensor, first_id: int = 0) -> bytes:
     """write_codes_csv (io.cpp:312-330) of codes [rows, k] (float32, device), ids first_id + row."""
     codes = _cuda(codes, torch.float32, "codes")

@@ -240,6 +240,341 @@ __device__ int format_g17(double v, char* out) {
   return n;
 }
 
+
+// ---------------------------------------------------------------- parse_double (io.cpp:78-88)
+// std::stod on a trimmed cell, which must be consumed entirely: optional sign; decimal
+// digits with optional point and exponent; "inf" / "infinity" / "nan[(...)]" in any case;
+// hexadecimal "0x..[p..]".  Results that glibc's strtod flags with ERANGE (overflow to
+// infinity, any subnormal or zero result of non-zero digits) make std::stod throw, which
+// the reference reports as "expected a number" — status 2 here.  Decimal conversion is
+// exact: a double estimate is corrected against the exact midpoints with multi-limb
+// integer comparisons (all significant digits kept, up to kMaxDigits), i.e. the correctly
+// rounded (round-half-even) result that glibc returns.
+constexpr int kBig = 96;         // 32-bit limbs: 3072 bits
+constexpr int kMaxDigits = 700;  // significant decimal digits kept exactly
+
+struct Big {
+  uint32_t w[kBig];
+  int n;  // limbs in use
+};
+__device__ inline void big_set(Big& a, uint64_t v) {
+  a.w[0] = static_cast<uint32_t>(v);
+  a.w[1] = static_cast<uint32_t>(v >> 32);
+  a.n = a.w[1] ? 2 : (a.w[0] ? 1 : 0);
+}
+__device__ inline void big_mul_small(Big& a, uint32_t m, uint32_t add = 0) {
+  uint64_t carry = add;
+  for (int i = 0; i < a.n; ++i) {
+    const uint64_t cur = static_cast<uint64_t>(a.w[i]) * m + carry;
+    a.w[i] = static_cast<uint32_t>(cur);
+    carry = cur >> 32;
+  }
+  if (carry && a.n < kBig) a.w[a.n++] = static_cast<uint32_t>(carry);
+}
+__device__ inline void big_mul_pow10(Big& a, int k) {
+  while (k >= 9) {
+    big_mul_small(a, 1000000000u);
+    k -= 9;
+  }
+  static const uint32_t p10[9] = {1, 10, 100, 1000, 10000, 100000, 1000000, 10000000, 100000000};
+  if (k > 0) big_mul_small(a, p10[k]);
+}
+__device__ inline void big_shl(Big& a, int s) {
+  if (a.n == 0 || s == 0) return;
+  const int w = s >> 5, b = s & 31;
+  int n = a.n + w + 1;
+  if (n > kBig) n = kBig;
+  for (int i = n - 1; i >= 0; --i) {
+    const int src = i - w;
+    uint32_t v = 0;
+    if (src >= 0 && src < a.n) v = a.w[src] << b;
+    if (b && src - 1 >= 0 && src - 1 < a.n) v |= a.w[src - 1] >> (32 - b);
+    a.w[i] = v;
+  }
+  a.n = n;
+  while (a.n > 0 && a.w[a.n - 1] == 0) --a.n;
+}
+__device__ inline int big_cmp(const Big& a, const Big& b) {
+  if (a.n != b.n) return a.n < b.n ? -1 : 1;
+  for (int i = a.n - 1; i >= 0; --i)
+    if (a.w[i] != b.w[i]) return a.w[i] < b.w[i] ? -1 : 1;
+  return 0;
+}
+
+// sign of (D * 10^q) - (num * 2^p)
+__device__ int cmp_dec_bin(const Big& D, int q, uint64_t num, int p) {
+  Big A = D, B;
+  big_set(B, num);
+  if (q >= 0) big_mul_pow10(A, q);
+  else big_mul_pow10(B, -q);
+  if (p >= 0) big_shl(B, p);
+  else big_shl(A, -p);
+  return big_cmp(A, B);
+}
+
+__device__ inline char lower(char c) { return (c >= 'A' && c <= 'Z') ? static_cast<char>(c + 32) : c; }
+
+// Correctly rounded D * 10^q (D > 0); status 2 when glibc would set ERANGE.
+__device__ double dec_to_double(const Big& D, uint64_t top19, int ntop, int nd, int q, int* status) {
+  // nd significant digits in total, the leading min(nd, 19) of them in top19 (ntop digits)
+  const int e10 = nd + q;  // value in [10^(e10-1), 10^e10)
+  if (e10 > 310) {
+    *status = 2;
+    return INFINITY;
+  }
+  if (e10 < -324) {
+    *status = 2;
+    return 0.0;
+  }
+  // estimate: top19 * 10^(q + nd - ntop)
+  double x = static_cast<double>(top19);
+  int k = q + nd - ntop;
+  while (k > 22) {
+    x *= 1e22;
+    k -= 22;
+  }
+  while (k < -22) {
+    x /= 1e22;
+    k += 22;
+  }
+  const double p10[23] = {1e0,  1e1,  1e2,  1e3,  1e4,  1e5,  1e6,  1e7,  1e8,  1e9,  1e10, 1e11,
+                          1e12, 1e13, 1e14, 1e15, 1e16, 1e17, 1e18, 1e19, 1e20, 1e21, 1e22};
+  x = k >= 0 ? x * p10[k] : x / p10[-k];
+  if (!(x < INFINITY)) x = 1.7976931348623157e308;
+  if (x < 4.9406564584124654e-324) x = 4.9406564584124654e-324;
+  for (int iter = 0; iter < 64; ++iter) {
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(x));
+    const int be = static_cast<int>(bits >> 52);
+    uint64_t m = bits & 0xfffffffffffffull;
+    int e;
+    if (be == 0) {
+      e = -1074;
+    } else {
+      m |= 1ull << 52;
+      e = be - 1075;
+    }
+    // upper midpoint (2m + 1) * 2^(e - 1)
+    const int cu = cmp_dec_bin(D, q, 2 * m + 1, e - 1);
+    if (cu > 0 || (cu == 0 && (m & 1))) {
+      if (be == 0x7fe && m == 0x1fffffffffffffull) {
+        *status = 2;
+        return INFINITY;
+      }
+      x = __longlong_as_double(static_cast<long long>(bits + 1));
+      if (cu == 0) break;
+      continue;
+    }
+    // lower midpoint: (2m - 1) * 2^(e - 1), or (4m - 1) * 2^(e - 2) below a power of two
+    const bool pow2 = be > 1 && m == (1ull << 52);
+    const int cl = pow2 ? cmp_dec_bin(D, q, 4 * m - 1, e - 2) : cmp_dec_bin(D, q, 2 * m - 1, e - 1);
+    if (cl < 0 || (cl == 0 && (m & 1))) {
+      if (bits == 1) {  // below half the smallest subnormal: rounds to zero
+        *status = 2;
+        return 0.0;
+      }
+      x = __longlong_as_double(static_cast<long long>(bits - 1));
+      if (cl == 0) break;
+      continue;
+    }
+    break;
+  }
+  if (x < 2.2250738585072014e-308) {  // glibc: ERANGE on an inexact subnormal result
+    const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(x));
+    if (cmp_dec_bin(D, q, bits, -1074) != 0) *status = 2;
+  }
+  return x;
+}
+
+// Hexadecimal float body after "0x": mantissa hex digits [. hex digits] [p exp]; exact.
+__device__ double hex_to_double(const char* s, int len, int* used, int* status) {
+  int i = 0;
+  uint64_t mant = 0;
+  int shift = 0;       // binary exponent adjustment
+  bool sticky = false, any = false, point = false;
+  int sig_bits = 0;
+  for (; i < len; ++i) {
+    const char c = lower(s[i]);
+    int d;
+    if (c >= '0' && c <= '9') d = c - '0';
+    else if (c >= 'a' && c <= 'f') d = c - 'a' + 10;
+    else if (c == '.' && !point) {
+      point = true;
+      continue;
+    } else break;
+    any = true;
+    if (mant == 0 && d == 0) {
+      if (point) shift -= 4;
+      continue;
+    }
+    if (sig_bits <= 60) {
+      mant = (mant << 4) | static_cast<uint64_t>(d);
+      sig_bits += 4;
+      if (point) shift -= 4;
+    } else {
+      if (d) sticky = true;
+      if (!point) shift += 4;
+    }
+  }
+  if (!any) {
+    *used = 0;
+    return 0.0;
+  }
+  if (i < len && lower(s[i]) == 'p') {
+    int j = i + 1;
+    bool neg = false;
+    if (j < len && (s[j] == '+' || s[j] == '-')) neg = s[j++] == '-';
+    int ex = 0;
+    bool dig = false;
+    while (j < len && s[j] >= '0' && s[j] <= '9') {
+      if (ex < 100000) ex = ex * 10 + (s[j] - '0');
+      ++j;
+      dig = true;
+    }
+    if (dig) {
+      shift += neg ? -ex : ex;
+      i = j;
+    }
+  }
+  *used = i;
+  if (mant == 0) return 0.0;
+  // value = mant * 2^shift (+ sticky); normalise mant to 64 bits
+  const int lz = __clzll(static_cast<long long>(mant));
+  mant <<= lz;
+  shift -= lz;
+  int e = shift + 63;  // value = 1.xxx * 2^e
+  if (e > 1023) {
+    *status = 2;
+    return INFINITY;
+  }
+  int keep = 53;  // significant bits the result can hold
+  if (e < -1022) keep = 53 - (-1022 - e);
+  if (keep <= 0) {
+    // below the smallest subnormal: rounds to zero or to 2^-1074
+    const bool up = keep == 0 && (((mant << 1) != 0) || sticky);
+    *status = 2;
+    return up ? 4.9406564584124654e-324 : 0.0;
+  }
+  const int drop = 64 - keep;
+  uint64_t q = mant >> drop;
+  const uint64_t rem = mant & ((1ull << drop) - 1ull);
+  const uint64_t half = 1ull << (drop - 1);
+  const bool inexact = rem != 0 || sticky;
+  if (rem > half || (rem == half && (sticky || (q & 1)))) ++q;
+  if (q >> keep) {  // carry into a new bit
+    q >>= 1;
+    ++e;
+    if (e > 1023) {
+      *status = 2;
+      return INFINITY;
+    }
+  }
+  const double r = ldexp(static_cast<double>(q), e - (keep - 1));
+  if (r < 2.2250738585072014e-308 && inexact) *status = 2;  // glibc: ERANGE on inexact underflow
+  return r;
+}
+
+// Parse a trimmed cell [s, s + len); returns status 0 ok, 1 not a number / trailing junk,
+// 2 out of range (ERANGE).
+__device__ double parse_cell(const char* s, int len, int* status) {
+  *status = 0;
+  int i = 0;
+  while (i < len && (s[i] == ' ' || (s[i] >= '\t' && s[i] <= '\r'))) ++i;  // strtod skips isspace
+  bool neg = false;
+  if (i < len && (s[i] == '+' || s[i] == '-')) neg = s[i++] == '-';
+  const int rest = len - i;
+  // inf / infinity / nan[(...)]
+  if (rest >= 3 && lower(s[i]) == 'i' && lower(s[i + 1]) == 'n' && lower(s[i + 2]) == 'f') {
+    int end = i + 3;
+    if (rest >= 8) {
+      const char* w = "inity";
+      bool ok = true;
+      for (int j = 0; j < 5; ++j) ok &= lower(s[i + 3 + j]) == w[j];
+      if (ok) end = i + 8;
+    }
+    if (end != len) *status = 1;
+    return neg ? -INFINITY : INFINITY;
+  }
+  if (rest >= 3 && lower(s[i]) == 'n' && lower(s[i + 1]) == 'a' && lower(s[i + 2]) == 'n') {
+    int end = i + 3;
+    if (end < len && s[end] == '(') {
+      int j = end + 1;
+      while (j < len && (s[j] == '_' || (s[j] >= '0' && s[j] <= '9') || (lower(s[j]) >= 'a' && lower(s[j]) <= 'z'))) ++j;
+      if (j < len && s[j] == ')') end = j + 1;
+    }
+    if (end != len) *status = 1;
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
+    return neg ? -nan : nan;
+  }
+  if (rest >= 2 && s[i] == '0' && lower(s[i + 1]) == 'x') {
+    int used = 0;
+    const double v = hex_to_double(s + i + 2, len - i - 2, &used, status);
+    if (used == 0) {  // "0x" without digits: strtod reads "0"
+      if (i + 1 != len) *status = 1;
+      return neg ? -0.0 : 0.0;
+    }
+    if (i + 2 + used != len) *status = 1;
+    return neg ? -v : v;
+  }
+  // decimal
+  Big D;
+  D.n = 0;
+  uint64_t top = 0;
+  int ntop = 0, nd = 0, q = 0;
+  bool any = false, point = false, dropped = false;
+  for (; i < len; ++i) {
+    const char c = s[i];
+    if (c == '.' && !point) {
+      point = true;
+      continue;
+    }
+    if (c < '0' || c > '9') break;
+    any = true;
+    const uint32_t d = static_cast<uint32_t>(c - '0');
+    if (nd == 0 && d == 0) {
+      if (point) --q;
+      continue;
+    }
+    if (nd < kMaxDigits) {
+      big_mul_small(D, 10u, d);
+      if (ntop < 19) {
+        top = top * 10 + d;
+        ++ntop;
+      }
+      ++nd;
+      if (point) --q;
+    } else {
+      if (d) dropped = true;  // beyond kMaxDigits: too long to be exact
+      if (!point) ++q;
+    }
+  }
+  if (!any) {
+    *status = 1;
+    return 0.0;
+  }
+  if (i < len && lower(s[i]) == 'e') {
+    int j = i + 1;
+    bool eneg = false;
+    if (j < len && (s[j] == '+' || s[j] == '-')) eneg = s[j++] == '-';
+    int ex = 0;
+    bool dig = false;
+    while (j < len && s[j] >= '0' && s[j] <= '9') {
+      if (ex < 100000) ex = ex * 10 + (s[j] - '0');
+      ++j;
+      dig = true;
+    }
+    if (dig) {
+      q += eneg ? -ex : ex;
+      i = j;
+    }
+  }
+  if (i != len || dropped) *status = 1;
+  if (nd == 0) return neg ? -0.0 : 0.0;
+  int st = 0;
+  const double v = dec_to_double(D, top, ntop, nd, q - 0, &st);
+  if (st) *status = *status ? *status : st;
+  return neg ? -v : v;
+}
+
 __global__ void g17_kernel(const double* __restrict__ v, int64_t n, char* __restrict__ slots,
                            uint8_t* __restrict__ lens) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
@@ -248,6 +583,15 @@ __global__ void g17_kernel(const double* __restrict__ v, int64_t n, char* __rest
     char* o = slots + i * kSlot;
     for (int j = 0; j < len; ++j) o[j] = buf[j];
     lens[i] = static_cast<uint8_t>(len);
+  }
+}
+
+__global__ void parse_slots_kernel(const char* __restrict__ slots, const uint8_t* __restrict__ lens, int64_t n,
+                                   int stride, double* __restrict__ out, int8_t* __restrict__ status) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    int st = 0;
+    out[i] = parse_cell(slots + i * stride, lens[i], &st);
+    status[i] = static_cast<int8_t>(st);
   }
 }
 
@@ -343,6 +687,17 @@ int hc_format_g17(hc_ctx ctx, const double* v, int64_t n, char* slots, uint8_t* 
   HC_REQUIRE(v && slots && lens, HC_EINVAL, "format_g17: null buffer");
   g17_kernel<<<grid_for(ctx, n), 256, 0, ctx->stream>>>(v, n, slots, lens);
   HC_CHECK_LAUNCH(ctx, "g17_kernel");
+  return HC_OK;
+}
+
+int hc_parse_doubles(hc_ctx ctx, const char* slots, const uint8_t* lens, int64_t n, int stride, double* out,
+                     int8_t* status) {
+  HC_REQUIRE(ctx, HC_EINVAL, "parse_doubles: null context");
+  HC_REQUIRE(n >= 0 && stride > 0, HC_EINVAL, "parse_doubles: bad shape");
+  if (n == 0) return HC_OK;
+  HC_REQUIRE(slots && lens && out && status, HC_EINVAL, "parse_doubles: null buffer");
+  parse_slots_kernel<<<grid_for(ctx, n), 128, 0, ctx->stream>>>(slots, lens, n, stride, out, status);
+  HC_CHECK_LAUNCH(ctx, "parse_slots_kernel");
   return HC_OK;
 }
 

@@ -62,3 +62,57 @@ def test_codes_csv_matches_reference_writer(api, ctx, tmp_path, rows, k):
         assert got.startswith(b"id,c0")  # the reference writes an empty header for no codes
     else:
         assert got == want
+
+
+def _glibc_strtod(cells):
+    """(value, status) as the reference's parse_double sees them: std::stod = strtod + ERANGE
+    -> throw, and the whole cell must be consumed (io.cpp:78-88)."""
+    import ctypes
+
+    libc = ctypes.CDLL("libc.so.6", use_errno=True)
+    libc.strtod.restype = ctypes.c_double
+    libc.strtod.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_char_p)]
+    vals, sts = [], []
+    for c in cells:
+        ctypes.set_errno(0)
+        end = ctypes.c_char_p()
+        v = libc.strtod(c, ctypes.byref(end))
+        rest = end.value if end.value is not None else b""
+        consumed = len(c) - len(rest)
+        err = ctypes.get_errno()
+        if consumed == 0 or consumed != len(c):
+            st = 1
+        elif err:
+            st = 2
+        else:
+            st = 0
+        vals.append(v)
+        sts.append(st)
+    return np.array(vals), np.array(sts)
+
+
+def test_parse_doubles_matches_glibc_strtod(api, ctx):
+    rng = np.random.default_rng(3)
+    cells = [b"0", b"-0", b"1", b"+1.5", b".5", b"5.", b"1e5", b"1E-5", b"1e+", b"1e5x", b"abc", b"", b"-", b".",
+             b"inf", b"-Infinity", b"NaN", b"nan(123)", b"infx", b"0x1p3", b"0x1.8p-1", b"0X.8", b"0x", b"0x1p-1074",
+             b"0x1p-1075", b"0x1.0000000000001p0", b"4.9406564584124654e-324", b"2.2250738585072014e-308",
+             b"2.2250738585072009e-308", b"1e-320", b"1e309", b"1.7976931348623157e308", b"1.7976931348623159e308",
+             b"1e-400", b"0.000000000000000000000000000001", b"123456789012345678901234567890",
+             b"9007199254740993", b"9007199254740992.5", b"1.00000000000000011102230246251565404236316680908203125",
+             b"1.00000000000000011102230246251565404236316680908203124", b"2.4703282292062327e-324",
+             b"2.4703282292062328e-324", b"00012.50", b"1_0", b"1,5", b" 1"]
+    # %.17g strings of every exponent, short decimals, long digit strings
+    bits = rng.integers(0, 2**63 - 1, 30000, dtype=np.int64).view(np.float64)
+    cells += [("%.17g" % v).encode() for v in bits if np.isfinite(v)]
+    cells += [("%.*g" % (int(p), v)).encode() for p, v in zip(rng.integers(1, 17, 20000), rng.lognormal(0, 30, 20000))]
+    cells += [("%de%d" % (int(a), int(b))).encode() for a, b in zip(rng.integers(1, 10**15, 5000), rng.integers(-340, 320, 5000))]
+    long_digits = ["".join(rng.choice(list("0123456789"), int(n))) for n in rng.integers(20, 60, 2000)]
+    cells += [(d[:3] + "." + d[3:] + "e" + str(int(e))).encode() for d, e in zip(long_digits, rng.integers(-320, 300, 2000))]
+    got, gst = api.parse_doubles(ctx, cells)
+    want, wst = _glibc_strtod(cells)
+    bad = []
+    for c, g, s, w, t in zip(cells, got, gst, want, wst):
+        same = (s == t) and (t != 0 or (np.isnan(g) and np.isnan(w)) or g.tobytes() == w.tobytes())
+        if not same:
+            bad.append((c, g, s, w, t))
+    assert not bad, f"{len(bad)} mismatches, e.g. {bad[:6]}"
