@@ -256,6 +256,14 @@ int hc_codes_csv_write(hc_ctx ctx, const float* codes, int64_t rows, int k, uint
  * status[i] 0 ok, 1 not a number / trailing junk, 2 out of range (ERANGE: std::stod throws). */
 int hc_parse_doubles(hc_ctx ctx, const char* slots, const uint8_t* lens, int64_t n, int stride, double* out,
                      int8_t* status);
+/* read_codes_csv (io.cpp:267-310) of a file image on the device (text, len bytes): header
+ * "id,c0,...,c{k-1}" on the first non-empty line, one row per non-empty line after it.
+ * *k_out, *rows_out (host) always; with codes / ids NULL it is a size query, else codes
+ * (device, rows x k doubles) and ids (device, rows x 2 int64: byte offset and length of the
+ * trimmed id cell in text) are filled (capacity_rows >= rows).  HC_EINVAL with the 1-based
+ * line in hc_last_error() for a bad header, a wrong cell count or a cell std::stod rejects. */
+int hc_codes_csv_read(hc_ctx ctx, const char* text, int64_t len, int* k_out, int64_t* rows_out, double* codes,
+                      int64_t* ids, int64_t capacity_rows);
 
 /* ------------------------------------------------------------------ host-buffer entry points
  * Reference-facing value calls: inputs and outputs in HOST memory (pinned for

@@ -676,6 +676,28 @@ int ref_write_codes_csv(const char* path, const float* Z, int64_t rows, int k, u
   }
 }
 
+// read_codes_csv (io.cpp:267-310): returns 0 and fills rows / k / codes (row-major,
+// capacity doubles) / ids (concatenated with '\n'), or 1 with the error text in ids.
+int ref_read_codes_csv(const char* path, int64_t* rows, int* k, double* codes, int64_t capacity, char* ids,
+                       int64_t ids_capacity) {
+  try {
+    const CodesCsv c = read_codes_csv(path);
+    *rows = static_cast<int64_t>(c.codes.size());
+    *k = c.codes.empty() ? 0 : c.codes.front().k();
+    int64_t n = 0;
+    for (const auto& z : c.codes)
+      for (double v : z.z)
+        if (n < capacity) codes[n++] = v;
+    std::string all;
+    for (const auto& id : c.ids) all += id + "\n";
+    std::strncpy(ids, all.c_str(), static_cast<size_t>(ids_capacity));
+    return 0;
+  } catch (const std::exception& e) {
+    std::strncpy(ids, e.what(), static_cast<size_t>(ids_capacity));
+    return 1;
+  }
+}
+
 int ref_thread_count() { return render_thread_count(); }
 
 }  // extern "C"

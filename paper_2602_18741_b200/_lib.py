@@ -55,6 +55,7 @@ SIGNATURES: dict[str, tuple] = {
     "hc_format_g17": (i32, [vp, vp, i64, vp, vp]),
     "hc_codes_csv_write": (i32, [vp, vp, i64, i32, u64, vp, i64, C.POINTER(i64)]),
     "hc_parse_doubles": (i32, [vp, vp, vp, i64, i32, vp, vp]),
+    "hc_codes_csv_read": (i32, [vp, vp, i64, C.POINTER(i32), C.POINTER(i64), vp, vp, i64]),
     "hc_render": (i32, [vp, vp, vp, vp, vp, vp, vp]),
     "hc_render_latent_multipass": (i32, [vp, vp, vp, vp, vp, vp]),
     "hc_shade_latent_host": (i32, [vp, vp, i32, vp, i32, vp, vp, i64, vp, vp]),

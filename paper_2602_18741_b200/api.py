@@ -450,6 +450,25 @@ def codes_csv(ctx: Context, codes: torch.Tensor, first_id: int = 0) -> bytes:
     return bytes(out.cpu().numpy())
 
 
+def read_codes_csv(ctx: Context, data: bytes, text: Optional[torch.Tensor] = None) -> tuple[list, torch.Tensor]:
+    """read_codes_csv (io.cpp:267-310) of a file image, parsed on the device: (ids, codes [rows, k]
+    float64 CUDA tensor).  `text` may be the file already resident as a uint8 CUDA tensor."""
+    if text is None:
+        text = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda() if data else torch.empty(0, dtype=torch.uint8,
+                                                                                                      device="cuda")
+    k, rows = C.c_int(), C.c_int64()
+    ctx.bind_stream()
+    n = text.numel()
+    _check(_lib.lib().hc_codes_csv_read(ctx.h, _p(text), n, C.byref(k), C.byref(rows), None, None, 0))
+    codes = torch.empty(rows.value, k.value, dtype=torch.float64, device="cuda")
+    spans = torch.empty(rows.value, 2, dtype=torch.int64, device="cuda")
+    _check(_lib.lib().hc_codes_csv_read(ctx.h, _p(text), n, C.byref(k), C.byref(rows), _p(codes), _p(spans),
+                                        rows.value))
+    raw = data if data is not None else bytes(text.cpu().numpy())
+    ids = [raw[a:a + ln].decode() for a, ln in spans.cpu().numpy().tolist()]
+    return ids, codes
+
+
 # ------------------------------------------------------------ colour-metric tail (SURVEY §8f row 1)
 def _image(t: torch.Tensor, codec: "Codec", name: str) -> tuple[torch.Tensor, int, int]:
     t = _cuda(t, torch.float32, name)

@@ -16,7 +16,10 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cctype>
 #include <cstring>
+#include <string>
+#include <vector>
 
 #include "hadacodec_b200.h"
 #include "hc_internal.h"
@@ -668,6 +671,146 @@ __global__ void csv_write_kernel(const float* __restrict__ Z, int64_t rows, int 
   }
 }
 
+
+// ---------------------------------------------------------------- codes CSV reader (io.cpp:267-310)
+// Newline index (chunk counts -> scan -> positions), header parsed on the host from the
+// first non-empty line, then one thread per physical line: trim, split on ',', cell count,
+// id span, parse_double of every value cell.  Row numbers of the non-empty data lines come
+// from an exclusive scan, so rows keep the file order.  The first failing physical line
+// (1-based, as the reference's FormatError) is reported.
+constexpr int kChunk = 16384;  // bytes per block in the newline passes
+
+__device__ inline bool is_space(char c) { return c == ' ' || (c >= '\t' && c <= '\r'); }
+
+__global__ void nl_count_kernel(const char* __restrict__ text, int64_t len, int64_t* __restrict__ counts) {
+  const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kChunk;
+  int64_t cnt = 0;
+  for (int64_t i = b0 + threadIdx.x; i < b0 + kChunk && i < len; i += blockDim.x) cnt += text[i] == '\n';
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  __shared__ int64_t ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += ws[w];
+    counts[blockIdx.x] = t;
+  }
+}
+
+// newline positions: block b writes its chunk's '\n' offsets from offset[b], in order
+__global__ void nl_write_kernel(const char* __restrict__ text, int64_t len, const int64_t* __restrict__ offset,
+                                int64_t* __restrict__ pos) {
+  const int64_t b0 = static_cast<int64_t>(blockIdx.x) * kChunk;
+  __shared__ int64_t base;
+  __shared__ int ws[32];
+  if (threadIdx.x == 0) base = offset[blockIdx.x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t c0 = b0; c0 < b0 + kChunk && c0 < len; c0 += blockDim.x) {  // block-uniform
+    const int64_t i = c0 + threadIdx.x;
+    const bool nl = i < len && i < b0 + kChunk && text[i] == '\n';
+    const unsigned int ball = __ballot_sync(0xffffffffu, nl);
+    if (lane == 0) ws[warp] = __popc(ball);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < nw; ++w) {
+      if (w < warp) before += ws[w];
+      total += ws[w];
+    }
+    if (nl) pos[base + before + __popc(ball & ((1u << lane) - 1u))] = i;
+    __syncthreads();
+    if (threadIdx.x == 0) base += total;
+    __syncthreads();
+  }
+}
+
+// single-CTA exclusive scan (in place), total in *sum
+__global__ void __launch_bounds__(1024) scan_excl_kernel(int64_t* __restrict__ a, int64_t n, int64_t* __restrict__ sum) {
+  __shared__ int64_t carry_s;
+  __shared__ int64_t warp_tot[32];
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int64_t b0 = 0; b0 < n; b0 += 1024) {
+    const int64_t i = b0 + threadIdx.x;
+    const int64_t x = i < n ? a[i] : 0;
+    int64_t incl = x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[w] = incl;
+    __syncthreads();
+    int64_t wb = 0;
+    for (int j = 0; j < w; ++j) wb += warp_tot[j];
+    const int64_t carry = carry_s;
+    if (i < n) a[i] = carry + wb + incl - x;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry_s = carry + wb + incl;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && sum) *sum = carry_s;
+}
+
+__device__ inline void line_span(const int64_t* pos, int64_t nnl, int64_t len, int64_t li, int64_t* a, int64_t* b) {
+  *a = li == 0 ? 0 : pos[li - 1] + 1;
+  *b = li < nnl ? pos[li] : len;
+}
+
+// flag[l] = 1 for non-empty data lines (after the header line)
+__global__ void line_flag_kernel(const char* __restrict__ text, int64_t len, const int64_t* __restrict__ pos,
+                                 int64_t nnl, int64_t first, int64_t nlines, int64_t* __restrict__ flag) {
+  for (int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; l < nlines; l += int64_t(gridDim.x) * blockDim.x) {
+    int64_t a, b;
+    line_span(pos, nnl, len, first + l, &a, &b);
+    bool nonempty = false;
+    for (int64_t i = a; i < b && !nonempty; ++i) nonempty = !is_space(text[i]);
+    flag[l] = nonempty ? 1 : 0;
+  }
+}
+
+__global__ void line_parse_kernel(const char* __restrict__ text, int64_t len, const int64_t* __restrict__ pos,
+                                  int64_t nnl, int64_t first, int64_t nlines, const int64_t* __restrict__ row_of,
+                                  int k, double* __restrict__ codes, int64_t* __restrict__ ids,
+                                  unsigned long long* __restrict__ bad_line) {
+  for (int64_t l = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; l < nlines; l += int64_t(gridDim.x) * blockDim.x) {
+    int64_t a, b;
+    line_span(pos, nnl, len, first + l, &a, &b);
+    while (a < b && is_space(text[a])) ++a;  // trim(line)
+    while (b > a && is_space(text[b - 1])) --b;
+    if (a == b) continue;
+    const int64_t row = row_of[l];
+    const unsigned long long lineno = static_cast<unsigned long long>(first + l + 1);
+    // cell count first (split keeps empty cells)
+    int cells = 1;
+    for (int64_t i = a; i < b; ++i) cells += text[i] == ',';
+    if (cells != k + 1) {
+      atomicMin(bad_line, lineno);
+      continue;
+    }
+    int64_t c0 = a;
+    for (int cell = 0; cell <= k; ++cell) {
+      int64_t c1 = c0;
+      while (c1 < b && text[c1] != ',') ++c1;
+      int64_t x = c0, y = c1;  // trim(cell)
+      while (x < y && is_space(text[x])) ++x;
+      while (y > x && is_space(text[y - 1])) --y;
+      if (cell == 0) {
+        if (ids) {
+          ids[2 * row] = x;
+          ids[2 * row + 1] = y - x;
+        }
+      } else {
+        int st = 0;
+        const double v = parse_cell(text + x, static_cast<int>(y - x < 1 << 30 ? y - x : 1 << 30), &st);
+        if (st) atomicMin(bad_line, lineno);
+        if (codes) codes[row * k + cell - 1] = v;
+      }
+      c0 = c1 + 1;
+    }
+  }
+}
+
 int grid_for(hc_ctx ctx, int64_t n) {
   const int64_t g = (n + 255) / 256;
   return static_cast<int>(g < 1 ? 1 : (g > int64_t(ctx->sm_count) * 16 ? int64_t(ctx->sm_count) * 16 : g));
@@ -733,6 +876,110 @@ int hc_codes_csv_write(hc_ctx ctx, const float* codes, int64_t rows, int k, uint
     HC_CHECK_LAUNCH(ctx, "csv_write_kernel");
   }
   HC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  return HC_OK;
+}
+
+
+int hc_codes_csv_read(hc_ctx ctx, const char* text, int64_t len, int* k_out, int64_t* rows_out, double* codes,
+                      int64_t* ids, int64_t capacity_rows) {
+  HC_REQUIRE(ctx && k_out && rows_out, HC_EINVAL, "codes_csv_read: null argument");
+  HC_REQUIRE(len >= 0 && (len == 0 || text), HC_EINVAL, "codes_csv_read: bad text");
+  const int64_t nblocks = (len + kChunk - 1) / kChunk;
+  // scratch: counts[nblocks + 1] | newline positions | flags / row numbers
+  // (newlines <= len; lines <= newlines + 1)
+  auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
+  int rc = ensure_scratch(ctx, up(sizeof(int64_t) * (nblocks + 2)) + 2 * up(sizeof(int64_t) * (len + 2)) + 256);
+  if (rc != HC_OK) return rc;
+  char* base = static_cast<char*>(ctx->scratch);
+  int64_t* counts = reinterpret_cast<int64_t*>(base);
+  int64_t* pos = reinterpret_cast<int64_t*>(base + up(sizeof(int64_t) * (nblocks + 2)));
+  int64_t* flag = reinterpret_cast<int64_t*>(base + up(sizeof(int64_t) * (nblocks + 2)) + up(sizeof(int64_t) * (len + 2)));
+  int64_t* misc = counts + nblocks;  // [0] newline count, [1] row count
+  unsigned long long* bad = reinterpret_cast<unsigned long long*>(pos + len + 1);  // spare slot after positions
+  int64_t nnl = 0;
+  if (nblocks > 0) {
+    nl_count_kernel<<<static_cast<int>(nblocks), 256, 0, ctx->stream>>>(text, len, counts);
+    HC_CHECK_LAUNCH(ctx, "nl_count_kernel");
+    scan_excl_kernel<<<1, 1024, 0, ctx->stream>>>(counts, nblocks, misc);
+    HC_CHECK_LAUNCH(ctx, "scan_excl_kernel");
+    nl_write_kernel<<<static_cast<int>(nblocks), 256, 0, ctx->stream>>>(text, len, counts, pos);
+    HC_CHECK_LAUNCH(ctx, "nl_write_kernel");
+    HC_CUDA_TRY(cudaMemcpyAsync(&nnl, misc, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    HC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  }
+  const int64_t total_lines = len > 0 ? nnl + 1 : 0;  // the segment after the last '\n' may be empty
+  // header: first non-empty line, parsed on the host (io.cpp:276-288); searched among the
+  // first 4096 lines
+  int64_t hline = -1;
+  std::vector<int64_t> hpos(static_cast<size_t>(nnl < 4096 ? nnl : 4096));
+  if (!hpos.empty())
+    HC_CUDA_TRY(cudaMemcpy(hpos.data(), pos, sizeof(int64_t) * hpos.size(), cudaMemcpyDeviceToHost));
+  std::string line;
+  for (int64_t li = 0; li < total_lines && li <= static_cast<int64_t>(hpos.size()); ++li) {
+    const int64_t a = li == 0 ? 0 : hpos[static_cast<size_t>(li - 1)] + 1;
+    int64_t b = len;
+    if (li < nnl) {
+      if (li >= static_cast<int64_t>(hpos.size())) break;
+      b = hpos[static_cast<size_t>(li)];
+    }
+    if (b - a > (1 << 20)) return set_error(HC_EINVAL, "codes_csv_read: header line too long");
+    line.assign(static_cast<size_t>(b - a), '\0');
+    if (b > a) HC_CUDA_TRY(cudaMemcpy(&line[0], text + a, static_cast<size_t>(b - a), cudaMemcpyDeviceToHost));
+    size_t x = 0, y = line.size();
+    while (x < y && std::isspace(static_cast<unsigned char>(line[x]))) ++x;
+    while (y > x && std::isspace(static_cast<unsigned char>(line[y - 1]))) --y;
+    if (x == y) continue;
+    line = line.substr(x, y - x);
+    hline = li;
+    break;
+  }
+  if (hline < 0) return set_error(HC_EINVAL, "codes_csv_read: missing codes header");
+  {
+    std::vector<std::string> cells(1);
+    for (char ch : line) {
+      if (ch == ',') cells.emplace_back();
+      else cells.back().push_back(ch);
+    }
+    auto trim = [](const std::string& t) {
+      size_t x = 0, y = t.size();
+      while (x < y && std::isspace(static_cast<unsigned char>(t[x]))) ++x;
+      while (y > x && std::isspace(static_cast<unsigned char>(t[y - 1]))) --y;
+      return t.substr(x, y - x);
+    };
+    const std::string where = " (line " + std::to_string(hline + 1) + ")";
+    if (cells.size() < 2 || trim(cells[0]) != "id")
+      return set_error(HC_EINVAL, "codes_csv_read: bad codes header (expected id,c0,...)" + where);
+    for (size_t i = 1; i < cells.size(); ++i)
+      if (trim(cells[i]) != "c" + std::to_string(i - 1))
+        return set_error(HC_EINVAL, "codes_csv_read: bad codes header column " + std::to_string(i - 1) + where);
+    *k_out = static_cast<int>(cells.size()) - 1;
+  }
+  const int k = *k_out;
+  const int64_t first = hline + 1, nlines = total_lines - first;
+  int64_t rows = 0;
+  if (nlines > 0) {
+    line_flag_kernel<<<grid_for(ctx, nlines), 256, 0, ctx->stream>>>(text, len, pos, nnl, first, nlines, flag);
+    HC_CHECK_LAUNCH(ctx, "line_flag_kernel");
+    scan_excl_kernel<<<1, 1024, 0, ctx->stream>>>(flag, nlines, misc + 1);
+    HC_CHECK_LAUNCH(ctx, "scan_excl_kernel");
+    HC_CUDA_TRY(cudaMemcpyAsync(&rows, misc + 1, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    HC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+  }
+  *rows_out = rows;
+  if (!codes && !ids) return HC_OK;  // size query
+  HC_REQUIRE(rows <= capacity_rows, HC_EINVAL, "codes_csv_read: output capacity too small");
+  if (nlines > 0) {
+    const unsigned long long none = ~0ull;
+    HC_CUDA_TRY(cudaMemcpyAsync(bad, &none, sizeof(none), cudaMemcpyHostToDevice, ctx->stream));
+    line_parse_kernel<<<grid_for(ctx, nlines), 128, 0, ctx->stream>>>(text, len, pos, nnl, first, nlines, flag, k,
+                                                                        codes, ids, bad);
+    HC_CHECK_LAUNCH(ctx, "line_parse_kernel");
+    unsigned long long bad_line = 0;
+    HC_CUDA_TRY(cudaMemcpyAsync(&bad_line, bad, sizeof(bad_line), cudaMemcpyDeviceToHost, ctx->stream));
+    HC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
+    if (bad_line != ~0ull)
+      return set_error(HC_EINVAL, "codes_csv_read: malformed data (line " + std::to_string(bad_line) + ")");
+  }
   return HC_OK;
 }
 

@@ -116,3 +116,68 @@ def test_parse_doubles_matches_glibc_strtod(api, ctx):
         if not same:
             bad.append((c, g, s, w, t))
     assert not bad, f"{len(bad)} mismatches, e.g. {bad[:6]}"
+
+
+def _ref_read(ref, path, cap_rows=200_000, k=9):
+    import ctypes
+
+    rows, kk = ctypes.c_int64(), ctypes.c_int()
+    codes = np.zeros(cap_rows * k, np.float64)
+    ids = ctypes.create_string_buffer(cap_rows * 24 + 4096)
+    rc = ref.ref_read_codes_csv(str(path).encode(), ctypes.byref(rows), ctypes.byref(kk), codes, codes.size, ids,
+                                len(ids))
+    if rc:
+        return None, ids.value.decode()
+    n = rows.value * kk.value
+    return (ids.value.decode().split("\n")[:rows.value], codes[:n].reshape(rows.value, kk.value)), None
+
+
+@pytest.mark.parametrize("rows,k", [(1, 3), (5000, 6), (123_457, 9)])
+def test_codes_csv_round_trip_matches_reference_reader(api, ctx, tmp_path, rows, k):
+    ref = oracle.reference(81)
+    if ref is None:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    rng = np.random.default_rng(rows)
+    Z = (rng.lognormal(-1, 3, (rows, k)) * (rng.random((rows, k)) > 0.05)).astype(np.float32)
+    data = api.codes_csv(ctx, torch.from_numpy(Z).cuda(), first_id=7)
+    path = tmp_path / "c.csv"
+    path.write_bytes(data)
+    ids, codes = api.read_codes_csv(ctx, data)
+    (rids, rcodes), err = _ref_read(ref, path, rows, k)
+    assert err is None
+    assert ids == rids == [str(7 + r) for r in range(rows)]
+    got = codes.cpu().numpy()
+    assert got.tobytes() == rcodes.tobytes()
+    assert np.array_equal(got, Z.astype(np.float64))  # %.17g round-trips the widened floats exactly
+
+
+CASES = [
+    b"id,c0,c1\na,1,2\nb,3.5,-4e-3\n",
+    b"\n  \nid , c0 ,c1\r\n  x , 1e5 , .5 \r\n\n y,inf,-0x1p-3\n",   # blank lines, CRLF, spaces, inf, hex
+    b"id,c0\nr0,1\nr1,2",                                          # no trailing newline
+    b"id,c0,c1\na,1\n",                                            # wrong cell count
+    b"id,c0,c1\na,1,2x\n",                                         # trailing junk
+    b"id,c0,c1\na,1,1e400\n",                                      # out of range
+    b"ix,c0\na,1\n",                                               # bad header
+    b"id,c0,c2\na,1,2\n",                                          # bad header column
+    b"   \n\n",                                                    # missing header
+    b"id,c0,c1\n,1,2\nb,,3\n",                                     # empty id, empty cell
+]
+
+
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_codes_csv_reader_edge_cases_match_reference(api, ctx, tmp_path, case):
+    ref = oracle.reference(81)
+    if ref is None:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    data = CASES[case]
+    path = tmp_path / "c.csv"
+    path.write_bytes(data)
+    want, err = _ref_read(ref, path, 16, 4)
+    if err is not None:
+        with pytest.raises(ValueError):
+            api.read_codes_csv(ctx, data)
+        return
+    ids, codes = api.read_codes_csv(ctx, data)
+    assert ids == want[0]
+    assert codes.cpu().numpy().tobytes() == want[1].tobytes()
