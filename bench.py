@@ -63,6 +63,12 @@ CONFIGS = {
     # the reference's path tracer, latent k = 6 (naive: spectral n = 81).
     # Units are pixel-samples; the algorithmic bytes are the image writes (k floats per pixel
     # over spp samples), so the HBM fraction is ~0: the tracer is fp64 / latency bound.
+    # codes CSV on the device — write_codes_csv (%.17g) then read_codes_csv
+    # (exact strtod) of 2^21 rows x k = 6 codes; algorithmic bytes per code: 4 B float in, the
+    # ~20 B of text written and read back, 8 B double out.
+    "8": dict(name="codes CSV round trip on the device: write_codes_csv (%.17g) + read_codes_csv (exact "
+                   "strtod), 2^21 rows x k=6", units=(1 << 21) * 6, rows=1 << 21, k=6, unit="M codes/s",
+              bytes_per_unit=52, rot=1, graph=False),
     "7": dict(name="Cornell box path trace (bm_render scene + block + 2nd light), 256x256, 64 spp, depth 3, "
                    "latent k=6 (naive: spectral n=81)", W=256, H=256, spp=64, depth=3, k=6,
               unit="M samples/s", bytes_per_unit=6 * 4 / 64, rot=1, graph=False),
@@ -217,6 +223,25 @@ def cpu_reference_run(cfg_key: str, budget_s: float, threads: int = 0, rank: int
             ref.ref_mlp_forward(rgb, P, 64, 6, w["w1"], w["b1"], w["w2"], w["b2"], w["w3"], w["b3"], out, nthreads)
 
         sample = f"{P} texels (8 rows)"
+    elif cfg_key == "8":
+        import ctypes as C
+        import tempfile
+
+        rows = 1 << 15
+        Zs = np.exp(synth.uniform_np(SEED, "csv.codes", 0, rows * k) * 20.0 - 10.0).astype(np.float32)
+        tmp = tempfile.mkdtemp()
+        path = (tmp + "/codes.csv").encode()
+        buf_codes = np.zeros(rows * k, np.float64)
+        ids = C.create_string_buffer(rows * 24 + 4096)
+        r_rows, r_k = C.c_int64(), C.c_int()
+        P = rows * k
+        nthreads = 1
+
+        def run():
+            ref.ref_write_codes_csv(path, Zs, rows, k, 0)
+            ref.ref_read_codes_csv(path, C.byref(r_rows), C.byref(r_k), buf_codes, buf_codes.size, ids, len(ids))
+
+        sample = f"{rows} rows x k={k}: the reference's write_codes_csv + read_codes_csv (single-threaded, /tmp file)"
     elif cfg_key == "7":
         import ctypes as C
 
@@ -388,6 +413,28 @@ class Workload:
                 gt, test, out, prev = self.sets[i % R]
                 api.scene_color_report_dev(codec, gt, test, out=out, preview=prev)
             self.step = step
+        elif cfg_key == "8":
+            rows, k = cfg["rows"], cfg["k"]
+            Z = api.synth_uniform(ctx, SEED + rank, "csv.codes", 0, rows * k).reshape(rows, k)
+            Z = torch.exp(Z * 20.0 - 10.0)  # codes across many decades
+            self.units = rows * k
+            self.sets.append({"rgb": None})
+            length = C_int64()
+            api._check(api._lib.lib().hc_codes_csv_write(ctx.h, Z.data_ptr(), rows, k, 0, None, 0,
+                                                        api.C.byref(length)))
+            self.text = torch.empty(length.value, dtype=torch.uint8, device="cuda")
+            self.codes = torch.empty(rows, k, dtype=torch.float64, device="cuda")
+            self.ids = torch.empty(rows, 2, dtype=torch.int64, device="cuda")
+
+            def step(i):
+                lib = api._lib.lib()
+                ln, kk, rr = C_int64(), api.C.c_int(), C_int64()
+                ctx.bind_stream()
+                api._check(lib.hc_codes_csv_write(ctx.h, Z.data_ptr(), rows, k, 0, self.text.data_ptr(),
+                                                  self.text.numel(), api.C.byref(ln)))
+                api._check(lib.hc_codes_csv_read(ctx.h, self.text.data_ptr(), ln.value, api.C.byref(kk),
+                                                 api.C.byref(rr), self.codes.data_ptr(), self.ids.data_ptr(), rows))
+            self.step = step
         elif cfg_key == "7":
             W, H, spp, depth = cfg["W"], cfg["H"], cfg["spp"], cfg["depth"]
             scene = synth.cornell_scene(N_SPEC, block=True)
@@ -505,6 +552,12 @@ def time_graph(torch, wl, steps: int, warmup: int, stream) -> tuple[float, int]:
         g.replay()
         torch.cuda.synchronize()
     return g, per_step, n_in_graph
+
+
+def C_int64():
+    import ctypes
+
+    return ctypes.c_int64()
 
 
 def run_ours(args) -> int:
@@ -701,10 +754,10 @@ def run_ours(args) -> int:
             "config": {"workload": cfg["name"], "config_id": args.config, "units_per_gpu": wl.units,
                        "l2": (f"{R} rotating input/output buffer sets"
                               f" ({'each' if R == 1 else 'rotation'} > 2x 126 MB L2)") if cfg.get("graph", True)
-                             else "compute-bound step; scene tables are KB-sized (no L2 rotation needed)",
+                             else "compute-bound step (no L2 rotation needed)",
                        "timing": ("CUDA graph of the step replayed K times; CUDA events; max over ranks"
                                   if cfg.get("graph", True) else
-                                  "K synchronous render calls (host scene compile included); CUDA events; "
+                                  "K synchronous library calls (host-side setup included); CUDA events; "
                                   "max over ranks"),
                        "parallelism": f"row bands, {args.scaling} scaling, {world} rank(s), no data-path collective"},
             "roofline": roof,
