@@ -31,12 +31,14 @@ def _values(seed: int, n: int) -> np.ndarray:
     uni = rng.random(n)                                                              # [0, 1)
     ints = rng.integers(-10**17, 10**17, n).astype(np.float64)                      # integers, 1e17 edge
     f32 = rng.normal(0, 1, n).astype(np.float32).astype(np.float64) * 10.0 ** rng.integers(-12, 12, n)
+    f32w = rng.normal(0, 1, n).astype(np.float32).astype(np.float64) * 2.0 ** rng.integers(-60, 60, n)  # widened floats
+    dyad = rng.integers(1, 2**40, n) / 2.0 ** rng.integers(0, 70, n)                # exact 17th-digit ties
     sub = rng.integers(1, 2**52, n // 10, dtype=np.int64).view(np.float64)          # subnormals
     special = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 5e-324, 1.7976931348623157e308, 2.2250738585072014e-308,
                         1e-5, 1e-4, 0.0001234, 1e16, 1e17, 9.9999999999999995e16, 99999999999999999.0,
                         1234567890123456.75, 1234567890123456.25, 0.1, 0.5, 1.0, 123.0, 2.0**63, 2.0**-1074,
                         0.30000000000000004, 9.5367431640625e-07, 1e22, 1e23, 4.35e-6])
-    return np.concatenate([bits, uni, -uni, ints, f32, sub, special])
+    return np.concatenate([bits, uni, -uni, ints, f32, f32w, -dyad, dyad, sub, special])
 
 
 def test_format_g17_matches_glibc(api, ctx):
@@ -181,3 +183,53 @@ def test_codes_csv_reader_edge_cases_match_reference(api, ctx, tmp_path, case):
     ids, codes = api.read_codes_csv(ctx, data)
     assert ids == want[0]
     assert codes.cpu().numpy().tobytes() == want[1].tobytes()
+
+
+def _messy_csv(seed: int, rows: int, k: int) -> bytes:
+    """Valid codes CSV with the whitespace, blank lines, long lines and number spellings
+    read_codes_csv accepts: isspace bytes (\\t \\v \\f \\r, space) around cells and next to
+    newlines, >19-digit decimals (exact path), leading zeros, exponents, hex, inf."""
+    rng = np.random.default_rng(seed)
+    ws = [b"", b" ", b"\t", b"\x0b", b"\x0c", b"\r", b"  \x0b"]
+    out = [b"id," + b",".join(b"c%d" % j for j in range(k)) + b"\n"]
+    for r in range(rows):
+        if rng.random() < 0.05:
+            out.append(rng.choice(ws) + b"\n")  # blank (whitespace-only) line
+        cells = [b"r%d" % r]
+        for _ in range(k):
+            kind = rng.integers(0, 6)
+            if kind == 0:
+                cells.append(b"%.17g" % rng.lognormal(0, 20))
+            elif kind == 1:
+                cells.append(b"0.000" + bytes(rng.integers(48, 58, rng.integers(20, 60)).astype(np.uint8)))
+            elif kind == 2:
+                cells.append(b"-%de%d" % (rng.integers(1, 10**9), rng.integers(-300, 290)))
+            elif kind == 3:
+                cells.append(b"00%d.%d" % (rng.integers(0, 1000), rng.integers(0, 10**6)))
+            elif kind == 4:
+                cells.append(b"0x1.%xp%d" % (rng.integers(0, 2**40), rng.integers(-1000, 1000)))
+            else:
+                cells.append(b"%.9g" % rng.standard_normal())
+        pad = b" " * int(rng.integers(300, 900)) if rng.random() < 0.02 else b""  # long lines
+        line = b",".join(bytes(rng.choice(ws)) + c + bytes(rng.choice(ws)) for c in cells)
+        out.append(bytes(rng.choice(ws)) + line + pad + bytes(rng.choice(ws)) + b"\n")
+    return b"".join(out)
+
+
+@pytest.mark.parametrize("shift", [0, 1, 3, 7, 13])
+def test_codes_csv_reader_messy_text_unaligned_matches_reference(api, ctx, tmp_path, shift):
+    ref = oracle.reference(81)
+    if ref is None:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    rows, k = 3000, 5
+    data = _messy_csv(shift, rows, k)
+    assert len(data) > 4 * 16384  # several newline chunks
+    path = tmp_path / "c.csv"
+    path.write_bytes(data)
+    (rids, rcodes), err = _ref_read(ref, path, rows, k)
+    assert err is None, err
+    buf = torch.zeros(len(data) + 32, dtype=torch.uint8, device="cuda")
+    buf[shift:shift + len(data)] = torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda()
+    ids, codes = api.read_codes_csv(ctx, data, text=buf[shift:shift + len(data)])
+    assert ids == rids
+    assert codes.cpu().numpy().tobytes() == rcodes.tobytes()
