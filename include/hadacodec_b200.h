@@ -251,6 +251,15 @@ int hc_format_g17(hc_ctx ctx, const double* v, int64_t n, char* slots, uint8_t* 
  * bytes) receives the file.  Synchronous. */
 int hc_codes_csv_write(hc_ctx ctx, const float* codes, int64_t rows, int k, uint64_t first_id, char* out,
                        int64_t capacity, int64_t* length);
+/* The general write_codes_csv (io.cpp:312-330; the reference's LatentCode values are
+ * doubles): codes [rows][k] in device memory as HC_DTYPE_F32 or HC_DTYPE_F64; ids either
+ * NULL (decimal first_id + row) or id_bytes (device) with id_offsets[rows + 1] (device,
+ * int64) delimiting row r's id, written verbatim as `f << ids[r]` does.  rows == 0
+ * writes "id\n" (k = 0 for no codes, as the reference does).  Size query as above. */
+enum { HC_DTYPE_F32 = 0, HC_DTYPE_F64 = 1 };
+int hc_codes_csv_write_ids(hc_ctx ctx, const void* codes, int dtype, int64_t rows, int k, const char* id_bytes,
+                           const int64_t* id_offsets, uint64_t first_id, char* out, int64_t capacity,
+                           int64_t* length);
 /* parse_double (io.cpp:78-88: std::stod of a trimmed cell, fully consumed) of n cells held
  * in fixed slots (stride bytes, lens[i] used): out[i] the correctly rounded double,
  * status[i] 0 ok, 1 not a number / trailing junk, 2 out of range (ERANGE: std::stod throws). */

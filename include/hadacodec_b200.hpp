@@ -212,6 +212,22 @@ struct SceneColorReport {  // evaluation.hpp:50-55
 };
 SceneColorReport scene_color_report(const Codec& c, const ChannelImage& ground_truth, const ChannelImage& test);
 
+// ---- codes CSV (io.hpp:19-23, :48-56): %.17g formatting and strtod parsing on the GPU,
+// byte-identical files / bit-identical values.  Malformed input raises FormatError with
+// the path and the first bad line, as the reference does (the message text differs); a
+// ragged code set is rejected before anything is written.
+class FormatError : public std::runtime_error {
+ public:
+  using std::runtime_error::runtime_error;
+};
+struct CodesCsv {
+  std::vector<std::string> ids;
+  std::vector<LatentCode> codes;
+};
+CodesCsv read_codes_csv(Device& dev, const std::string& path);
+void write_codes_csv(Device& dev, const std::string& path, const std::vector<std::string>& ids,
+                     const std::vector<LatentCode>& codes);
+
 // ---- G-buffer latent shading (configs 2/3): one frame, host buffers.
 struct GBuffer {
   int width = 0, height = 0, lights = 0;

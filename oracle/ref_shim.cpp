@@ -676,6 +676,25 @@ int ref_write_codes_csv(const char* path, const float* Z, int64_t rows, int k, u
   }
 }
 
+// write_codes_csv with double codes and string ids (bytes [off[r], off[r+1]) of idblob).
+int ref_write_codes_csv_ids(const char* path, const double* Z, int64_t rows, int k, const char* idblob,
+                            const int64_t* off) {
+  try {
+    std::vector<std::string> ids;
+    std::vector<LatentCode> codes;
+    for (int64_t r = 0; r < rows; ++r) {
+      ids.emplace_back(idblob + off[r], static_cast<size_t>(off[r + 1] - off[r]));
+      LatentCode z;
+      z.z.assign(Z + r * k, Z + (r + 1) * k);
+      codes.push_back(z);
+    }
+    write_codes_csv(path, ids, codes);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
 // read_codes_csv (io.cpp:267-310): returns 0 and fills rows / k / codes (row-major,
 // capacity doubles) / ids (concatenated with '\n'), or 1 with the error text in ids.
 int ref_read_codes_csv(const char* path, int64_t* rows, int* k, double* codes, int64_t capacity, char* ids,

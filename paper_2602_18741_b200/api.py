@@ -437,16 +437,33 @@ def parse_doubles(ctx: Context, cells: Sequence[bytes]) -> tuple[np.ndarray, np.
     return out.cpu().numpy(), st.cpu().numpy()
 
 
-def codes_csv(ctx: Context, codes: torch.Tensor, first_id: int = 0) -> bytes:
-    """write_codes_csv (io.cpp:312-330) of codes [rows, k] (float32, device), ids first_id + row."""
-    codes = _cuda(codes, torch.float32, "codes")
+def codes_csv(ctx: Context, codes: torch.Tensor, first_id: int = 0, ids: Optional[Sequence[str]] = None) -> bytes:
+    """write_codes_csv (io.cpp:312-330) of codes [rows, k] (float32 or float64, device); ids
+    first_id + row, or the given strings written verbatim (the reference's `ids` argument)."""
+    if codes.dtype not in (torch.float32, torch.float64):
+        codes = codes.float()
+    dtype = 1 if codes.dtype == torch.float64 else 0
+    codes = _cuda(codes, codes.dtype, "codes")
     rows, k = codes.shape
+    id_bytes = id_off = None
+    if ids is not None:
+        if len(ids) != rows:
+            raise ValueError("codes_csv: one id per row")
+        enc = [str(i).encode() for i in ids]
+        blob = b"".join(enc)
+        off = np.zeros(rows + 1, np.int64)
+        np.cumsum([len(e) for e in enc], out=off[1:])
+        id_bytes = torch.frombuffer(bytearray(blob), dtype=torch.uint8).cuda() if blob else \
+            torch.zeros(1, dtype=torch.uint8, device="cuda")
+        id_off = torch.from_numpy(off).cuda()
     length = C.c_int64()
     ctx.bind_stream()
-    _check(_lib.lib().hc_codes_csv_write(ctx.h, _p(codes), rows, k, first_id, None, 0, C.byref(length)))
+    lib = _lib.lib()
+    ib, io = (_p(id_bytes), _p(id_off)) if id_bytes is not None else (None, None)
+    _check(lib.hc_codes_csv_write_ids(ctx.h, _p(codes), dtype, rows, k, ib, io, first_id, None, 0, C.byref(length)))
     out = torch.empty(length.value, dtype=torch.uint8, device=codes.device)
-    _check(_lib.lib().hc_codes_csv_write(ctx.h, _p(codes), rows, k, first_id, _p(out), length.value,
-                                         C.byref(length)))
+    _check(lib.hc_codes_csv_write_ids(ctx.h, _p(codes), dtype, rows, k, ib, io, first_id, _p(out), length.value,
+                                      C.byref(length)))
     return bytes(out.cpu().numpy())
 
 

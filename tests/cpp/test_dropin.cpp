@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <limits>
 #include <stdexcept>
+#include <string>
 #include <vector>
 
 #include "hadacodec_b200.hpp"
@@ -295,6 +296,37 @@ int main() {
     job.spp = 2;
     sc.wall_material[4] = 9;
     CHECK_THROWS_AS(render(codec, sc, job), std::invalid_argument);
+  }
+
+  {  // codes CSV round trip and validation (test_io.cpp:133-155)
+    const std::string path = "/tmp/hc_b200_dropin_codes.csv";
+    LatentCode a, b;
+    a.z = {0.1, 0.25, 1.0 / 3.0, 0.0, 5e-17, 2.0};
+    b.z = {1, 2, 3, 4, 5, 6};
+    write_codes_csv(dev, path, {"x", "y"}, {a, b});
+    const CodesCsv back = read_codes_csv(dev, path);
+    CHECK(back.codes.size() == 2u);
+    CHECK(back.ids.size() == 2u && back.ids[0] == "x" && back.ids[1] == "y");
+    CHECK(back.codes[0].k() == 6);
+    for (int i = 0; i < 6; ++i) {
+      CHECK(back.codes[0][i] == a[i]);  // %.17g round-trips doubles bit-exactly
+      CHECK(back.codes[1][i] == b[i]);
+    }
+    auto write_text = [&](const char* t) {
+      FILE* f = std::fopen(path.c_str(), "wb");
+      std::fputs(t, f);
+      std::fclose(f);
+    };
+    write_text("id,c0,c9\nx,1,2\n");  // wrong column labels
+    CHECK_THROWS_AS(read_codes_csv(dev, path), FormatError);
+    write_text("id,c0,c1\nx,1\n");  // short row
+    CHECK_THROWS_AS(read_codes_csv(dev, path), FormatError);
+    LatentCode c;
+    c.z = {1, 2};
+    CHECK_THROWS_AS(write_codes_csv(dev, path, {"x", "y"}, {a, c}), FormatError);  // inconsistent dimensions
+    CHECK_THROWS_AS(write_codes_csv(dev, path, {"x"}, {a, b}), FormatError);       // id count
+    CHECK_THROWS_AS(read_codes_csv(dev, "/nonexistent/dir/codes.csv"), FormatError);
+    std::remove(path.c_str());
   }
 
   std::printf("drop-in: %d checks, %d failures, %lld kernel launches\n", g_checks, g_fail,

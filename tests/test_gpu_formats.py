@@ -60,10 +60,39 @@ def test_codes_csv_matches_reference_writer(api, ctx, tmp_path, rows, k):
     path = tmp_path / "codes.csv"
     assert ref.ref_write_codes_csv(str(path).encode(), np.ascontiguousarray(Z.reshape(-1)), rows, k, 1000) == 0
     want = path.read_bytes()
-    if rows == 0:
-        assert got.startswith(b"id,c0")  # the reference writes an empty header for no codes
+    assert got == want  # rows == 0: "id\n" (the reference's k is 0 for no codes)
+
+
+def _ids_blob(ids):
+    enc = [i.encode() for i in ids]
+    off = np.zeros(len(enc) + 1, np.int64)
+    np.cumsum([len(e) for e in enc], out=off[1:])
+    return b"".join(enc) or b"\0", off
+
+
+@pytest.mark.parametrize("rows,k", [(2, 6), (5000, 9), (0, 6)])
+def test_codes_csv_double_codes_string_ids_match_reference_writer(api, ctx, tmp_path, rows, k):
+    """The reference's own signature: LatentCode (double) values and arbitrary string ids."""
+    ref = oracle.reference(81)
+    if ref is None:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    rng = np.random.default_rng(rows)
+    if rows == 2:  # test_io.cpp "codes CSV round trip and validation"
+        Z = np.array([[0.1, 0.25, 1.0 / 3.0, 0.0, 5e-17, 2.0], [1, 2, 3, 4, 5, 6]], np.float64)
+        ids = ["x", "y"]
     else:
-        assert got == want
+        Z = rng.lognormal(0, 30, (rows, k)) * rng.choice([-1.0, 1.0], (rows, k))
+        Z[rng.random((rows, k)) < 0.05] = 0.0
+        ids = [("row%d" % r) if r % 3 else ("sample_%x-%d" % (r * 7919, r)) for r in range(rows)]
+    got = api.codes_csv(ctx, torch.from_numpy(Z).cuda().reshape(rows, k), ids=ids)
+    blob, off = _ids_blob(ids)
+    path = tmp_path / "codes.csv"
+    assert ref.ref_write_codes_csv_ids(str(path).encode(), np.ascontiguousarray(Z.reshape(-1)), rows, k, blob, off) == 0
+    assert got == path.read_bytes()
+    if rows:
+        back_ids, back = api.read_codes_csv(ctx, got)
+        assert back_ids == ids
+        assert back.cpu().numpy().tobytes() == Z.tobytes()  # %.17g round-trips doubles bit-exactly
 
 
 def _glibc_strtod(cells):
