@@ -358,6 +358,7 @@ class Workload:
         E, D = synth.codec_weights(SEED, k, N_SPEC)
         self.codec = codec = api.Codec(ctx, E, D)
         self.sets = []
+        self.extra = {}  # workload facts added to the JSON line's config
         R = cfg["rot"]
         from paper_2602_18741_b200.sharding import row_band
 
@@ -423,6 +424,7 @@ class Workload:
             api._check(api._lib.lib().hc_codes_csv_write(ctx.h, Z.data_ptr(), rows, k, 0, None, 0,
                                                         api.C.byref(length)))
             self.text = torch.empty(length.value, dtype=torch.uint8, device="cuda")
+            self.extra = {"text_bytes": length.value}
             self.codes = torch.empty(rows, k, dtype=torch.float64, device="cuda")
             self.ids = torch.empty(rows, 2, dtype=torch.int64, device="cuda")
 
@@ -759,7 +761,8 @@ def run_ours(args) -> int:
                                   if cfg.get("graph", True) else
                                   "K synchronous library calls (host-side setup included); CUDA events; "
                                   "max over ranks"),
-                       "parallelism": f"row bands, {args.scaling} scaling, {world} rank(s), no data-path collective"},
+                       "parallelism": f"row bands, {args.scaling} scaling, {world} rank(s), no data-path collective",
+                       **wl.extra},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -252,14 +252,24 @@ int hc_format_g17(hc_ctx ctx, const double* v, int64_t n, char* slots, uint8_t* 
 int hc_codes_csv_write(hc_ctx ctx, const float* codes, int64_t rows, int k, uint64_t first_id, char* out,
                        int64_t capacity, int64_t* length);
 /* The general write_codes_csv (io.cpp:312-330; the reference's LatentCode values are
- * doubles): codes [rows][k] in device memory as HC_DTYPE_F32 or HC_DTYPE_F64; ids either
- * NULL (decimal first_id + row) or id_bytes (device) with id_offsets[rows + 1] (device,
- * int64) delimiting row r's id, written verbatim as `f << ids[r]` does.  rows == 0
+ * doubles): codes [rows][k] in device memory as HC_DTYPE_F32 or HC_DTYPE_F64.  Ids:
+ * id_bytes (device) with id_spans (device, rows x 2 int64: start, length — the layout
+ * hc_codes_csv_read / hc_spectra_csv_read return, so a file's ids pass straight through),
+ * written verbatim as `f << ids[r]` does; or, with id_bytes NULL, id_prefix (host string,
+ * may be NULL) followed by the decimal first_id + row (run_encode's "row" + r).  rows == 0
  * writes "id\n" (k = 0 for no codes, as the reference does).  Size query as above. */
 enum { HC_DTYPE_F32 = 0, HC_DTYPE_F64 = 1 };
 int hc_codes_csv_write_ids(hc_ctx ctx, const void* codes, int dtype, int64_t rows, int k, const char* id_bytes,
-                           const int64_t* id_offsets, uint64_t first_id, char* out, int64_t capacity,
-                           int64_t* length);
+                           const int64_t* id_spans, const char* id_prefix, uint64_t first_id, char* out,
+                           int64_t capacity, int64_t* length);
+/* write_spectra_csv (io.cpp:165-186): header ["id,"] + the n wavelengths (host array, the
+ * canonical grid) in %.9g, then one row per curve: [id ","] values in %.9g (print_g9,
+ * io.cpp:102-106; exact, round half to even, as glibc).  values [rows][n] (device, f32 or
+ * f64).  with_ids = 0: no id column (the reference's empty ids); else ids as in
+ * hc_codes_csv_write_ids.  Size query with out == NULL. */
+int hc_spectra_csv_write(hc_ctx ctx, const void* values, int dtype, int64_t rows, int n, const double* wavelengths,
+                         int with_ids, const char* id_bytes, const int64_t* id_spans, const char* id_prefix,
+                         uint64_t first_id, char* out, int64_t capacity, int64_t* length);
 /* parse_double (io.cpp:78-88: std::stod of a trimmed cell, fully consumed) of n cells held
  * in fixed slots (stride bytes, lens[i] used): out[i] the correctly rounded double,
  * status[i] 0 ok, 1 not a number / trailing junk, 2 out of range (ERANGE: std::stod throws). */
@@ -273,6 +283,31 @@ int hc_parse_doubles(hc_ctx ctx, const char* slots, const uint8_t* lens, int64_t
  * line in hc_last_error() for a bad header, a wrong cell count or a cell std::stod rejects. */
 int hc_codes_csv_read(hc_ctx ctx, const char* text, int64_t len, int* k_out, int64_t* rows_out, double* codes,
                       int64_t* ids, int64_t capacity_rows);
+/* read_spectra_csv (io.cpp:119-163) of a file image on the device: the first non-empty
+ * line is the header — an optional "id" cell (*has_id), then the wavelengths (parsed as
+ * the reference does, written to the host array wavelengths, up to wavelength_capacity;
+ * *m_out = their count); every later non-empty line has m (+1 with ids) cells.  values
+ * (device, rows x m doubles) and ids (device, rows x 2 int64 spans, only with an id
+ * column) as in hc_codes_csv_read; both NULL = size query.  HC_EINVAL with the line for
+ * a missing / empty / unparsable header, a wrong cell count or a cell std::stod rejects. */
+int hc_spectra_csv_read(hc_ctx ctx, const char* text, int64_t len, int* has_id, double* wavelengths,
+                        int wavelength_capacity, int* m_out, int64_t* rows_out, double* values, int64_t* ids,
+                        int64_t capacity_rows);
+
+/* ------------------------------------------------------------------ fp64 codec of the encode / decode tools
+ * run_encode (tools/main.cpp:285-308) per curve: resample(src_wavelengths, row,
+ * zero_outside) onto the canonical grid wavelength_at(i) = lambda_min + lambda_step * i
+ * (spectrum.cpp:60-98; the codec's n samples), then encode (codec.cpp:36-46) in fp64
+ * with the reference's summation order: codes (device, rows x k doubles) bit-identical to
+ * the reference.  values: device, rows x m doubles; src_wavelengths: host, m entries,
+ * strictly increasing (HC_EINVAL "resample: ..." otherwise, as the reference throws). */
+int hc_encode_resampled_f64(hc_codec codec, const double* src_wavelengths, int m, const double* values, int64_t rows,
+                            double lambda_min, double lambda_step, int zero_outside, double* codes);
+/* run_decode (tools/main.cpp:310-328) per code: decode (codec.cpp:52-71) in fp64, spectra
+ * (device, rows x n doubles) bit-identical to the reference.  A code with an entry that is
+ * not >= 0 (NaN included) makes the call return HC_EDOMAIN (the reference's domain_error)
+ * with *first_negative_row (host, may be NULL) = the first such row; -1 otherwise. */
+int hc_decode_f64(hc_codec codec, const double* codes, int64_t rows, double* spectra, int64_t* first_negative_row);
 
 /* ------------------------------------------------------------------ host-buffer entry points
  * Reference-facing value calls: inputs and outputs in HOST memory (pinned for

@@ -717,6 +717,103 @@ int ref_read_codes_csv(const char* path, int64_t* rows, int* k, double* codes, i
   }
 }
 
+// ---- the encode / decode tools (tools/main.cpp:285-328) without their manifests, from
+// the reference's own functions: 0 = ok, 1 = error (message in err).
+namespace {
+CodecWeights shim_weights(int k, double beta, const double* raw_enc, const double* raw_dec) {
+  CodecWeights w;
+  w.k = k;
+  w.n = N;
+  w.beta = beta;
+  w.raw_enc.assign(raw_enc, raw_enc + static_cast<size_t>(k) * N);
+  w.raw_dec.assign(raw_dec, raw_dec + static_cast<size_t>(N) * k);
+  return w;
+}
+int shim_fail(const std::exception& e, char* err, int64_t errcap) {
+  if (err && errcap > 0) {
+    std::strncpy(err, e.what(), static_cast<size_t>(errcap - 1));
+    err[errcap - 1] = '\0';
+  }
+  return 1;
+}
+}  // namespace
+
+int ref_run_encode(const char* in_path, int k, double beta, const double* raw_enc, const double* raw_dec,
+                   const char* out_path, char* err, int64_t errcap) {
+  try {
+    const CodecWeights w = shim_weights(k, beta, raw_enc, raw_dec);
+    const EffectiveWeights eff = effective_weights(w);
+    const SpectraCsv csv = read_spectra_csv(in_path);
+    std::vector<std::string> ids;
+    std::vector<LatentCode> codes;
+    for (std::size_t r = 0; r < csv.rows.size(); ++r) {
+      const SpectralCurve s = resample(csv.wavelengths, csv.rows[r], /*zero_outside=*/true);
+      codes.push_back(encode(eff, s));
+      ids.push_back(r < csv.ids.size() ? csv.ids[r] : "row" + std::to_string(r));
+    }
+    write_codes_csv(out_path, ids, codes);
+    return 0;
+  } catch (const std::exception& e) {
+    return shim_fail(e, err, errcap);
+  }
+}
+
+int ref_run_decode(const char* in_path, int k, double beta, const double* raw_enc, const double* raw_dec,
+                   const char* out_path, char* err, int64_t errcap) {
+  try {
+    const CodecWeights w = shim_weights(k, beta, raw_enc, raw_dec);
+    const CodesCsv csv = read_codes_csv(in_path);
+    std::vector<SpectralCurve> curves;
+    for (const auto& z : csv.codes) curves.push_back(decode(w, z));
+    write_spectra_csv(out_path, csv.ids, curves);
+    return 0;
+  } catch (const std::exception& e) {
+    return shim_fail(e, err, errcap);
+  }
+}
+
+// write_spectra_csv of rows x N doubles; ids = bytes [spans[2r], +spans[2r+1]) of idblob, or
+// none when spans is NULL.
+int ref_write_spectra_csv(const char* path, const double* vals, int64_t rows, const char* idblob,
+                          const int64_t* spans) {
+  try {
+    std::vector<std::string> ids;
+    std::vector<SpectralCurve> curves(static_cast<size_t>(rows));
+    for (int64_t r = 0; r < rows; ++r) {
+      for (int i = 0; i < N; ++i) curves[static_cast<size_t>(r)][i] = vals[r * N + i];
+      if (spans) ids.emplace_back(idblob + spans[2 * r], static_cast<size_t>(spans[2 * r + 1]));
+    }
+    write_spectra_csv(path, ids, curves);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+// read_spectra_csv: wavelengths / values (row-major) / ids ('\n'-joined) up to the
+// capacities, or 1 with the error text in ids.
+int ref_read_spectra_csv(const char* path, int* has_id, double* wl, int wl_cap, int* m, int64_t* rows, double* vals,
+                         int64_t cap, char* ids, int64_t ids_cap) {
+  try {
+    const SpectraCsv c = read_spectra_csv(path);
+    *has_id = c.ids.empty() ? 0 : 1;
+    *m = static_cast<int>(c.wavelengths.size());
+    for (int i = 0; i < *m && i < wl_cap; ++i) wl[i] = c.wavelengths[static_cast<size_t>(i)];
+    *rows = static_cast<int64_t>(c.rows.size());
+    int64_t n = 0;
+    for (const auto& row : c.rows)
+      for (double v : row)
+        if (n < cap) vals[n++] = v;
+    std::string all;
+    for (const auto& id : c.ids) all += id + "\n";
+    std::strncpy(ids, all.c_str(), static_cast<size_t>(ids_cap));
+    return 0;
+  } catch (const std::exception& e) {
+    std::strncpy(ids, e.what(), static_cast<size_t>(ids_cap));
+    return 1;
+  }
+}
+
 int ref_thread_count() { return render_thread_count(); }
 
 }  // extern "C"

@@ -54,7 +54,13 @@ SIGNATURES: dict[str, tuple] = {
     "hc_delta_e94_report": (i32, [vp, vp, vp, i64, vp, vp, vp]),
     "hc_format_g17": (i32, [vp, vp, i64, vp, vp]),
     "hc_codes_csv_write": (i32, [vp, vp, i64, i32, u64, vp, i64, C.POINTER(i64)]),
-    "hc_codes_csv_write_ids": (i32, [vp, vp, i32, i64, i32, vp, vp, u64, vp, i64, C.POINTER(i64)]),
+    "hc_codes_csv_write_ids": (i32, [vp, vp, i32, i64, i32, vp, vp, C.c_char_p, u64, vp, i64, C.POINTER(i64)]),
+    "hc_spectra_csv_write": (i32, [vp, vp, i32, i64, i32, vp, i32, vp, vp, C.c_char_p, u64, vp, i64,
+                                   C.POINTER(i64)]),
+    "hc_spectra_csv_read": (i32, [vp, vp, i64, C.POINTER(i32), vp, i32, C.POINTER(i32), C.POINTER(i64), vp, vp,
+                                  i64]),
+    "hc_encode_resampled_f64": (i32, [vp, vp, i32, vp, i64, C.c_double, C.c_double, i32, vp]),
+    "hc_decode_f64": (i32, [vp, vp, i64, vp, C.POINTER(i64)]),
     "hc_parse_doubles": (i32, [vp, vp, vp, i64, i32, vp, vp]),
     "hc_codes_csv_read": (i32, [vp, vp, i64, C.POINTER(i32), C.POINTER(i64), vp, vp, i64]),
     "hc_render": (i32, [vp, vp, vp, vp, vp, vp, vp]),

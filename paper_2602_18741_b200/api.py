@@ -30,7 +30,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .colorimetry import cmf_matrix, grid
+from .colorimetry import cmf_matrix, grid, wavelengths
 
 _check = _lib.check
 
@@ -437,34 +437,170 @@ def parse_doubles(ctx: Context, cells: Sequence[bytes]) -> tuple[np.ndarray, np.
     return out.cpu().numpy(), st.cpu().numpy()
 
 
-def codes_csv(ctx: Context, codes: torch.Tensor, first_id: int = 0, ids: Optional[Sequence[str]] = None) -> bytes:
-    """write_codes_csv (io.cpp:312-330) of codes [rows, k] (float32 or float64, device); ids
-    first_id + row, or the given strings written verbatim (the reference's `ids` argument)."""
-    if codes.dtype not in (torch.float32, torch.float64):
-        codes = codes.float()
-    dtype = 1 if codes.dtype == torch.float64 else 0
-    codes = _cuda(codes, codes.dtype, "codes")
-    rows, k = codes.shape
-    id_bytes = id_off = None
-    if ids is not None:
-        if len(ids) != rows:
-            raise ValueError("codes_csv: one id per row")
-        enc = [str(i).encode() for i in ids]
-        blob = b"".join(enc)
-        off = np.zeros(rows + 1, np.int64)
-        np.cumsum([len(e) for e in enc], out=off[1:])
-        id_bytes = torch.frombuffer(bytearray(blob), dtype=torch.uint8).cuda() if blob else \
-            torch.zeros(1, dtype=torch.uint8, device="cuda")
-        id_off = torch.from_numpy(off).cuda()
+def _id_args(ids, rows: int):
+    """(id_bytes, id_spans) device tensors for a list of id strings (None: no ids)."""
+    if ids is None:
+        return None, None
+    if len(ids) != rows:
+        raise ValueError("csv: one id per row")
+    enc = [str(i).encode() for i in ids]
+    lens = np.array([len(e) for e in enc], np.int64)
+    spans = np.zeros((max(rows, 1), 2), np.int64)  # never an empty (NULL) tensor
+    if rows:
+        spans[1:, 0] = np.cumsum(lens)[:-1]
+        spans[:, 1] = lens
+    blob = b"".join(enc) + b"\0"
+    return (torch.frombuffer(bytearray(blob), dtype=torch.uint8).cuda(), torch.from_numpy(spans).cuda())
+
+
+def _values_dtype(t: torch.Tensor, name: str) -> tuple[torch.Tensor, int]:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype not in (torch.float32, torch.float64):
+        t = t.float()
+    return t.contiguous(), (1 if t.dtype == torch.float64 else 0)
+
+
+def _sized_write(fn, device) -> bytes:
     length = C.c_int64()
+    _check(fn(None, 0, C.byref(length)))
+    out = torch.empty(length.value, dtype=torch.uint8, device=device)
+    _check(fn(_p(out), length.value, C.byref(length)))
+    return bytes(out.cpu().numpy())
+
+
+def codes_csv(ctx: Context, codes: torch.Tensor, first_id: int = 0, ids: Optional[Sequence[str]] = None,
+              id_prefix: Optional[str] = None) -> bytes:
+    """write_codes_csv (io.cpp:312-330) of codes [rows, k] (float32 or float64, device); ids
+    id_prefix + (first_id + row), or the given strings written verbatim (the reference's
+    `ids` argument)."""
+    codes, dtype = _values_dtype(codes, "codes")
+    rows, k = codes.shape
+    ib, isp = _id_args(ids, rows)
     ctx.bind_stream()
     lib = _lib.lib()
-    ib, io = (_p(id_bytes), _p(id_off)) if id_bytes is not None else (None, None)
-    _check(lib.hc_codes_csv_write_ids(ctx.h, _p(codes), dtype, rows, k, ib, io, first_id, None, 0, C.byref(length)))
-    out = torch.empty(length.value, dtype=torch.uint8, device=codes.device)
-    _check(lib.hc_codes_csv_write_ids(ctx.h, _p(codes), dtype, rows, k, ib, io, first_id, _p(out), length.value,
-                                      C.byref(length)))
-    return bytes(out.cpu().numpy())
+    pre = id_prefix.encode() if id_prefix else None
+    return _sized_write(lambda out, cap, ln: lib.hc_codes_csv_write_ids(
+        ctx.h, _p(codes), dtype, rows, k, _p(ib) if ib is not None else None, _p(isp) if isp is not None else None,
+        pre, first_id, out, cap, ln), codes.device)
+
+
+def spectra_csv(ctx: Context, values: torch.Tensor, wavelengths: np.ndarray, ids: Optional[Sequence[str]] = None
+                ) -> bytes:
+    """write_spectra_csv (io.cpp:165-186) of curves [rows, n] on the canonical grid (the n
+    `wavelengths`), %.9g; ids = None writes no id column (the reference's empty ids)."""
+    values, dtype = _values_dtype(values, "values")
+    rows, n = values.shape
+    wl = np.ascontiguousarray(wavelengths, dtype=np.float64)
+    if wl.size != n:
+        raise ValueError("spectra_csv: one wavelength per column")
+    ib, isp = _id_args(ids, rows)
+    ctx.bind_stream()
+    lib = _lib.lib()
+    return _sized_write(lambda out, cap, ln: lib.hc_spectra_csv_write(
+        ctx.h, _p(values), dtype, rows, n, _np_ptr(wl), 1 if ids is not None else 0,
+        _p(ib) if ib is not None else None, _p(isp) if isp is not None else None, None, 0, out, cap, ln),
+        values.device)
+
+
+def _device_text(data: Optional[bytes], text: Optional[torch.Tensor]) -> torch.Tensor:
+    if text is not None:
+        return text
+    return torch.frombuffer(bytearray(data), dtype=torch.uint8).cuda() if data else \
+        torch.empty(0, dtype=torch.uint8, device="cuda")
+
+
+def read_spectra_csv(ctx: Context, data: Optional[bytes], text: Optional[torch.Tensor] = None
+                     ) -> tuple[np.ndarray, Optional[list], torch.Tensor, Optional[torch.Tensor]]:
+    """read_spectra_csv (io.cpp:119-163) on the device: (wavelengths, ids or None, values
+    [rows, m] float64 CUDA tensor, id spans [rows, 2] CUDA tensor or None)."""
+    text = _device_text(data, text)
+    lib = _lib.lib()
+    has_id, m, rows = C.c_int(), C.c_int(), C.c_int64()
+    ctx.bind_stream()
+    n = text.numel()
+    _check(lib.hc_spectra_csv_read(ctx.h, _p(text), n, C.byref(has_id), None, 0, C.byref(m), C.byref(rows), None,
+                                   None, 0))
+    wl = np.zeros(m.value, np.float64)
+    vals = torch.empty(rows.value, m.value, dtype=torch.float64, device="cuda")
+    spans = torch.empty(rows.value, 2, dtype=torch.int64, device="cuda")
+    _check(lib.hc_spectra_csv_read(ctx.h, _p(text), n, C.byref(has_id), _np_ptr(wl), m.value, C.byref(m),
+                                   C.byref(rows), _p(vals), _p(spans) if has_id.value else None, rows.value))
+    ids = None
+    if has_id.value:
+        raw = data if data is not None else bytes(text.cpu().numpy())
+        ids = [raw[a:a + ln].decode() for a, ln in spans.cpu().numpy().tolist()]
+    return wl, ids, vals, (spans if has_id.value else None)
+
+
+def encode_resampled(codec: "Codec", wavelengths: np.ndarray, values: torch.Tensor, zero_outside: bool = True
+                     ) -> torch.Tensor:
+    """resample (spectrum.cpp:60-98) of curves [rows, m] given on `wavelengths` onto the
+    codec's canonical grid, then encode (codec.cpp:36-46), all in fp64 as the reference:
+    codes [rows, k] float64, bit-identical to the reference's."""
+    values = _cuda(values, torch.float64, "values")
+    wl = np.ascontiguousarray(wavelengths, dtype=np.float64)
+    rows, m = values.shape if values.dim() == 2 else (0, wl.size)
+    if m != wl.size:
+        raise ValueError("resample: grid/value size mismatch")
+    lo, step = grid(codec.n)
+    codes = torch.empty(rows, codec.k, dtype=torch.float64, device=values.device)
+    codec.ctx.bind_stream()
+    _check(_lib.lib().hc_encode_resampled_f64(codec.h, _np_ptr(wl), wl.size, _p(values), rows, lo, step,
+                                              1 if zero_outside else 0, _p(codes)))
+    return codes
+
+
+def decode_f64(codec: "Codec", codes: torch.Tensor) -> torch.Tensor:
+    """decode (codec.cpp:52-71) in fp64 as the reference: spectra [rows, n] float64; a
+    negative (or NaN) code entry raises ArithmeticError (the reference's std::domain_error)."""
+    codes = _cuda(codes, torch.float64, "codes")
+    rows, k = codes.shape
+    if k != codec.k:
+        raise ValueError("decode: code dimension mismatch")
+    out = torch.empty(rows, codec.n, dtype=torch.float64, device=codes.device)
+    codec.ctx.bind_stream()
+    first = C.c_int64()
+    _check(_lib.lib().hc_decode_f64(codec.h, _p(codes), rows, _p(out), C.byref(first)))
+    return out
+
+
+def encode_tool(codec: "Codec", spectra_csv_bytes: bytes) -> bytes:
+    """The reference's `encode` tool (tools/main.cpp:285-308, without its manifest) on the
+    device: spectra CSV -> resample + encode (fp64) -> codes CSV (%.17g).  Byte-identical
+    to the reference; ids come from the input's id column, else "row" + r."""
+    ctx = codec.ctx
+    text = _device_text(spectra_csv_bytes, None)
+    wl, _, vals, spans = read_spectra_csv(ctx, spectra_csv_bytes, text=text)
+    codes = encode_resampled(codec, wl, vals, zero_outside=True)
+    rows = codes.shape[0]
+    lib = _lib.lib()
+    ctx.bind_stream()
+    if spans is not None:
+        return _sized_write(lambda out, cap, ln: lib.hc_codes_csv_write_ids(
+            ctx.h, _p(codes), 1, rows, codec.k, _p(text), _p(spans), None, 0, out, cap, ln), codes.device)
+    return _sized_write(lambda out, cap, ln: lib.hc_codes_csv_write_ids(
+        ctx.h, _p(codes), 1, rows, codec.k, None, None, b"row", 0, out, cap, ln), codes.device)
+
+
+def decode_tool(codec: "Codec", codes_csv_bytes: bytes) -> bytes:
+    """The reference's `decode` tool (tools/main.cpp:310-328, without its manifest) on the
+    device: codes CSV -> decode (fp64) -> spectra CSV (%.9g), ids passed through."""
+    ctx = codec.ctx
+    text = _device_text(codes_csv_bytes, None)
+    lib = _lib.lib()
+    k, rows = C.c_int(), C.c_int64()
+    ctx.bind_stream()
+    _check(lib.hc_codes_csv_read(ctx.h, _p(text), text.numel(), C.byref(k), C.byref(rows), None, None, 0))
+    codes = torch.empty(rows.value, k.value, dtype=torch.float64, device="cuda")
+    spans = torch.empty(rows.value, 2, dtype=torch.int64, device="cuda")
+    _check(lib.hc_codes_csv_read(ctx.h, _p(text), text.numel(), C.byref(k), C.byref(rows), _p(codes), _p(spans),
+                                 rows.value))
+    spectra = decode_f64(codec, codes)
+    wl = wavelengths(codec.n)
+    return _sized_write(lambda out, cap, ln: lib.hc_spectra_csv_write(
+        ctx.h, _p(spectra), 1, rows.value, codec.n, _np_ptr(wl), 1, _p(text), _p(spans), None, 0, out, cap, ln),
+        spectra.device)
 
 
 def read_codes_csv(ctx: Context, data: bytes, text: Optional[torch.Tensor] = None) -> tuple[list, torch.Tensor]:

@@ -45,7 +45,8 @@ namespace hcb {
 int set_error(int code, const std::string& msg);
 int cuda_error(cudaError_t e, const char* where);
 void note_launch(hc_ctx ctx, int n = 1);
-int ensure_scratch(hc_ctx ctx, size_t bytes);
+// Grows the context scratch to >= bytes; the first `keep` bytes survive a reallocation.
+int ensure_scratch(hc_ctx ctx, size_t bytes, size_t keep = 0);
 int ensure_aux_streams(hc_ctx ctx);
 
 #define HC_CUDA_TRY(expr)                                        \

@@ -32,15 +32,17 @@ int cuda_error(cudaError_t e, const char* where) {
 
 void note_launch(hc_ctx ctx, int n) { ctx->launches.fetch_add(n, std::memory_order_relaxed); }
 
-int ensure_scratch(hc_ctx ctx, size_t bytes) {
+int ensure_scratch(hc_ctx ctx, size_t bytes, size_t keep) {
   if (ctx->scratch_bytes >= bytes) return HC_OK;
+  void* fresh = nullptr;
+  HC_CUDA_TRY(cudaMalloc(&fresh, bytes));
   if (ctx->scratch) {
+    if (keep) HC_CUDA_TRY(cudaMemcpyAsync(fresh, ctx->scratch, std::min(keep, ctx->scratch_bytes),
+                                          cudaMemcpyDeviceToDevice, ctx->stream));
     HC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));
     cudaFree(ctx->scratch);
   }
-  ctx->scratch = nullptr;
-  ctx->scratch_bytes = 0;
-  HC_CUDA_TRY(cudaMalloc(&ctx->scratch, bytes));
+  ctx->scratch = fresh;
   ctx->scratch_bytes = bytes;
   return HC_OK;
 }

@@ -20,7 +20,10 @@ from collections import defaultdict
 from pathlib import Path
 
 ALGO_BYTES = {"1": 696 * (1 << 20), "2": 60 * 1920 * 1080, "3": 468 * 3840 * 2160, "4": 1368 * 2048 * 2048,
-              "5a": 36 * 4096 * 4096, "5b": 648 * (1 << 24), "6": 27 * 1920 * 1080, "7": 6 * 4 * 256 * 256}
+              "5a": 36 * 4096 * 4096, "5b": 648 * (1 << 24), "6": 27 * 1920 * 1080, "7": 6 * 4 * 256 * 256,
+              # 8 (line_parse_kernel): the 264 557 378-byte codes CSV text + 8 B per code + 32 B per row
+              # (id span, newline position, row flag)
+              "8": 264557378 + 8 * 6 * (1 << 21) + 32 * (1 << 21)}
 METRICS = [
     ("gpu__time_duration.sum", "duration (us)"),
     ("dram__bytes_read.sum", "DRAM read (bytes)"),
@@ -114,11 +117,41 @@ def summarize_launches(src: Path, dst: Path) -> None:
     (dst / "ncu_launches_default.md").write_text("\n".join(lines) + "\n")
 
 
+def summarize_config_launches(src: Path, dst: Path, cfgs: list) -> None:
+    """launches_c<cfg>.csv (ncu --metrics gpu__time_duration.sum[,dram__bytes_*] of
+    `bench.py --config <cfg> --plain`) -> ncu_launches_config<cfg>.md: per-kernel share of the step."""
+    for cfg in cfgs:
+        f = src / f"launches_c{cfg}.csv"
+        if not f.exists():
+            continue
+        rows = list(csv.reader(f.open()))
+        hi = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+        h = rows[hi]
+        ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+        per = defaultdict(lambda: {"n": 0, "ns": 0.0, "dram": 0.0})
+        for r in rows[hi + 1:]:
+            name = r[ki].split("(")[0][:110]
+            if r[mi] == "gpu__time_duration.sum":
+                per[name]["n"] += 1
+                per[name]["ns"] += num(r[vi])
+            elif r[mi].startswith("dram__bytes"):
+                per[name]["dram"] += num(r[vi])
+        total = sum(v["ns"] for v in per.values()) or 1.0
+        lines = [f"# ncu launch list of config {cfg} (`bench.py --config {cfg} --plain`)",
+                 "(`gpu__time_duration.sum`, DRAM bytes; cold-cache, serialised: compare shares)", "",
+                 "| kernel | launches | avg us | share | avg DRAM MB |", "|---|---|---|---|---|"]
+        for name, v in sorted(per.items(), key=lambda kv: -kv[1]["ns"]):
+            lines.append(f"| `{name}` | {v['n']} | {v['ns'] / max(v['n'], 1) / 1e3:.1f} | {v['ns'] / total * 100:.1f}% "
+                         f"| {v['dram'] / max(v['n'], 1) / 1e6:.1f} |")
+        (dst / f"ncu_launches_config{cfg}.md").write_text("\n".join(lines) + "\n")
+
+
 def main() -> int:
     src, dst = Path(sys.argv[1]), Path(sys.argv[2])
     dst.mkdir(parents=True, exist_ok=True)
     summarize_full(src, dst)
     summarize_launches(src, dst)
+    summarize_config_launches(src, dst, sys.argv[3:])  # e.g. `... gpurun_out profiles/r01 8`
     if (src / "launches_default.csv").exists():
         (dst / "ncu_launches_default.csv").write_text((src / "launches_default.csv").read_text())
     return 0
