@@ -74,6 +74,10 @@ int hc_codec_create(hc_ctx ctx, int k, int n, const float* E, const float* D, co
                     double dlambda, hc_codec* out);
 /* Same from raw softplus-parameterised weights (raw_enc k x n, raw_dec n x k,
  * beta): effective_weights (codec.cpp:21-34) is applied on the host. */
+/* As hc_codec_create with the effective weights in fp64 (EffectiveWeights, codec.hpp:52-58),
+ * kept exactly for the fp64 entry points (the fp32 kernels use them rounded to float). */
+int hc_codec_create_f64(hc_ctx ctx, int k, int n, const double* E, const double* D, const double* cmf,
+                        double dlambda, hc_codec* out);
 int hc_codec_create_raw(hc_ctx ctx, int k, int n, double beta, const double* raw_enc,
                         const double* raw_dec, const double* cmf, double dlambda, hc_codec* out);
 int hc_codec_destroy(hc_codec codec);
@@ -308,6 +312,10 @@ int hc_encode_resampled_f64(hc_codec codec, const double* src_wavelengths, int m
  * not >= 0 (NaN included) makes the call return HC_EDOMAIN (the reference's domain_error)
  * with *first_negative_row (host, may be NULL) = the first such row; -1 otherwise. */
 int hc_decode_f64(hc_codec codec, const double* codes, int64_t rows, double* spectra, int64_t* first_negative_row);
+/* encode (codec.cpp:36-46) of curves already on the canonical grid (device, rows x n
+ * doubles) in fp64: codes bit-identical to the reference's.  With a codec made by
+ * hc_codec_create_f64 / hc_codec_create_raw the weights are the reference's doubles. */
+int hc_encode_f64(hc_codec codec, const double* spectra, int64_t rows, double* codes);
 
 /* ------------------------------------------------------------------ host-buffer entry points
  * Reference-facing value calls: inputs and outputs in HOST memory (pinned for

@@ -8,7 +8,9 @@
 // Differences a caller should know:
 //   * the grid is a runtime property (n = 47 reference grid, or 81 = BASELINE grid)
 //     instead of the compile-time kSampleCount, so SpectralCurve is a vector;
-//   * arithmetic is fp32 on the GPU (reference: fp64), agreeing to ~1e-6 relative;
+//   * the batched / image calls compute in fp32 on the GPU (reference: fp64), agreeing to
+//     ~1e-6 relative; the by-value encode / decode and the file tools' paths run fp64
+//     kernels in the reference's operation order and are bit-identical;
 //   * every call runs on a Device (one per GPU, one CUDA stream); the by-value
 //     calls copy in and out and synchronise, the *_batch / shade_* calls take
 //     whole images — the form the hot path should use.
@@ -118,12 +120,14 @@ class Codec {
   hc_codec handle() const { return codec_; }
   int k() const { return k_; }
   int n() const { return n_; }
+  const Grid& grid() const { return grid_; }
   Device& device() const { return *dev_; }
 
  private:
   Device* dev_;
   hc_codec codec_ = nullptr;
   int k_ = 0, n_ = 0;
+  Grid grid_;
 };
 
 // ---- codec.hpp:46-82
@@ -131,8 +135,13 @@ double softplus(double raw, double beta);
 double softplus_derivative(double raw, double beta);
 EffectiveWeights effective_weights(const CodecWeights& w);
 void validate(const CodecWeights& w, const Grid& grid);
+// By-value encode / decode run the fp64 kernels: bit-identical to the reference's.
 LatentCode encode(const Codec& c, const SpectralCurve& s);
 SpectralCurve decode(const Codec& c, const LatentCode& z);  // throws std::domain_error on negative codes
+// resample (spectrum.cpp:60-98) of curves given on `wavelengths` onto the codec's grid, then
+// encode — run_encode's per-curve step for a whole file at once, fp64, bit-identical.
+std::vector<LatentCode> encode_resampled(const Codec& c, const std::vector<double>& wavelengths,
+                                         const std::vector<std::vector<double>>& rows, bool zero_outside = true);
 LatentCode blockwise_hadamard(const LatentCode& a, const LatentCode& b);
 std::vector<std::array<double, 3>> split_blocks(const LatentCode& z);
 LatentCode join_blocks(const std::vector<std::array<double, 3>>& blocks);
@@ -225,6 +234,16 @@ struct CodesCsv {
   std::vector<LatentCode> codes;
 };
 CodesCsv read_codes_csv(Device& dev, const std::string& path);
+// Spectra CSV (io.hpp:26-40): %.9g writer and exact reader on the GPU.  The writer's grid is
+// the curves' (Grid::for_samples(curve size)); ids empty = no id column.
+struct SpectraCsv {
+  std::vector<double> wavelengths;
+  std::vector<std::string> ids;  // empty when the file has no id column
+  std::vector<std::vector<double>> rows;
+};
+SpectraCsv read_spectra_csv(Device& dev, const std::string& path);
+void write_spectra_csv(Device& dev, const std::string& path, const std::vector<std::string>& ids,
+                       const std::vector<SpectralCurve>& curves);
 void write_codes_csv(Device& dev, const std::string& path, const std::vector<std::string>& ids,
                      const std::vector<LatentCode>& codes);
 

@@ -28,6 +28,7 @@ SIGNATURES: dict[str, tuple] = {
     "hc_ctx_launch_count": (i64, [vp]),
     "hc_codec_create": (i32, [vp, i32, i32, vp, vp, vp, f64, C.POINTER(vp)]),
     "hc_codec_create_raw": (i32, [vp, i32, i32, f64, vp, vp, vp, f64, C.POINTER(vp)]),
+    "hc_codec_create_f64": (i32, [vp, i32, i32, vp, vp, vp, C.c_double, C.POINTER(vp)]),
     "hc_codec_destroy": (i32, [vp]),
     "hc_codec_dims": (i32, [vp, C.POINTER(i32), C.POINTER(i32)]),
     "hc_codec_xyz_projection": (i32, [vp, vp]),
@@ -61,6 +62,7 @@ SIGNATURES: dict[str, tuple] = {
                                   i64]),
     "hc_encode_resampled_f64": (i32, [vp, vp, i32, vp, i64, C.c_double, C.c_double, i32, vp]),
     "hc_decode_f64": (i32, [vp, vp, i64, vp, C.POINTER(i64)]),
+    "hc_encode_f64": (i32, [vp, vp, i64, vp]),
     "hc_parse_doubles": (i32, [vp, vp, vp, i64, i32, vp, vp]),
     "hc_codes_csv_read": (i32, [vp, vp, i64, C.POINTER(i32), C.POINTER(i64), vp, vp, i64]),
     "hc_render": (i32, [vp, vp, vp, vp, vp, vp, vp]),

@@ -551,6 +551,19 @@ def encode_resampled(codec: "Codec", wavelengths: np.ndarray, values: torch.Tens
     return codes
 
 
+def encode_f64(codec: "Codec", spectra: torch.Tensor) -> torch.Tensor:
+    """encode (codec.cpp:36-46) of curves [rows, n] on the canonical grid in fp64 with the
+    reference's summation order: codes [rows, k] float64, bit-identical to the reference."""
+    spectra = _cuda(spectra, torch.float64, "spectra")
+    rows, n = spectra.shape
+    if n != codec.n:
+        raise ValueError("encode: spectrum size does not match the grid")
+    out = torch.empty(rows, codec.k, dtype=torch.float64, device=spectra.device)
+    codec.ctx.bind_stream()
+    _check(_lib.lib().hc_encode_f64(codec.h, _p(spectra), rows, _p(out)))
+    return out
+
+
 def decode_f64(codec: "Codec", codes: torch.Tensor) -> torch.Tensor:
     """decode (codec.cpp:52-71) in fp64 as the reference: spectra [rows, n] float64; a
     negative (or NaN) code entry raises ArithmeticError (the reference's std::domain_error)."""

@@ -28,7 +28,7 @@ namespace {
 constexpr double kActiveBandMin = 400.0;  // spectrum.hpp:18-19
 constexpr double kActiveBandMax = 700.0;
 
-enum : int8_t { kFront = 0, kBack = 1, kLerp = 2, kZero = 3 };
+enum : int8_t { kFront = 0, kBack = 1, kLerp = 2, kZero = 3, kIdent = 4 };
 
 template <int K, int N>
 __global__ void __launch_bounds__(128) resample_encode_kernel(const double* __restrict__ vals, int64_t rows, int m,
@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(128) resample_encode_kernel(const double* __re
       if (md == kLerp) {
         const double a = v[slo[i]], b = v[slo[i] + 1];
         s = a + st[i] * (b - a);  // spectrum.cpp:84-86
+      } else if (md == kIdent) {
+        s = v[i];  // plain encode of a curve already on the grid
       } else if (md == kFront) {
         s = v[0];
       } else if (md == kBack) {
@@ -118,6 +120,9 @@ int dispatch_kn(int k, int n, F&& f) {
   return set_error(HC_EUNSUPPORTED, "codec64: compiled for n in {47, 81}, k in {3, 6, 9}");
 }
 
+int launch_encode(hc_codec codec, const double* values, int64_t rows, int m, const std::vector<int>& lo,
+                  const std::vector<double>& t, const std::vector<int8_t>& mode, double* codes);
+
 }  // namespace
 }  // namespace hcb
 
@@ -136,8 +141,7 @@ int hc_encode_resampled_f64(hc_codec codec, const double* src_wavelengths, int m
                "resample: source grid must be strictly increasing");
   if (rows == 0) return HC_OK;
   HC_REQUIRE(values && codes, HC_EINVAL, "encode_resampled: null buffer");
-  hc_ctx ctx = codec->ctx;
-  const int n = codec->n, k = codec->k;
+  const int n = codec->n;
   // the plan, as resample computes it per curve (spectrum.cpp:74-90)
   std::vector<int> lo(n, 0);
   std::vector<double> t(n, 0.0);
@@ -156,6 +160,29 @@ int hc_encode_resampled_f64(hc_codec codec, const double* src_wavelengths, int m
     }
     if (zero_outside && (lambda < kActiveBandMin || lambda > kActiveBandMax)) mode[i] = kZero;
   }
+  return launch_encode(codec, values, rows, m, lo, t, mode, codes);
+}
+
+int hc_encode_f64(hc_codec codec, const double* spectra, int64_t rows, double* codes) {
+  HC_REQUIRE(codec, HC_EINVAL, "encode_f64: null codec");
+  HC_REQUIRE(rows >= 0, HC_EINVAL, "encode_f64: negative row count");
+  if (rows == 0) return HC_OK;
+  HC_REQUIRE(spectra && codes, HC_EINVAL, "encode_f64: null buffer");
+  const int n = codec->n;
+  std::vector<int> lo(n);
+  for (int i = 0; i < n; ++i) lo[i] = i;
+  return launch_encode(codec, spectra, rows, n, lo, std::vector<double>(n, 0.0), std::vector<int8_t>(n, kIdent),
+                       codes);
+}
+
+}  // extern "C"
+
+namespace hcb {
+namespace {
+int launch_encode(hc_codec codec, const double* values, int64_t rows, int m, const std::vector<int>& lo,
+                  const std::vector<double>& t, const std::vector<int8_t>& mode, double* codes) {
+  hc_ctx ctx = codec->ctx;
+  const int n = codec->n, k = codec->k;
   // device copies: E (k x n), plan
   const size_t eb = sizeof(double) * k * n, pb = (sizeof(int) + sizeof(double) + 1) * n;
   int rc = ensure_scratch(ctx, eb + pb + 64);
@@ -179,6 +206,10 @@ int hc_encode_resampled_f64(hc_codec codec, const double* src_wavelengths, int m
   HC_CUDA_TRY(cudaStreamSynchronize(ctx->stream));  // host plan buffers go out of scope
   return HC_OK;
 }
+}  // namespace
+}  // namespace hcb
+
+extern "C" {
 
 int hc_decode_f64(hc_codec codec, const double* codes, int64_t rows, double* spectra, int64_t* first_negative_row) {
   HC_REQUIRE(codec, HC_EINVAL, "decode_f64: null codec");

@@ -370,6 +370,16 @@ int hc_codec_create(hc_ctx ctx, int k, int n, const float* E, const float* D, co
   return codec_finish(ctx, k, n, std::move(e), std::move(d), cmf, dlambda, out);
 }
 
+int hc_codec_create_f64(hc_ctx ctx, int k, int n, const double* E, const double* D, const double* cmf,
+                        double dlambda, hc_codec* out) {
+  int rc = validate_dims(ctx, k, n, E, D, cmf, dlambda, out);
+  if (rc != HC_OK) return rc;
+  std::vector<double> e(E, E + k * n), d(D, D + n * k);
+  for (double v : e) HC_REQUIRE(std::isfinite(v), HC_EINVAL, "codec weights: non-finite encoder entry");
+  for (double v : d) HC_REQUIRE(std::isfinite(v), HC_EINVAL, "codec weights: non-finite decoder entry");
+  return codec_finish(ctx, k, n, std::move(e), std::move(d), cmf, dlambda, out);
+}
+
 int hc_codec_create_raw(hc_ctx ctx, int k, int n, double beta, const double* raw_enc, const double* raw_dec,
                         const double* cmf, double dlambda, hc_codec* out) {
   int rc = validate_dims(ctx, k, n, raw_enc, raw_dec, cmf, dlambda, out);

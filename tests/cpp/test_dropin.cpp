@@ -73,7 +73,8 @@ int main() {
   for (double v : e.enc) CHECK(v > 0.0);
   for (double v : e.dec) CHECK(v > 0.0);
 
-  // encode / decode = explicit mat-vec (test_codec.cpp:81-111) at fp32 tolerance
+  // encode / decode = explicit mat-vec (test_codec.cpp:81-111): the by-value calls run the
+  // fp64 kernels in the reference's order, so they equal the plain sequential loops exactly
   Codec codec(dev, e, g47);
   uint64_t s = 99;
   SpectralCurve sc(47);
@@ -82,21 +83,28 @@ int main() {
   CHECK(z.k() == 6);
   for (int j = 0; j < 6; ++j) {
     double acc = 0.0;
-    for (int i = 0; i < 47; ++i) acc += static_cast<double>(static_cast<float>(e.enc[j * 47 + i])) *
-                                        static_cast<double>(static_cast<float>(sc[i]));
-    CHECK(rel_close(z[j], acc, 2e-6));
+    for (int i = 0; i < 47; ++i) acc += e.enc[j * 47 + i] * sc[i];
+    CHECK(z[j] == acc);
     CHECK(z[j] >= 0.0);
   }
   const SpectralCurve d = decode(codec, z);
   for (int i = 0; i < 47; ++i) {
     double acc = 0.0;
-    for (int j = 0; j < 6; ++j) acc += static_cast<double>(static_cast<float>(e.dec[i * 6 + j])) * z[j];
-    CHECK(rel_close(d[i], acc, 2e-6));
+    for (int j = 0; j < 6; ++j) acc += e.dec[i * 6 + j] * z[j];
+    CHECK(d[i] == acc);
   }
-  // CodecWeights overload agrees with the EffectiveWeights path
+  // CodecWeights overload agrees with the EffectiveWeights path (same softplus, bit for bit)
   Codec codec_raw(dev, w, g47);
   const LatentCode z2 = encode(codec_raw, sc);
-  for (int j = 0; j < 6; ++j) CHECK(rel_close(z2[j], z[j], 1e-6));
+  for (int j = 0; j < 6; ++j) CHECK(z2[j] == z[j]);
+  // encode_resampled on the codec's own grid without zeroing = encode
+  {
+    std::vector<double> wl(47);
+    for (int i = 0; i < 47; ++i) wl[static_cast<size_t>(i)] = g47.wavelength_at(i);
+    const std::vector<LatentCode> zr = encode_resampled(codec, wl, {sc.v}, /*zero_outside=*/false);
+    CHECK(zr.size() == 1u && zr[0].z == z.z);
+    CHECK_THROWS_AS(encode_resampled(codec, {400.0, 400.0}, {{1.0, 2.0}}), std::invalid_argument);
+  }
 
   // linearity (test_codec.cpp:113-137) at fp32 tolerance
   for (int it = 0; it < 20; ++it) {
@@ -296,6 +304,38 @@ int main() {
     job.spp = 2;
     sc.wall_material[4] = 9;
     CHECK_THROWS_AS(render(codec, sc, job), std::invalid_argument);
+  }
+
+  {  // spectra CSV round trip with and without ids, malformed files (test_io.cpp:43-86)
+    const std::string path = "/tmp/hc_b200_dropin_spectra.csv";
+    std::vector<SpectralCurve> curves(2, SpectralCurve(47));
+    for (int i = 0; i < 47; ++i) {
+      const double l = g47.wavelength_at(i);
+      curves[0][i] = 0.8 * std::exp(-0.5 * (l - 550.0) * (l - 550.0) / (40.0 * 40.0));
+      curves[1][i] = 0.25;
+    }
+    write_spectra_csv(dev, path, {"a", "b"}, curves);
+    const SpectraCsv back = read_spectra_csv(dev, path);
+    CHECK(back.rows.size() == 2u && back.wavelengths.size() == 47u);
+    CHECK(back.ids == std::vector<std::string>({"a", "b"}));
+    CHECK(back.wavelengths[0] == 368.0);
+    for (int i = 0; i < 47; ++i) CHECK(rel_close(back.rows[0][static_cast<size_t>(i)], curves[0][i], 1e-8));
+    write_spectra_csv(dev, path, {}, curves);
+    const SpectraCsv noid = read_spectra_csv(dev, path);
+    CHECK(noid.ids.empty() && noid.rows.size() == 2u);
+    auto put = [&](const char* t) {
+      FILE* f = std::fopen(path.c_str(), "wb");
+      std::fputs(t, f);
+      std::fclose(f);
+    };
+    put("");
+    CHECK_THROWS_AS(read_spectra_csv(dev, path), FormatError);
+    put("400,500\n0.5\n");  // row shorter than header
+    CHECK_THROWS_AS(read_spectra_csv(dev, path), FormatError);
+    put("400,500\n0.5,abc\n");  // non-numeric value
+    CHECK_THROWS_AS(read_spectra_csv(dev, path), FormatError);
+    CHECK_THROWS_AS(read_spectra_csv(dev, "/nonexistent/dir/spectra.csv"), FormatError);
+    std::remove(path.c_str());
   }
 
   {  // codes CSV round trip and validation (test_io.cpp:133-155)

@@ -212,3 +212,24 @@ def test_spectra_csv_reader_errors_match_reference(api, ctx, ref, tmp_path, case
                                     ctypes.byref(rows), vals, vals.size, idbuf, len(idbuf)) == 1
     with pytest.raises(ValueError):
         api.read_spectra_csv(ctx, data)
+
+
+@pytest.mark.parametrize("k", [3, 6, 9])
+def test_fp64_encode_decode_bit_identical_to_reference(api, ctx, ref, k):
+    """hc_encode_f64 / hc_decode_f64 (the drop-in's by-value encode / decode) against the
+    reference's encode / decode on the same (float-valued) weights and inputs."""
+    rng = np.random.default_rng(40 + k)
+    E = rng.uniform(0, 1, (k, N)).astype(np.float32)
+    D = rng.uniform(0, 1, (N, k)).astype(np.float32)
+    codec = api.Codec(ctx, E, D)
+    rows = 4096
+    S = rng.uniform(0, 2, (rows, N)).astype(np.float32)
+    Z = api.encode_f64(codec, torch.from_numpy(S.astype(np.float64)).cuda()).cpu().numpy()
+    Zr = np.zeros((rows, k))
+    ref.ref_encode_rows_d(E.reshape(-1), k, S.reshape(-1), rows, Zr.reshape(-1), 1)
+    assert Z.tobytes() == Zr.tobytes()
+    Sd = api.decode_f64(codec, torch.from_numpy(Z).cuda()).cpu().numpy()
+    Sr = np.zeros((rows, N))
+    assert ref.ref_decode_rows_d(np.ascontiguousarray(D.reshape(-1)), k, np.ascontiguousarray(Z.reshape(-1)), rows,
+                                 Sr.reshape(-1)) == 0
+    assert Sd.tobytes() == Sr.tobytes()
