@@ -69,6 +69,13 @@ CONFIGS = {
     "8": dict(name="codes CSV round trip on the device: write_codes_csv (%.17g) + read_codes_csv (exact "
                    "strtod), 2^21 rows x k=6", units=(1 << 21) * 6, rows=1 << 21, k=6, unit="M codes/s",
               bytes_per_unit=52, rot=1, graph=False),
+    # the reference's `encode` tool (tools/main.cpp:285-308) on the device —
+    # read_spectra_csv of 2^17 curves measured on a 4 nm 360-800 grid (111 samples, %.9g), resample
+    # onto the 81-sample grid + zero outside 400-700 + fp64 encode (k = 6), write_codes_csv
+    # (%.17g); algorithmic bytes per curve: its ~1.2 KB of input text + ~120 B of output text.
+    "9": dict(name="encode tool on the device: spectra CSV (2^17 curves x 111 samples, 4 nm) -> resample + "
+                   "fp64 encode (k=6) -> codes CSV", units=1 << 17, rows=1 << 17, m=111, k=6, unit="M curves/s",
+              bytes_per_unit=1330, rot=1, graph=False),
     "7": dict(name="Cornell box path trace (bm_render scene + block + 2nd light), 256x256, 64 spp, depth 3, "
                    "latent k=6 (naive: spectral n=81)", W=256, H=256, spp=64, depth=3, k=6,
               unit="M samples/s", bytes_per_unit=6 * 4 / 64, rot=1, graph=False),
@@ -147,6 +154,30 @@ def dist_env():
 
 def emit(obj: dict) -> None:
     print(json.dumps(obj), flush=True)
+
+
+# ---------------------------------------------------------------------------- config 9 inputs
+TOOL_GRID = (360.0, 4.0)  # the measured grid of the encode-tool input: 360, 364, ..., 800 nm
+
+
+def tool_raw_weights(k: int) -> tuple:
+    """Raw codec weights (CodecWeights, softplus beta = 10) for the encode tool, k x 81 / 81 x k."""
+    from paper_2602_18741_b200 import synth
+
+    re_ = (synth.uniform_np(SEED, "tool.raw_enc", 0, k * N_SPEC) - 0.5) / np.sqrt(N_SPEC)
+    rd = (synth.uniform_np(SEED, "tool.raw_dec", 0, N_SPEC * k) - 0.5) / np.sqrt(N_SPEC)
+    return np.ascontiguousarray(re_, np.float64), np.ascontiguousarray(rd, np.float64)
+
+
+def tool_spectra_text_np(rows: int, m: int) -> bytes:
+    """A spectra CSV (ids s<r>, %.9g) of `rows` seeded curves on TOOL_GRID, formatted on the host."""
+    from paper_2602_18741_b200 import synth
+
+    lo, step = TOOL_GRID
+    v = synth.uniform_np(SEED, "tool.spectra", 0, rows * m).reshape(rows, m).astype(np.float64)
+    head = "id," + ",".join("%.9g" % (lo + step * i) for i in range(m))
+    lines = [head] + ["s%d," % r + ",".join("%.9g" % x for x in row) for r, row in enumerate(v)]
+    return ("\n".join(lines) + "\n").encode()
 
 
 # ---------------------------------------------------------------------------- CPU reference
@@ -242,6 +273,27 @@ def cpu_reference_run(cfg_key: str, budget_s: float, threads: int = 0, rank: int
             ref.ref_read_codes_csv(path, C.byref(r_rows), C.byref(r_k), buf_codes, buf_codes.size, ids, len(ids))
 
         sample = f"{rows} rows x k={k}: the reference's write_codes_csv + read_codes_csv (single-threaded, /tmp file)"
+    elif cfg_key == "9":
+        import ctypes as C
+        import tempfile
+
+        rows, m = 2048, cfg["m"]
+        raw_e, raw_d = tool_raw_weights(k)
+        text = tool_spectra_text_np(rows, m)
+        tmp = tempfile.mkdtemp()
+        src, dst = (tmp + "/spectra.csv").encode(), (tmp + "/codes.csv").encode()
+        with open(src, "wb") as f:
+            f.write(text)
+        err = C.create_string_buffer(256)
+        P = rows
+        nthreads = 1
+
+        def run():
+            if ref.ref_run_encode(src, k, 10.0, raw_e, raw_d, dst, err, 256) != 0:
+                raise RuntimeError(err.value.decode())
+
+        sample = (f"{rows} curves x {m} samples: the reference's encode tool steps (read_spectra_csv, resample, "
+                  "encode, write_codes_csv; single-threaded, /tmp files)")
     elif cfg_key == "7":
         import ctypes as C
 
@@ -436,6 +488,47 @@ class Workload:
                                                   self.text.numel(), api.C.byref(ln)))
                 api._check(lib.hc_codes_csv_read(ctx.h, self.text.data_ptr(), ln.value, api.C.byref(kk),
                                                  api.C.byref(rr), self.codes.data_ptr(), self.ids.data_ptr(), rows))
+            self.step = step
+        elif cfg_key == "9":
+            rows, m, k = cfg["rows"], cfg["m"], cfg["k"]
+            lib = api._lib.lib()
+            raw_e, raw_d = tool_raw_weights(k)
+            self.codec = api.Codec.from_raw(ctx, raw_e.reshape(k, N_SPEC), raw_d.reshape(N_SPEC, k), beta=10.0)
+            vals = api.synth_uniform(ctx, SEED + rank, "tool.spectra", 0, rows * m).reshape(rows, m).double()
+            lo, step = TOOL_GRID
+            self.src_wl = np.array([lo + step * i for i in range(m)], np.float64)
+            ln = C_int64()  # setup: the input file (ids s0, s1, ...), written by the device writer
+            api._check(lib.hc_spectra_csv_write(ctx.h, vals.data_ptr(), 1, rows, m, api._np_ptr(self.src_wl), 1, None,
+                                                None, b"s", 0, None, 0, api.C.byref(ln)))
+            self.text = torch.empty(ln.value, dtype=torch.uint8, device="cuda")
+            api._check(lib.hc_spectra_csv_write(ctx.h, vals.data_ptr(), 1, rows, m, api._np_ptr(self.src_wl), 1, None,
+                                                None, b"s", 0, self.text.data_ptr(), ln.value, api.C.byref(ln)))
+            self.vals = torch.empty(rows, m, dtype=torch.float64, device="cuda")
+            self.spans = torch.empty(rows, 2, dtype=torch.int64, device="cuda")
+            self.codes = torch.empty(rows, k, dtype=torch.float64, device="cuda")
+            self.wl = np.zeros(m, np.float64)
+            self.units = rows
+            self.sets.append({"rgb": None})
+            gl, gs = api.grid(N_SPEC)
+            self.out = None
+
+            def step(i):
+                hid, mm, rr, olen = api.C.c_int(), api.C.c_int(), C_int64(), C_int64()
+                ctx.bind_stream()
+                api._check(lib.hc_spectra_csv_read(ctx.h, self.text.data_ptr(), self.text.numel(), api.C.byref(hid),
+                                                   api._np_ptr(self.wl), m, api.C.byref(mm), api.C.byref(rr),
+                                                   self.vals.data_ptr(), self.spans.data_ptr(), rows))
+                api._check(lib.hc_encode_resampled_f64(self.codec.h, api._np_ptr(self.wl), m, self.vals.data_ptr(),
+                                                       rows, gl, gs, 1, self.codes.data_ptr()))
+                if self.out is None:
+                    api._check(lib.hc_codes_csv_write_ids(ctx.h, self.codes.data_ptr(), 1, rows, k,
+                                                          self.text.data_ptr(), self.spans.data_ptr(), None, 0, None,
+                                                          0, api.C.byref(olen)))
+                    self.out = torch.empty(olen.value, dtype=torch.uint8, device="cuda")
+                api._check(lib.hc_codes_csv_write_ids(ctx.h, self.codes.data_ptr(), 1, rows, k, self.text.data_ptr(),
+                                                      self.spans.data_ptr(), None, 0, self.out.data_ptr(),
+                                                      self.out.numel(), api.C.byref(olen)))
+            self.extra = {"text_bytes_in": int(self.text.numel())}
             self.step = step
         elif cfg_key == "7":
             W, H, spp, depth = cfg["W"], cfg["H"], cfg["spp"], cfg["depth"]

@@ -56,7 +56,8 @@ def _spectra_text(seed, rows, grid, ids):
 
 GRIDS = {"1nm_360_830": np.arange(360.0, 830.5, 1.0), "5nm_400_700": np.arange(400.0, 700.5, 5.0),
          "irregular": np.cumsum(np.r_[372.5, np.random.default_rng(3).uniform(0.5, 9.0, 70)]),
-         "narrow_450_650": np.linspace(450.0, 650.0, 17), "single": np.array([555.0])}
+         "narrow_450_650": np.linspace(450.0, 650.0, 17), "single": np.array([555.0]),
+         "half_nm_941": np.arange(360.0, 830.25, 0.5)}  # > 512 cells per row: the one-lane fallback
 
 
 @pytest.mark.parametrize("grid_name", list(GRIDS))
@@ -233,3 +234,39 @@ def test_fp64_encode_decode_bit_identical_to_reference(api, ctx, ref, k):
     assert ref.ref_decode_rows_d(np.ascontiguousarray(D.reshape(-1)), k, np.ascontiguousarray(Z.reshape(-1)), rows,
                                  Sr.reshape(-1)) == 0
     assert Sd.tobytes() == Sr.tobytes()
+
+
+@pytest.mark.parametrize("kind", ["junk", "short", "range", "ok"])
+def test_long_line_errors_report_the_reference_line(api, ctx, ref, tmp_path, kind):
+    """Errors inside long (cooperatively parsed) spectra rows: same first bad line."""
+    lines = _spectra_text(3, 1500, GRIDS["1nm_360_830"], True).decode().split("\n")
+    if kind == "junk":
+        cells = lines[901].split(",")
+        cells[200] = cells[200] + "x"
+        lines[901] = ",".join(cells)
+        cells = lines[1200].split(",")
+        cells[3] = "abc"
+        lines[1200] = ",".join(cells)
+    elif kind == "short":
+        lines[640] = ",".join(lines[640].split(",")[:-1])
+    elif kind == "range":
+        cells = lines[77].split(",")
+        cells[-1] = "1e-400"
+        lines[77] = ",".join(cells)
+    data = "\n".join(lines).encode()
+    path = tmp_path / "s.csv"
+    path.write_bytes(data)
+    has_id, m, rows = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()
+    wl, vals = np.zeros(1024), np.zeros(1500 * 480)
+    idbuf = ctypes.create_string_buffer(1500 * 16 + 1024)
+    rc = ref.ref_read_spectra_csv(str(path).encode(), ctypes.byref(has_id), wl, 1024, ctypes.byref(m),
+                                  ctypes.byref(rows), vals, vals.size, idbuf, len(idbuf))
+    if kind == "ok":
+        assert rc == 0
+        _, _, gv, _ = api.read_spectra_csv(ctx, data)
+        assert gv.cpu().numpy().tobytes() == vals[: rows.value * m.value].tobytes()
+        return
+    assert rc == 1
+    line = idbuf.value.decode().split(":")[1]
+    with pytest.raises(ValueError, match=rf"\(line {line}\)"):
+        api.read_spectra_csv(ctx, data)
