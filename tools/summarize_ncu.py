@@ -23,7 +23,10 @@ ALGO_BYTES = {"1": 696 * (1 << 20), "2": 60 * 1920 * 1080, "3": 468 * 3840 * 216
               "5a": 36 * 4096 * 4096, "5b": 648 * (1 << 24), "6": 27 * 1920 * 1080, "7": 6 * 4 * 256 * 256,
               # 8 (line_parse_kernel): the 264 557 378-byte codes CSV text + 8 B per code + 32 B per row
               # (id span, newline position, row flag)
-              "8": 264557378 + 8 * 6 * (1 << 21) + 32 * (1 << 21)}
+              "8": 264557378 + 8 * 6 * (1 << 21) + 32 * (1 << 21),
+              # 9 (line_parse_kernel): the 175 525 094-byte spectra CSV + 8 B per value (111 per curve)
+              # + 32 B per row
+              "9": 175525094 + 8 * 111 * (1 << 17) + 32 * (1 << 17)}
 METRICS = [
     ("gpu__time_duration.sum", "duration (us)"),
     ("dram__bytes_read.sum", "DRAM read (bytes)"),
