@@ -57,6 +57,13 @@ struct LatentCode {
   const double& operator[](int i) const { return z[static_cast<size_t>(i)]; }
 };
 
+// codec.hpp:24-29
+struct CodecTrainingMeta {
+  std::uint64_t seed = 0;
+  std::array<double, 5> lambda_weights{};  // e2e, rec, code, col, alg
+  int epochs = 0;
+};
+
 // codec.hpp:34-43
 struct CodecWeights {
   int k = 6;
@@ -64,6 +71,7 @@ struct CodecWeights {
   double beta = 10.0;
   std::vector<double> raw_enc;  // k x n
   std::vector<double> raw_dec;  // n x k
+  CodecTrainingMeta meta;
   int blocks() const { return k / 3; }
 };
 
@@ -234,6 +242,10 @@ struct CodesCsv {
   std::vector<LatentCode> codes;
 };
 CodesCsv read_codes_csv(Device& dev, const std::string& path);
+// Codec weight files (io.hpp:62-66, JSON): byte-identical to the reference's (same library,
+// nlohmann::json dump(2)); FormatError for unreadable / malformed / invalid files.
+CodecWeights load_codec_weights(const std::string& path);
+void save_codec_weights(const std::string& path, const CodecWeights& w);
 // Spectra CSV (io.hpp:26-40): %.9g writer and exact reader on the GPU.  The writer's grid is
 // the curves' (Grid::for_samples(curve size)); ids empty = no id column.
 struct SpectraCsv {

@@ -149,6 +149,9 @@ _REF_SIGS = {
     "ref_delta_e94_report": (None, [_f32p, _f32p, C.c_int64, _f32n, _f64p]),
     # formats
     "ref_write_codes_csv": (C.c_int, [C.c_char_p, _f32p, C.c_int64, C.c_int, C.c_uint64]),
+    "ref_save_codec_weights": (C.c_int, [C.c_char_p, C.c_int, C.c_double, _f64p, _f64p, C.c_uint64, _f64p, C.c_int]),
+    "ref_load_codec_weights": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_double), _f64p, _f64p,
+                                         C.c_int64, C.c_char_p, C.c_int64]),
     "ref_run_encode": (C.c_int, [C.c_char_p, C.c_int, C.c_double, _f64p, _f64p, C.c_char_p, C.c_char_p, C.c_int64]),
     "ref_run_decode": (C.c_int, [C.c_char_p, C.c_int, C.c_double, _f64p, _f64p, C.c_char_p, C.c_char_p, C.c_int64]),
     "ref_write_spectra_csv": (C.c_int, [C.c_char_p, _f64p, C.c_int64, C.c_char_p, C.c_void_p]),

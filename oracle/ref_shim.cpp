@@ -814,6 +814,35 @@ int ref_read_spectra_csv(const char* path, int* has_id, double* wl, int wl_cap, 
   }
 }
 
+// save_codec_weights / load_codec_weights (io.cpp:370-403) of raw k x N / N x k weights.
+int ref_save_codec_weights(const char* path, int k, double beta, const double* raw_enc, const double* raw_dec,
+                           uint64_t seed, const double* lambda_weights, int epochs) {
+  try {
+    CodecWeights w = shim_weights(k, beta, raw_enc, raw_dec);
+    w.meta.seed = seed;
+    for (int i = 0; i < 5; ++i) w.meta.lambda_weights[static_cast<size_t>(i)] = lambda_weights[i];
+    w.meta.epochs = epochs;
+    save_codec_weights(path, w);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
+int ref_load_codec_weights(const char* path, int* k, double* beta, double* raw_enc, double* raw_dec, int64_t cap,
+                           char* err, int64_t errcap) {
+  try {
+    const CodecWeights w = load_codec_weights(path);
+    *k = w.k;
+    *beta = w.beta;
+    for (size_t i = 0; i < w.raw_enc.size() && static_cast<int64_t>(i) < cap; ++i) raw_enc[i] = w.raw_enc[i];
+    for (size_t i = 0; i < w.raw_dec.size() && static_cast<int64_t>(i) < cap; ++i) raw_dec[i] = w.raw_dec[i];
+    return 0;
+  } catch (const std::exception& e) {
+    return shim_fail(e, err, errcap);
+  }
+}
+
 int ref_thread_count() { return render_thread_count(); }
 
 }  // extern "C"

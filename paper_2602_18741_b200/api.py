@@ -131,6 +131,12 @@ class Codec:
         obj.E, obj.D = sp(re).astype(np.float32), sp(rd).astype(np.float32)
         return obj
 
+    @classmethod
+    def from_weights_file(cls, ctx: Context, path) -> "Codec":
+        """A codec from the reference's weight file (load_codec_weights, io.cpp:370-393)."""
+        w = load_codec_weights(path)
+        return cls.from_raw(ctx, w["raw_enc"], w["raw_dec"], beta=w["beta"])
+
     def __del__(self):
         try:
             if getattr(self, "h", None):
@@ -576,6 +582,43 @@ def decode_f64(codec: "Codec", codes: torch.Tensor) -> torch.Tensor:
     first = C.c_int64()
     _check(_lib.lib().hc_decode_f64(codec.h, _p(codes), rows, _p(out), C.byref(first)))
     return out
+
+
+def load_codec_weights(path) -> dict:
+    """load_codec_weights (io.cpp:370-393): the reference's codec weight file (JSON) as
+    {k, n, beta, raw_enc [k, n], raw_dec [n, k], meta}; ValueError (the reference's
+    FormatError) for a file that is not a valid codec weights file.  Python's float parsing
+    is correctly rounded, as the reference's strtod is, so the doubles are identical."""
+    import json as _json
+
+    try:
+        with open(path, "r") as f:
+            j = _json.load(f)
+    except OSError as e:
+        raise ValueError(f"{path}: cannot open for reading") from e
+    except _json.JSONDecodeError as e:
+        raise ValueError(f"{path}: JSON parse error: {e}") from e
+    try:
+        if j["format"] != "codec-weights":
+            raise ValueError(f"{path}: not a codec weights file")
+        k, n, beta = int(j["k"]), int(j["n"]), float(j["beta"])
+        re_ = np.asarray(j["raw_enc"], dtype=np.float64)
+        rd = np.asarray(j["raw_dec"], dtype=np.float64)
+        meta = j.get("meta")
+    except (KeyError, TypeError) as e:
+        raise ValueError(f"{path}: bad codec weights: {e}") from e
+    # validate (codec.cpp:111-135)
+    if k <= 0 or k % 3:
+        raise ValueError(f"{path}: codec weights: k must be a positive multiple of 3")
+    if n not in (47, 81):
+        raise ValueError(f"{path}: codec weights: n must match the canonical grid")
+    if not beta > 0.0:
+        raise ValueError(f"{path}: codec weights: beta must be positive")
+    if re_.size != k * n or rd.size != n * k:
+        raise ValueError(f"{path}: codec weights: parameter array size mismatch")
+    if not (np.isfinite(re_).all() and np.isfinite(rd).all()):
+        raise ValueError(f"{path}: codec weights: non-finite entry")
+    return {"k": k, "n": n, "beta": beta, "raw_enc": re_.reshape(k, n), "raw_dec": rd.reshape(n, k), "meta": meta}
 
 
 def encode_tool(codec: "Codec", spectra_csv_bytes: bytes) -> bytes:
