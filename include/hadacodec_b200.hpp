@@ -246,6 +246,15 @@ CodesCsv read_codes_csv(Device& dev, const std::string& path);
 // nlohmann::json dump(2)); FormatError for unreadable / malformed / invalid files.
 CodecWeights load_codec_weights(const std::string& path);
 void save_codec_weights(const std::string& path, const CodecWeights& w);
+// HCF1 raw channel images and binary PPM (io.hpp:71-84), same checks and FormatError causes.
+ChannelImage read_raw_image(const std::string& path);
+void write_raw_image(const std::string& path, const ChannelImage& img);
+struct Ppm8 {
+  int width = 0, height = 0;
+  std::vector<unsigned char> rgb;
+};
+void write_ppm(const std::string& path, int width, int height, const std::vector<unsigned char>& rgb8);
+Ppm8 read_ppm(const std::string& path);
 // Spectra CSV (io.hpp:26-40): %.9g writer and exact reader on the GPU.  The writer's grid is
 // the curves' (Grid::for_samples(curve size)); ids empty = no id column.
 struct SpectraCsv {

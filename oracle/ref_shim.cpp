@@ -843,6 +843,52 @@ int ref_load_codec_weights(const char* path, int* k, double* beta, double* raw_e
   }
 }
 
+// HCF1 / PPM (io.cpp:450-536).
+int ref_write_raw_image(const char* path, int w, int h, int c, const float* data) {
+  try {
+    ChannelImage img;
+    img.width = w;
+    img.height = h;
+    img.channels = c;
+    img.data.assign(data, data + static_cast<size_t>(w) * h * c);
+    write_raw_image(path, img);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+int ref_read_raw_image(const char* path, int* w, int* h, int* c, float* data, int64_t cap, char* err, int64_t errcap) {
+  try {
+    const ChannelImage img = read_raw_image(path);
+    *w = img.width;
+    *h = img.height;
+    *c = img.channels;
+    for (size_t i = 0; i < img.data.size() && static_cast<int64_t>(i) < cap; ++i) data[i] = img.data[i];
+    return 0;
+  } catch (const std::exception& e) {
+    return shim_fail(e, err, errcap);
+  }
+}
+int ref_write_ppm(const char* path, int w, int h, const uint8_t* rgb, int64_t n) {
+  try {
+    write_ppm(path, w, h, std::vector<unsigned char>(rgb, rgb + n));
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+int ref_read_ppm(const char* path, int* w, int* h, uint8_t* rgb, int64_t cap, char* err, int64_t errcap) {
+  try {
+    const Ppm8 img = read_ppm(path);
+    *w = img.width;
+    *h = img.height;
+    for (size_t i = 0; i < img.rgb.size() && static_cast<int64_t>(i) < cap; ++i) rgb[i] = img.rgb[i];
+    return 0;
+  } catch (const std::exception& e) {
+    return shim_fail(e, err, errcap);
+  }
+}
+
 int ref_thread_count() { return render_thread_count(); }
 
 }  // extern "C"

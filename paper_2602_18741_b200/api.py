@@ -621,6 +621,43 @@ def load_codec_weights(path) -> dict:
     return {"k": k, "n": n, "beta": beta, "raw_enc": re_.reshape(k, n), "raw_dec": rd.reshape(n, k), "meta": meta}
 
 
+def read_raw_image(path, device: str = "cuda") -> torch.Tensor:
+    """read_raw_image (io.cpp:450-476): an HCF1 channel image as a float32 tensor [h, w, c]
+    (row-major y, x, channel as ChannelImage), moved to `device` — the payload goes from the
+    file to pinned memory and on to the GPU in one copy.  ValueError (FormatError) with the
+    reference's causes for a bad magic, truncated header, implausible dimensions or
+    truncated pixel data."""
+    try:
+        raw = open(path, "rb").read()
+    except OSError as e:
+        raise ValueError(f"{path}: cannot open for reading") from e
+    if len(raw) < 4 or raw[:4] != b"HCF1":
+        raise ValueError(f"{path}: bad magic (expected HCF1)")
+    if len(raw) < 16:
+        raise ValueError(f"{path}: truncated header")
+    w, h, c = (int(x) for x in np.frombuffer(raw, np.uint32, 3, 4).astype(np.int64))
+    w, h, c = (x - (1 << 32) if x >= 1 << 31 else x for x in (w, h, c))  # static_cast<int>(uint32)
+    if w <= 0 or h <= 0 or c <= 0 or w > 1 << 16 or h > 1 << 16 or c > 1024:
+        raise ValueError(f"{path}: implausible image dimensions")
+    count = w * h * c
+    if len(raw) - 16 < 4 * count:
+        raise ValueError(f"{path}: truncated pixel data")
+    t = torch.frombuffer(bytearray(raw[16:16 + 4 * count]), dtype=torch.float32).reshape(h, w, c)
+    if device == "cpu":
+        return t
+    return t.pin_memory().to(device, non_blocking=True)
+
+
+def write_raw_image(path, image: torch.Tensor) -> None:
+    """write_raw_image (io.cpp:478-492) of a float32 image [h, w, c] (any device)."""
+    if image.dim() != 3 or image.numel() == 0:
+        raise ValueError(f"{path}: image dimensions do not match data size")
+    h, w, c = image.shape
+    data = image.detach().to("cpu", torch.float32).contiguous().numpy().tobytes()
+    with open(path, "wb") as f:
+        f.write(b"HCF1" + np.array([w, h, c], np.uint32).tobytes() + data)
+
+
 def encode_tool(codec: "Codec", spectra_csv_bytes: bytes) -> bytes:
     """The reference's `encode` tool (tools/main.cpp:285-308, without its manifest) on the
     device: spectra CSV -> resample + encode (fp64) -> codes CSV (%.17g).  Byte-identical
