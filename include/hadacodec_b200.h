@@ -317,6 +317,22 @@ int hc_decode_f64(hc_codec codec, const double* codes, int64_t rows, double* spe
  * hc_codec_create_f64 / hc_codec_create_raw the weights are the reference's doubles. */
 int hc_encode_f64(hc_codec codec, const double* spectra, int64_t rows, double* codes);
 
+/* ------------------------------------------------------------------ codec training step
+ * compute_losses + gradients (trainer.cpp:108-373) of CodecWeights {k, n, beta, raw_enc
+ * (k x n), raw_dec (n x k)} (host) over a batch of m (reflectance, illumination) pairs
+ * (device, m x n doubles each), with LossWeights loss_weights[5] = {e2e, rec, code, col,
+ * alg}; cmf = the 3 x n colour-matching rows (CmfTable xbar / ybar / zbar), lambda_step the
+ * grid step.  g_raw_enc / g_raw_dec (host, k x n / n x k; both NULL for losses only) and
+ * losses[6] = {e2e, rec, code, col, alg, total} (host, may be NULL) are bit-identical to the
+ * reference's gradients() / compute_losses(). */
+int hc_codec_train_grad(hc_ctx ctx, int k, int n, double beta, const double* raw_enc, const double* raw_dec,
+                        const double* cmf, double lambda_step, const double* refl, const double* illum, int64_t m,
+                        const double* loss_weights, double* g_raw_enc, double* g_raw_dec, double* losses);
+/* adam_step (trainer.cpp:399-411) on device arrays: params -= lr * mhat / (sqrt(vhat) +
+ * 1e-8) with the first / second moments m1 / v1 updated in place; step >= 1.  Bit-identical. */
+int hc_adam_step(hc_ctx ctx, double* params, const double* grad, double* m1, double* v1, int64_t count, double lr,
+                 int64_t step);
+
 /* ------------------------------------------------------------------ host-buffer entry points
  * Reference-facing value calls: inputs and outputs in HOST memory (pinned for
  * full copy speed), copies and compute on the context stream, synchronised on

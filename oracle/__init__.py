@@ -158,6 +158,8 @@ _REF_SIGS = {
     "ref_write_ppm": (C.c_int, [C.c_char_p, C.c_int, C.c_int, C.c_char_p, C.c_int64]),
     "ref_read_ppm": (C.c_int, [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_char_p, C.c_int64, C.c_char_p,
                                C.c_int64]),
+    "ref_codec_gradients": (C.c_int, [C.c_int, C.c_double, _f64p, _f64p, _f64p, _f64p, C.c_int64, _f64p,
+                                      C.c_void_p, C.c_void_p, _f64p]),
     "ref_run_encode": (C.c_int, [C.c_char_p, C.c_int, C.c_double, _f64p, _f64p, C.c_char_p, C.c_char_p, C.c_int64]),
     "ref_run_decode": (C.c_int, [C.c_char_p, C.c_int, C.c_double, _f64p, _f64p, C.c_char_p, C.c_char_p, C.c_int64]),
     "ref_write_spectra_csv": (C.c_int, [C.c_char_p, _f64p, C.c_int64, C.c_char_p, C.c_void_p]),

@@ -38,6 +38,7 @@
 #include "hadacodec/renderer.hpp"
 #include "hadacodec/rng.hpp"
 #include "hadacodec/spectrum.hpp"
+#include "hadacodec/trainer.hpp"
 #include "hadacodec/upsampler.hpp"
 #include "hadacodec_b200.h"  // POD scene / job structs only (ref_render)
 
@@ -886,6 +887,49 @@ int ref_read_ppm(const char* path, int* w, int* h, uint8_t* rgb, int64_t cap, ch
     return 0;
   } catch (const std::exception& e) {
     return shim_fail(e, err, errcap);
+  }
+}
+
+// gradients() + compute_losses() (trainer.cpp:108-373) of raw weights over m pairs (row-major
+// m x N); g_enc / g_dec may be NULL; losses = {e2e, rec, code, col, alg, total}.
+int ref_codec_gradients(int k, double beta, const double* raw_enc, const double* raw_dec, const double* refl,
+                        const double* illum, int64_t m, const double* lw5, double* g_enc, double* g_dec,
+                        double* losses) {
+  try {
+    const CodecWeights w = shim_weights(k, beta, raw_enc, raw_dec);
+    Batch b;
+    for (int64_t j = 0; j < m; ++j) {
+      SpectralCurve r, l;
+      for (int i = 0; i < N; ++i) {
+        r[i] = refl[j * N + i];
+        l[i] = illum[j * N + i];
+      }
+      b.refl.push_back(r);
+      b.illum.push_back(l);
+    }
+    LossWeights lw;
+    lw.e2e = lw5[0];
+    lw.rec = lw5[1];
+    lw.code = lw5[2];
+    lw.col = lw5[3];
+    lw.alg = lw5[4];
+    if (g_enc) {
+      const Gradients g = gradients(w, b, lw);
+      std::copy(g.raw_enc.begin(), g.raw_enc.end(), g_enc);
+      std::copy(g.raw_dec.begin(), g.raw_dec.end(), g_dec);
+    }
+    if (losses) {
+      const LossBreakdown lb = compute_losses(w, b, lw);
+      losses[0] = lb.e2e;
+      losses[1] = lb.rec;
+      losses[2] = lb.code;
+      losses[3] = lb.col;
+      losses[4] = lb.alg;
+      losses[5] = lb.total;
+    }
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
   }
 }
 

@@ -658,6 +658,47 @@ def write_raw_image(path, image: torch.Tensor) -> None:
         f.write(b"HCF1" + np.array([w, h, c], np.uint32).tobytes() + data)
 
 
+LOSS_WEIGHTS = (0.5, 0.75, 1.0, 0.5, 0.0)  # LossWeights defaults {e2e, rec, code, col, alg} (trainer.hpp:13-19)
+LOSS_NAMES = ("e2e", "rec", "code", "col", "alg", "total")
+
+
+def codec_train_grad(ctx: Context, raw_enc: np.ndarray, raw_dec: np.ndarray, beta: float, refl: torch.Tensor,
+                     illum: torch.Tensor, loss_weights=LOSS_WEIGHTS, grads: bool = True):
+    """compute_losses + gradients (trainer.cpp:108-373) of raw codec weights over a batch of
+    (reflectance, illumination) pairs [m, n] (float64 CUDA tensors), on the GPU, bit-identical
+    to the reference: ({loss name: value}, g_raw_enc [k, n], g_raw_dec [n, k]) — the
+    gradients are None with grads=False."""
+    re_ = np.ascontiguousarray(raw_enc, dtype=np.float64)
+    rd = np.ascontiguousarray(raw_dec, dtype=np.float64)
+    k, n = re_.shape
+    refl = _cuda(refl, torch.float64, "refl")
+    illum = _cuda(illum, torch.float64, "illum")
+    if refl.shape != illum.shape or refl.dim() != 2 or refl.shape[1] != n:
+        raise ValueError("batch: reflectance/illumination size mismatch")
+    lw = np.ascontiguousarray(loss_weights, dtype=np.float64)
+    cmf = np.ascontiguousarray(cmf_matrix(n), dtype=np.float64)
+    ge = np.zeros((k, n), np.float64) if grads else None
+    gd = np.zeros((n, k), np.float64) if grads else None
+    losses = np.zeros(6, np.float64)
+    ctx.bind_stream()
+    _check(_lib.lib().hc_codec_train_grad(ctx.h, k, n, float(beta), _np_ptr(re_), _np_ptr(rd), _np_ptr(cmf),
+                                          grid(n)[1], _p(refl), _p(illum), refl.shape[0], _np_ptr(lw),
+                                          _np_ptr(ge) if grads else None, _np_ptr(gd) if grads else None,
+                                          _np_ptr(losses)))
+    return dict(zip(LOSS_NAMES, losses.tolist())), ge, gd
+
+
+def adam_step(ctx: Context, params: torch.Tensor, grad: torch.Tensor, m1: torch.Tensor, v1: torch.Tensor, lr: float,
+              step: int) -> None:
+    """adam_step (trainer.cpp:399-411) in place on float64 CUDA tensors, bit-identical."""
+    for t, name in ((params, "params"), (grad, "grad"), (m1, "m"), (v1, "v")):
+        _cuda(t, torch.float64, name)
+        if not t.is_contiguous() or t.numel() != params.numel():
+            raise ValueError("adam: parameter / state size mismatch")
+    ctx.bind_stream()
+    _check(_lib.lib().hc_adam_step(ctx.h, _p(params), _p(grad), _p(m1), _p(v1), params.numel(), float(lr), int(step)))
+
+
 def encode_tool(codec: "Codec", spectra_csv_bytes: bytes) -> bytes:
     """The reference's `encode` tool (tools/main.cpp:285-308, without its manifest) on the
     device: spectra CSV -> resample + encode (fp64) -> codes CSV (%.17g).  Byte-identical
