@@ -23,6 +23,7 @@
 
 #include "hadacodec_b200.h"
 #include "hc_internal.h"
+#include "hc_tma.cuh"
 
 namespace hcb {
 namespace {
@@ -33,25 +34,30 @@ struct LossW {
   double e2e, rec, code, col, alg;
 };
 
-// Per-pair outputs, structure of arrays over the batch (m pairs).
+// Per-pair outputs, stored transposed — [element][pair] — so that the per-weight batch
+// reductions read contiguous streams (and a warp of consecutive pairs stores coalesced).
 struct PairBufs {
-  double* gshat;   // m x n   dL/ds_hat (e2e + col terms)
-  double* grr;     // m x n   rec residual factor for R
-  double* grl;     // m x n   rec residual factor for L
-  double* zp;      // m x k
-  double* zr;      // m x k
-  double* zl;      // m x k
-  double* gc;      // m x k   code-term gradient per code
-  double* gzr;     // m x k   accumulated dL/dzr
-  double* gzl;     // m x k   accumulated dL/dzl
-  double* terms;   // m x 4   e2e, rec, code, col per pair
+  double* gshat;   // n x m   dL/ds_hat (e2e + col terms)
+  double* grr;     // n x m   rec residual factor for R
+  double* grl;     // n x m   rec residual factor for L
+  double* rT;      // n x m   R, transposed
+  double* lT;      // n x m   L, transposed
+  double* zp;      // k x m
+  double* zr;      // k x m
+  double* zl;      // k x m
+  double* gc;      // k x m   code-term gradient per code
+  double* gzr;     // k x m   accumulated dL/dzr
+  double* gzl;     // k x m   accumulated dL/dzl
+  double* terms;   // 4 x m   e2e, rec, code, col per pair
 };
+// Rows of the transposed arrays are ld = m rounded up to an even count apart, so every
+// 64-pair chunk of a row is a 16-byte-aligned 512-byte run (one bulk copy).
 
 template <int K, int N>
 __global__ void __launch_bounds__(128) pair_kernel(const double* __restrict__ E, const double* __restrict__ D,
                                                    const double* __restrict__ T, double lstep,
                                                    const double* __restrict__ refl, const double* __restrict__ illum,
-                                                   int64_t m, LossW lw, PairBufs pb) {
+                                                   int64_t m, int64_t ld, LossW lw, PairBufs pb) {
   const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
   if (j >= m) return;
   const double* r = refl + j * N;
@@ -112,10 +118,10 @@ __global__ void __launch_bounds__(128) pair_kernel(const double* __restrict__ E,
     dcol[c] = d;
     cols += d * d;
   }
-  pb.terms[j * 4 + 0] = mse * (2.0 - cosv);
-  pb.terms[j * 4 + 1] = mr / N + ml / N;
-  pb.terms[j * 4 + 2] = codes / K;
-  pb.terms[j * 4 + 3] = cols / 3.0;
+  pb.terms[0 * ld + j] = mse * (2.0 - cosv);
+  pb.terms[1 * ld + j] = mr / N + ml / N;
+  pb.terms[2 * ld + j] = codes / K;
+  pb.terms[3 * ld + j] = cols / 3.0;
   // gradients (trainer.cpp:236-359), per pair
   const double md = static_cast<double>(m);
   for (int i = 0; i < N; ++i) g[i] = 0.0;
@@ -143,7 +149,7 @@ __global__ void __launch_bounds__(128) pair_kernel(const double* __restrict__ E,
   for (int c = 0; c < K; ++c) gzp[c] = gzr[c] = gzl[c] = 0.0;
   for (int i = 0; i < N; ++i) {  // backprop s_hat = W_dec zp
     const double gs = g[i];
-    pb.gshat[j * N + i] = gs;
+    pb.gshat[i * ld + j] = gs;
     if (gs == 0.0) continue;
     for (int c = 0; c < K; ++c) gzp[c] += D[i * K + c] * gs;
   }
@@ -153,7 +159,7 @@ __global__ void __launch_bounds__(128) pair_kernel(const double* __restrict__ E,
       gcv = lw.code / md * (2.0 / K) * (zp[c] - zc[c]);
       gzp[c] += gcv;
     }
-    pb.gc[j * K + c] = gcv;
+    pb.gc[c * ld + j] = gcv;
   }
   for (int c = 0; c < K; ++c) {  // zp = zr o zl
     gzr[c] += gzp[c] * zl[c];
@@ -170,71 +176,234 @@ __global__ void __launch_bounds__(128) pair_kernel(const double* __restrict__ E,
         gzl[c] += D[i * K + c] * gl;
       }
     }
-    pb.grr[j * N + i] = gr;
-    pb.grl[j * N + i] = gl;
+    pb.grr[i * ld + j] = gr;
+    pb.grl[i * ld + j] = gl;
+    pb.rT[i * ld + j] = r[i];
+    pb.lT[i * ld + j] = l[i];
   }
   for (int c = 0; c < K; ++c) {
-    pb.zp[j * K + c] = zp[c];
-    pb.zr[j * K + c] = zr[c];
-    pb.zl[j * K + c] = zl[c];
-    pb.gzr[j * K + c] = gzr[c];
-    pb.gzl[j * K + c] = gzl[c];
+    pb.zp[c * ld + j] = zp[c];
+    pb.zr[c * ld + j] = zr[c];
+    pb.zl[c * ld + j] = zl[c];
+    pb.gzr[c * ld + j] = gzr[c];
+    pb.gzl[c * ld + j] = gzl[c];
   }
 }
 
-// One thread per weight: encoder weights (c, i) first (K*N), then decoder weights (i, c).
+// ------------------------------------------------------------------ ordered batch reductions
+// Each weight's gradient (and each batch-mean loss) is a sequential sum over the pairs in
+// batch order, as in the reference, so the parallelism is across weights only — and each
+// chain must not wait on memory.  One warp per block: the warp's lanes own up to 32
+// weights, lane -> (code lane % K, wavelength w * (32 / K) + lane / K), so their inputs are
+// at most ~45 contiguous per-pair streams (rows of the transposed buffers: three per code,
+// two or three per wavelength); a 4-stage ring of 128-pair chunks of all those streams is
+// filled by bulk copies
+// (cp.async.bulk, one mbarrier per stage) while the lanes run their chains from shared
+// memory.  Stream rows in shared memory are 528 B apart, so the lanes' double2 reads of
+// different streams spread over the banks.  The reference's skipped adds are adds of a
+// selected 0.0 here (branch-free, so the shared-memory loads pipeline ahead of the chain):
+// the same sums, since an accumulator that starts at +0.0 never holds -0.0 and x + 0.0 = x
+// for every other x.
+constexpr int kChunkPairs = 128;
+constexpr int kStages = 4;
+constexpr int kMaxStreams = 48;
+constexpr int kStreamStride = kChunkPairs * 8 + 16;  // bytes
+constexpr size_t kRingBytes = size_t(kStages) * kMaxStreams * kStreamStride;
+
+struct StreamRing {
+  unsigned char* buf;  // kStages x kMaxStreams x kStreamStride
+  uint64_t* bar;       // kStages
+  const double* const* base;
+  int count;
+  __device__ const double* stream(int stage, int q) const {
+    return reinterpret_cast<const double*>(buf + (size_t(stage) * kMaxStreams + q) * kStreamStride);
+  }
+  // all lanes: copies of chunk t into its stage (lane 0 sets the byte count)
+  __device__ void issue(int64_t t, int lane) const {
+    const int st = static_cast<int>(t % kStages);
+    if (lane == 0) mbar_arrive_expect_tx(&bar[st], static_cast<uint32_t>(count) * kChunkPairs * 8);
+    for (int q = lane; q < count; q += 32)
+      bulk_g2s(buf + (size_t(st) * kMaxStreams + q) * kStreamStride, base[q] + t * kChunkPairs, kChunkPairs * 8,
+               &bar[st]);
+  }
+  __device__ void wait(int64_t t) const {
+    mbar_wait(&bar[t % kStages], static_cast<uint32_t>((t / kStages) & 1));
+  }
+};
+
+__device__ inline void ring_init(uint64_t* bar, int lane) {
+  if (lane == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+}
+
+// Grid: enc warps [0, ceil(KN/32)), then dec warps.  Dynamic smem: kRingBytes.
 template <int K, int N>
-__global__ void __launch_bounds__(128) grad_reduce_kernel(const double* __restrict__ D,
-                                                          const double* __restrict__ refl,
-                                                          const double* __restrict__ illum, int64_t m, LossW lw,
-                                                          PairBufs pb, const double* __restrict__ sd_enc,
-                                                          const double* __restrict__ sd_dec,
-                                                          double* __restrict__ g_enc, double* __restrict__ g_dec) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < K * N) {  // g_enc[c][i]
-    const int c = t / N, i = t % N;
-    double acc = 0.0;
-    for (int64_t j = 0; j < m; ++j) {
-      const double rv = refl[j * N + i], lv = illum[j * N + i];
-      if (lw.code != 0.0) acc -= pb.gc[j * K + c] * (rv * lv);
-      const double gr = pb.gzr[j * K + c], gl = pb.gzl[j * K + c];
-      if (gr == 0.0 && gl == 0.0) continue;
-      acc += gr * rv + gl * lv;
-    }
-    g_enc[t] = acc * sd_enc[t];
+__device__ void loss_reduce(const double* __restrict__ D, int64_t m, int64_t ld, LossW lw,
+                            const double* __restrict__ terms, double* __restrict__ out);
+
+template <int K, int N>
+__global__ void __launch_bounds__(32) grad_reduce_kernel(const double* __restrict__ D, int64_t m, int64_t ld, LossW lw,
+                                                         PairBufs pb, const double* __restrict__ sd_enc,
+                                                         const double* __restrict__ sd_dec,
+                                                         double* __restrict__ g_enc, double* __restrict__ g_dec,
+                                                         double* __restrict__ losses, int loss_block) {
+  constexpr int kPerWarp = 32 / K;                          // wavelengths per warp
+  constexpr int kWarpsPerHalf = (N + kPerWarp - 1) / kPerWarp;
+  if (static_cast<int>(blockIdx.x) == loss_block) {  // the batch-mean losses, concurrently with the weights
+    loss_reduce<K, N>(D, m, ld, lw, pb.terms, losses);
     return;
   }
-  const int u = t - K * N;
-  if (u >= N * K) return;
-  const int i = u / K, c = u % K;  // g_dec[i][c]
+  extern __shared__ __align__(128) unsigned char ring_buf[];
+  __shared__ uint64_t bar[kStages];
+  __shared__ const double* base[kMaxStreams];
+  const int lane = threadIdx.x;
+  const bool dec = blockIdx.x >= kWarpsPerHalf;
+  const int w = dec ? blockIdx.x - kWarpsPerHalf : blockIdx.x;
+  const int i_lo = w * kPerWarp;
+  const int ni = min(kPerWarp, N - i_lo);
+  const int c = lane % K;
+  const int il = min(lane / K, ni - 1);  // idle lanes repeat a live weight
+  const int i = i_lo + il;
+  const bool live = lane < K * kPerWarp && lane / K < ni;
+  const bool code = lw.code != 0.0, rec = lw.rec != 0.0;
+  // streams: per code c: 3 rows [0, 3K); per wavelength: enc R, L (2) / dec gshat, grr, grl (3)
+  int count, s0, s1, s2, s3, s4, s5;
+  if (lane < K) {
+    base[3 * lane + 0] = (dec ? pb.zp : pb.gc) + lane * ld;
+    base[3 * lane + 1] = (dec ? pb.zr : pb.gzr) + lane * ld;
+    base[3 * lane + 2] = (dec ? pb.zl : pb.gzl) + lane * ld;
+  }
+  if (!dec) {  // weight (c, i) of the encoder: gc, gzr, gzl of code c; R, L at wavelength i
+    count = 3 * K + 2 * ni;
+    if (lane < ni) {
+      base[3 * K + lane] = pb.rT + (i_lo + lane) * ld;
+      base[3 * K + ni + lane] = pb.lT + (i_lo + lane) * ld;
+    }
+    s0 = 3 * c;
+    s1 = s0 + 1;
+    s2 = s0 + 2;
+    s3 = 3 * K + il;
+    s4 = 3 * K + ni + il;
+    s5 = 0;
+  } else {  // weight (i, c) of the decoder: gshat, grr, grl at wavelength i; zp, zr, zl of code c
+    count = 3 * K + 3 * ni;
+    if (lane < ni) {
+      base[3 * K + 3 * lane + 0] = pb.gshat + (i_lo + lane) * ld;
+      base[3 * K + 3 * lane + 1] = pb.grr + (i_lo + lane) * ld;
+      base[3 * K + 3 * lane + 2] = pb.grl + (i_lo + lane) * ld;
+    }
+    s0 = 3 * K + 3 * il;
+    s1 = s0 + 1;
+    s2 = s0 + 2;
+    s3 = 3 * c;
+    s4 = s3 + 1;
+    s5 = s3 + 2;
+  }
+  ring_init(bar, lane);
+  const StreamRing ring{ring_buf, bar, base, count};
+  const int64_t nfull = m / kChunkPairs;
+  for (int64_t t = 0; t < nfull && t < kStages; ++t) ring.issue(t, lane);
   double acc = 0.0;
-  for (int64_t j = 0; j < m; ++j) {
-    const double gs = pb.gshat[j * N + i];
-    if (gs != 0.0) acc += gs * pb.zp[j * K + c];
-    if (lw.rec != 0.0) acc += pb.grr[j * N + i] * pb.zr[j * K + c] + pb.grl[j * N + i] * pb.zl[j * K + c];
+  for (int64_t t = 0; t < nfull; ++t) {
+    ring.wait(t);
+    const int st = static_cast<int>(t % kStages);
+    if (!dec) {
+      const double2* gc = reinterpret_cast<const double2*>(ring.stream(st, s0));
+      const double2* gr = reinterpret_cast<const double2*>(ring.stream(st, s1));
+      const double2* gl = reinterpret_cast<const double2*>(ring.stream(st, s2));
+      const double2* rv = reinterpret_cast<const double2*>(ring.stream(st, s3));
+      const double2* lv = reinterpret_cast<const double2*>(ring.stream(st, s4));
+#pragma unroll 8
+      for (int p = 0; p < kChunkPairs / 2; ++p) {
+        const double2 a = gc[p], b = gr[p], x = gl[p], y = rv[p], z = lv[p];
+        acc = acc - (code ? a.x * (y.x * z.x) : 0.0);
+        acc = acc + ((b.x == 0.0 && x.x == 0.0) ? 0.0 : b.x * y.x + x.x * z.x);
+        acc = acc - (code ? a.y * (y.y * z.y) : 0.0);
+        acc = acc + ((b.y == 0.0 && x.y == 0.0) ? 0.0 : b.y * y.y + x.y * z.y);
+      }
+    } else {
+      const double2* gs = reinterpret_cast<const double2*>(ring.stream(st, s0));
+      const double2* rr = reinterpret_cast<const double2*>(ring.stream(st, s1));
+      const double2* rl = reinterpret_cast<const double2*>(ring.stream(st, s2));
+      const double2* zp = reinterpret_cast<const double2*>(ring.stream(st, s3));
+      const double2* zr = reinterpret_cast<const double2*>(ring.stream(st, s4));
+      const double2* zl = reinterpret_cast<const double2*>(ring.stream(st, s5));
+#pragma unroll 8
+      for (int p = 0; p < kChunkPairs / 2; ++p) {
+        const double2 a = gs[p], q = zp[p], r1 = rr[p], r2 = rl[p], w1 = zr[p], w2 = zl[p];
+        acc = acc + (a.x != 0.0 ? a.x * q.x : 0.0);
+        acc = acc + (rec ? r1.x * w1.x + r2.x * w2.x : 0.0);
+        acc = acc + (a.y != 0.0 ? a.y * q.y : 0.0);
+        acc = acc + (rec ? r1.y * w1.y + r2.y * w2.y : 0.0);
+      }
+    }
+    __syncwarp();
+    if (t + kStages < nfull) ring.issue(t + kStages, lane);
+  }
+  // the last m % kChunkPairs pairs straight from global memory
+  for (int64_t j = nfull * kChunkPairs; j < m; ++j) {
+    if (!dec) {
+      const double a = base[s0][j], b = base[s1][j], x = base[s2][j], y = base[s3][j], z = base[s4][j];
+      if (code) acc -= a * (y * z);
+      if (!(b == 0.0 && x == 0.0)) acc += b * y + x * z;
+    } else {
+      const double a = base[s0][j];
+      if (a != 0.0) acc += a * base[s3][j];
+      if (rec) acc += base[s1][j] * base[s4][j] + base[s2][j] * base[s5][j];
+    }
+  }
+  if (!live) return;
+  if (!dec) {
+    g_enc[c * N + i] = acc * sd_enc[c * N + i];
+    return;
   }
   if (lw.alg != 0.0) {  // trainer.cpp:336-355
     const double off_terms = K > 1 ? static_cast<double>(K) * (K - 1) : 1.0;
-    const double* w = D + i * K;
+    const double* wr = D + i * K;
     double gg = 0.0;
     for (int q = 0; q < K; ++q) {
       if (q == c) continue;
-      gg += 4.0 * w[c] * w[q] * w[q] / off_terms;
+      gg += 4.0 * wr[c] * wr[q] * wr[q] / off_terms;
     }
-    const double bi = w[c];
+    const double bi = wr[c];
     gg += 2.0 * (bi * bi - bi) * (2.0 * bi - 1.0) / K;
     acc += lw.alg * gg;
   }
-  g_dec[u] = acc * sd_dec[u];
+  g_dec[i * K + c] = acc * sd_dec[i * K + c];
 }
 
-// Batch means in batch order, loss_alg (trainer.cpp:174-201), the weighted total.
+// Batch means in batch order (lanes 0-3: one loss term each, from the same staged ring),
+// loss_alg (trainer.cpp:174-201) and the weighted total.  One warp.
 template <int K, int N>
-__global__ void loss_reduce_kernel(const double* __restrict__ D, int64_t m, LossW lw, const double* __restrict__ terms,
-                                   double* __restrict__ out) {
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t j = 0; j < m; ++j)
-    for (int q = 0; q < 4; ++q) acc[q] += terms[j * 4 + q];
+__device__ void loss_reduce(const double* __restrict__ D, int64_t m, int64_t ld, LossW lw,
+                            const double* __restrict__ terms, double* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char ring_buf[];
+  __shared__ uint64_t bar[kStages];
+  __shared__ const double* base[kMaxStreams];
+  const int lane = threadIdx.x;
+  if (lane < 4) base[lane] = terms + lane * ld;
+  ring_init(bar, lane);
+  const StreamRing ring{ring_buf, bar, base, 4};
+  const int64_t nfull = m / kChunkPairs;
+  for (int64_t t = 0; t < nfull && t < kStages; ++t) ring.issue(t, lane);
+  const int q = lane < 4 ? lane : 0;
+  double acc = 0.0;
+  for (int64_t t = 0; t < nfull; ++t) {
+    ring.wait(t);
+    const double* v = ring.stream(static_cast<int>(t % kStages), q);
+#pragma unroll 8
+    for (int p = 0; p < kChunkPairs; ++p) acc += v[p];
+    __syncwarp();
+    if (t + kStages < nfull) ring.issue(t + kStages, lane);
+  }
+  for (int64_t j = nfull * kChunkPairs; j < m; ++j) acc += base[q][j];
+  __shared__ double sums[4];
+  if (lane < 4) sums[lane] = acc;
+  __syncwarp();
+  if (lane != 0) return;
   const double md = static_cast<double>(m);
   double off = 0.0, idem = 0.0;
   for (int i = 0; i < K; ++i)
@@ -257,7 +426,7 @@ __global__ void loss_reduce_kernel(const double* __restrict__ D, int64_t m, Loss
     idem += s;
   }
   const double off_terms = K > 1 ? static_cast<double>(K) * (K - 1) : 1.0;
-  const double e2e = acc[0] / md, rec = acc[1] / md, code = acc[2] / md, col = acc[3] / md;
+  const double e2e = sums[0] / md, rec = sums[1] / md, code = sums[2] / md, col = sums[3] / md;
   const double alg = off / off_terms + idem / K;
   out[0] = e2e;
   out[1] = rec;
@@ -338,37 +507,36 @@ int hc_codec_train_grad(hc_ctx ctx, int k, int n, double beta, const double* raw
     sdd[i] = softplus_derivative_h(raw_dec[i], beta);
   }
   for (int i = 0; i < 3 * n; ++i) T[i] = cmf[i];
-  // scratch: weights | per-pair buffers | gradients | losses
+  // scratch: weights | per-pair buffers (rows of ld doubles, 16-byte aligned) | gradients | losses
+  const int64_t ld = (m + 1) & ~int64_t(1);
+  auto up32 = [](size_t x) { return (x + 31) & ~size_t(31); };  // doubles
+  const size_t wdoubles = up32(host.size());
+  const size_t rows = static_cast<size_t>(5 * n + 6 * k + 4);
+  const size_t pdoubles = rows * static_cast<size_t>(ld);
   const size_t wbytes = sizeof(double) * host.size();
-  const size_t per_pair = static_cast<size_t>(3 * n + 6 * k + 4);
-  const size_t pbytes = sizeof(double) * per_pair * static_cast<size_t>(m);
-  const size_t gbytes = sizeof(double) * 2 * kn;
-  int rc = ensure_scratch(ctx, wbytes + pbytes + gbytes + sizeof(double) * 8);
+  int rc = ensure_scratch(ctx, sizeof(double) * (wdoubles + pdoubles + 2 * kn + 8) + 256);
   if (rc != HC_OK) return rc;
-  double* base = static_cast<double*>(ctx->scratch);
+  double* base = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(ctx->scratch) + 255) & ~uintptr_t(255));
   double* dW = base;
   PairBufs pb;
-  double* q = base + host.size();
-  pb.gshat = q;
-  q += static_cast<size_t>(m) * n;
-  pb.grr = q;
-  q += static_cast<size_t>(m) * n;
-  pb.grl = q;
-  q += static_cast<size_t>(m) * n;
-  pb.zp = q;
-  q += static_cast<size_t>(m) * k;
-  pb.zr = q;
-  q += static_cast<size_t>(m) * k;
-  pb.zl = q;
-  q += static_cast<size_t>(m) * k;
-  pb.gc = q;
-  q += static_cast<size_t>(m) * k;
-  pb.gzr = q;
-  q += static_cast<size_t>(m) * k;
-  pb.gzl = q;
-  q += static_cast<size_t>(m) * k;
-  pb.terms = q;
-  q += static_cast<size_t>(m) * 4;
+  double* q = base + wdoubles;
+  auto take = [&](int nrows) {
+    double* p = q;
+    q += static_cast<size_t>(nrows) * ld;
+    return p;
+  };
+  pb.gshat = take(n);
+  pb.grr = take(n);
+  pb.grl = take(n);
+  pb.rT = take(n);
+  pb.lT = take(n);
+  pb.zp = take(k);
+  pb.zr = take(k);
+  pb.zl = take(k);
+  pb.gc = take(k);
+  pb.gzr = take(k);
+  pb.gzl = take(k);
+  pb.terms = take(4);
   double* dg = q;
   double* dloss = dg + 2 * kn;
   HC_CUDA_TRY(cudaMemcpyAsync(dW, host.data(), wbytes, cudaMemcpyHostToDevice, ctx->stream));
@@ -380,16 +548,16 @@ int hc_codec_train_grad(hc_ctx ctx, int k, int n, double beta, const double* raw
   rc = dispatch_train(k, n, [&](auto Kc, auto Nc) {
     constexpr int K = decltype(Kc)::value, N = decltype(Nc)::value;
     pair_kernel<K, N><<<static_cast<int>((m + 127) / 128), 128, 0, ctx->stream>>>(dE, dD, dT, lambda_step, refl,
-                                                                                  illum, m, lw, pb);
+                                                                                  illum, m, ld, lw, pb);
     HC_CHECK_LAUNCH(ctx, "pair_kernel");
-    if (g_raw_enc) {
-      grad_reduce_kernel<K, N><<<(2 * K * N + 127) / 128, 128, 0, ctx->stream>>>(dD, refl, illum, m, lw, pb, dsde,
-                                                                                 dsdd, dg, dg + kn);
+    if (g_raw_enc || losses) {  // weights' chains (when asked) + one warp for the losses
+      auto kern = grad_reduce_kernel<K, N>;
+      HC_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kRingBytes)));
+      constexpr int kHalf = (N + 32 / K - 1) / (32 / K);
+      const int blocks = (g_raw_enc ? 2 * kHalf : 0) + (losses ? 1 : 0);
+      const int loss_block = losses ? blocks - 1 : -1;
+      kern<<<blocks, 32, kRingBytes, ctx->stream>>>(dD, m, ld, lw, pb, dsde, dsdd, dg, dg + kn, dloss, loss_block);
       HC_CHECK_LAUNCH(ctx, "grad_reduce_kernel");
-    }
-    if (losses) {
-      loss_reduce_kernel<K, N><<<1, 1, 0, ctx->stream>>>(dD, m, lw, pb.terms, dloss);
-      HC_CHECK_LAUNCH(ctx, "loss_reduce_kernel");
     }
     return HC_OK;
   });

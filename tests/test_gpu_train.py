@@ -81,3 +81,11 @@ def test_adam_step_bit_identical(api, ctx):
         pw -= 1e-3 * (st_m / c1) / (np.sqrt(st_v / c2) + 1e-8)
     assert p.cpu().numpy().tobytes() == pw.tobytes()
     assert gm.cpu().numpy().tobytes() == st_m.tobytes() and gv.cpu().numpy().tobytes() == st_v.tobytes()
+
+
+def test_losses_only_matches_full_call(api, ctx):
+    re_, rd, refl, illum = _case(6, 300, 5)
+    r, l = torch.from_numpy(refl).cuda(), torch.from_numpy(illum).cuda()
+    full, _, _ = api.codec_train_grad(ctx, re_, rd, 10.0, r, l)
+    only, ge, gd = api.codec_train_grad(ctx, re_, rd, 10.0, r, l, grads=False)
+    assert ge is None and gd is None and only == full
