@@ -2,7 +2,7 @@
 """hadacodec-b200 benchmark (driver contract: one JSON line from rank 0).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 1|2|3|4|5a|5b] [--all] [--no-cpu-baseline]
+                    [--config 1|2|3|4|5a|5b|6|7|8|9|10] [--all] [--no-cpu-baseline]
 
 Default workload = BASELINE.json configs[1] ("config 2"): 1920x1080 G-buffer,
 k = 6 (2 RGB passes), 8 lights, latent Hadamard shade + reassembly + decode
@@ -59,7 +59,7 @@ CONFIGS = {
     # SURVEY §8f row 1 (the next row): the colour-metric tail of a config-2 frame.
     "6": dict(name="1920x1080 colour-metric tail: scene_color_report(naive n=81 sRGB, latent k=6 sRGB) "
                    "+ tonemap_srgb8 preview of the latent frame", W=1920, H=1080, k=6, L=8, unit="Mpixel/s",
-              bytes_per_unit=27, rot=8),
+              bytes_per_unit=27, rot=8, dtype="f64"),
     # the reference's path tracer, latent k = 6 (naive: spectral n = 81).
     # Units are pixel-samples; the algorithmic bytes are the image writes (k floats per pixel
     # over spp samples), so the HBM fraction is ~0: the tracer is fp64 / latency bound.
@@ -68,17 +68,23 @@ CONFIGS = {
     # ~20 B of text written and read back, 8 B double out.
     "8": dict(name="codes CSV round trip on the device: write_codes_csv (%.17g) + read_codes_csv (exact "
                    "strtod), 2^21 rows x k=6", units=(1 << 21) * 6, rows=1 << 21, k=6, unit="M codes/s",
-              bytes_per_unit=52, rot=1, graph=False),
+              bytes_per_unit=52, rot=1, graph=False, dtype="f64"),
     # the reference's `encode` tool (tools/main.cpp:285-308) on the device —
     # read_spectra_csv of 2^17 curves measured on a 4 nm 360-800 grid (111 samples, %.9g), resample
     # onto the 81-sample grid + zero outside 400-700 + fp64 encode (k = 6), write_codes_csv
     # (%.17g); algorithmic bytes per curve: its ~1.2 KB of input text + ~120 B of output text.
     "9": dict(name="encode tool on the device: spectra CSV (2^17 curves x 111 samples, 4 nm) -> resample + "
                    "fp64 encode (k=6) -> codes CSV", units=1 << 17, rows=1 << 17, m=111, k=6, unit="M curves/s",
-              bytes_per_unit=1330, rot=1, graph=False),
+              bytes_per_unit=1330, rot=1, graph=False, dtype="f64"),
+    # the codec training objective — compute_losses + gradients
+    # (trainer.cpp:108-373), bit-identical — over one batch of 2^16 (reflectance, illumination)
+    # pairs, k = 6, default LossWeights; algorithmic bytes per pair: its two 81-sample curves.
+    "10": dict(name="codec training objective: losses + analytic gradients (bit-identical fp64) over 2^16 "
+                    "pairs, k=6, n=81", units=1 << 16, m=1 << 16, k=6, unit="M pairs/s", bytes_per_unit=2 * 81 * 8,
+               rot=1, graph=False, dtype="f64"),
     "7": dict(name="Cornell box path trace (bm_render scene + block + 2nd light), 256x256, 64 spp, depth 3, "
                    "latent k=6 (naive: spectral n=81)", W=256, H=256, spp=64, depth=3, k=6,
-              unit="M samples/s", bytes_per_unit=6 * 4 / 64, rot=1, graph=False),
+              unit="M samples/s", bytes_per_unit=6 * 4 / 64, rot=1, graph=False, dtype="f64"),
 }
 
 
@@ -273,6 +279,20 @@ def cpu_reference_run(cfg_key: str, budget_s: float, threads: int = 0, rank: int
             ref.ref_read_codes_csv(path, C.byref(r_rows), C.byref(r_k), buf_codes, buf_codes.size, ids, len(ids))
 
         sample = f"{rows} rows x k={k}: the reference's write_codes_csv + read_codes_csv (single-threaded, /tmp file)"
+    elif cfg_key == "10":
+        m = 2048
+        raw_e, raw_d = tool_raw_weights(k)
+        refl = synth.uniform_np(SEED, "train.refl", 0, m * N_SPEC).astype(np.float64)
+        illum = synth.uniform_np(SEED, "train.illum", 0, m * N_SPEC).astype(np.float64) * 2.0
+        ge, gd, lo = np.zeros(k * N_SPEC), np.zeros(N_SPEC * k), np.zeros(6)
+        lw = np.array([0.5, 0.75, 1.0, 0.5, 0.0])
+        P = m
+        nthreads = 1
+
+        def run():
+            ref.ref_codec_gradients(k, 10.0, raw_e, raw_d, refl, illum, m, lw, ge.ctypes.data, gd.ctypes.data, lo)
+
+        sample = f"{m} pairs: the reference's gradients() + compute_losses() (single-threaded)"
     elif cfg_key == "9":
         import ctypes as C
         import tempfile
@@ -488,6 +508,21 @@ class Workload:
                                                   self.text.numel(), api.C.byref(ln)))
                 api._check(lib.hc_codes_csv_read(ctx.h, self.text.data_ptr(), ln.value, api.C.byref(kk),
                                                  api.C.byref(rr), self.codes.data_ptr(), self.ids.data_ptr(), rows))
+            self.step = step
+        elif cfg_key == "10":
+            m, k = cfg["m"], cfg["k"]
+            self.raw_e, self.raw_d = tool_raw_weights(k)
+            self.raw_e = self.raw_e.reshape(k, N_SPEC)
+            self.raw_d = self.raw_d.reshape(N_SPEC, k)
+            base = api.synth_uniform(ctx, SEED + rank, "train.refl", 0, m * N_SPEC).reshape(m, N_SPEC)
+            self.refl = base.double().contiguous()
+            self.illum = (api.synth_uniform(ctx, SEED + rank, "train.illum", 0, m * N_SPEC).reshape(m, N_SPEC)
+                          .double() * 2.0).contiguous()
+            self.units = m
+            self.sets.append({"rgb": None})
+
+            def step(i):
+                api.codec_train_grad(ctx, self.raw_e, self.raw_d, 10.0, self.refl, self.illum)
             self.step = step
         elif cfg_key == "9":
             rows, m, k = cfg["rows"], cfg["m"], cfg["k"]
@@ -845,7 +880,8 @@ def run_ours(args) -> int:
             "metric": METRIC if args.config == "2" else f"{cfg['unit']} config {args.config}",
             "value": value, "unit": cfg["unit"], "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
-            "dtype": "bf16" if args.config == "5a" else "f32", "data": "synthetic (seeded, DESIGN.md Inputs)",
+            "dtype": cfg.get("dtype", "bf16" if args.config == "5a" else "f32"),
+            "data": "synthetic (seeded, DESIGN.md Inputs)",
             "config": {"workload": cfg["name"], "config_id": args.config, "units_per_gpu": wl.units,
                        "l2": (f"{R} rotating input/output buffer sets"
                               f" ({'each' if R == 1 else 'rotation'} > 2x 126 MB L2)") if cfg.get("graph", True)

@@ -76,30 +76,37 @@ __global__ void __launch_bounds__(128) pair_kernel(const double* __restrict__ E,
     zc[c] = as;
   }
   for (int c = 0; c < K; ++c) zp[c] = zr[c] * zl[c];
-  double shat[N], recr[N], recl[N], g[N];
-  for (int i = 0; i < N; ++i) {
+  // s_hat[i] = D zp, rec_r[i] = D zr, rec_l[i] = D zl (matvec_dec, trainer.cpp:39-47), each
+  // recomputed where needed (same expression, same value) instead of kept in arrays
+  auto dec3 = [&](int i, double* sh, double* rr, double* rl) {
     double a = 0.0, b = 0.0, d = 0.0;
+#pragma unroll
     for (int c = 0; c < K; ++c) {
       a += D[i * K + c] * zp[c];
       b += D[i * K + c] * zr[c];
       d += D[i * K + c] * zl[c];
     }
-    shat[i] = a;
-    recr[i] = b;
-    recl[i] = d;
-  }
-  // per-pair loss terms (loss_e2e / loss_rec / loss_code / loss_col, trainer.cpp:108-172)
-  double mse = 0.0, dot = 0.0, na = 0.0, nb = 0.0, mr = 0.0, ml = 0.0;
+    *sh = a;
+    *rr = b;
+    *rl = d;
+  };
+  // pass 1: the per-pair loss sums (loss_e2e / loss_rec / loss_col, trainer.cpp:108-172);
+  // every accumulator runs over i in order, as in its own loop in the reference
+  double mse = 0.0, dot = 0.0, na = 0.0, nb = 0.0, mr = 0.0, ml = 0.0, dcol[3] = {0.0, 0.0, 0.0};
   for (int i = 0; i < N; ++i) {
+    double sh, rr, rl;
+    dec3(i, &sh, &rr, &rl);
     const double s = r[i] * l[i];
-    const double d = shat[i] - s;
+    const double d = sh - s;
     mse += d * d;
-    dot += shat[i] * s;
-    na += shat[i] * shat[i];
+    dot += sh * s;
+    na += sh * sh;
     nb += s * s;
-    const double dr = recr[i] - r[i], dl = recl[i] - l[i];
+    const double dr = rr - r[i], dl = rl - l[i];
     mr += dr * dr;
     ml += dl * dl;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) dcol[c] += T[c * N + i] * (sh - s);
   }
   mse = mse / N;
   const double a = sqrt(na), bb = sqrt(nb);
@@ -110,50 +117,44 @@ __global__ void __launch_bounds__(128) pair_kernel(const double* __restrict__ E,
     codes += d * d;
   }
   double cols = 0.0;
-  double dcol[3];
   for (int c = 0; c < 3; ++c) {
-    double d = 0.0;
-    for (int i = 0; i < N; ++i) d += T[c * N + i] * (shat[i] - r[i] * l[i]);
-    d *= lstep;
-    dcol[c] = d;
-    cols += d * d;
+    dcol[c] *= lstep;
+    cols += dcol[c] * dcol[c];
   }
   pb.terms[0 * ld + j] = mse * (2.0 - cosv);
   pb.terms[1 * ld + j] = mr / N + ml / N;
   pb.terms[2 * ld + j] = codes / K;
   pb.terms[3 * ld + j] = cols / 3.0;
-  // gradients (trainer.cpp:236-359), per pair
+  // pass 2: dL/ds_hat (trainer.cpp:255-285: the e2e term, then the three col terms, per i)
+  // and its backprop into zp (:288-297)
   const double md = static_cast<double>(m);
-  for (int i = 0; i < N; ++i) g[i] = 0.0;
-  if (lw.e2e != 0.0) {
-    const double u = 1.0 / ((a + kCosEps) * (bb + kCosEps));
-    const double cs = dot * u;
-    const double w_pair = lw.e2e / md;
-    for (int i = 0; i < N; ++i) {
-      const double s = r[i] * l[i];
-      double gi = (2.0 - cs) * (2.0 / N) * (shat[i] - s);
-      double dcos = s * u;
-      if (a > 0.0) dcos -= dot * shat[i] / (a * (a + kCosEps) * (a + kCosEps) * (bb + kCosEps));
-      gi -= mse * dcos;
-      g[i] += w_pair * gi;
-    }
-  }
-  if (lw.col != 0.0) {
-    const double w_pair = lw.col / md;
-    for (int c = 0; c < 3; ++c) {
-      const double coef = w_pair * (2.0 / 3.0) * dcol[c] * lstep;
-      for (int i = 0; i < N; ++i) g[i] += coef * T[c * N + i];
-    }
-  }
+  const double u = 1.0 / ((a + kCosEps) * (bb + kCosEps));
+  const double cs = dot * u;
+  const double w_e2e = lw.e2e / md, w_col = lw.col / md;
+  double coef[3];
+  for (int c = 0; c < 3; ++c) coef[c] = w_col * (2.0 / 3.0) * dcol[c] * lstep;
   double gzp[K], gzr[K], gzl[K];
   for (int c = 0; c < K; ++c) gzp[c] = gzr[c] = gzl[c] = 0.0;
-  for (int i = 0; i < N; ++i) {  // backprop s_hat = W_dec zp
-    const double gs = g[i];
+  for (int i = 0; i < N; ++i) {
+    double sh, rr, rl;
+    dec3(i, &sh, &rr, &rl);
+    double gs = 0.0;
+    if (lw.e2e != 0.0) {
+      const double s = r[i] * l[i];
+      double gi = (2.0 - cs) * (2.0 / N) * (sh - s);
+      double dcos = s * u;
+      if (a > 0.0) dcos -= dot * sh / (a * (a + kCosEps) * (a + kCosEps) * (bb + kCosEps));
+      gi -= mse * dcos;
+      gs += w_e2e * gi;
+    }
+    if (lw.col != 0.0)
+      for (int c = 0; c < 3; ++c) gs += coef[c] * T[c * N + i];
     pb.gshat[i * ld + j] = gs;
     if (gs == 0.0) continue;
+#pragma unroll
     for (int c = 0; c < K; ++c) gzp[c] += D[i * K + c] * gs;
   }
-  for (int c = 0; c < K; ++c) {  // code term
+  for (int c = 0; c < K; ++c) {  // code term (trainer.cpp:300-311)
     double gcv = 0.0;
     if (lw.code != 0.0) {
       gcv = lw.code / md * (2.0 / K) * (zp[c] - zc[c]);
@@ -165,12 +166,16 @@ __global__ void __launch_bounds__(128) pair_kernel(const double* __restrict__ E,
     gzr[c] += gzp[c] * zl[c];
     gzl[c] += gzp[c] * zr[c];
   }
+  // pass 3: rec (trainer.cpp:321-336)
   const double w_rec = lw.rec / md;
-  for (int i = 0; i < N; ++i) {  // rec
+  for (int i = 0; i < N; ++i) {
     double gr = 0.0, gl = 0.0;
     if (lw.rec != 0.0) {
-      gr = w_rec * (2.0 / N) * (recr[i] - r[i]);
-      gl = w_rec * (2.0 / N) * (recl[i] - l[i]);
+      double sh, rr, rl;
+      dec3(i, &sh, &rr, &rl);
+      gr = w_rec * (2.0 / N) * (rr - r[i]);
+      gl = w_rec * (2.0 / N) * (rl - l[i]);
+#pragma unroll
       for (int c = 0; c < K; ++c) {
         gzr[c] += D[i * K + c] * gr;
         gzl[c] += D[i * K + c] * gl;

@@ -10,7 +10,7 @@ if [ "${LAUNCHES:-1}" = 1 ]; then
     > gpurun_out/ncu_default.log 2>&1; echo "launches rc=$?"
 fi
 for c in ${FULL:-2 3}; do
-  case $c in 5a) K=regex:mlp_kernel;; 4) K=regex:chain;; 6) K=regex:de76;; 7) K=regex:render_samples;; 8|9) K=regex:line_parse;; *) K=regex:tile_pipeline;; esac
+  case $c in 5a) K=regex:mlp_kernel;; 4) K=regex:chain;; 6) K=regex:de76;; 7) K=regex:render_samples;; 8|9) K=regex:line_parse;; 10) K=regex:grad_reduce;; *) K=regex:tile_pipeline;; esac
   timeout 900 ncu --set full --clock-control none --import-source on -k $K -s 2 -c 1 -f -o gpurun_out/full_c$c \
     python bench.py --config $c --plain --steps 4 > gpurun_out/ncu_full_c$c.log 2>&1; echo "ncu full c$c rc=$?"
 done

@@ -26,7 +26,9 @@ ALGO_BYTES = {"1": 696 * (1 << 20), "2": 60 * 1920 * 1080, "3": 468 * 3840 * 216
               "8": 264557378 + 8 * 6 * (1 << 21) + 32 * (1 << 21),
               # 9 (line_parse_kernel): the 175 525 094-byte spectra CSV + 8 B per value (111 per curve)
               # + 32 B per row
-              "9": 175525094 + 8 * 111 * (1 << 17) + 32 * (1 << 17)}
+              "9": 175525094 + 8 * 111 * (1 << 17) + 32 * (1 << 17),
+              # 10 (grad_reduce_kernel): the per-pair rows it streams — 5 x 81 + 6 x 6 doubles per pair
+              "10": 8 * (5 * 81 + 6 * 6) * (1 << 16)}
 METRICS = [
     ("gpu__time_duration.sum", "duration (us)"),
     ("dram__bytes_read.sum", "DRAM read (bytes)"),
