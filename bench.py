@@ -614,7 +614,7 @@ class Workload:
             W, H = cfg["W"], cfg["H"]
             first, P = span(H, W)
             w = synth.mlp_weights(SEED, 6, 64)
-            self.mlp = api.Upsampler(ctx, w)
+            self.mlp = api.CodeMLP(ctx, w)
             for r in range(R):
                 rgb = api.synth_uniform(ctx, SEED + r, "mlp.input", first * 3, P * 3).reshape(P, 3)
                 self.sets.append((rgb, ctx.empty(P, 6)))

@@ -47,6 +47,7 @@ extern "C" {
 typedef struct hc_ctx_s* hc_ctx;
 typedef struct hc_codec_s* hc_codec;
 typedef struct hc_mlp_s* hc_mlp;
+typedef struct hc_upsampler_s* hc_upsampler;
 
 /* ------------------------------------------------------------------ runtime */
 const char* hc_last_error(void);
@@ -332,6 +333,20 @@ int hc_codec_train_grad(hc_ctx ctx, int k, int n, double beta, const double* raw
  * 1e-8) with the first / second moments m1 / v1 updated in place; step >= 1.  Bit-identical. */
 int hc_adam_step(hc_ctx ctx, double* params, const double* grad, double* m1, double* v1, int64_t count, double lr,
                  int64_t step);
+
+/* ------------------------------------------------------------------ the reference's upsampler
+ * UpsamplerWeights (upsampler.hpp:13-24): k, hidden (<= 512), w1 (hidden x 3), b1, w2
+ * (hidden x hidden), b2, w3 (k x hidden), b3 — fp64, host; validated as validate() does.
+ * hc_upsample_f64: upsample (clamp = 1: negative outputs -> 0, the count added to
+ * *clamped_entries) or upsample_raw (clamp = 0) of P linear-sRGB triples (device, P x 3
+ * doubles) into codes (device, P x k doubles): the reference's fp64 network and
+ * summation order; SiLU's exp is CUDA's (<= 1 ulp from glibc), so results agree with the
+ * reference to ~1e-15 relative. */
+int hc_upsampler_create(hc_ctx ctx, int k, int hidden, const double* w1, const double* b1, const double* w2,
+                        const double* b2, const double* w3, const double* b3, hc_upsampler* out);
+int hc_upsampler_destroy(hc_upsampler up);
+int hc_upsample_f64(hc_upsampler up, const double* rgb, int64_t P, int clamp, double* codes,
+                    uint64_t* clamped_entries);
 
 /* ------------------------------------------------------------------ host-buffer entry points
  * Reference-facing value calls: inputs and outputs in HOST memory (pinned for

@@ -933,6 +933,33 @@ int ref_codec_gradients(int k, double beta, const double* raw_enc, const double*
   }
 }
 
+// upsample / upsample_raw (upsampler.cpp:170-190) of P rgb triples with the given weights.
+int ref_upsample(int k, int hidden, const double* w1, const double* b1, const double* w2, const double* b2,
+                 const double* w3, const double* b3, const double* rgb, int64_t P, int clamp, double* codes,
+                 uint64_t* clamped) {
+  try {
+    UpsamplerWeights w;
+    w.k = k;
+    w.hidden = hidden;
+    const size_t h = static_cast<size_t>(hidden), kk = static_cast<size_t>(k);
+    w.w1.assign(w1, w1 + h * 3);
+    w.b1.assign(b1, b1 + h);
+    w.w2.assign(w2, w2 + h * h);
+    w.b2.assign(b2, b2 + h);
+    w.w3.assign(w3, w3 + kk * h);
+    w.b3.assign(b3, b3 + kk);
+    validate(w);
+    for (int64_t p = 0; p < P; ++p) {
+      const std::array<double, 3> c{rgb[p * 3], rgb[p * 3 + 1], rgb[p * 3 + 2]};
+      const LatentCode z = clamp ? upsample(w, c, clamped) : upsample_raw(w, c);
+      for (int i = 0; i < k; ++i) codes[p * k + i] = z[i];
+    }
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
 int ref_thread_count() { return render_thread_count(); }
 
 }  // extern "C"

@@ -15,8 +15,13 @@ of ``libhadacodec_b200.so``.  Calls are enqueued on torch's current stream.
   render(..., latent) / multipass            Codec.shade_latent / shade_latent_pass + reassemble
   render(..., spectral)                      Codec.shade_spectral
   multibounce chain (evaluation.cpp:50-76)   Codec.multibounce_latent / _spectral
-  upsample(UpsamplerWeights, rgb)            Upsampler.forward(rgb[P, 3]) -> codes[P, k]
+  upsample / upsample_raw (fp64, SiLU)       Upsampler.forward(rgb[P, 3], clamp) -> codes[P, k], clamped
+  BASELINE MLP (3-64-64-6, bf16 tcgen05)     CodeMLP.forward(rgb[P, 3]) -> codes[P, 6]
   loss residual (trainer.cpp:49-71)          Codec.hadamard_loss(A, B)
+  compute_losses + gradients, adam_step      codec_train_grad, adam_step
+  print_g17 / codes CSV / spectra CSV        format_g17, codes_csv, read_codes_csv, spectra_csv, read_spectra_csv
+  run_encode / run_decode tools              encode_tool, decode_tool (encode_resampled, decode_f64)
+  load_codec_weights, read/write_raw_image   load_codec_weights, read_raw_image, write_raw_image
   exposure_for / tonemap_srgb8 / error_map   exposure_for / tonemap_srgb8 / error_map
   scene_color_report (evaluation.cpp)        scene_color_report; delta_e94_report (per pixel)
   render / render_latent_multipass           render(codec, scene, mode, ..., multipass)
@@ -658,6 +663,43 @@ def write_raw_image(path, image: torch.Tensor) -> None:
         f.write(b"HCF1" + np.array([w, h, c], np.uint32).tobytes() + data)
 
 
+class Upsampler:
+    """The reference's RGB -> code upsampler (upsampler.hpp:13-50): fp64, 3 -> hidden -> hidden
+    -> k, SiLU, identity head; `forward` = upsample (clamp=True) / upsample_raw (clamp=False)
+    on the GPU in the reference's summation order (~1e-15 relative: SiLU uses CUDA's exp).
+    `w` holds w1 [hidden, 3], b1, w2 [hidden, hidden], b2, w3 [k, hidden], b3 (arrays)."""
+
+    KEYS = ("w1", "b1", "w2", "b2", "w3", "b3")
+
+    def __init__(self, ctx: Context, w: dict):
+        arrs = [np.ascontiguousarray(w[n], dtype=np.float64).reshape(-1) for n in self.KEYS]
+        hidden = arrs[1].size
+        k = arrs[5].size
+        self.ctx, self.k, self.hidden = ctx, k, hidden
+        h = C.c_void_p()
+        _check(_lib.lib().hc_upsampler_create(ctx.h, k, hidden, *[_np_ptr(a) for a in arrs], C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                _lib.lib().hc_upsampler_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    def forward(self, rgb: torch.Tensor, clamp: bool = True) -> tuple[torch.Tensor, int]:
+        """codes [P, k] float64 for linear-sRGB rows [P, 3] (float64 CUDA), and the number of
+        clamped entries (the reference's telemetry)."""
+        rgb = _cuda(rgb, torch.float64, "rgb")
+        P = rgb.shape[0]
+        codes = torch.empty(P, self.k, dtype=torch.float64, device=rgb.device)
+        n = C.c_uint64(0)
+        self.ctx.bind_stream()
+        _check(_lib.lib().hc_upsample_f64(self.h, _p(rgb), P, 1 if clamp else 0, _p(codes), C.byref(n)))
+        return codes, int(n.value)
+
+
 LOSS_WEIGHTS = (0.5, 0.75, 1.0, 0.5, 0.0)  # LossWeights defaults {e2e, rec, code, col, alg} (trainer.hpp:13-19)
 LOSS_NAMES = ("e2e", "rec", "code", "col", "alg", "total")
 
@@ -861,8 +903,9 @@ def join_blocks(blocks: Sequence[np.ndarray]) -> np.ndarray:
     return np.concatenate([np.asarray(b) for b in blocks], axis=-1)
 
 
-class Upsampler:
-    """RGB -> code MLP (upsampler.cpp:42-72; ReLU / softplus head, bf16 tcgen05)."""
+class CodeMLP:
+    """The BASELINE.json RGB -> code MLP (3 -> 64 -> 64 -> 6, ReLU, softplus head) in bf16 on the
+    tensor cores (tcgen05) — config 5a; the reference's own fp64 SiLU network is `Upsampler`."""
 
     def __init__(self, ctx: Context, w: dict):
         self.ctx = ctx

@@ -393,7 +393,7 @@ def test_hadamard_loss_golden(api, ctx, golden):
 def test_mlp_vs_oracle(api, ctx, orc, k, P):
     """Multiple tiles per stream, ragged tails (generic path), k in {3, 6, 9}."""
     w = synth.mlp_weights(SEED, k, 64)
-    mlp = api.Upsampler(ctx, w)
+    mlp = api.CodeMLP(ctx, w)
     rgb = api.synth_uniform(ctx, SEED, "mlp.input", 0, P * 3).reshape(P, 3)
     got = host(mlp.forward(rgb))
     ref = np.zeros((P, k), np.float32)
@@ -405,7 +405,7 @@ def test_mlp_vs_oracle(api, ctx, orc, k, P):
 def test_mlp_unaligned_input_and_repeat(api, ctx, orc):
     """rgb base not 16-byte aligned (no bulk copies), and two calls give identical codes."""
     w = synth.mlp_weights(SEED, 6, 64)
-    mlp = api.Upsampler(ctx, w)
+    mlp = api.CodeMLP(ctx, w)
     P = 128 * 300 + 3
     buf = api.synth_uniform(ctx, SEED, "mlp.input", 0, P * 3 + 1)
     rgb = buf[1:].reshape(P, 3)
@@ -423,6 +423,6 @@ def test_mlp_unaligned_input_and_repeat(api, ctx, orc):
 
 def test_mlp_golden(api, ctx, golden):
     w = {k: golden[f"c5_{k}"] for k in ("w1", "b1", "w2", "b2", "w3", "b3")}
-    mlp = api.Upsampler(ctx, w)
+    mlp = api.CodeMLP(ctx, w)
     got = host(mlp.forward(torch.from_numpy(np.ascontiguousarray(golden["c5_rgb"])).cuda()))
     _check("golden mlp", got, golden["c5_codes"], MLP_TOL)
