@@ -154,6 +154,40 @@ LatentCode blockwise_hadamard(const LatentCode& a, const LatentCode& b);
 std::vector<std::array<double, 3>> split_blocks(const LatentCode& z);
 LatentCode join_blocks(const std::vector<std::array<double, 3>>& blocks);
 
+// ---- upsampler.hpp:13-50: the reference's fp64 RGB -> code network (3 -> hidden -> hidden
+// -> k, SiLU, identity head) on the GPU; results within ~1e-15 relative of the reference
+// (SiLU's exp is CUDA's).
+struct UpsamplerWeights {
+  int k = 6;
+  int hidden = 128;
+  std::vector<double> w1, b1;  // hidden x 3, hidden
+  std::vector<double> w2, b2;  // hidden x hidden, hidden
+  std::vector<double> w3, b3;  // k x hidden, k
+  CodecTrainingMeta meta;
+};
+void validate(const UpsamplerWeights& w);  // std::invalid_argument, as upsampler.cpp:130-144
+class Upsampler {
+ public:
+  Upsampler(Device& dev, const UpsamplerWeights& w);
+  ~Upsampler();
+  Upsampler(const Upsampler&) = delete;
+  Upsampler& operator=(const Upsampler&) = delete;
+  hc_upsampler handle() const { return up_; }
+  int k() const { return k_; }
+  Device& device() const { return *dev_; }
+
+ private:
+  Device* dev_;
+  hc_upsampler up_ = nullptr;
+  int k_ = 0;
+};
+LatentCode upsample_raw(const Upsampler& u, const std::array<double, 3>& linear_rgb);
+LatentCode upsample(const Upsampler& u, const std::array<double, 3>& linear_rgb,
+                    std::uint64_t* clamped_entries = nullptr);
+// A whole texture at once (the form the tools should use): rows of (r, g, b) -> codes.
+std::vector<LatentCode> upsample_batch(const Upsampler& u, const std::vector<std::array<double, 3>>& linear_rgb,
+                                       std::uint64_t* clamped_entries = nullptr);
+
 // ---- batched codec (row-major host buffers; rows x n spectra, rows x k codes)
 std::vector<float> encode_batch(const Codec& c, const std::vector<float>& spectra);
 struct RoundTrip {
@@ -246,6 +280,8 @@ CodesCsv read_codes_csv(Device& dev, const std::string& path);
 // nlohmann::json dump(2)); FormatError for unreadable / malformed / invalid files.
 CodecWeights load_codec_weights(const std::string& path);
 void save_codec_weights(const std::string& path, const CodecWeights& w);
+UpsamplerWeights load_upsampler_weights(const std::string& path);  // io.cpp:405-431
+void save_upsampler_weights(const std::string& path, const UpsamplerWeights& w);  // io.cpp:433-445
 // HCF1 raw channel images and binary PPM (io.hpp:71-84), same checks and FormatError causes.
 ChannelImage read_raw_image(const std::string& path);
 void write_raw_image(const std::string& path, const ChannelImage& img);

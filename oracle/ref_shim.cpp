@@ -960,6 +960,27 @@ int ref_upsample(int k, int hidden, const double* w1, const double* b1, const do
   }
 }
 
+int ref_save_upsampler_weights(const char* path, int k, int hidden, const double* w1, const double* b1,
+                               const double* w2, const double* b2, const double* w3, const double* b3, int epochs) {
+  try {
+    UpsamplerWeights w;
+    w.k = k;
+    w.hidden = hidden;
+    const size_t h = static_cast<size_t>(hidden), kk = static_cast<size_t>(k);
+    w.w1.assign(w1, w1 + h * 3);
+    w.b1.assign(b1, b1 + h);
+    w.w2.assign(w2, w2 + h * h);
+    w.b2.assign(b2, b2 + h);
+    w.w3.assign(w3, w3 + kk * h);
+    w.b3.assign(b3, b3 + kk);
+    w.meta.epochs = epochs;
+    save_upsampler_weights(path, w);
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
 int ref_thread_count() { return render_thread_count(); }
 
 }  // extern "C"

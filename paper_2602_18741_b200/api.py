@@ -688,6 +688,11 @@ class Upsampler:
         except Exception:
             pass
 
+    @classmethod
+    def from_weights_file(cls, ctx: Context, path) -> "Upsampler":
+        """An upsampler from the reference's weight file (load_upsampler_weights, io.cpp:405-431)."""
+        return cls(ctx, load_upsampler_weights(path))
+
     def forward(self, rgb: torch.Tensor, clamp: bool = True) -> tuple[torch.Tensor, int]:
         """codes [P, k] float64 for linear-sRGB rows [P, 3] (float64 CUDA), and the number of
         clamped entries (the reference's telemetry)."""
@@ -739,6 +744,34 @@ def adam_step(ctx: Context, params: torch.Tensor, grad: torch.Tensor, m1: torch.
             raise ValueError("adam: parameter / state size mismatch")
     ctx.bind_stream()
     _check(_lib.lib().hc_adam_step(ctx.h, _p(params), _p(grad), _p(m1), _p(v1), params.numel(), float(lr), int(step)))
+
+
+def load_upsampler_weights(path) -> dict:
+    """load_upsampler_weights (io.cpp:405-431): {k, hidden, w1 [h, 3], b1, w2 [h, h], b2, w3 [k, h],
+    b3, meta}; ValueError (FormatError) for a file that is not valid upsampler weights."""
+    import json as _json
+
+    try:
+        with open(path, "r") as f:
+            j = _json.load(f)
+    except OSError as e:
+        raise ValueError(f"{path}: cannot open for reading") from e
+    except _json.JSONDecodeError as e:
+        raise ValueError(f"{path}: JSON parse error: {e}") from e
+    try:
+        if j["format"] != "upsampler-weights":
+            raise ValueError(f"{path}: not an upsampler weights file")
+        k, h = int(j["k"]), int(j["hidden"])
+        arr = {n: np.asarray(j[n], dtype=np.float64) for n in ("w1", "b1", "w2", "b2", "w3", "b3")}
+    except (KeyError, TypeError) as e:
+        raise ValueError(f"{path}: bad upsampler weights: {e}") from e
+    shapes = {"w1": h * 3, "b1": h, "w2": h * h, "b2": h, "w3": k * h, "b3": k}  # validate (upsampler.cpp:130-144)
+    if k <= 0 or h <= 0 or any(arr[n].size != sz for n, sz in shapes.items()):
+        raise ValueError(f"{path}: upsampler: weight shapes do not match k / hidden")
+    if not all(np.isfinite(a).all() for a in arr.values()):
+        raise ValueError(f"{path}: upsampler: weights must be finite")
+    return {"k": k, "hidden": h, "w1": arr["w1"].reshape(h, 3), "b1": arr["b1"], "w2": arr["w2"].reshape(h, h),
+            "b2": arr["b2"], "w3": arr["w3"].reshape(k, h), "b3": arr["b3"], "meta": j.get("meta")}
 
 
 def encode_tool(codec: "Codec", spectra_csv_bytes: bytes) -> bytes:

@@ -82,7 +82,67 @@ void save_codec_weights(const std::string& path, const CodecWeights& w) {  // io
   if (!f.good()) throw FormatError(path + ": write failed");
 }
 
+UpsamplerWeights load_upsampler_weights(const std::string& path) {  // io.cpp:405-431
+  std::ifstream f(path);
+  if (!f) throw FormatError(path + ": cannot open for reading");
+  json j;
+  try {
+    j = json::parse(f);
+  } catch (const json::exception& e) {
+    throw FormatError(path + ": JSON parse error: " + e.what());
+  }
+  UpsamplerWeights w;
+  try {
+    if (j.at("format").get<std::string>() != "upsampler-weights")
+      throw FormatError(path + ": not an upsampler weights file");
+    w.k = j.at("k").get<int>();
+    w.hidden = j.at("hidden").get<int>();
+    w.w1 = j.at("w1").get<std::vector<double>>();
+    w.b1 = j.at("b1").get<std::vector<double>>();
+    w.w2 = j.at("w2").get<std::vector<double>>();
+    w.b2 = j.at("b2").get<std::vector<double>>();
+    w.w3 = j.at("w3").get<std::vector<double>>();
+    w.b3 = j.at("b3").get<std::vector<double>>();
+    if (j.contains("meta")) {
+      const json& m = j.at("meta");
+      w.meta.seed = m.at("seed").get<std::uint64_t>();
+      const auto lw = m.at("lambda_weights").get<std::vector<double>>();
+      if (lw.size() != w.meta.lambda_weights.size())
+        throw FormatError("weights file: lambda_weights must have 5 entries");
+      for (size_t i = 0; i < lw.size(); ++i) w.meta.lambda_weights[i] = lw[i];
+      w.meta.epochs = m.at("epochs").get<int>();
+    }
+  } catch (const json::exception& e) {
+    throw FormatError(path + ": bad upsampler weights: " + e.what());
+  }
+  try {
+    validate(w);
+  } catch (const std::invalid_argument& e) {
+    throw FormatError(path + ": " + e.what());
+  }
+  return w;
+}
+
+void save_upsampler_weights(const std::string& path, const UpsamplerWeights& w) {  // io.cpp:433-445
+  validate(w);
+  const json meta{{"seed", w.meta.seed}, {"lambda_weights", w.meta.lambda_weights}, {"epochs", w.meta.epochs}};
+  const json j{{"format", "upsampler-weights"}, {"version", kToolVersion}, {"k", w.k}, {"hidden", w.hidden},
+               {"w1", w.w1}, {"b1", w.b1}, {"w2", w.w2}, {"b2", w.b2}, {"w3", w.w3}, {"b3", w.b3}, {"meta", meta}};
+  std::ofstream f(path);
+  if (!f) throw FormatError(path + ": cannot open for writing");
+  f << j.dump(2) << '\n';
+  f.flush();
+  if (!f.good()) throw FormatError(path + ": write failed");
+}
+
 #else
+
+UpsamplerWeights load_upsampler_weights(const std::string& path) {
+  throw FormatError(path + ": built without nlohmann/json (weight files unavailable)");
+}
+void save_upsampler_weights(const std::string& path, const UpsamplerWeights&) {
+  throw FormatError(path + ": built without nlohmann/json (weight files unavailable)");
+}
 
 CodecWeights load_codec_weights(const std::string& path) {
   throw FormatError(path + ": built without nlohmann/json (weight files unavailable)");

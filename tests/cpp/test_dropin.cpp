@@ -306,6 +306,52 @@ int main() {
     CHECK_THROWS_AS(render(codec, sc, job), std::invalid_argument);
   }
 
+  {  // the reference's upsampler (upsampler.cpp:42-72, :170-190) against plain fp64 loops here
+    UpsamplerWeights uw;
+    uw.k = 6;
+    uw.hidden = 24;
+    uint64_t us = 7;
+    auto fill = [&](std::vector<double>& v, size_t n, double scale) {
+      v.resize(n);
+      for (double& x : v) x = scale * (2.0 * lcg(us) - 1.0);
+    };
+    fill(uw.w1, 24 * 3, 0.8);
+    fill(uw.b1, 24, 0.1);
+    fill(uw.w2, 24 * 24, 0.4);
+    fill(uw.b2, 24, 0.1);
+    fill(uw.w3, 6 * 24, 0.5);
+    fill(uw.b3, 6, 0.1);
+    Upsampler up(dev, uw);
+    auto silu = [](double x) { return x * (1.0 / (1.0 + std::exp(-x))); };
+    std::uint64_t clamped = 0, want_clamped = 0;
+    for (int t = 0; t < 16; ++t) {
+      const std::array<double, 3> rgb{lcg(us), lcg(us), lcg(us)};
+      double h1[24], h2[24];
+      for (int i = 0; i < 24; ++i) {
+        double a = uw.b1[i];
+        for (int j = 0; j < 3; ++j) a += uw.w1[i * 3 + j] * rgb[j];
+        h1[i] = silu(a);
+      }
+      for (int i = 0; i < 24; ++i) {
+        double a = uw.b2[i];
+        for (int j = 0; j < 24; ++j) a += uw.w2[i * 24 + j] * h1[j];
+        h2[i] = silu(a);
+      }
+      const LatentCode raw = upsample_raw(up, rgb);
+      const LatentCode z = upsample(up, rgb, &clamped);
+      for (int i = 0; i < 6; ++i) {
+        double a = uw.b3[i];
+        for (int j = 0; j < 24; ++j) a += uw.w3[i * 24 + j] * h2[j];
+        CHECK(rel_close(raw[i], a, 1e-13));
+        CHECK(z[i] == (raw[i] < 0.0 ? 0.0 : raw[i]));
+        if (raw[i] < 0.0) ++want_clamped;
+      }
+    }
+    CHECK(clamped == want_clamped && want_clamped > 0);
+    uw.w2[5] = std::nan("");
+    CHECK_THROWS_AS(Upsampler(dev, uw), std::invalid_argument);
+  }
+
   {  // spectra CSV round trip with and without ids, malformed files (test_io.cpp:43-86)
     const std::string path = "/tmp/hc_b200_dropin_spectra.csv";
     std::vector<SpectralCurve> curves(2, SpectralCurve(47));

@@ -94,3 +94,34 @@ def test_malformed_weight_files_rejected_like_reference(ref, prog, tmp_path, cas
     assert r.returncode == 3, (r.returncode, r.stderr)
     with pytest.raises(ValueError):
         api.load_codec_weights(a)
+
+
+def _up_weights(k, hidden, seed):
+    rng = np.random.default_rng(seed)
+    return [rng.normal(0, 0.3, hidden * 3), rng.normal(0, 0.1, hidden), rng.normal(0, 0.1, hidden * hidden),
+            rng.normal(0, 0.1, hidden), rng.normal(0, 0.2, k * hidden), rng.normal(0, 0.1, k)]
+
+
+@pytest.mark.parametrize("k,hidden", [(6, 32), (9, 128)])
+def test_upsampler_weight_file_resave_is_byte_identical(ref, prog, tmp_path, k, hidden):
+    """test_io.cpp:196-212 (upsampler weight JSON round trip), against the reference's writer."""
+    ws = _up_weights(k, hidden, hidden)
+    a, b = tmp_path / "up.json", tmp_path / "up2.json"
+    assert ref.ref_save_upsampler_weights(str(a).encode(), k, hidden, *ws, 123) == 0
+    r = subprocess.run([str(prog), "upsampler", str(a), str(b)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    assert f"k={k} hidden={hidden} epochs=123" in r.stdout
+    assert b.read_bytes() == a.read_bytes()
+
+
+def test_weight_loaders_reject_each_others_files(ref, prog, tmp_path):
+    """test_io.cpp:175-194: the upsampler loader rejects codec files and vice versa."""
+    re_, rd = _weights(6, 2)
+    codec, up = tmp_path / "c.json", tmp_path / "u.json"
+    assert ref.ref_save_codec_weights(str(codec).encode(), 6, 10.0, re_.reshape(-1), rd.reshape(-1), 1, np.zeros(5),
+                                      0) == 0
+    assert ref.ref_save_upsampler_weights(str(up).encode(), 6, 16, *_up_weights(6, 16, 1), 0) == 0
+    r = subprocess.run([str(prog), "upsampler", str(codec), str(tmp_path / "x.json")], capture_output=True, text=True)
+    assert r.returncode == 3 and "not an upsampler weights file" in r.stderr
+    r = subprocess.run([str(prog), str(up), str(tmp_path / "y.json")], capture_output=True, text=True)
+    assert r.returncode == 3 and "not a codec weights file" in r.stderr
