@@ -82,6 +82,9 @@ int hc_codec_create_f64(hc_ctx ctx, int k, int n, const double* E, const double*
 int hc_codec_create_raw(hc_ctx ctx, int k, int n, double beta, const double* raw_enc,
                         const double* raw_dec, const double* cmf, double dlambda, hc_codec* out);
 int hc_codec_destroy(hc_codec codec);
+/* The codec's effective weights in fp64 (host copies, k x n and n x k): the doubles it was
+ * created with, or softplus_beta(raw) computed as effective_weights does. */
+int hc_codec_effective_f64(hc_codec codec, double* E, double* D);
 int hc_codec_dims(hc_codec codec, int* k, int* n);
 /* Folded 3 x k XYZ projection dlambda * CMF * D (host copy, f32). */
 int hc_codec_xyz_projection(hc_codec codec, float* out_3k);
@@ -347,6 +350,21 @@ int hc_upsampler_create(hc_ctx ctx, int k, int hidden, const double* w1, const d
 int hc_upsampler_destroy(hc_upsampler up);
 int hc_upsample_f64(hc_upsampler up, const double* rgb, int64_t P, int clamp, double* codes,
                     uint64_t* clamped_entries);
+
+/* upsample_loss + upsample_gradients (upsampler.cpp:207-369) of UpsamplerWeights (host, as
+ * hc_upsampler_create) over a batch of B samples: rgb (device, B x 3) and target codes
+ * (device, B x k) of the frozen codec whose effective decoder codec_dec (host, n x k) and
+ * CmfTable D65 rows wxyz (host, 3 x n: wx, wy, wz) and white (host, 3) define the colour
+ * term; lambda_maxabs / lambda_color as UpsampleTrainConfig.  losses[4] = {latent_mse,
+ * latent_maxabs, color, total} and grads (host, w1 | b1 | w2 | b2 | w3 | b3 concatenated in
+ * UpsamplerWeights layout) may be NULL.  Within ~1e-12 of the reference (exp, cbrt). */
+int hc_upsample_train_grad(hc_ctx ctx, int k, int hidden, const double* w1, const double* b1, const double* w2,
+                           const double* b2, const double* w3, const double* b3, int n, const double* codec_dec,
+                           const double* wxyz, const double* white, const double* rgb, const double* target, int64_t B,
+                           double lambda_maxabs, double lambda_color, double* losses, double* grads);
+/* adamw_step (upsampler.cpp:378-391) on device arrays, decoupled weight decay. */
+int hc_adamw_step(hc_ctx ctx, double* params, const double* grad, double* m1, double* v1, int64_t count, double lr,
+                  double weight_decay, int64_t step);
 
 /* ------------------------------------------------------------------ host-buffer entry points
  * Reference-facing value calls: inputs and outputs in HOST memory (pinned for

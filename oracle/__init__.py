@@ -164,6 +164,8 @@ _REF_SIGS = {
                                _f64p, C.POINTER(C.c_uint64)]),
     "ref_save_upsampler_weights": (C.c_int, [C.c_char_p, C.c_int, C.c_int, _f64p, _f64p, _f64p, _f64p, _f64p, _f64p,
                                              C.c_int]),
+    "ref_upsample_train": (C.c_int, [C.c_int, C.c_int, _f64p, _f64p, _f64p, _f64p, _f64p, _f64p, C.c_double, _f64p,
+                                     _f64p, _f64p, _f64p, C.c_int64, C.c_double, C.c_double, _f64p, C.c_void_p]),
     "ref_run_encode": (C.c_int, [C.c_char_p, C.c_int, C.c_double, _f64p, _f64p, C.c_char_p, C.c_char_p, C.c_int64]),
     "ref_run_decode": (C.c_int, [C.c_char_p, C.c_int, C.c_double, _f64p, _f64p, C.c_char_p, C.c_char_p, C.c_int64]),
     "ref_write_spectra_csv": (C.c_int, [C.c_char_p, _f64p, C.c_int64, C.c_char_p, C.c_void_p]),

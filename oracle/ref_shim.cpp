@@ -981,6 +981,48 @@ int ref_save_upsampler_weights(const char* path, int k, int hidden, const double
   }
 }
 
+// upsample_loss + upsample_gradients (upsampler.cpp:207-369) with the frozen codec given by
+// raw weights (k x N / N x k, beta); grads = w1 | b1 | w2 | b2 | w3 | b3 (may be NULL).
+int ref_upsample_train(int k, int hidden, const double* w1, const double* b1, const double* w2, const double* b2,
+                       const double* w3, const double* b3, double beta, const double* raw_enc, const double* raw_dec,
+                       const double* rgb, const double* target, int64_t B, double lambda_maxabs, double lambda_color,
+                       double* losses, double* grads) {
+  try {
+    UpsamplerWeights w;
+    w.k = k;
+    w.hidden = hidden;
+    const size_t h = static_cast<size_t>(hidden), kk = static_cast<size_t>(k);
+    w.w1.assign(w1, w1 + h * 3);
+    w.b1.assign(b1, b1 + h);
+    w.w2.assign(w2, w2 + h * h);
+    w.b2.assign(b2, b2 + h);
+    w.w3.assign(w3, w3 + kk * h);
+    w.b3.assign(b3, b3 + kk);
+    const EffectiveWeights eff = effective_weights(shim_weights(k, beta, raw_enc, raw_dec));
+    std::vector<UpsampleSample> batch(static_cast<size_t>(B));
+    for (int64_t b = 0; b < B; ++b) {
+      batch[static_cast<size_t>(b)].rgb = {rgb[b * 3], rgb[b * 3 + 1], rgb[b * 3 + 2]};
+      batch[static_cast<size_t>(b)].target.z.assign(target + b * k, target + (b + 1) * k);
+    }
+    UpsampleTrainConfig cfg;
+    cfg.lambda_maxabs = lambda_maxabs;
+    cfg.lambda_color = lambda_color;
+    const UpsampleLossBreakdown lb = upsample_loss(w, eff, batch, cfg);
+    losses[0] = lb.latent_mse;
+    losses[1] = lb.latent_maxabs;
+    losses[2] = lb.color;
+    losses[3] = lb.total;
+    if (grads) {
+      const UpsamplerGradients g = upsample_gradients(w, eff, batch, cfg);
+      double* o = grads;
+      for (const auto* v : {&g.w1, &g.b1, &g.w2, &g.b2, &g.w3, &g.b3}) o = std::copy(v->begin(), v->end(), o);
+    }
+    return 0;
+  } catch (const std::exception&) {
+    return 1;
+  }
+}
+
 int ref_thread_count() { return render_thread_count(); }
 
 }  // extern "C"

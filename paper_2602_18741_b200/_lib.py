@@ -63,11 +63,15 @@ SIGNATURES: dict[str, tuple] = {
     "hc_encode_resampled_f64": (i32, [vp, vp, i32, vp, i64, C.c_double, C.c_double, i32, vp]),
     "hc_decode_f64": (i32, [vp, vp, i64, vp, C.POINTER(i64)]),
     "hc_encode_f64": (i32, [vp, vp, i64, vp]),
+    "hc_codec_effective_f64": (i32, [vp, vp, vp]),
     "hc_codec_train_grad": (i32, [vp, i32, i32, C.c_double, vp, vp, vp, C.c_double, vp, vp, i64, vp, vp, vp, vp]),
     "hc_adam_step": (i32, [vp, vp, vp, vp, vp, i64, C.c_double, i64]),
     "hc_upsampler_create": (i32, [vp, i32, i32, vp, vp, vp, vp, vp, vp, C.POINTER(vp)]),
     "hc_upsampler_destroy": (i32, [vp]),
     "hc_upsample_f64": (i32, [vp, vp, i64, i32, vp, C.POINTER(C.c_uint64)]),
+    "hc_upsample_train_grad": (i32, [vp, i32, i32, vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, i64, C.c_double,
+                                     C.c_double, vp, vp]),
+    "hc_adamw_step": (i32, [vp, vp, vp, vp, vp, i64, C.c_double, C.c_double, i64]),
     "hc_parse_doubles": (i32, [vp, vp, vp, i64, i32, vp, vp]),
     "hc_codes_csv_read": (i32, [vp, vp, i64, C.POINTER(i32), C.POINTER(i64), vp, vp, i64]),
     "hc_render": (i32, [vp, vp, vp, vp, vp, vp, vp]),

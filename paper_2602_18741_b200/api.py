@@ -150,6 +150,13 @@ class Codec:
         except Exception:
             pass
 
+    def effective_f64(self) -> tuple[np.ndarray, np.ndarray]:
+        """(E [k, n], D [n, k]) in fp64 as the library holds them (effective_weights)."""
+        E = np.zeros((self.k, self.n), np.float64)
+        D = np.zeros((self.n, self.k), np.float64)
+        _check(_lib.lib().hc_codec_effective_f64(self.h, _np_ptr(E), _np_ptr(D)))
+        return E, D
+
     @property
     def xyz_projection(self) -> np.ndarray:
         out = np.zeros((3, self.k), np.float32)
@@ -744,6 +751,58 @@ def adam_step(ctx: Context, params: torch.Tensor, grad: torch.Tensor, m1: torch.
             raise ValueError("adam: parameter / state size mismatch")
     ctx.bind_stream()
     _check(_lib.lib().hc_adam_step(ctx.h, _p(params), _p(grad), _p(m1), _p(v1), params.numel(), float(lr), int(step)))
+
+
+def upsample_train_grad(ctx: Context, w: dict, codec: "Codec", rgb: torch.Tensor, target: torch.Tensor,
+                        lambda_maxabs: float = 0.3, lambda_color: float = 0.05, grads: bool = True):
+    """upsample_loss + upsample_gradients (upsampler.cpp:207-369) on the GPU: the network `w`
+    (Upsampler's dict layout), the frozen `codec` (its fp64 effective decoder), a batch of rgb
+    [B, 3] and target codes [B, k] (float64 CUDA).  Returns ({latent_mse, latent_maxabs,
+    color, total}, {w1: grad, ...} or None); within ~1e-12 of the reference (exp, cbrt)."""
+    from .colorimetry import cmf_table, white_xyz
+
+    arrs = [np.ascontiguousarray(w[n], dtype=np.float64).reshape(-1) for n in Upsampler.KEYS]
+    hidden, k = arrs[1].size, arrs[5].size
+    rgb = _cuda(rgb, torch.float64, "rgb")
+    target = _cuda(target, torch.float64, "target")
+    n = codec.n
+    t = cmf_table(n)
+    ys = [float(a) * float(b) for a, b in zip(t["ybar"], t["d65"])]
+    norm = 0.0
+    for v in ys:  # CmfTable (colorimetry.cpp:51-59), in the reference's order
+        norm += v
+    scale = 100.0 / norm
+    wxyz = np.ascontiguousarray(np.stack([scale * t[c] * t["d65"] for c in ("xbar", "ybar", "zbar")]), np.float64)
+    white = np.ascontiguousarray(white_xyz(n), dtype=np.float64)
+    dec = np.ascontiguousarray(codec.effective_f64()[1], dtype=np.float64)
+    ng = sum(a.size for a in arrs)
+    g = np.zeros(ng) if grads else None
+    losses = np.zeros(4)
+    ctx.bind_stream()
+    _check(_lib.lib().hc_upsample_train_grad(ctx.h, k, hidden, *[_np_ptr(a) for a in arrs], n, _np_ptr(dec),
+                                             _np_ptr(wxyz), _np_ptr(white), _p(rgb), _p(target), rgb.shape[0],
+                                             float(lambda_maxabs), float(lambda_color), _np_ptr(losses),
+                                             _np_ptr(g) if grads else None))
+    names = ("latent_mse", "latent_maxabs", "color", "total")
+    out = None
+    if grads:
+        out, o = {}, 0
+        for name, a in zip(Upsampler.KEYS, arrs):
+            out[name] = g[o:o + a.size].reshape(np.asarray(w[name]).shape)
+            o += a.size
+    return dict(zip(names, losses.tolist())), out
+
+
+def adamw_step(ctx: Context, params: torch.Tensor, grad: torch.Tensor, m1: torch.Tensor, v1: torch.Tensor, lr: float,
+               weight_decay: float, step: int) -> None:
+    """adamw_step (upsampler.cpp:378-391) in place on float64 CUDA tensors."""
+    for t_, name in ((params, "params"), (grad, "grad"), (m1, "m"), (v1, "v")):
+        _cuda(t_, torch.float64, name)
+        if not t_.is_contiguous() or t_.numel() != params.numel():
+            raise ValueError("adamw: parameter / state size mismatch")
+    ctx.bind_stream()
+    _check(_lib.lib().hc_adamw_step(ctx.h, _p(params), _p(grad), _p(m1), _p(v1), params.numel(), float(lr),
+                                    float(weight_decay), int(step)))
 
 
 def load_upsampler_weights(path) -> dict:

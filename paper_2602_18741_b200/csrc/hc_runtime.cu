@@ -400,6 +400,13 @@ int hc_codec_destroy(hc_codec c) {
   return HC_OK;
 }
 
+int hc_codec_effective_f64(hc_codec c, double* E, double* D) {
+  HC_REQUIRE(c, HC_EINVAL, "null codec");
+  if (E) std::copy(c->Ed.begin(), c->Ed.end(), E);
+  if (D) std::copy(c->Dd.begin(), c->Dd.end(), D);
+  return HC_OK;
+}
+
 int hc_codec_dims(hc_codec c, int* k, int* n) {
   HC_REQUIRE(c, HC_EINVAL, "null codec");
   if (k) *k = c->k;
