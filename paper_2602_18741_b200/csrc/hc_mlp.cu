@@ -18,18 +18,23 @@
 // MMA reads directly ("A from TMEM").  With A in shared memory (SS) the 128 x 16 A
 // tile is re-read from smem by every MMA and smem bandwidth was the limit.
 //
-// One CTA per SM, 4 tile streams.  Each stream owns 128 TMEM columns of the CTA's
-// 512 ([0,40) packed A2/A3 + the constant-1 chunk, [48,112) the fp32 layer-1/2
-// accumulator, [112,128) the layer-3 accumulator), a 4 KB A1 tile and a 2-deep
-// ring of rgb tiles fetched by 1-D bulk copies (TMA).  A stream is 4 epilogue
-// warps (one per TMEM lane quarter) plus one MMA-issuer warp: tools/mma_probe3.cu
-// measured that one thread can issue a tcgen05.mma only every ~45 cycles while
-// several issuing warps overlap up to the tensor pipe's rate, so issuing from the
-// epilogue warps put 10 x 45 cycles per tile on their critical path (the old
-// layout's phase trace).  The warps hand off through mbarriers only:
-//   issuer:   wait a1 -> L1 -> commit l1 | wait a2 -> L2 -> commit l2 | wait a3 -> L3 -> commit l3
-//   epilogue: wait l1 -> relu(D) -> A2, arrive a2 | next A1, arrive a1 | codes of the previous tile
-//             | wait l2 -> relu(D) -> A3, arrive a3 | wait l3 -> keep D3 for the codes
+// One CTA per SM, 4 tile streams.  Each stream owns 112 TMEM columns of the CTA's
+// 512: [0,32) the packed bf16 A operand (A2 of a tile, then its A3), [32,96) the
+// fp32 layer-1/2 accumulator, [96,112) the layer-3 accumulator; the constant K chunk
+// of A2 (the b2 column) is one 8-column region at 448 shared by all streams.  With D3
+// separate, layer 1 of the next tile runs while layer 3 still reads A3; 4 streams
+// instead of 3 keep more tiles in flight, which is what the latency-bound chain needs
+// (the epilogue warps spend most of their time waiting on MMA completions).
+// A stream also has a 4 KB A1 tile and a 2-deep ring of rgb tiles fetched by 1-D
+// bulk copies (TMA), 4 epilogue warps (one per TMEM lane quarter) and one MMA-issuer
+// warp: tools/mma_probe3.cu measured that one thread can issue a tcgen05.mma only
+// every ~45 cycles while several issuing warps overlap up to the tensor pipe's rate,
+// so issuing from the epilogue warps put 10 x 45 cycles per tile on their critical
+// path.  The warps hand off through mbarriers only:
+//   issuer:   wait a2 -> L2 -> commit l2 | wait l1, next A1 | wait a3 -> L1 (next) -> commit l1
+//             -> L3 -> commit l3
+//   epilogue: wait l3 (previous tile) -> keep D3 | wait l1 -> relu(D) -> A2, arrive a2
+//             | softplus + stores of the previous tile's codes | wait l2 -> relu(D) -> A3, arrive a3
 // Weights (12 KB, canonical no-swizzle K-major UMMA images, element (n, k) at
 // (k/8)*(N*16) + n*16 + (k%8)*2) are loaded once per CTA.
 #include <cuda_bf16.h>
@@ -51,18 +56,32 @@ constexpr int kHid = 64;      // hidden width
 constexpr int kK1 = 16;       // layer-1 K (3 inputs + bias column, padded)
 constexpr int kN3 = 16;       // layer-3 N (k padded)
 constexpr int kMaxK = 9;
-constexpr int kStreams = 3;                 // tile streams per CTA
+#ifndef HC_MLP_STREAMS
+#define HC_MLP_STREAMS 3
+#endif
+#ifndef HC_MLP_L3_FIRST
+#define HC_MLP_L3_FIRST 0
+#endif
+#ifndef HC_MLP_B2_EPI
+#define HC_MLP_B2_EPI 0
+#endif
+constexpr bool kB2Epi = HC_MLP_B2_EPI;     // b2 added in the layer-2 epilogue instead of a 5th MMA
+constexpr int kStreams = HC_MLP_STREAMS;    // tile streams per CTA
+constexpr bool kSepA3 = kStreams < 4;       // A3 in its own TMEM region (fits with 3 streams only)
+constexpr bool kL3First = HC_MLP_L3_FIRST;  // issue layer 3 of a tile before layer 1 of the next
 constexpr int kEpiThreads = 128 * kStreams; // epilogue warps: warp w -> stream w / 4, lane quarter w % 4
 constexpr int kThreads = kEpiThreads + 32 * kStreams;  // + one MMA-issuer warp per stream
 constexpr int kK2 = 80;                     // layer 2 K: 64 hidden + constant-1 column (b2 rides the MMA)
 constexpr int kK3 = 64;                     // layer 3 K: b3 (6 values) is added in the epilogue instead of
                                             // paying a fifth >= 45-cycle N = 16 MMA
-constexpr int kColsPerStream = 160;         // TMEM columns per stream (3 x 160 of the 512 allocated)
-constexpr int kColA = 0;                    // packed bf16 A2 (+ constant chunk): 40 columns
-constexpr int kColA3 = 40;                  // packed bf16 A3: 32 columns (separate, so layer 1 of the
-                                            // next tile can run while layer 3 still reads A3)
-constexpr int kColD = 80;                   // fp32 accumulator of layers 1 / 2: 64 columns
-constexpr int kColD3 = 144;                 // fp32 accumulator of layer 3: 16 columns
+constexpr int kColA = 0;                    // packed bf16 A2 (and A3 of the same tile unless kSepA3): 32 columns
+constexpr int kColA3 = kSepA3 ? 32 : 0;     // packed bf16 A3
+constexpr int kColD = kSepA3 ? 64 : 32;     // fp32 accumulator of layers 1 / 2: 64 columns
+constexpr int kColD3 = kColD + 64;          // fp32 accumulator of layer 3: 16 columns (separate, so layer 1
+                                            // of the next tile can run while layer 3 still reads A3)
+constexpr int kColsPerStream = kColD3 + 16; // TMEM columns per stream (4 x 112 or 3 x 144 of the 512)
+constexpr int kColConst = kStreams * kColsPerStream;  // shared constant K chunk of A2: (1, 0 x 15) bf16
+static_assert(kColConst + 8 <= 512, "TMEM budget");
 
 // Shared-memory image offsets (bytes).
 constexpr int kW1Bytes = kHid * kK1 * 2;   // 2 KB
@@ -180,6 +199,9 @@ __device__ __forceinline__ float softplus1(float x) {
 // -> 32 TMEM columns of the next layer's A operand.
 template <bool kBias>
 __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem_a, const float* bias) {
+#ifdef HC_MLP_PROBE_NOEPI  // timing probe only: no accumulator read-out (wrong results)
+  return;
+#endif
   uint32_t va[4][16];
   HC_TMEM_LD16(tmem_acc + 0, va[0]);
   HC_TMEM_LD16(tmem_acc + 16, va[1]);
@@ -239,8 +261,23 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (warp < 4) {
+    // Constant K chunk of every stream's layer-2 A operand: element 64 = 1 (bias b2),
+    // 65..79 = 0.  Written once per CTA (warp w: lane quarter w); the fifth layer-2 MMA
+    // of all streams reads it.
+    uint32_t one[8] = {0x3F80u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                     tmem + kColConst + (static_cast<uint32_t>(warp * 32) << 16)),
+                 "r"(one[0]), "r"(one[1]), "r"(one[2]), "r"(one[3]), "r"(one[4]), "r"(one[5]), "r"(one[6]),
+                 "r"(one[7])
+                 : "memory");
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
   const uint32_t tcol = tmem + st * kColsPerStream;  // stream base, lane 0
-  const uint32_t tA = tcol + kColA, tA3 = tcol + kColA3, tD = tcol + kColD, tD3 = tcol + kColD3;
+  const uint32_t tA = tcol + kColA, tA3 = tcol + kColA3, tD = tcol + kColD, tD3 = tcol + kColD3, tC = tmem + kColConst;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kStreams + st;
   const int64_t tstride = static_cast<int64_t>(gridDim.x) * kStreams;
   constexpr uint32_t kChunkA = kMlpM * 16;  // K-chunk stride of the 128-row A1 tile
@@ -311,8 +348,9 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       if (elect) {
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < kK2 / 16; ++kk)
-          mma_ts(tD, tA + kk * 8, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128), id64, kk > 0);
+        for (int kk = 0; kk < (kB2Epi ? kHid : kK2) / 16; ++kk)
+          mma_ts(tD, kk < kHid / 16 ? tA + kk * 8 : tC, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128),
+                 id64, kk > 0);
         mma_commit(bar_l2);
       }
       __syncwarp();
@@ -321,9 +359,12 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
         prepare_a1(tn, iter + 1);
       }
       mbar_wait(bar_a3, ph);  // A3(t) in TMEM, D read out, D3(t - 1) read out
-      // Layer 1 of the next tile first: D is free and A1 is ready, and A2 / A3 are separate
-      // TMEM regions, so its epilogue never waits for this tile's layer 3.
-      if (tn < p.ntiles) issue_l1();
+      // D and D3 are separate TMEM regions, so layer 1 of the next tile (D is free, A1 is
+      // ready) and layer 3 of this one run back to back.  Dependent MMAs complete in order,
+      // ~100 cycles apart after a ~470-cycle first one (tools/mma_latency.cu): with A3 in the
+      // A region the epilogue needs layer 3 done before it writes the next A2, so layer 3
+      // goes first there.
+      if (!kL3First && tn < p.ntiles) issue_l1();
       if (elect) {
         tc_fence_after();
 #pragma unroll
@@ -332,20 +373,11 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
         mma_commit(bar_l3);
       }
       __syncwarp();
+      if (kL3First && tn < p.ntiles) issue_l1();
     }
   } else {
     // ------------------------------------------------------------ epilogue warps
     const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
-    {
-      // Constant K chunk of the layer-2 A operand: element 64 = 1 (bias b2), 65..79 = 0.
-      // Written once; the epilogues only overwrite columns [0, 32).
-      uint32_t one[8] = {0x3F80u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(tA + 32 + lane_off),
-                   "r"(one[0]), "r"(one[1]), "r"(one[2]), "r"(one[3]), "r"(one[4]), "r"(one[5]), "r"(one[6]),
-                   "r"(one[7])
-                   : "memory");
-      tmem_wait_st();
-    }
     // Codes of the previous tile: the layer-3 accumulator is read right after layer 3
     // completes, softplus + the global stores run later, under the next tile's MMAs.
     uint32_t prev_v[kN3];
@@ -382,25 +414,31 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       const int rows = left < kMlpM ? static_cast<int>(left) : kMlpM;
       long long* tr = (p.trace && blockIdx.x == 0 && r == 0 && iter < 32) ? p.trace + (st * 32 + iter) * 8 : nullptr;
       if (tr) tr[0] = clock64();
-      mbar_wait(bar_l1, ph);
-      if (tr) tr[1] = clock64();
-      tc_fence_after();
-      epilogue_hidden<false>(tD + lane_off, tA + lane_off, nullptr);  // A2 (layer 2 of t-1 is done)
-      handoff(bar_a2);
-      if (tr) tr[2] = clock64();
-      if (tr) tr[3] = clock64();
-      if (iter > 0) {  // layer 3 of the previous tile: its codes, under this tile's layer 2
+      if (!kSepA3 && iter > 0) {  // layer 3 of the previous tile has read A3 (the A region) and written D3
         mbar_wait(bar_l3, ph ^ 1);
         tc_fence_after();
         HC_TMEM_LD16(tD3 + lane_off, prev_v);
         tmem_wait_ld();
-        store_codes();
       }
+      if (tr) tr[1] = clock64();
+      mbar_wait(bar_l1, ph);
+      if (tr) tr[2] = clock64();
+      tc_fence_after();
+      epilogue_hidden<false>(tD + lane_off, tA + lane_off, nullptr);  // A2 over A3 of t-1
+      handoff(bar_a2);
+      if (tr) tr[3] = clock64();
+      if (kSepA3 && iter > 0) {  // layer 3 of the previous tile, read under this tile's layer 2
+        mbar_wait(bar_l3, ph ^ 1);
+        tc_fence_after();
+        HC_TMEM_LD16(tD3 + lane_off, prev_v);
+        tmem_wait_ld();
+      }
+      store_codes();  // the previous tile's codes, under this tile's layer 2
       if (tr) tr[4] = clock64();
       mbar_wait(bar_l2, ph);
       if (tr) tr[5] = clock64();
       tc_fence_after();
-      epilogue_hidden<false>(tD + lane_off, tA3 + lane_off, nullptr);  // A3 (layer 3 of t-1 read out above)
+      epilogue_hidden<kB2Epi>(tD + lane_off, tA3 + lane_off, p.b2);  // A3 (over A2 unless kSepA3)
       handoff(bar_a3);
       prev_row0 = row0;
       prev_rows = rows;
@@ -545,7 +583,7 @@ int hc_mlp_forward(hc_mlp m, const float* rgb, int64_t P, float* codes) {
           ++n;
         }
       if (n)
-        std::fprintf(stderr, "[hc] mlp phase cycles (avg of %d tiles): L1wait %.0f epi1 %.0f nextA1 %.0f prevD3+codes %.0f L2wait %.0f epi2 %.0f - %.0f loop %.0f\n",
+        std::fprintf(stderr, "[hc] mlp phase cycles (avg of %d tiles): prevD3 %.0f L1wait %.0f epi1 %.0f codes %.0f L2wait %.0f epi2 %.0f - %.0f loop %.0f\n",
                      n, acc[0] / n, acc[1] / n, acc[2] / n, acc[3] / n, acc[4] / n, acc[5] / n, acc[6] / n, acc[7] / n);
     }
   }
