@@ -40,12 +40,14 @@ __device__ __forceinline__ void mma(bool ts, uint32_t tD, uint32_t tA, uint64_t 
 __global__ void probe(int mode, int ts, int N, int nmma, int R, long long* out) {
   extern __shared__ __align__(1024) unsigned char sm[];
   __shared__ uint64_t bar[2];
+  __shared__ uint64_t wbar[8];
   __shared__ uint32_t slot;
   const int tid = threadIdx.x, warp = tid >> 5;
   for (int i = tid; i < 48 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u;
   if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[0])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(smem_u32(&bar[1])));
+    for (int w = 0; w < 8; ++w) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&wbar[w])));
     asm volatile("fence.mbarrier_init.release.cluster;");
   }
   if (warp == 0) {
@@ -70,6 +72,17 @@ __global__ void probe(int mode, int ts, int N, int nmma, int R, long long* out) 
         asm volatile("tcgen05.fence::after_thread_sync;");
       }
     }
+  } else if (mode == 4) {  // W = nmma >> 8 warps, each (nmma & 255) MMAs + commit + wait, R times
+    const int W = nmma >> 8, n = nmma & 255;
+    if (warp < W && (tid & 31) == 0) {
+      for (int i = 0; i < R; ++i) {
+        for (int j = 0; j < n; ++j) mma(ts, tmem + 128 + warp * 64, tmem + j * 8, ad, bd, id, j > 0);
+        commit(&wbar[warp]);
+        wait_bar(&wbar[warp], i & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+      }
+    }
+    __syncthreads();
   } else if (mode == 1 || mode == 2) {
     if (warp < 4) {
       uint32_t v[16];
@@ -175,5 +188,13 @@ int main() {
   run("ping-pong SS N=64 x1 -> ld64/st32 -> arrive", 3, 0, 64, 1);
   run("ping-pong TS N=64 x5 -> ld64/st32 -> arrive", 3, 1, 64, 5);
   run("ping-pong TS N=16 x4 -> ld64/st32 -> arrive", 3, 1, 16, 4);
+  // mode 4: is a commit round trip a per-warp latency or a per-SM serialising cost?
+  const int ns[3] = {1, 2, 5};
+  for (int w = 1; w <= 4; w *= 2)
+    for (int q = 0; q < 3; ++q) {
+      char name[64];
+      snprintf(name, sizeof name, "%d warps x (TS N=64 x%d + commit + wait)", w, ns[q]);
+      run(name, 4, 1, 64, (w << 8) | ns[q]);
+    }
   return 0;
 }
