@@ -758,6 +758,19 @@ def run_ours(args) -> int:
         ms = float(t.item())
     launches_timed = per_step * steps  # graph replays do not pass through the host counter
     ms_per_step = ms / steps
+    # Per-replay distribution (after the timed region, so it does not perturb it): each
+    # graph replay (n_in_graph steps) bracketed by its own events.
+    nrep = max(8, min(64, steps // n_in_graph))
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(nrep + 1)]
+    with torch.cuda.stream(stream):
+        evs[0].record(stream)
+        for j in range(nrep):
+            g.replay()
+            evs[j + 1].record(stream)
+    torch.cuda.synchronize()
+    per = np.array([evs[j].elapsed_time(evs[j + 1]) / n_in_graph for j in range(nrep)])
+    dist_ms = {"p10": float(np.percentile(per, 10)), "p50": float(np.median(per)),
+               "p90": float(np.percentile(per, 90)), "replays": nrep, "steps_per_replay": n_in_graph}
     value = wl.units * world * steps / (ms / 1e3) / 1e6
 
     pk = peaks()
@@ -871,6 +884,9 @@ def run_ours(args) -> int:
         try:
             cpu = cpu_reference_run(args.config, budget_s=args.cpu_seconds)
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "seconds", "cpu")}
+            if cpu["cores"] > 1:  # the single-thread rate beside the all-core one
+                one = cpu_reference_run(args.config, budget_s=max(2.0, args.cpu_seconds / 4), threads=1)
+                cpu["single_thread_value"] = one["value"]
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": cfg["unit"], "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
@@ -896,6 +912,7 @@ def run_ours(args) -> int:
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches_timed),
+            "ms_per_step_dist": dist_ms,
             "clocks": clocks.summary(),
             "wall_s_timed": t_wall,
         }
