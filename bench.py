@@ -871,13 +871,41 @@ def run_ours(args) -> int:
             t = torch.tensor([el], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        e2e = {"value": P * world * esteps / el / 1e6, "unit": cfg["unit"],
-               "h2d_bytes_per_step": int(h_idx.numel() * 4 + h_cos.numel() * 4 + h_pal.nbytes),
-               "d2h_bytes_per_step": int(h_xyz.numel() * 4 + h_rgb.numel() * 4), "ms_per_step": el / esteps * 1e3,
-               "api": "hc_shade_latent_host (pinned host buffers)"}
-        # parity spot check of the e2e result against the device path
+        single = {"value": P * world * esteps / el / 1e6, "ms_per_step": el / esteps * 1e3,
+                  "api": "hc_shade_latent_host, one synchronous call per frame"}
+        # parity spot check of the single-frame e2e result against the device path
         dev_rgb = wl.sets[0][2]["rgb"].cpu().numpy()
         extra["e2e_matches_device"] = bool(np.array_equal(dev_rgb, nr))
+        # Frame stream: the same frames through hc_shade_latent_host_frames (one pipeline
+        # across frames: frame f + 1's uploads overlap frame f's downloads).  Two pinned
+        # input / output sets alternate (frames 2j and 2j + 1 differ); every frame's H2D of
+        # its G-buffer and D2H of its XYZ + sRGB are inside the timed region.
+        idx1, cosv1, _ = wl.sets[1]
+        h_idx1 = torch.empty(P, dtype=torch.int32, pin_memory=True)
+        h_cos1 = torch.empty(P, cfg["L"], pin_memory=True)
+        h_idx1.copy_(idx1)
+        h_cos1.copy_(cosv1)
+        h_xyz1 = torch.empty(P, 3, pin_memory=True)
+        h_rgb1 = torch.empty(P, 3, pin_memory=True)
+        sets_h = [(ni, nc, nx, nr), (h_idx1.numpy(), h_cos1.numpy(), h_xyz1.numpy(), h_rgb1.numpy())]
+        frames = [sets_h[f % 2] for f in range(esteps)]
+        with torch.cuda.stream(stream):
+            wl.codec.shade_latent_host_frames(h_pal, wl.light_codes, frames[:4])
+            barrier()
+            t0 = time.perf_counter()
+            wl.codec.shade_latent_host_frames(h_pal, wl.light_codes, frames)
+            el2 = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([el2], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            el2 = float(t.item())
+        extra["e2e_stream_matches_device"] = bool(
+            np.array_equal(wl.sets[1][2]["rgb"].cpu().numpy(), sets_h[1][3]) and np.array_equal(dev_rgb, nr))
+        e2e = {"value": P * world * esteps / el2 / 1e6, "unit": cfg["unit"],
+               "h2d_bytes_per_step": int(h_idx.numel() * 4 + h_cos.numel() * 4),
+               "d2h_bytes_per_step": int(h_xyz.numel() * 4 + h_rgb.numel() * 4), "ms_per_step": el2 / esteps * 1e3,
+               "api": f"hc_shade_latent_host_frames (pinned host buffers, {esteps} frames per call)",
+               "single_frame": single}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the contract: rank 0 at N = 1 only

@@ -373,6 +373,15 @@ int hc_adamw_step(hc_ctx ctx, double* params, const double* grad, double* m1, do
 int hc_shade_latent_host(hc_codec codec, const float* pal_codes, int n_pal, const float* light_codes,
                          int L, const uint32_t* idx, const float* cosv, int64_t P, float* xyz,
                          float* rgb);
+/* A sequence of frames of the same scene (one palette / light table, per-frame G-buffers
+ * idx[f], cosv[f] and outputs xyz[f], rgb[f], all host, each P pixels): one copy / compute
+ * pipeline across all frames (frame f + 1's uploads overlap frame f's downloads), so a
+ * frame stream runs at the PCIe rate instead of paying pipeline fill / drain per frame.
+ * Outputs are identical to nframes hc_shade_latent_host calls.  xyz[f] / rgb[f] may be
+ * NULL (not computed / copied). */
+int hc_shade_latent_host_frames(hc_codec codec, const float* pal_codes, int n_pal, const float* light_codes,
+                                int L, int nframes, const uint32_t* const* idx, const float* const* cosv,
+                                int64_t P, float* const* xyz, float* const* rgb);
 int hc_roundtrip_host(hc_codec codec, const float* S, int64_t rows, float* Z, float* S2, float* xyz,
                       float* rgb);
 

@@ -77,6 +77,7 @@ SIGNATURES: dict[str, tuple] = {
     "hc_render": (i32, [vp, vp, vp, vp, vp, vp, vp]),
     "hc_render_latent_multipass": (i32, [vp, vp, vp, vp, vp, vp]),
     "hc_shade_latent_host": (i32, [vp, vp, i32, vp, i32, vp, vp, i64, vp, vp]),
+    "hc_shade_latent_host_frames": (i32, [vp, vp, i32, vp, i32, i32, vp, vp, i64, vp, vp]),
     "hc_roundtrip_host": (i32, [vp, vp, i64, vp, vp, vp, vp]),
     "hc_stream_key": (u64, [u64, C.c_char_p]),
     "hc_synth_gm_spectra": (i32, [vp, u64, i64, i64, i32, f64, f64, vp]),

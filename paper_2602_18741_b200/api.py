@@ -292,6 +292,28 @@ class Codec:
                                                lc.shape[0], _np_ptr(idx), _np_ptr(cosv), idx.size, _np_ptr(xyz),
                                                _np_ptr(rgb)))
 
+    def shade_latent_host_frames(self, pal_codes: np.ndarray, light_codes: np.ndarray, frames) -> None:
+        """A frame stream through one host-buffer pipeline (hc_shade_latent_host_frames).
+
+        frames: sequence of (idx, cosv, xyz, rgb) host arrays of P pixels each (xyz / rgb may be
+        None); outputs are identical to one shade_latent_host call per frame."""
+        import ctypes as C
+
+        lc = np.ascontiguousarray(light_codes, dtype=np.float32)
+        nf = len(frames)
+        if nf == 0:
+            return
+        P = frames[0][0].size
+        for f in frames:
+            if f[0].size != P or f[1].size != P * lc.shape[0]:
+                raise ValueError("all frames must have P pixels and L cos terms per pixel")
+        tab = [(C.c_void_p * nf)(*[(_np_ptr(f[j]) if f[j] is not None else None) for f in frames])
+               for j in range(4)]
+        self.ctx.bind_stream()
+        _check(_lib.lib().hc_shade_latent_host_frames(self.h, _np_ptr(pal_codes), pal_codes.shape[0], _np_ptr(lc),
+                                                      lc.shape[0], nf, C.addressof(tab[0]), C.addressof(tab[1]), P,
+                                                      C.addressof(tab[2]), C.addressof(tab[3])))
+
     def roundtrip_host(self, S: np.ndarray, Z: Optional[np.ndarray] = None, S2: Optional[np.ndarray] = None,
                        xyz: Optional[np.ndarray] = None, rgb: Optional[np.ndarray] = None) -> None:
         """Host-buffer round trip (encode -> decode_image -> image_to_linear_rgb); outputs may be None."""

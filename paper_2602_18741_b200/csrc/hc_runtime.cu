@@ -549,52 +549,78 @@ int hc_hadamard_loss(hc_codec c, const float* A, const float* B, int64_t pairs, 
 }
 
 // ------------------------------------------------------------------ host-buffer entry points
-// Pipelined host-buffer call: chunk i's H2D copies, chunk i-1's kernel and chunk
-// i-2's D2H copies overlap on hc_ctx_s::kAux streams (round robin).  Measured on the
-// B200 host (tools/e2e_sweep.sh): 256K-pixel chunks (8 per 1080p
-// frame) balance the ~4 us per-copy cost against pipeline fill / drain; role streams
-// (all H2D on one stream, all D2H on another), a ramped chunk schedule, and letting
-// the kernel write pinned outputs over PCIe (zero copy) all measured slower.
-int hc_shade_latent_host(hc_codec c, const float* pal_codes, int n_pal, const float* light_codes, int L,
-                         const uint32_t* idx, const float* cosv, int64_t P, float* xyz, float* rgb) {
-  int rc = check_shade_args(c, pal_codes, n_pal, light_codes, L, idx, cosv, P);
-  if (rc != HC_OK) return rc;
-  if (P == 0) return HC_OK;
+// Pipelined host-buffer calls: every frame is cut into 256K-pixel chunks, and chunk i
+// (counted across all frames of the call) runs H2D copies -> kernel -> D2H copies on
+// aux stream i % kAux with device slot i % kAux, so chunk i's H2D, chunk i-1's kernel
+// and chunk i-2's D2H overlap, and stream order alone orders each slot's reuse.
+// Measured on the B200 host (tools/e2e_sweep.sh): 256K-pixel chunks
+// balance the ~4 us per-copy cost against pipeline fill / drain; role streams (all H2D
+// on one stream, all D2H on another), a ramped chunk schedule and letting the kernel
+// write pinned outputs over PCIe (zero copy) all measured slower.  With several frames
+// per call the pipeline does not drain between frames: frame f + 1's first uploads
+// run under frame f's last downloads.
+int hc_shade_latent_host_frames(hc_codec c, const float* pal_codes, int n_pal, const float* light_codes, int L,
+                                int nframes, const uint32_t* const* idx, const float* const* cosv, int64_t P,
+                                float* const* xyz, float* const* rgb) {
+  HC_REQUIRE(c, HC_EINVAL, "null codec");
+  HC_REQUIRE(nframes >= 0, HC_EINVAL, "shade_latent_host_frames: negative frame count");
+  HC_REQUIRE(nframes == 0 || (idx && cosv && xyz && rgb), HC_EINVAL, "shade_latent_host_frames: null frame table");
+  for (int f = 0; f < nframes; ++f) {
+    int rc = check_shade_args(c, pal_codes, n_pal, light_codes, L, idx[f], cosv[f], P);
+    if (rc != HC_OK) return rc;
+  }
+  if (P == 0 || nframes == 0) return HC_OK;
   hc_ctx ctx = c->ctx;
+  static const int64_t kChunk = [] {  // pixels (multiple of every tile size); HC_HOST_CHUNK: tuning only
+    const char* e = std::getenv("HC_HOST_CHUNK");
+    const int64_t v = e ? std::atoll(e) : 0;
+    return v >= 4096 && v % 4096 == 0 ? v : int64_t(262144);
+  }();
+  constexpr int kSlots = hc_ctx_s::kAux;
+  const int64_t cp = P < kChunk ? P : kChunk;
   const size_t pal_b = sizeof(float) * n_pal * c->k;
-  const size_t idx_b = sizeof(uint32_t) * P, cos_b = sizeof(float) * P * L, out_b = sizeof(float) * P * 3;
   auto up = [](size_t b) { return (b + 255) & ~size_t(255); };
-  rc = ensure_scratch(ctx, up(pal_b) + up(idx_b) + up(cos_b) + 2 * up(out_b));
+  const size_t idx_b = up(sizeof(uint32_t) * cp), cos_b = up(sizeof(float) * cp * L), out_b = up(sizeof(float) * cp * 3);
+  const size_t slot_b = idx_b + cos_b + 2 * out_b;
+  int rc = ensure_scratch(ctx, up(pal_b) + kSlots * slot_b);
   if (rc != HC_OK) return rc;
   rc = ensure_aux_streams(ctx);
   if (rc != HC_OK) return rc;
   char* base = static_cast<char*>(ctx->scratch);
   float* d_pal = reinterpret_cast<float*>(base);
-  uint32_t* d_idx = reinterpret_cast<uint32_t*>(base + up(pal_b));
-  float* d_cos = reinterpret_cast<float*>(base + up(pal_b) + up(idx_b));
-  float* d_xyz = reinterpret_cast<float*>(base + up(pal_b) + up(idx_b) + up(cos_b));
-  float* d_rgb = reinterpret_cast<float*>(base + up(pal_b) + up(idx_b) + up(cos_b) + up(out_b));
   HC_CUDA_TRY(cudaMemcpyAsync(d_pal, pal_codes, pal_b, cudaMemcpyHostToDevice, ctx->stream));
   HC_CUDA_TRY(cudaEventRecord(ctx->ev_fork, ctx->stream));
   for (auto st : ctx->aux) HC_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_fork, 0));
-  constexpr int64_t kChunk = 262144;  // pixels (multiple of every tile size)
   cudaStream_t home = ctx->stream;
-  int ci = 0;
-  for (int64_t p0 = 0; p0 < P; p0 += kChunk, ++ci) {
-    const int64_t n = P - p0 < kChunk ? P - p0 : kChunk;
-    cudaStream_t st = ctx->aux[ci % hc_ctx_s::kAux];
-    HC_CUDA_TRY(cudaMemcpyAsync(d_idx + p0, idx + p0, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
-    HC_CUDA_TRY(cudaMemcpyAsync(d_cos + p0 * L, cosv + p0 * L, sizeof(float) * n * L, cudaMemcpyHostToDevice, st));
-    ctx->stream = st;
-    rc = shade_latent_launch(c, d_pal, n_pal, light_codes, L, d_idx + p0, d_cos + p0 * L, n, nullptr, nullptr,
-                             xyz ? d_xyz + p0 * 3 : nullptr, rgb ? d_rgb + p0 * 3 : nullptr);
-    ctx->stream = home;
-    if (rc != HC_OK) return rc;
-    if (xyz) HC_CUDA_TRY(cudaMemcpyAsync(xyz + p0 * 3, d_xyz + p0 * 3, sizeof(float) * n * 3, cudaMemcpyDeviceToHost, st));
-    if (rgb) HC_CUDA_TRY(cudaMemcpyAsync(rgb + p0 * 3, d_rgb + p0 * 3, sizeof(float) * n * 3, cudaMemcpyDeviceToHost, st));
+  int64_t ci = 0;
+  for (int f = 0; f < nframes; ++f) {
+    for (int64_t p0 = 0; p0 < P; p0 += kChunk, ++ci) {
+      const int64_t n = P - p0 < kChunk ? P - p0 : kChunk;
+      const int s = static_cast<int>(ci % kSlots);
+      cudaStream_t st = ctx->aux[ci % hc_ctx_s::kAux];
+      char* slot = base + up(pal_b) + s * slot_b;
+      uint32_t* d_idx = reinterpret_cast<uint32_t*>(slot);
+      float* d_cos = reinterpret_cast<float*>(slot + idx_b);
+      float* d_xyz = reinterpret_cast<float*>(slot + idx_b + cos_b);
+      float* d_rgb = reinterpret_cast<float*>(slot + idx_b + cos_b + out_b);
+      HC_CUDA_TRY(cudaMemcpyAsync(d_idx, idx[f] + p0, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, st));
+      HC_CUDA_TRY(cudaMemcpyAsync(d_cos, cosv[f] + p0 * L, sizeof(float) * n * L, cudaMemcpyHostToDevice, st));
+      ctx->stream = st;
+      rc = shade_latent_launch(c, d_pal, n_pal, light_codes, L, d_idx, d_cos, n, nullptr, nullptr,
+                               xyz[f] ? d_xyz : nullptr, rgb[f] ? d_rgb : nullptr);
+      ctx->stream = home;
+      if (rc != HC_OK) return rc;
+      if (xyz[f]) HC_CUDA_TRY(cudaMemcpyAsync(xyz[f] + p0 * 3, d_xyz, sizeof(float) * n * 3, cudaMemcpyDeviceToHost, st));
+      if (rgb[f]) HC_CUDA_TRY(cudaMemcpyAsync(rgb[f] + p0 * 3, d_rgb, sizeof(float) * n * 3, cudaMemcpyDeviceToHost, st));
+    }
   }
   for (auto st : ctx->aux) HC_CUDA_TRY(cudaStreamSynchronize(st));
   return hc_ctx_synchronize(ctx);
+}
+
+int hc_shade_latent_host(hc_codec c, const float* pal_codes, int n_pal, const float* light_codes, int L,
+                         const uint32_t* idx, const float* cosv, int64_t P, float* xyz, float* rgb) {
+  return hc_shade_latent_host_frames(c, pal_codes, n_pal, light_codes, L, 1, &idx, &cosv, P, &xyz, &rgb);
 }
 
 int hc_roundtrip_host(hc_codec c, const float* S, int64_t rows, float* Z, float* S2, float* xyz, float* rgb) {

@@ -236,6 +236,26 @@ def test_shade_latent_host_buffers(api, ctx, k, L, P, pinned):
     assert np.array_equal(xyz, host(dev["xyz"])) and np.array_equal(rgb, host(dev["rgb"]))
 
 
+@pytest.mark.parametrize("k,L,P,nf", [(6, 8, 600_011, 3), (9, 32, 65_536, 5), (3, 5, 999, 4), (6, 8, 262_144, 1)])
+def test_shade_latent_host_frames(api, ctx, k, L, P, nf):
+    """hc_shade_latent_host_frames: one pipeline across a frame stream (chunk slots reused
+    across frame boundaries, ragged last chunk, frames of different G-buffers, a frame
+    without xyz) == one device-resident call per frame, bit for bit."""
+    codec, E, D, pal, lts, pal_d, pal_codes, light_codes = _scene(api, ctx, k, L)
+    frames, want = [], []
+    for f in range(nf):
+        idx, cosv = api.synth_gbuffer(ctx, SEED + f, 7 * f, P, L, 256)
+        dev = codec.shade_latent(pal_codes, light_codes, idx, cosv)
+        want.append((host(dev["xyz"]), host(dev["rgb"])))
+        xyz = None if (f == 1 and nf > 1) else torch.zeros(P, 3).pin_memory().numpy()
+        frames.append((host(idx).view(np.uint32), host(cosv), xyz, torch.zeros(P, 3).pin_memory().numpy()))
+    codec.shade_latent_host_frames(host(pal_codes), light_codes, frames)
+    for f in range(nf):
+        if frames[f][2] is not None:
+            assert np.array_equal(frames[f][2], want[f][0]), f"frame {f} xyz"
+        assert np.array_equal(frames[f][3], want[f][1]), f"frame {f} rgb"
+
+
 def test_roundtrip_host_buffers(api, ctx, orc):
     codec, E, D = _codec(api, ctx, 6)
     rows = 20_001
