@@ -319,6 +319,12 @@ struct ShadedFrame {
 // as compile_scene does, renderer.cpp:201-225).
 ShadedFrame shade_latent(const Codec& c, const std::vector<float>& palette_codes,
                          const std::vector<float>& light_codes, const GBuffer& g);
+// A stream of frames of one scene through the host-buffer pipeline
+// (hc_shade_latent_host_frames): xyz and linear_rgb of every frame (latent left empty),
+// identical to shade_latent frame by frame.
+std::vector<ShadedFrame> shade_latent_frames(const Codec& c, const std::vector<float>& palette_codes,
+                                             const std::vector<float>& light_codes,
+                                             const std::vector<GBuffer>& frames);
 // Naive n-sample path on the same G-buffer (palette_spectra n_pal x n, light_spectra L x n).
 ShadedFrame shade_spectral(const Codec& c, const std::vector<float>& palette_spectra,
                            const std::vector<float>& light_spectra, const GBuffer& g);

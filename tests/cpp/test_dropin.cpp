@@ -223,6 +223,21 @@ int main() {
     }
     CHECK(std::isfinite(nf.xyz.data[p * 3 + 1]) && nf.xyz.data[p * 3 + 1] >= 0.f);
   }
+  {  // frame stream through the host pipeline == frame by frame
+    GBuffer gb2 = gb;
+    for (float& x : gb2.cos_terms) x = 1.f - x;
+    const std::vector<ShadedFrame> fs = shade_latent_frames(codec, pal_codes, light_codes, {gb, gb2, gb});
+    const ShadedFrame lf2 = shade_latent(codec, pal_codes, light_codes, gb2);
+    CHECK(fs.size() == 3u);
+    CHECK(fs[0].xyz.data == lf.xyz.data && fs[0].linear_rgb.data == lf.linear_rgb.data);
+    CHECK(fs[1].xyz.data == lf2.xyz.data && fs[1].linear_rgb.data == lf2.linear_rgb.data);
+    CHECK(fs[2].linear_rgb.data == lf.linear_rgb.data);
+    GBuffer small = gb;
+    small.width = 8;
+    small.palette_index.resize(64);
+    small.cos_terms.resize(64 * 8);
+    CHECK_THROWS_AS(shade_latent_frames(codec, pal_codes, light_codes, {gb, small}), std::invalid_argument);
+  }
   gb.palette_index[3] = 77;  // out of range of the 4-entry palette
   CHECK_THROWS_AS(shade_latent(codec, pal_codes, light_codes, gb), std::invalid_argument);
 
