@@ -46,8 +46,8 @@ __global__ void __launch_bounds__(256) chain_latent_kernel(const __grid_constant
   extern __shared__ __align__(16) float tab[];
   float* pal = tab;
   float* ill = tab + p.n_pal * K;
-  for (int i = threadIdx.x; i < p.n_pal * K; i += blockDim.x) pal[i] = p.pal[i];
-  for (int i = threadIdx.x; i < p.n_ill * K; i += blockDim.x) ill[i] = p.ill[i];
+  block_load_table(pal, p.pal, p.n_pal * K);
+  block_load_table(ill, p.ill, p.n_ill * K);
   __syncthreads();
 
   const int lane = threadIdx.x & 31;
@@ -137,13 +137,22 @@ __global__ void __launch_bounds__(256) chain_latent_rep_kernel(const __grid_cons
   constexpr int KP = (K + 1) / 2;  // float2 per code
   extern __shared__ __align__(16) float2 rep[];
   const int n_ent = p.n_pal + p.n_ill;
-  for (int i = threadIdx.x; i < n_ent * KP * 16; i += blockDim.x) {
-    const int q = i >> 4;
-    const int e = q / KP, c2 = q - e * KP;
-    const float* src = e < p.n_pal ? p.pal + e * K : p.ill + (e - p.n_pal) * K;
-    const float lo = src[2 * c2];
-    const float hi = 2 * c2 + 1 < K ? src[2 * c2 + 1] : 0.f;
-    rep[i] = make_float2(lo, hi);
+  constexpr int R = 8;  // loads in flight per thread before its stores (block_load_table)
+  for (int base = threadIdx.x; base < n_ent * KP * 16; base += R * blockDim.x) {
+    float2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = base + r * blockDim.x;
+      if (i < n_ent * KP * 16) {
+        const int q = i >> 4;
+        const int e = q / KP, c2 = q - e * KP;
+        const float* src = e < p.n_pal ? p.pal + e * K : p.ill + (e - p.n_pal) * K;
+        v[r] = make_float2(__ldg(src + 2 * c2), 2 * c2 + 1 < K ? __ldg(src + 2 * c2 + 1) : 0.f);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (base + r * blockDim.x < n_ent * KP * 16) rep[base + r * blockDim.x] = v[r];
   }
   __syncthreads();
 
@@ -292,8 +301,8 @@ __global__ void __launch_bounds__(256) chain_spectral_kernel(const __grid_consta
   extern __shared__ __align__(16) float tab[];
   float* pal = tab;
   float* ill = tab + p.n_pal * N;
-  for (int i = threadIdx.x; i < p.n_pal * N; i += blockDim.x) pal[i] = p.pal[i];
-  for (int i = threadIdx.x; i < p.n_ill * N; i += blockDim.x) ill[i] = p.ill[i];
+  block_load_table(pal, p.pal, p.n_pal * N);
+  block_load_table(ill, p.ill, p.n_ill * N);
   __syncthreads();
 
   const int lane = threadIdx.x & 31;

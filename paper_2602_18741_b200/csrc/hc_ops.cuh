@@ -216,8 +216,10 @@ struct ShadeLatentOp {
     return k == kOutXyz ? p.xyz : (k == kOutRgb ? p.rgb : (k == kOutLatent ? p.latent : p.spectra));
   }
   __device__ static void setup(const Params& p, unsigned char* extra) {
-    float* pal = reinterpret_cast<float*>(extra);
-    for (int i = threadIdx.x; i < p.n_pal * K; i += blockDim.x) pal[i] = p.pal_codes[i];
+#ifdef HC_PROBE_NO_PAL_COPY  // timing probe only: palette left uninitialised (wrong results)
+    return;
+#endif
+    block_load_table(reinterpret_cast<float*>(extra), p.pal_codes, p.n_pal * K);
   }
   __device__ static void finish(const Params&, State&, unsigned char*) {}
 
@@ -326,8 +328,7 @@ struct ShadeSpectralOp {
     return i == 0 ? p.xyz : (i == 1 ? p.rgb : p.spectra);
   }
   __device__ static void setup(const Params& p, unsigned char* extra) {
-    float* pal = reinterpret_cast<float*>(extra);
-    for (int i = threadIdx.x; i < p.n_pal * N; i += blockDim.x) pal[i] = p.pal_spectra[i];
+    block_load_table(reinterpret_cast<float*>(extra), p.pal_spectra, p.n_pal * N);
   }
   __device__ static void finish(const Params&, State&, unsigned char*) {}
 

@@ -41,8 +41,8 @@ struct GenericLatentParams {
 
 template <int N, int K>
 __global__ void __launch_bounds__(256) shade_latent_generic_kernel(const __grid_constant__ GenericLatentParams<N, K> p) {
-  __shared__ float pal[kMaxPalette * K];
-  for (int i = threadIdx.x; i < p.n_pal * K; i += blockDim.x) pal[i] = p.pal[i];
+  __shared__ __align__(16) float pal[kMaxPalette * K];
+  block_load_table(pal, p.pal, p.n_pal * K);
   __syncthreads();
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t px = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; px < p.P; px += stride) {
