@@ -251,7 +251,10 @@ int shade_latent_launch(hc_codec c, const float* pal, int n_pal, const float* li
 template <int N, int L, bool SPEC>
 int shade_spectral_nl(hc_codec c, const float* pal, int n_pal, const float* light, const uint32_t* idx,
                       const float* cosv, int64_t P, float* spectra, float* xyz, float* rgb) {
-  constexpr int T = SPEC ? 64 : 128;
+#ifndef HC_NAIVE_T
+#define HC_NAIVE_T 256  // measured: 128 -> 256 threads per CTA +9.5 % (tools/sweep_naive.sh)
+#endif
+  constexpr int T = SPEC ? 64 : HC_NAIVE_T;
   using Op = ShadeSpectralOp<N, L, SPEC, T, T, 2>;
   typename Op::Params p;
   for (int i = 0; i < L * N; ++i) p.light[i] = light[i];

@@ -1,0 +1,5 @@
+# Naive n=81 shading (config 2 naive leg) over tools/bin/libhc_naive_*.so
+for lib in paper_2602_18741_b200/libhadacodec_b200.so tools/bin/libhc_naive_*.so; do
+  HC_LIB=$lib timeout 200 python bench.py --config 2 --no-cpu-baseline --steps 400 > gpurun_out/sw.log 2>&1
+  echo "$lib $(tail -1 gpurun_out/sw.log | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(round(d["value"]), round(d["naive_n81"]["value"]))')"
+done
