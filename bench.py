@@ -913,7 +913,17 @@ def run_ours(args) -> int:
             cpu = cpu_reference_run(args.config, budget_s=args.cpu_seconds)
             cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "seconds", "cpu")}
             if cpu["cores"] > 1:  # the single-thread rate beside the all-core one
-                one = cpu_reference_run(args.config, budget_s=max(2.0, args.cpu_seconds / 4), threads=1)
+                # (config 7 runs the reference's own render thread pool, sized by
+                # HADACODEC_THREADS, renderer.cpp:615-621)
+                old = os.environ.get("HADACODEC_THREADS")
+                os.environ["HADACODEC_THREADS"] = "1"
+                try:
+                    one = cpu_reference_run(args.config, budget_s=max(2.0, args.cpu_seconds / 4), threads=1)
+                finally:
+                    if old is None:
+                        os.environ.pop("HADACODEC_THREADS", None)
+                    else:
+                        os.environ["HADACODEC_THREADS"] = old
                 cpu["single_thread_value"] = one["value"]
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": cfg["unit"], "cores": 0, "kind": "reference",
