@@ -188,7 +188,11 @@ struct ShadeLatentOp {
   // Pipeline choice (measured, profiles/README.md): the spectra-writing variant runs the
   // warp-specialised pipeline (78 -> 85 % HBM); the small-output variant streams its
   // inputs with an L2 evict-first policy (80 -> 81 %).
+#ifdef HC_C2_WS  // tuning only: force the warp-specialised pipeline for every output set
+  static constexpr bool kWarpSpecialized = true;
+#else
   static constexpr bool kWarpSpecialized = (OUTS & kOutSpectra) != 0;
+#endif
   static constexpr bool kEvictFirstLoads = (OUTS & kOutSpectra) == 0;
 
   struct Params {

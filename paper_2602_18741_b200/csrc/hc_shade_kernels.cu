@@ -15,7 +15,7 @@
 #define HC_C2_THREADS 256
 #endif
 #ifndef HC_C2_STAGES
-#define HC_C2_STAGES 3
+#define HC_C2_STAGES 4
 #endif
 
 namespace hcb {
