@@ -14,6 +14,12 @@
 #ifndef HC_C2_THREADS
 #define HC_C2_THREADS 256
 #endif
+#ifndef HC_SPEC_T  // spectra-writing variants (config 3)
+#define HC_SPEC_T 64
+#endif
+#ifndef HC_SPEC_STAGES
+#define HC_SPEC_STAGES 2
+#endif
 #ifndef HC_C2_STAGES
 #define HC_C2_STAGES 4
 #endif
@@ -195,9 +201,9 @@ int shade_latent_nkl(hc_codec c, const float* pal, int n_pal, const float* light
                      float* rgb) {
   constexpr bool SPEC = (OUTS & kOutSpectra) != 0;
   constexpr bool C2 = L == 8 && OUTS == (kOutXyz | kOutRgb);
-  constexpr int T = SPEC ? 64 : (C2 ? HC_C2_T : 256);
+  constexpr int T = SPEC ? HC_SPEC_T : (C2 ? HC_C2_T : 256);
   constexpr int THREADS = C2 ? HC_C2_THREADS : T;
-  constexpr int STAGES = SPEC ? 2 : (C2 ? HC_C2_STAGES : 3);
+  constexpr int STAGES = SPEC ? HC_SPEC_STAGES : (C2 ? HC_C2_STAGES : 3);
   using Op = ShadeLatentOp<N, K, L, OUTS, T, THREADS, STAGES>;
   typename Op::Params p;
   fill_codec_const<N, K>(c, &p.cc);
