@@ -398,10 +398,10 @@ def run_reference_arm(args) -> int:
         return 0
     cfg = CONFIGS[args.config]
     # calibrate one step, then time K steps of the bounded sample
-    cal = cpu_reference_run(args.config, budget_s=0.0)
+    cal = cpu_reference_run(args.config, budget_s=0.0)  # warm-up step 1 (also the calibration)
     per_step = cal["step_s"]
-    for _ in range(args.warmup):
-        pass
+    for _ in range(max(0, args.warmup - 1)):  # the remaining untimed warm-up steps
+        cpu_reference_run(args.config, budget_s=0.0)
     res = cpu_reference_run(args.config, budget_s=max(per_step * args.steps, 1.0))
     line = {"metric": METRIC if args.config == "2" else f"{cfg['unit']} config {args.config}",
             "value": res["value"], "unit": cfg["unit"], "n_gpus": world, "steps": args.steps,
