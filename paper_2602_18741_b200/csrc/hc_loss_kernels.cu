@@ -21,9 +21,17 @@ __global__ void sum_partials_kernel(const double* partials, int count, double* o
   }
 }
 
+#ifndef HC_LOSS_T
+#define HC_LOSS_T 64
+#endif
+#ifndef HC_LOSS_STAGES
+#define HC_LOSS_STAGES 2
+#endif
+
 template <int N, int K>
 int loss_nk(hc_codec c, const float* A, const float* B, int64_t pairs, double* sum_dev) {
-  using Op = LossOp<N, K, 64, 64, 2>;  // 83 KB smem: 2 CTAs / SM, one tile computing + one loading each
+  // 64-pair tiles x 2 stages = 83 KB smem: 2 CTAs / SM, one tile computing + one loading each
+  using Op = LossOp<N, K, HC_LOSS_T, HC_LOSS_T, HC_LOSS_STAGES>;
   hc_ctx ctx = c->ctx;
   int rc = configure_tile_op<Op>();
   if (rc != HC_OK) return rc;
