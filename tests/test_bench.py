@@ -1,0 +1,59 @@
+"""bench.py's JSON contract: the reference arm on CPU, the rank handling, and (GPU) our arm."""
+import json
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+BASELINE = json.loads((ROOT / "BASELINE.json").read_text())
+
+
+def _run(args, env_extra=None, timeout=600):
+    env = dict(os.environ)
+    env.update(env_extra or {})
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], cwd=ROOT, env=env, capture_output=True,
+                       text=True, timeout=timeout)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    return [json.loads(ln) for ln in lines]
+
+
+def _needs_reference():
+    if not (ROOT / "oracle" / "_ref" / "libhcref81.so").exists():
+        pytest.skip("oracle/_ref not built")
+
+
+def test_reference_arm_line():
+    _needs_reference()
+    (line,) = _run(["--impl", "reference", "--steps", "2", "--warmup", "1"])
+    assert line["impl"] == "reference"
+    assert line["metric"] == BASELINE["metric"] and line["unit"] == "Mpixel/s"
+    assert line["higher_is_better"] is True and line["steps"] == 2 and line["warmup"] == 3  # W >= 3 enforced
+    assert line["value"] > 0 and line["cpu_baseline"]["value"] == line["value"]
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"] == {"value": line["value"], "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
+                           "d2h_bytes_per_step": 0}
+    assert line["config"]["workload"].startswith("1920x1080")
+
+
+def test_reference_arm_other_ranks_exit_quietly():
+    assert _run(["--impl", "reference", "--steps", "2", "--warmup", "1"],
+                {"RANK": "1", "LOCAL_RANK": "1", "WORLD_SIZE": "2"}) == []
+
+
+@pytest.mark.gpu
+def test_gpu_arm_line():
+    (line,) = _run(["--steps", "40", "--warmup", "3", "--no-cpu-baseline"])
+    assert line["metric"] == BASELINE["metric"] and line["n_gpus"] == 1 and line["steps"] == 40
+    assert line["value"] > 1e4 and 0 < line["roofline"]["frac"] <= 1.0 and line["roofline"]["bound"] == "hbm"
+    assert line["gpu_launches"] >= 40
+    e2e = line["e2e"]
+    assert e2e["h2d_bytes_per_step"] == 1920 * 1080 * 36 and e2e["d2h_bytes_per_step"] == 1920 * 1080 * 24
+    assert 0 < e2e["value"] < line["value"]
+    assert line["e2e_matches_device"] and line["e2e_stream_matches_device"]
+    assert line["clocks"]["sm_max_mhz"] > 0
+    d = line["ms_per_step_dist"]
+    assert d["p10"] <= d["p50"] <= d["p90"]
