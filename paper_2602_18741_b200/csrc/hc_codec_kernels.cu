@@ -11,7 +11,13 @@ template <int N, int K, int MODE>
 struct CodecTile;
 template <int N, int K>
 struct CodecTile<N, K, kRoundtrip> {
-  static constexpr int T = 64, THREADS = 64, STAGES = 2;
+#ifndef HC_RT_T
+#define HC_RT_T 64
+#endif
+#ifndef HC_RT_STAGES
+#define HC_RT_STAGES 2
+#endif
+  static constexpr int T = HC_RT_T, THREADS = HC_RT_T, STAGES = HC_RT_STAGES;
 };
 template <int N, int K>
 struct CodecTile<N, K, kEncode> {
