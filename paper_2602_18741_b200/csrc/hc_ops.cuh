@@ -304,9 +304,25 @@ struct ShadeSpectralOp {
   __host__ __device__ static constexpr int in_bytes(int i) { return i == 0 ? 4 : L * 4; }
   static constexpr int NOUT = SPEC ? 3 : 2;  // XYZ, sRGB, [spectra]
   __host__ __device__ static constexpr int out_bytes(int i) { return i < 2 ? 12 : N * 4; }
-  static constexpr int EXTRA_SMEM = kMaxPalette * N * 4;
+#ifndef HC_NAIVE_PALG_SPEC
+#define HC_NAIVE_PALG_SPEC 1
+#endif
+#ifndef HC_NAIVE_PALG
+#define HC_NAIVE_PALG 0
+#endif
+  // kPalG: palette rows read through L1 (__ldg) instead of an 83 KB shared-memory copy per
+  // CTA, and the light SPDs as shared-memory rows [lambda][light] read by broadcast LDS.128
+  // instead of L x n constant-bank operands (10 KB at L = 32, beyond the constant cache).
+  // The spectra-writing variant ran 1 CTA (2 warps) per SM with the smem palette.
+  static constexpr bool kPalG = SPEC ? HC_NAIVE_PALG_SPEC : HC_NAIVE_PALG;
+#ifndef HC_NAIVE_LSMEM
+#define HC_NAIVE_LSMEM 0
+#endif
+  static constexpr bool kLightSmem = kPalG || HC_NAIVE_LSMEM;  // light rows in smem (else constant bank)
+  static constexpr int kPalOff = kLightSmem ? N * L * 4 : 0;   // palette copy after the light rows
+  static constexpr int EXTRA_SMEM = kPalOff + (kPalG ? 0 : kMaxPalette * N * 4);
   static constexpr int kTensorStream = -1;
-  static constexpr bool kWarpSpecialized = false;
+  static constexpr bool kWarpSpecialized = kPalG && SPEC;
   static constexpr bool kEvictFirstLoads = false;
 
   struct Params {
@@ -332,7 +348,14 @@ struct ShadeSpectralOp {
     return i == 0 ? p.xyz : (i == 1 ? p.rgb : p.spectra);
   }
   __device__ static void setup(const Params& p, unsigned char* extra) {
-    block_load_table(reinterpret_cast<float*>(extra), p.pal_spectra, p.n_pal * N);
+    if constexpr (kLightSmem) {
+      float* ls = reinterpret_cast<float*>(extra);  // [lambda][light]
+      for (int x = threadIdx.x; x < N * L; x += blockDim.x) {
+        const int i = x / L, l = x - i * L;
+        ls[x] = p.light[l * N + i];
+      }
+    }
+    if constexpr (!kPalG) block_load_table(reinterpret_cast<float*>(extra + kPalOff), p.pal_spectra, p.n_pal * N);
   }
   __device__ static void finish(const Params&, State&, unsigned char*) {}
 
@@ -353,15 +376,33 @@ struct ShadeSpectralOp {
       w[l4 + 2] = w4.z;
       w[l4 + 3] = w4.w;
     }
-    const float* R = reinterpret_cast<const float*>(extra) + id * N;
+    const float* R = kPalG ? p.pal_spectra + id * N : reinterpret_cast<const float*>(extra + kPalOff) + id * N;
     float* os = SPEC ? reinterpret_cast<float*>(outs[2]) + item * N : nullptr;
     float xyz[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      float illum = w[0] * p.light[i];
+      float illum;
+      if constexpr (kLightSmem) {
+        const float4* lr = reinterpret_cast<const float4*>(extra) + i * (L / 4);  // broadcast row
+        float lv[L];
 #pragma unroll
-      for (int l = 1; l < L; ++l) illum = fmaf(w[l], p.light[l * N + i], illum);
-      const float s = R[i] * illum;
+        for (int c4 = 0; c4 < L / 4; ++c4) {
+          const float4 v = lr[c4];
+          lv[4 * c4] = v.x;
+          lv[4 * c4 + 1] = v.y;
+          lv[4 * c4 + 2] = v.z;
+          lv[4 * c4 + 3] = v.w;
+        }
+        illum = w[0] * lv[0];
+#pragma unroll
+        for (int l = 1; l < L; ++l) illum = fmaf(w[l], lv[l], illum);
+      } else {
+        illum = w[0] * p.light[i];
+#pragma unroll
+        for (int l = 1; l < L; ++l) illum = fmaf(w[l], p.light[l * N + i], illum);
+      }
+      const float Ri = kPalG ? __ldg(R + i) : R[i];
+      const float s = Ri * illum;
       if constexpr (SPEC) os[i] = s;
       xyz[0] = fmaf(p.cmf[i], s, xyz[0]);
       xyz[1] = fmaf(p.cmf[N + i], s, xyz[1]);
