@@ -88,6 +88,14 @@ CONFIGS = {
 }
 
 
+# fp32-issue bound of the naive n = 81 paths: lane-ops per unit at 148 SMs x 128
+# fp32 lanes x the max SM clock (1.965 GHz).
+FP32_LANE_OPS_PER_S = 148 * 128 * 1.965e9
+NAIVE_BOUND = {"2": {"lane_ops_per_unit": 981, "lane_ops_per_s": FP32_LANE_OPS_PER_S},
+               "3": {"lane_ops_per_unit": 2925, "lane_ops_per_s": FP32_LANE_OPS_PER_S},
+               "4": {"lane_ops_per_unit": 62460, "lane_ops_per_s": FP32_LANE_OPS_PER_S}}
+
+
 # ---------------------------------------------------------------------------- helpers
 def peaks() -> dict:
     if PEAKS_PATH.exists():
@@ -187,13 +195,39 @@ def tool_spectra_text_np(rows: int, m: int) -> bytes:
 
 
 # ---------------------------------------------------------------------------- CPU reference
-def cpu_reference_run(cfg_key: str, budget_s: float, threads: int = 0, rank: int = 0) -> dict:
-    """Time the reference's CPU implementation (oracle/_ref) on a bounded sample."""
+def cpu_reference_run(cfg_key: str, budget_s: float, threads: int = 0, rank: int = 0, min_reps: int = 1) -> dict:
+    """Time the reference's CPU implementation (oracle/_ref) on its per-step workload
+    (the full frame for configs 2 / 3, a bounded sample otherwise) for >= budget_s and
+    >= min_reps steps."""
+    case = cpu_reference_case(cfg_key, threads, rank)
+    return time_cpu_case(case, budget_s, min_reps)
+
+
+def time_cpu_case(case: dict, budget_s: float, min_reps: int = 1, warmup: int = 1) -> dict:
+    run = case["run"]
+    for _ in range(warmup):
+        run()
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        run()
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s and reps >= min_reps:
+            break
+    value = case["P"] * reps / el / 1e6
+    return {"value": value, "unit": case["unit"], "cores": case["cores"], "kind": "reference",
+            "sample": case["sample"], "seconds": round(el, 3), "units_per_rep": case["P"], "reps": reps,
+            "step_s": el / reps, "cpu": _cpu_model()}
+
+
+def cpu_reference_case(cfg_key: str, threads: int = 0, rank: int = 0) -> dict:
+    """The reference's CPU implementation of one step of config `cfg_key` (oracle/_ref: the
+    reference core compiled from its sources, plus the G-buffer restatement SURVEY §8c R1)."""
     import oracle
     from paper_2602_18741_b200 import synth
 
     ref = oracle.reference(81)
-    kind = "reference"
     if ref is None:
         raise RuntimeError("oracle/_ref not built (python __graft_entry__.py build)")
     cfg = CONFIGS[cfg_key]
@@ -203,16 +237,15 @@ def cpu_reference_run(cfg_key: str, budget_s: float, threads: int = 0, rank: int
 
     if cfg_key in ("2", "3"):
         L = cfg["L"]
-        W = cfg["W"]
+        W, H = cfg["W"], cfg["H"]
         pal = synth.palette(SEED, 256, N_SPEC)
         lts = synth.lights(SEED, L, N_SPEC)
         pc = np.zeros((256, k), np.float32)
         lc = np.zeros((L, k), np.float32)
         ref.ref_asset_codes(E, k, pal, 256, pc)
         ref.ref_asset_codes(E, k, lts, L, lc)
-        rows = max(1, min(cfg["H"], 64))
-        P = rows * W
-        idx, cosv = synth.gbuffer_np(SEED, rank * cfg["H"] * W, P, L, 256)
+        P = W * H  # the whole frame, as the GPU arm's step
+        idx, cosv = synth.gbuffer_np(SEED, rank * H * W, P, L, 256)
         cosv = np.ascontiguousarray(cosv)
         outs = {"xyz": np.zeros((P, 3), np.float32), "rgb": np.zeros((P, 3), np.float32)}
         spec = np.zeros((P, N_SPEC), np.float32) if cfg_key == "3" else None
@@ -221,7 +254,8 @@ def cpu_reference_run(cfg_key: str, budget_s: float, threads: int = 0, rank: int
             ref.ref_shade_latent(E, D, k, pc, lc, L, idx, cosv, P, None, spec,
                                  None if cfg_key == "3" else outs["xyz"], outs["rgb"], nthreads)
 
-        sample = f"{rows} rows x {W} px of the frame (R1 latent shade + decode_image + image_to_linear_rgb)"
+        sample = (f"the full {W}x{H} frame per step (R1 latent shade + decode_image + image_to_linear_rgb, "
+                  f"{nthreads} threads)")
     elif cfg_key == "1":
         P = 1 << 14
         S = synth.gm_spectra_ctr(SEED, "codec.spectra", 0, 2048, N_SPEC)
@@ -367,19 +401,7 @@ def cpu_reference_run(cfg_key: str, budget_s: float, threads: int = 0, rank: int
 
         sample = f"{P} pairs"
 
-    run()  # warm
-    t0 = time.perf_counter()
-    reps = 0
-    while True:
-        run()
-        reps += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s:
-            break
-    value = P * reps / el / 1e6
-    return {"value": value, "unit": cfg["unit"], "cores": nthreads, "kind": kind, "sample": sample,
-            "seconds": round(el, 3), "units_per_rep": P, "reps": reps, "step_s": el / reps,
-            "cpu": _cpu_model()}
+    return {"run": run, "P": P, "sample": sample, "cores": nthreads, "unit": cfg["unit"]}
 
 
 def _cpu_model() -> str:
@@ -392,25 +414,44 @@ def _cpu_model() -> str:
     return "unknown"
 
 
+def config_dict(key: str) -> dict:
+    """The workload description both arms print (identical, so the driver can match them)."""
+    cfg = CONFIGS[key]
+    d = {"workload": cfg["name"], "config_id": key}
+    for f in ("W", "H", "units", "k", "L", "spp"):
+        if f in cfg:
+            d[f] = cfg[f]
+    return d
+
+
+def metric_name(key: str) -> str:
+    return METRIC if key == "2" else f"{CONFIGS[key]['unit']} config {key}"
+
+
 def run_reference_arm(args) -> int:
+    """The reference's own CPU implementation of the step (oracle/_ref, all host threads):
+    W untimed warm-up steps, then exactly K timed steps, each the same workload as one
+    GPU-arm step (the full frame for the default config).  Rank 0 only."""
     rank, world, local = dist_env()
     if rank != 0:
         return 0
     cfg = CONFIGS[args.config]
-    # calibrate one step, then time K steps of the bounded sample
-    cal = cpu_reference_run(args.config, budget_s=0.0)  # warm-up step 1 (also the calibration)
-    per_step = cal["step_s"]
-    for _ in range(max(0, args.warmup - 1)):  # the remaining untimed warm-up steps
-        cpu_reference_run(args.config, budget_s=0.0)
-    res = cpu_reference_run(args.config, budget_s=max(per_step * args.steps, 1.0))
-    line = {"metric": METRIC if args.config == "2" else f"{cfg['unit']} config {args.config}",
-            "value": res["value"], "unit": cfg["unit"], "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": res["step_s"] * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": cfg["name"], "config_id": args.config}, "impl": "reference",
-            "cpu_baseline": {"value": res["value"], "unit": cfg["unit"], "cores": res["cores"], "kind": res["kind"],
-                             "sample": res["sample"], "cpu": res["cpu"]},
-            "e2e": {"value": res["value"], "unit": cfg["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    case = cpu_reference_case(args.config)
+    for _ in range(args.warmup):
+        case["run"]()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        case["run"]()
+    el = time.perf_counter() - t0
+    value = case["P"] * args.steps / el / 1e6
+    line = {"metric": metric_name(args.config), "value": value, "unit": cfg["unit"], "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+            "dtype": cfg.get("dtype", "bf16" if args.config == "5a" else "f32"), "data": "synthetic",
+            "config": config_dict(args.config), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": cfg["unit"], "cores": case["cores"], "kind": "reference",
+                             "sample": case["sample"], "cpu": _cpu_model()},
+            "e2e": {"value": value, "unit": cfg["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
     return 0
 
@@ -638,56 +679,209 @@ class Workload:
         self.R = R
 
 
-class _PlainReplay:
-    """Stand-in for a CUDA graph for configs whose step cannot be captured (the path
-    tracer compiles the scene on the host and synchronises): replay() runs the steps."""
+class StepReplayer:
+    """Replays exactly n steps of a workload: CUDA graphs of one full buffer rotation
+    (R steps) plus a graph of the remainder, so any --steps is honoured exactly.
+    Configs whose step cannot be captured (host-side setup / synchronisation inside the
+    call) run the steps as plain library calls."""
 
-    def __init__(self, wl, n: int):
-        self.wl, self.n = wl, n
-
-    def replay(self):
-        for i in range(self.n):
-            self.wl.step(i)
-
-
-def time_graph(torch, wl, steps: int, warmup: int, stream) -> tuple[float, int]:
-    """Capture R steps (one per buffer set) in a CUDA graph; replay to cover `steps`.
-    Returns (elapsed ms over exactly `steps` steps, launches per step)."""
-    R = wl.R
-    if not wl.cfg.get("graph", True):
+    def __init__(self, torch, wl, warmup: int, stream, max_steps: int):
+        self.torch, self.wl, self.stream = torch, wl, stream
+        self.graph = wl.cfg.get("graph", True)
+        R = wl.R
+        ctx = wl.codec.ctx
         with torch.cuda.stream(stream):
-            for i in range(max(warmup, 1)):
+            for i in range(max(warmup, R if self.graph else 1)):
                 wl.step(i)
             torch.cuda.synchronize()
-            l0 = wl.codec.ctx.launches
+            l0 = ctx.launches
             wl.step(0)
             torch.cuda.synchronize()
-        return _PlainReplay(wl, min(R, steps)), wl.codec.ctx.launches - l0, min(R, steps)
-    reps = max(1, steps // R)
-    assert reps * R == steps or steps < R, "steps must be a multiple of the rotation"
-    ctx = wl.codec.ctx
-    with torch.cuda.stream(stream):
-        for i in range(max(warmup, R)):
-            wl.step(i)
-        torch.cuda.synchronize()
-        l0 = ctx.launches
-        wl.step(0)
-        torch.cuda.synchronize()
-        per_step = ctx.launches - l0
+            self.per_step = ctx.launches - l0
+        self.full = None
+        self.rem = {}
+        if self.graph and max_steps >= R:
+            self.full = self._capture(R)
+
+    def _capture(self, n: int):
+        torch = self.torch
         g = torch.cuda.CUDAGraph()
-        n_in_graph = min(R, steps)
-        with torch.cuda.graph(g, stream=stream):
-            for i in range(n_in_graph):
-                wl.step(i)
-        g.replay()
+        with torch.cuda.stream(self.stream):
+            with torch.cuda.graph(g, stream=self.stream):
+                for i in range(n):
+                    self.wl.step(i)
+            g.replay()
         torch.cuda.synchronize()
-    return g, per_step, n_in_graph
+        return g
+
+    def prepare(self, n: int) -> None:
+        """Capture the remainder graph for n steps (outside any timed region)."""
+        if self.graph and n % self.wl.R and (n % self.wl.R) not in self.rem:
+            self.rem[n % self.wl.R] = self._capture(n % self.wl.R)
+
+    def run(self, n: int) -> None:
+        """Issue exactly n steps on the stream (no synchronisation)."""
+        if not self.graph:
+            for i in range(n):
+                self.wl.step(i)
+            return
+        R = self.wl.R
+        for _ in range(n // R):
+            self.full.replay()
+        if n % R:
+            self.rem[n % R].replay()
 
 
 def C_int64():
     import ctypes
 
     return ctypes.c_int64()
+
+
+def _max_over_ranks(torch, dist, world: int, v: float) -> float:
+    if world == 1:
+        return v
+    t = torch.tensor([v], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def time_steps(torch, dist, world: int, rep: StepReplayer, steps: int, stream, clocks=None) -> tuple[float, float]:
+    """Exactly `steps` steps between two CUDA events on the launching stream, bracketed by
+    a barrier + synchronize on both sides; (ms max over ranks, host wall seconds)."""
+    rep.prepare(steps)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cm = clocks if clocks is not None else _NullCtx()
+    with cm:
+        w0 = time.perf_counter()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            rep.run(steps)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+    barrier()
+    return _max_over_ranks(torch, dist, world, e0.elapsed_time(e1)), wall
+
+
+class _NullCtx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def roofline_record(cfg: dict, units: int, kernel_us: float) -> dict:
+    pk = peaks()
+    if "flops_per_unit" in cfg:
+        achieved = units * cfg["flops_per_unit"] / (kernel_us * 1e-6) / 1e12
+        return {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / pk["bf16_tflops"], "traffic": None,
+                "peak_source": f"{pk['source']} bf16_tflops (burst)", "flops_per_unit": cfg["flops_per_unit"],
+                "units_per_launch": units, "kernel_us": kernel_us}
+    achieved = units * cfg["bytes_per_unit"] / (kernel_us * 1e-6) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_source": f"{pk['source']} hbm_gbs",
+            "bytes_per_unit": cfg["bytes_per_unit"], "units_per_launch": units, "kernel_us": kernel_us}
+
+
+def _traffic(key: str):
+    """ncu DRAM bytes per launch of the dominant kernel (profiles/traffic_config<key>.json:
+    dram__bytes_read.sum + dram__bytes_write.sum, steady-state window of back-to-back launches)."""
+    path = ROOT / "profiles" / f"traffic_config{key}.json"
+    if path.exists():
+        try:
+            d = json.loads(path.read_text())
+            return d.get("bytes_per_launch"), d
+        except Exception:  # noqa: BLE001
+            pass
+    return None, None
+
+
+def parity_gbuffer(wl, rows_stride: int = 1) -> dict:
+    """Set 0 of a config 2 / 3 workload against the reference (oracle/_ref, R1 restatement over
+    the reference's decode_image / image_to_linear_rgb) on the same inputs: every
+    `rows_stride`-th row of the frame.  Tolerance (north_star): 1e-5 relative, denominator
+    max(|ref|, ||ref_row||_inf)."""
+    import oracle
+
+    ref = oracle.reference(81)
+    cfg = wl.cfg
+    k, L, W = cfg["k"], cfg["L"], cfg["W"]
+    idx, cosv, outs = wl.sets[0]
+    P = wl.units
+    rows = np.arange(0, P // W, rows_stride)
+    sel = (rows[:, None] * W + np.arange(W)[None, :]).reshape(-1)
+    h_idx = idx.cpu().numpy().view(np.uint32)[sel].copy()
+    h_cos = np.ascontiguousarray(cosv.cpu().numpy()[sel])
+    m = sel.size
+    E, D = wl.codec.E, wl.codec.D
+    spec = cfg["W"] == 3840
+    r_spec = np.zeros((m, N_SPEC), np.float32) if spec else None
+    r_xyz = None if spec else np.zeros((m, 3), np.float32)
+    r_rgb = np.zeros((m, 3), np.float32)
+    ref.ref_shade_latent(E, D, k, wl.pal_codes.cpu().numpy(), wl.light_codes, L, h_idx, h_cos, m, None, r_spec,
+                         r_xyz, r_rgb, 0)
+    res = {"rows": f"every {rows_stride}th row" if rows_stride > 1 else "full frame", "pixels": int(m),
+           "tol": 1e-5, "checker": "oracle/_ref (the reference compiled from its sources)"}
+    worst = 0.0
+    for name, want in (("spectra", r_spec), ("xyz", r_xyz), ("rgb", r_rgb)):
+        if want is None:
+            continue
+        got = outs[name].cpu().numpy()[sel]
+        rel, mabs = rel_err_rows(got, want), float(np.max(np.abs(got.astype(np.float64) - want)))
+        res[name] = {"max_rel": rel, "max_abs": mabs}
+        worst = max(worst, rel)
+    res["pass"] = bool(worst <= 1e-5)
+    return res
+
+
+def rel_err_rows(got, ref) -> float:
+    """max |got - ref| / max(|ref|, ||ref_row||_inf), chunked for large arrays."""
+    worst = 0.0
+    n = ref.shape[0]
+    step = max(1, (1 << 24) // max(1, ref.shape[1] if ref.ndim > 1 else 1))
+    for a in range(0, n, step):
+        g = np.asarray(got[a:a + step], np.float64)
+        r = np.asarray(ref[a:a + step], np.float64)
+        row = np.max(np.abs(r), axis=-1, keepdims=True) if r.ndim > 1 else np.abs(r)
+        den = np.maximum(np.maximum(np.abs(r), row), 1e-30)
+        if r.size:
+            worst = max(worst, float(np.max(np.abs(g - r) / den)))
+    return worst
+
+
+def nccl_record(world: int, rank: int) -> dict | None:
+    """What NCCL reported at communicator init (NCCL_DEBUG=INFO, subsystem INIT, logged to a
+    per-process file): the version and the rank count of the communicator it built."""
+    import re
+
+    import torch
+
+    path = os.environ.get("NCCL_DEBUG_FILE", "")
+    rec = {"backend": "nccl", "world": world}
+    try:
+        v = torch.cuda.nccl.version()
+        rec["version"] = ".".join(map(str, v)) if isinstance(v, tuple) else str(v)
+    except Exception:  # noqa: BLE001
+        pass
+    if path:
+        f = Path(path.replace("%h", os.uname().nodename).replace("%p", str(os.getpid())))
+        if f.exists():
+            txt = f.read_text(errors="replace")
+            n = re.findall(r"nranks\s*[= ]\s*(\d+)", txt, re.I)
+            if n:
+                rec["comm_nranks"] = int(n[-1])
+            rec["init_lines"] = len([ln for ln in txt.splitlines() if "Init" in ln or "init" in ln])
+    return rec
 
 
 def run_ours(args) -> int:
@@ -697,19 +891,25 @@ def run_ours(args) -> int:
 
     rank, world, local = dist_env()
     if world > 1:
+        # NCCL's own account of the communicator (version, nranks) goes to a per-process
+        # file, read back into the JSON line (nccl_record); stdout stays one JSON line.
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/hc_bench_nccl.%h.%p.log")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()  # the communicator exists (and is logged) before the timed region
     else:
         torch.cuda.set_device(0)
     dev = torch.cuda.current_device()
     cfg = CONFIGS[args.config]
     stream = torch.cuda.Stream()
+    strong = args.scaling == "strong"
     with torch.cuda.stream(stream):
         ctx = api.Context(dev)
-        wl = Workload(api, ctx, args.config, rank, world=world, strong=args.scaling == "strong")
+        wl = Workload(api, ctx, args.config, rank, world=world, strong=strong)
     torch.cuda.synchronize()
-    R = wl.R
-    steps = max(R, (args.steps + R - 1) // R * R)
+    steps = args.steps
 
     if args.plain:
         # Profiling mode (ncu): plain stream launches, no graph, no extras, no JSON contract.
@@ -719,202 +919,143 @@ def run_ours(args) -> int:
         torch.cuda.synchronize()
         if args.naive_plain:
             with torch.cuda.stream(stream):
-                wn = Workload(api, ctx, args.config, rank, naive=True, world=world,
-                              strong=args.scaling == "strong")
+                wn = Workload(api, ctx, args.config, rank, naive=True, world=world, strong=strong)
                 for i in range(args.steps):
                     wn.step(i)
             torch.cuda.synchronize()
         print(json.dumps({"plain": True, "config": args.config, "steps": args.steps, "launches": ctx.launches}))
         return 0
 
-    g, per_step, n_in_graph = time_graph(torch, wl, steps, args.warmup, stream)
-    reps = steps // n_in_graph
+    rep = StepReplayer(torch, wl, args.warmup, stream, steps)
+    rep.prepare(steps)
+    with torch.cuda.stream(stream):  # the W warm-up steps again through the replay path
+        rep.run(min(args.warmup, max(steps, 1)))
+    torch.cuda.synchronize()
 
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    # ---- timed region: K steps, graph replays, CUDA events on the launching stream
-    for _ in range(max(1, args.warmup // n_in_graph)):
-        g.replay()
-    barrier()
-    launches0 = ctx.launches
-    t_ev0, t_ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(dev) as clocks:
-        t_wall0 = time.perf_counter()
-        with torch.cuda.stream(stream):
-            t_ev0.record(stream)
-            for _ in range(reps):
-                g.replay()
-            t_ev1.record(stream)
-        torch.cuda.synchronize()
-        t_wall = time.perf_counter() - t_wall0
-    barrier()
-    ms = t_ev0.elapsed_time(t_ev1)
-    if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    launches_timed = per_step * steps  # graph replays do not pass through the host counter
+    # ---- timed region: exactly K steps, CUDA events on the launching stream, max over ranks
+    clocks = ClockSampler(dev)
+    ms, t_wall = time_steps(torch, dist, world, rep, steps, stream, clocks)
+    launches_timed = rep.per_step * steps  # graph replays do not pass through the host counter
     ms_per_step = ms / steps
-    # Per-replay distribution (after the timed region, so it does not perturb it): each
-    # graph replay (n_in_graph steps) bracketed by its own events.
-    nrep = max(8, min(64, steps // n_in_graph))
+    # per-step distribution after the timed region (does not perturb it): groups of R steps
+    R = wl.R
+    nrep = 8
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(nrep + 1)]
     with torch.cuda.stream(stream):
         evs[0].record(stream)
         for j in range(nrep):
-            g.replay()
+            rep.run(R)
             evs[j + 1].record(stream)
     torch.cuda.synchronize()
-    per = np.array([evs[j].elapsed_time(evs[j + 1]) / n_in_graph for j in range(nrep)])
+    per = np.array([evs[j].elapsed_time(evs[j + 1]) / R for j in range(nrep)])
     dist_ms = {"p10": float(np.percentile(per, 10)), "p50": float(np.median(per)),
-               "p90": float(np.percentile(per, 90)), "replays": nrep, "steps_per_replay": n_in_graph}
+               "p90": float(np.percentile(per, 90)), "groups": nrep, "steps_per_group": R}
     value = wl.units * world * steps / (ms / 1e3) / 1e6
 
-    pk = peaks()
-    kernel_us = ms_per_step * 1e3  # one hot kernel per step (per_step launches)
-    if "flops_per_unit" in cfg:
-        achieved = wl.units * cfg["flops_per_unit"] / (kernel_us * 1e-6) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / pk["bf16_tflops"], "traffic": None,
-                "peak_source": f"{pk['source']} bf16_tflops (burst)"}
-    else:
-        achieved = wl.units * cfg["bytes_per_unit"] / (kernel_us * 1e-6) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": None, "peak_source": f"{pk['source']} hbm_gbs",
-                "bytes_per_unit": cfg["bytes_per_unit"], "units_per_launch": wl.units,
-                "kernel_us": kernel_us}
-    traffic = Path(ROOT / "profiles" / f"traffic_config{args.config}.json")
-    if traffic.exists():
-        try:
-            roof["traffic"] = json.loads(traffic.read_text()).get("bytes_per_launch")
-        except Exception:  # noqa: BLE001
-            pass
+    kernel_us = ms_per_step * 1e3 / max(1, rep.per_step) if rep.per_step <= 1 else ms_per_step * 1e3
+    roof = roofline_record(cfg, wl.units, kernel_us)
+    roof["traffic"], tr = _traffic(args.config)
+    if tr:
+        roof["traffic_note"] = tr.get("method")
 
     extra = {}
-    # ---- naive n = 81 comparison on the same inputs (configs 2 / 4)
+    # ---- naive n = 81 comparison on the same inputs
     if args.config in ("2", "3", "4", "7") and not args.no_naive:
-        wn = Workload.__new__(Workload)
-        wn.__dict__.update(wl.__dict__)
-        wn_step_ours = wl.step
-        # rebuild the step closure with the naive path over the same buffers
         with torch.cuda.stream(stream):
-            wl2 = Workload(api, ctx, args.config, rank, naive=True, world=world, strong=args.scaling == "strong")
-        gn, _, nn = time_graph(torch, wl2, steps if args.config not in ("4", "7") else R, 1, stream)
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        nreps = max(1, (steps if args.config not in ("4", "7") else R) // nn)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for _ in range(nreps):
-                gn.replay()
-            e1.record(stream)
-        torch.cuda.synchronize()
-        nms = e0.elapsed_time(e1)
-        if world > 1:
-            t = torch.tensor([nms], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            nms = float(t.item())
-        nsteps = nreps * nn
-        extra["naive_n81"] = {"value": wl2.units * world * nsteps / (nms / 1e3) / 1e6, "unit": cfg["unit"],
-                              "ms_per_step": nms / nsteps}
-        extra["speedup_latent_vs_naive"] = extra["naive_n81"]["ms_per_step"] and (nms / nsteps) / ms_per_step
-        del wl2, gn
-        _ = wn_step_ours
+            wn = Workload(api, ctx, args.config, rank, naive=True, world=world, strong=strong)
+        nsteps = steps if args.config not in ("4", "7") else wn.R
+        nrep_ = StepReplayer(torch, wn, 1, stream, nsteps)
+        nms, _ = time_steps(torch, dist, world, nrep_, nsteps, stream)
+        extra["naive_n81"] = {"value": wn.units * world * nsteps / (nms / 1e3) / 1e6, "unit": cfg["unit"],
+                              "ms_per_step": nms / nsteps, "steps": nsteps}
+        nb = NAIVE_BOUND.get(args.config)
+        if nb:
+            nb_ms = wn.units * nb["lane_ops_per_unit"] / nb["lane_ops_per_s"] * 1e3
+            extra["naive_n81"]["roofline"] = {
+                "bound": "fp32 issue", "lane_ops_per_unit": nb["lane_ops_per_unit"],
+                "ideal_ms_per_step": nb_ms, "frac": nb_ms / (nms / nsteps),
+                "peak": f"148 SMs x 128 fp32 lanes x {nb['lane_ops_per_s'] / 148 / 128 / 1e9:.3f} GHz"}
+        extra["speedup_latent_vs_naive"] = (nms / nsteps) / ms_per_step
+        del wn, nrep_
 
     # ---- gather of the sRGB band to rank 0 (compute + gather), N > 1 only
     if world > 1 and args.config in ("2", "3", "4"):
-        rgb_local = wl.sets[0][-1]["rgb"]
-        gathered = [torch.empty_like(rgb_local) for _ in range(world)] if rank == 0 else None
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        from paper_2602_18741_b200.sharding import gather_rows, row_band
+
+        H = cfg["H"]
+        band = row_band(rank, world, H * world if not strong else H, cfg["W"])
         gsteps = min(steps, 20)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             e0.record(stream)
             for i in range(gsteps):
                 wl.step(i)
-                dist.gather(rgb_local, gathered, dst=0)
+                gather_rows(wl.sets[i % R][-1]["rgb"], band, H * world if not strong else H)
             e1.record(stream)
         torch.cuda.synchronize()
-        gms = e0.elapsed_time(e1)
-        t = torch.tensor([gms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        gms = float(t.item())
+        gms = _max_over_ranks(torch, dist, world, e0.elapsed_time(e1))
         extra["with_gather"] = {"value": wl.units * world * gsteps / (gms / 1e3) / 1e6, "unit": cfg["unit"],
-                                "ms_per_step": gms / gsteps, "gathered": "linear-sRGB row bands -> rank 0 (NCCL)"}
+                                "ms_per_step": gms / gsteps,
+                                "gathered": "linear-sRGB row bands -> rank 0 (sharding.gather_rows, NCCL)"}
 
     # ---- e2e through the host-buffer C-ABI call (config 2)
     e2e = None
     if args.config == "2":
-        P = wl.units
-        idx, cosv, _ = wl.sets[0]
-        h_idx = torch.empty(P, dtype=torch.int32, pin_memory=True)
-        h_cos = torch.empty(P, cfg["L"], pin_memory=True)
-        h_idx.copy_(idx)
-        h_cos.copy_(cosv)
-        h_pal = wl.pal_codes.cpu().numpy()
-        h_xyz = torch.empty(P, 3, pin_memory=True)
-        h_rgb = torch.empty(P, 3, pin_memory=True)
-        ni, nc, nx, nr = h_idx.numpy(), h_cos.numpy(), h_xyz.numpy(), h_rgb.numpy()
+        e2e, ok1, ok2 = e2e_config2(torch, dist, world, wl, stream, steps)
+        extra["e2e_matches_device"] = ok1
+        extra["e2e_stream_matches_device"] = ok2
+
+    # ---- parity of the timed outputs against the reference (config 2: the full frame)
+    if args.config in ("2", "3") and rank == 0 and not args.no_parity:
+        try:
+            extra["parity"] = parity_gbuffer(wl, 1 if args.config == "2" else 16)
+        except Exception as e:  # noqa: BLE001
+            extra["parity"] = {"unavailable": str(e)}
+
+    # ---- the k = 9 path (config 3: 4K, 32 lights, full spectra written) beside config 2
+    if args.config == "2" and not args.no_k9:
+        n_in = wl.units
+        del wl, rep
+        torch.cuda.empty_cache()
         with torch.cuda.stream(stream):
-            for _ in range(3):
-                wl.codec.shade_latent_host(h_pal, wl.light_codes, ni, nc, nx, nr)
-            barrier()
-            esteps = max(5, min(steps, 50))
-            t0 = time.perf_counter()
-            for _ in range(esteps):
-                wl.codec.shade_latent_host(h_pal, wl.light_codes, ni, nc, nx, nr)
-            el = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([el], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
-        single = {"value": P * world * esteps / el / 1e6, "ms_per_step": el / esteps * 1e3,
-                  "api": "hc_shade_latent_host, one synchronous call per frame"}
-        # parity spot check of the single-frame e2e result against the device path
-        dev_rgb = wl.sets[0][2]["rgb"].cpu().numpy()
-        extra["e2e_matches_device"] = bool(np.array_equal(dev_rgb, nr))
-        # Frame stream: the same frames through hc_shade_latent_host_frames (one pipeline
-        # across frames: frame f + 1's uploads overlap frame f's downloads).  Two pinned
-        # input / output sets alternate (frames 2j and 2j + 1 differ); every frame's H2D of
-        # its G-buffer and D2H of its XYZ + sRGB are inside the timed region.
-        idx1, cosv1, _ = wl.sets[1]
-        h_idx1 = torch.empty(P, dtype=torch.int32, pin_memory=True)
-        h_cos1 = torch.empty(P, cfg["L"], pin_memory=True)
-        h_idx1.copy_(idx1)
-        h_cos1.copy_(cosv1)
-        h_xyz1 = torch.empty(P, 3, pin_memory=True)
-        h_rgb1 = torch.empty(P, 3, pin_memory=True)
-        sets_h = [(ni, nc, nx, nr), (h_idx1.numpy(), h_cos1.numpy(), h_xyz1.numpy(), h_rgb1.numpy())]
-        frames = [sets_h[f % 2] for f in range(esteps)]
-        with torch.cuda.stream(stream):
-            wl.codec.shade_latent_host_frames(h_pal, wl.light_codes, frames[:4])
-            barrier()
-            t0 = time.perf_counter()
-            wl.codec.shade_latent_host_frames(h_pal, wl.light_codes, frames)
-            el2 = time.perf_counter() - t0
-        if world > 1:
-            t = torch.tensor([el2], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el2 = float(t.item())
-        extra["e2e_stream_matches_device"] = bool(
-            np.array_equal(wl.sets[1][2]["rgb"].cpu().numpy(), sets_h[1][3]) and np.array_equal(dev_rgb, nr))
-        e2e = {"value": P * world * esteps / el2 / 1e6, "unit": cfg["unit"],
-               "h2d_bytes_per_step": int(h_idx.numel() * 4 + h_cos.numel() * 4),
-               "d2h_bytes_per_step": int(h_xyz.numel() * 4 + h_rgb.numel() * 4), "ms_per_step": el2 / esteps * 1e3,
-               "api": f"hc_shade_latent_host_frames (pinned host buffers, {esteps} frames per call)",
-               "single_frame": single}
+            w3 = Workload(api, ctx, "3", rank, world=world, strong=strong)
+        torch.cuda.synchronize()
+        s3 = max(4, min(steps, 20))
+        r3 = StepReplayer(torch, w3, 3, stream, s3)
+        ms3, _ = time_steps(torch, dist, world, r3, s3, stream)
+        c3 = CONFIGS["3"]
+        k9 = {"config": config_dict("3"), "value": w3.units * world * s3 / (ms3 / 1e3) / 1e6,
+              "unit": c3["unit"], "steps": s3, "ms_per_step": ms3 / s3,
+              "roofline": roofline_record(c3, w3.units, ms3 / s3 * 1e3)}
+        k9["roofline"]["traffic"], _ = _traffic("3")
+        if not args.no_naive:
+            with torch.cuda.stream(stream):
+                wn3 = Workload(api, ctx, "3", rank, naive=True, world=world, strong=strong)
+            rn3 = StepReplayer(torch, wn3, 1, stream, wn3.R)
+            nms3, _ = time_steps(torch, dist, world, rn3, wn3.R, stream)
+            k9["naive_n81"] = {"value": wn3.units * world * wn3.R / (nms3 / 1e3) / 1e6, "unit": c3["unit"],
+                               "ms_per_step": nms3 / wn3.R}
+            k9["speedup_latent_vs_naive"] = (nms3 / wn3.R) / (ms3 / s3)
+            del wn3, rn3
+        if rank == 0 and not args.no_parity:
+            try:
+                k9["parity"] = parity_gbuffer(w3, 16)
+            except Exception as e:  # noqa: BLE001
+                k9["parity"] = {"unavailable": str(e)}
+        extra["k9"] = k9
+        del w3, r3
+        wl_units = n_in
+    else:
+        wl_units = wl.units
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:  # the contract: rank 0 at N = 1 only
         try:
-            cpu = cpu_reference_run(args.config, budget_s=args.cpu_seconds)
-            cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample", "seconds", "cpu")}
+            c = cpu_reference_run(args.config, budget_s=args.cpu_seconds)
+            cpu = {k_: c[k_] for k_ in ("value", "unit", "cores", "kind", "sample", "seconds", "cpu", "reps")}
             if cpu["cores"] > 1:  # the single-thread rate beside the all-core one
-                # (config 7 runs the reference's own render thread pool, sized by
-                # HADACODEC_THREADS, renderer.cpp:615-621)
                 old = os.environ.get("HADACODEC_THREADS")
                 os.environ["HADACODEC_THREADS"] = "1"
                 try:
@@ -931,21 +1072,21 @@ def run_ours(args) -> int:
 
     if rank == 0:
         line = {
-            "metric": METRIC if args.config == "2" else f"{cfg['unit']} config {args.config}",
+            "metric": metric_name(args.config),
             "value": value, "unit": cfg["unit"], "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": cfg.get("dtype", "bf16" if args.config == "5a" else "f32"),
             "data": "synthetic (seeded, DESIGN.md Inputs)",
-            "config": {"workload": cfg["name"], "config_id": args.config, "units_per_gpu": wl.units,
-                       "l2": (f"{R} rotating input/output buffer sets"
-                              f" ({'each' if R == 1 else 'rotation'} > 2x 126 MB L2)") if cfg.get("graph", True)
-                             else "compute-bound step (no L2 rotation needed)",
-                       "timing": ("CUDA graph of the step replayed K times; CUDA events; max over ranks"
-                                  if cfg.get("graph", True) else
-                                  "K synchronous library calls (host-side setup included); CUDA events; "
-                                  "max over ranks"),
-                       "parallelism": f"row bands, {args.scaling} scaling, {world} rank(s), no data-path collective",
-                       **wl.extra},
+            "config": config_dict(args.config),
+            "units_per_gpu": wl_units,
+            "method": {
+                "l2": (f"{R} rotating input/output buffer sets ({'each' if R == 1 else 'rotation'} > 2x 126 MB L2)"
+                       if cfg.get("graph", True) else "compute-bound step (no L2 rotation needed)"),
+                "timing": ("CUDA graphs (one buffer rotation + the remainder) replaying exactly K steps; CUDA "
+                           "events on the launching stream; max over ranks" if cfg.get("graph", True) else
+                           "K library calls (host-side setup included); CUDA events; max over ranks"),
+                "parallelism": (f"row bands, {args.scaling} scaling, {world} rank(s), one process per GPU, "
+                                "no data-path collective")},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -954,12 +1095,199 @@ def run_ours(args) -> int:
             "clocks": clocks.summary(),
             "wall_s_timed": t_wall,
         }
+        if world > 1:
+            line["nccl"] = nccl_record(world, rank)
         line.update(extra)
         emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def e2e_config2(torch, dist, world, wl, stream, steps):
+    """Config 2 end to end through the reference-facing host-buffer C-ABI calls: pinned host
+    G-buffer in, XYZ + sRGB out, every frame's H2D and D2H inside the timed region."""
+    cfg = wl.cfg
+    P = wl.units
+    idx, cosv, _ = wl.sets[0]
+    h_idx = torch.empty(P, dtype=torch.int32, pin_memory=True)
+    h_cos = torch.empty(P, cfg["L"], pin_memory=True)
+    h_idx.copy_(idx)
+    h_cos.copy_(cosv)
+    h_pal = wl.pal_codes.cpu().numpy()
+    h_xyz = torch.empty(P, 3, pin_memory=True)
+    h_rgb = torch.empty(P, 3, pin_memory=True)
+    ni, nc, nx, nr = h_idx.numpy(), h_cos.numpy(), h_xyz.numpy(), h_rgb.numpy()
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            wl.codec.shade_latent_host(h_pal, wl.light_codes, ni, nc, nx, nr)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        esteps = max(5, min(steps, 50))
+        t0 = time.perf_counter()
+        for _ in range(esteps):
+            wl.codec.shade_latent_host(h_pal, wl.light_codes, ni, nc, nx, nr)
+        el = time.perf_counter() - t0
+    el = _max_over_ranks(torch, dist, world, el)
+    single = {"value": P * world * esteps / el / 1e6, "ms_per_step": el / esteps * 1e3,
+              "api": "hc_shade_latent_host, one synchronous call per frame"}
+    dev_rgb = wl.sets[0][2]["rgb"].cpu().numpy()
+    ok1 = bool(np.array_equal(dev_rgb, nr))
+    # Frame stream through hc_shade_latent_host_frames (one pipeline across frames); two
+    # pinned input / output sets alternate.
+    idx1, cosv1, _ = wl.sets[1]
+    h_idx1 = torch.empty(P, dtype=torch.int32, pin_memory=True)
+    h_cos1 = torch.empty(P, cfg["L"], pin_memory=True)
+    h_idx1.copy_(idx1)
+    h_cos1.copy_(cosv1)
+    h_xyz1 = torch.empty(P, 3, pin_memory=True)
+    h_rgb1 = torch.empty(P, 3, pin_memory=True)
+    sets_h = [(ni, nc, nx, nr), (h_idx1.numpy(), h_cos1.numpy(), h_xyz1.numpy(), h_rgb1.numpy())]
+    frames = [sets_h[f % 2] for f in range(esteps)]
+    with torch.cuda.stream(stream):
+        wl.codec.shade_latent_host_frames(h_pal, wl.light_codes, frames[:4])
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        wl.codec.shade_latent_host_frames(h_pal, wl.light_codes, frames)
+        el2 = time.perf_counter() - t0
+    el2 = _max_over_ranks(torch, dist, world, el2)
+    ok2 = bool(np.array_equal(wl.sets[1][2]["rgb"].cpu().numpy(), sets_h[1][3]) and np.array_equal(dev_rgb, nr))
+    e2e = {"value": P * world * esteps / el2 / 1e6, "unit": cfg["unit"],
+           "h2d_bytes_per_step": int(h_idx.numel() * 4 + h_cos.numel() * 4),
+           "d2h_bytes_per_step": int(h_xyz.numel() * 4 + h_rgb.numel() * 4), "ms_per_step": el2 / esteps * 1e3,
+           "steps": esteps,
+           "api": f"hc_shade_latent_host_frames (pinned host buffers, {esteps} frames per call)",
+           "single_frame": single}
+    return e2e, ok1, ok2
+
+
+# ---------------------------------------------------------------------------- full-size parity
+VERIFY_CONFIGS = ("1", "2", "3", "4", "5a", "5b")
+
+
+def _cmp(name: str, got, want, tol: float) -> dict:
+    got = np.asarray(got)
+    want = np.asarray(want)
+    if got.shape != want.shape:
+        return {"name": name, "pass": False, "error": f"shape {got.shape} vs {want.shape}"}
+    rel = rel_err_rows(got, want)
+    mabs = 0.0
+    for a in range(0, want.shape[0], 1 << 20):
+        mabs = max(mabs, float(np.max(np.abs(np.asarray(got[a:a + (1 << 20)], np.float64) - want[a:a + (1 << 20)]))))
+    return {"name": name, "max_rel": rel, "max_abs": mabs, "tol": tol, "pass": bool(rel <= tol)}
+
+
+def verify_config(key: str, rank: int = 0) -> dict:
+    """One step of config `key` at BASELINE size on the GPU (the bench's own inputs: buffer
+    set 0, seed SEED), against the reference on the host (oracle/_ref, all threads) on the
+    same inputs.  Config 4 checks every 16th row; the others the full output."""
+    import torch
+
+    import oracle
+    from paper_2602_18741_b200 import api, synth
+
+    ref = oracle.reference(81)
+    if ref is None:
+        raise RuntimeError("oracle/_ref not built")
+    torch.cuda.set_device(0)
+    cfg = CONFIGS[key]
+    t0 = time.perf_counter()
+    ctx = api.Context(0)
+    wl = Workload(api, ctx, key, rank)
+    wl.step(0)
+    torch.cuda.synchronize()
+    k = cfg["k"]
+    E, D = wl.codec.E, wl.codec.D
+    checks = []
+    if key in ("2", "3"):
+        par = parity_gbuffer(wl, 1)
+        for name in ("spectra", "xyz", "rgb"):
+            if name in par:
+                checks.append({"name": name, **par[name], "tol": 1e-5, "pass": par[name]["max_rel"] <= 1e-5})
+        sample = f"full {cfg['W']}x{cfg['H']} frame"
+    elif key == "1":
+        S, outs = wl.sets[0]
+        P = wl.units
+        hS = S.cpu().numpy()
+        want = {"codes": np.zeros((P, k), np.float32), "spectra": np.zeros((P, N_SPEC), np.float32),
+                "xyz": np.zeros((P, 3), np.float32), "rgb": np.zeros((P, 3), np.float32)}
+        ref.ref_codec_roundtrip(E, D, k, hS, P, want["codes"], want["spectra"], want["xyz"], want["rgb"], 0)
+        for name in ("codes", "spectra", "xyz", "rgb"):
+            checks.append(_cmp(name, outs[name].cpu().numpy(), want[name], 1e-5))
+        sample = f"all {P} spectra"
+    elif key == "4":
+        pidx, iidx, tw, outs = wl.sets[0]
+        W, H, spp = cfg["W"], cfg["H"], cfg["spp"]
+        rows = np.arange(0, H, 16)
+        sel = torch.from_numpy((rows[:, None] * W + np.arange(W)[None, :]).reshape(-1)).cuda()
+        m = sel.numel()
+        h_p = np.ascontiguousarray(pidx.reshape(wl.units, -1)[sel].cpu().numpy())
+        h_i = np.ascontiguousarray(iidx.reshape(wl.units, -1)[sel].cpu().numpy())
+        h_t = np.ascontiguousarray(tw.reshape(wl.units, -1)[sel].cpu().numpy())
+        pal = synth.palette(SEED, 256, N_SPEC)
+        ill = synth.lights(SEED, 16, N_SPEC, purpose="scene.illuminants")
+        pc, ic = np.zeros((256, k), np.float32), np.zeros((16, k), np.float32)
+        ref.ref_asset_codes(E, k, pal, 256, pc)
+        ref.ref_asset_codes(E, k, ill, 16, ic)
+        X, R = np.zeros((m, 3), np.float32), np.zeros((m, 3), np.float32)
+        ref.ref_multibounce_latent(E, D, k, pc, ic, h_p, h_i, h_t, m, spp, 4, None, X, R, 0)
+        checks.append(_cmp("xyz", outs["xyz"][sel].cpu().numpy(), X, 1e-5))
+        checks.append(_cmp("rgb", outs["rgb"][sel].cpu().numpy(), R, 1e-5))
+        sample = f"every 16th row ({m} px x {spp} spp)"
+    elif key == "5a":
+        rgb, out = wl.sets[0]
+        P = wl.units
+        w = synth.mlp_weights(SEED, 6, 64)
+        want = np.zeros((P, 6), np.float32)
+        ref.ref_mlp_forward(rgb.cpu().numpy(), P, 64, 6, w["w1"], w["b1"], w["w2"], w["b2"], w["w3"], w["b3"], want,
+                            0)
+        checks.append(_cmp("codes", out.cpu().numpy(), want, 1e-2))
+        sample = f"all {P} texels (bf16 tolerance 1e-2)"
+    else:  # 5b
+        A, B = wl.sets[0]
+        P = wl.units
+        got = float(wl.sum.cpu().numpy()[0])
+        hA, hB = A.cpu().numpy(), B.cpu().numpy()
+        want = ref.ref_hadamard_loss(E, D, k, hA, hB, P, 0)
+        del hA, hB
+        rel = abs(got - want) / abs(want)
+        checks.append({"name": "loss", "got": got, "want": want, "max_rel": rel, "tol": 1e-5, "pass": rel <= 1e-5})
+        sample = f"all {P} pairs"
+    res = {"verify": key, "workload": cfg["name"], "sample": sample, "checks": checks,
+           "pass": all(c["pass"] for c in checks), "seconds": round(time.perf_counter() - t0, 1),
+           "checker": "oracle/_ref (the reference compiled from its sources; SURVEY §8c R1-R4 restatements on "
+                      "top of its primitives), all host threads"}
+    del wl
+    torch.cuda.empty_cache()
+    return res
+
+
+def run_verify(args) -> int:
+    keys = [c.strip() for c in args.verify_configs.split(",") if c.strip()]
+    ok = True
+    for key in keys:
+        r = verify_config(key)
+        ok &= r["pass"]
+        emit(r)
+    return 0 if ok else 1
+
+
+def spawn_ranks(n: int, argv: list) -> int:
+    """`bench.py --gpus N` without a launcher: start N ranks (one process per GPU) through
+    torch.distributed.run on this node, rendezvous on 127.0.0.1; rank 0 prints the line."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *argv]
+    return subprocess.call(cmd)
 
 
 def main(argv=None) -> int:
@@ -974,13 +1302,22 @@ def main(argv=None) -> int:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-naive", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-k9", action="store_true", help="default config: skip the config 3 (k = 9) sub-record")
+    ap.add_argument("--no-parity", action="store_true", help="skip the parity record against the reference")
+    ap.add_argument("--verify", action="store_true",
+                    help="full-size parity of the configs' outputs against the reference (no timing)")
+    ap.add_argument("--verify-configs", default=",".join(VERIFY_CONFIGS))
     ap.add_argument("--plain", action="store_true", help="profiling mode: plain launches only")
     ap.add_argument("--naive-plain", action="store_true", help="with --plain: also run the naive path")
     args = ap.parse_args(argv)
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and not args.verify:
+        return spawn_ranks(args.gpus, sys.argv[1:] if argv is None else list(argv))
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.verify:
+        return run_verify(args)
     return run_ours(args)
 
 

@@ -56,6 +56,62 @@ def _cuda(t: torch.Tensor, dtype: torch.dtype, name: str) -> torch.Tensor:
     return t.contiguous()
 
 
+_IDX_DTYPES = (torch.int32,) + ((torch.uint32,) if hasattr(torch, "uint32") else ())
+
+
+def _shape_ok(shape, want) -> bool:
+    return len(shape) == len(want) and all(w is None or s == w for s, w in zip(shape, want))
+
+
+def _dev_in(t, dtypes, name: str, shape=None, numel=None) -> torch.Tensor:
+    """A device input: CUDA tensor of one of `dtypes`, made contiguous, with the exact
+    shape (None = any extent) or element count the C ABI will read."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    dtypes = dtypes if isinstance(dtypes, tuple) else (dtypes,)
+    if t.dtype not in dtypes:
+        raise TypeError(f"{name} must be {' or '.join(map(str, dtypes))}, got {t.dtype}")
+    if shape is not None and not _shape_ok(tuple(t.shape), shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {shape}")
+    if numel is not None and t.numel() != numel:
+        raise ValueError(f"{name}: {t.numel()} elements, expected {numel}")
+    return t.contiguous()
+
+
+def _dev_out(t, name: str, shape, dtype=torch.float32) -> Optional[torch.Tensor]:
+    """A caller-supplied device output: written in place, so it must already be contiguous."""
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dtype:
+        raise TypeError(f"{name} must be a {dtype} CUDA tensor")
+    if not t.is_contiguous() or t.numel() != int(np.prod(shape)):
+        raise ValueError(f"{name}: must be contiguous with shape {tuple(shape)}, got {tuple(t.shape)}")
+    return t
+
+
+def _host_arr(a, dtypes, name: str, numel: int, writable: bool = False) -> Optional[np.ndarray]:
+    """A host buffer the C ABI reads (or, writable, fills): exact dtype, C-contiguous, size."""
+    if a is None:
+        return None
+    if not isinstance(a, np.ndarray):
+        raise TypeError(f"{name} must be a numpy array")
+    dtypes = dtypes if isinstance(dtypes, tuple) else (dtypes,)
+    if a.dtype not in [np.dtype(d) for d in dtypes]:
+        raise TypeError(f"{name} must be {' or '.join(np.dtype(d).name for d in dtypes)}, got {a.dtype}")
+    if not a.flags.c_contiguous or (writable and not a.flags.writeable):
+        raise ValueError(f"{name} must be a C-contiguous{' writable' if writable else ''} array")
+    if a.size != numel:
+        raise ValueError(f"{name}: {a.size} elements, expected {numel}")
+    return a
+
+
+def _codes_table(a, k: int, name: str) -> np.ndarray:
+    lc = np.ascontiguousarray(a, dtype=np.float32)
+    if lc.ndim != 2 or lc.shape[1] != k:
+        raise ValueError(f"{name}: shape {lc.shape}, expected (rows, {k})")
+    return lc
+
+
 class Context:
     """One hc_ctx per device; enqueues on torch's current stream at each call."""
 
@@ -164,9 +220,14 @@ class Codec:
         return out
 
     # ------------------------------------------------------------ codec
+    def _rows(self, t: torch.Tensor, width: int, name: str) -> int:
+        if t.numel() % width:
+            raise ValueError(f"{name}: {t.numel()} elements is not a whole number of {width}-wide rows")
+        return t.numel() // width
+
     def encode(self, S: torch.Tensor) -> torch.Tensor:
         S = _cuda(S, torch.float32, "S")
-        rows = S.numel() // self.n
+        rows = self._rows(S, self.n, "S")
         Z = self.ctx.empty(rows, self.k)
         self.ctx.bind_stream()
         _check(_lib.lib().hc_encode(self.h, _p(S), rows, _p(Z)))
@@ -175,7 +236,7 @@ class Codec:
     def decode(self, Z: torch.Tensor, spectra: bool = True, xyz: bool = False, rgb: bool = False,
                check_negative: bool = False) -> dict:
         Z = _cuda(Z, torch.float32, "Z")
-        rows = Z.numel() // self.k
+        rows = self._rows(Z, self.k, "Z")
         out = {"spectra": self.ctx.empty(rows, self.n) if spectra else None,
                "xyz": self.ctx.empty(rows, 3) if xyz else None,
                "rgb": self.ctx.empty(rows, 3) if rgb else None}
@@ -189,12 +250,14 @@ class Codec:
     def roundtrip(self, S: torch.Tensor, codes: bool = True, spectra: bool = True, xyz: bool = True,
                   rgb: bool = True, out: Optional[dict] = None) -> dict:
         S = _cuda(S, torch.float32, "S")
-        rows = S.numel() // self.n
+        rows = self._rows(S, self.n, "S")
         if out is None:
             out = {"codes": self.ctx.empty(rows, self.k) if codes else None,
                    "spectra": self.ctx.empty(rows, self.n) if spectra else None,
                    "xyz": self.ctx.empty(rows, 3) if xyz else None,
                    "rgb": self.ctx.empty(rows, 3) if rgb else None}
+        for key, w in (("codes", self.k), ("spectra", self.n), ("xyz", 3), ("rgb", 3)):
+            _dev_out(out.get(key), key, (rows, w))
         self.ctx.bind_stream()
         _check(_lib.lib().hc_roundtrip(self.h, _p(S), rows, _p(out.get("codes")), _p(out.get("spectra")),
                                        _p(out.get("xyz")), _p(out.get("rgb"))))
@@ -202,25 +265,33 @@ class Codec:
 
     def spectra_to_xyz_rgb(self, S: torch.Tensor) -> dict:
         S = _cuda(S, torch.float32, "S")
-        rows = S.numel() // self.n
+        rows = self._rows(S, self.n, "S")
         out = {"xyz": self.ctx.empty(rows, 3), "rgb": self.ctx.empty(rows, 3)}
         self.ctx.bind_stream()
         _check(_lib.lib().hc_spectra_to_xyz_rgb(self.h, _p(S), rows, _p(out["xyz"]), _p(out["rgb"])))
         return out
 
     # ------------------------------------------------------------ shading
+    def _gbuffer(self, idx, cosv, L: int):
+        P = idx.numel() if isinstance(idx, torch.Tensor) else 0
+        idx = _dev_in(idx, _IDX_DTYPES, "idx", numel=P)
+        cosv = _dev_in(cosv, torch.float32, "cosv", numel=P * L)
+        return idx, cosv, P
+
     def shade_latent(self, pal_codes: torch.Tensor, light_codes: np.ndarray, idx: torch.Tensor,
                      cosv: torch.Tensor, latent: bool = False, spectra: bool = False, xyz: bool = True,
                      rgb: bool = True, out: Optional[dict] = None) -> dict:
-        pal_codes = _cuda(pal_codes, torch.float32, "pal_codes")
-        lc = np.ascontiguousarray(light_codes, dtype=np.float32)
+        pal_codes = _dev_in(pal_codes, torch.float32, "pal_codes", shape=(None, self.k))
+        lc = _codes_table(light_codes, self.k, "light_codes")
         L = lc.shape[0]
-        P = idx.numel()
+        idx, cosv, P = self._gbuffer(idx, cosv, L)
         if out is None:
             out = {"latent": self.ctx.empty(P, self.k) if latent else None,
                    "spectra": self.ctx.empty(P, self.n) if spectra else None,
                    "xyz": self.ctx.empty(P, 3) if xyz else None,
                    "rgb": self.ctx.empty(P, 3) if rgb else None}
+        for key, w in (("latent", self.k), ("spectra", self.n), ("xyz", 3), ("rgb", 3)):
+            _dev_out(out.get(key), key, (P, w))
         self.ctx.bind_stream()
         _check(_lib.lib().hc_shade_latent(self.h, _p(pal_codes), pal_codes.shape[0], _np_ptr(lc), L, _p(idx),
                                           _p(cosv), P, _p(out.get("latent")), _p(out.get("spectra")),
@@ -229,8 +300,9 @@ class Codec:
 
     def shade_latent_pass(self, pass_index: int, pal_codes: torch.Tensor, light_codes: np.ndarray,
                           idx: torch.Tensor, cosv: torch.Tensor) -> torch.Tensor:
-        lc = np.ascontiguousarray(light_codes, dtype=np.float32)
-        P = idx.numel()
+        pal_codes = _dev_in(pal_codes, torch.float32, "pal_codes", shape=(None, self.k))
+        lc = _codes_table(light_codes, self.k, "light_codes")
+        idx, cosv, P = self._gbuffer(idx, cosv, lc.shape[0])
         img = self.ctx.empty(P, 3)
         self.ctx.bind_stream()
         _check(_lib.lib().hc_shade_latent_pass(self.h, pass_index, _p(pal_codes), pal_codes.shape[0],
@@ -239,24 +311,39 @@ class Codec:
 
     def shade_spectral(self, pal_spectra: torch.Tensor, light_spectra: np.ndarray, idx: torch.Tensor,
                        cosv: torch.Tensor, spectra: bool = False, out: Optional[dict] = None) -> dict:
-        pal_spectra = _cuda(pal_spectra, torch.float32, "pal_spectra")
-        ls = np.ascontiguousarray(light_spectra, dtype=np.float32)
-        P = idx.numel()
+        pal_spectra = _dev_in(pal_spectra, torch.float32, "pal_spectra", shape=(None, self.n))
+        ls = _codes_table(light_spectra, self.n, "light_spectra")
+        idx, cosv, P = self._gbuffer(idx, cosv, ls.shape[0])
         if out is None:
             out = {"spectra": self.ctx.empty(P, self.n) if spectra else None,
                    "xyz": self.ctx.empty(P, 3), "rgb": self.ctx.empty(P, 3)}
+        for key, w in (("spectra", self.n), ("xyz", 3), ("rgb", 3)):
+            _dev_out(out.get(key), key, (P, w))
         self.ctx.bind_stream()
         _check(_lib.lib().hc_shade_spectral(self.h, _p(pal_spectra), pal_spectra.shape[0], _np_ptr(ls),
                                             ls.shape[0], _p(idx), _p(cosv), P, _p(out.get("spectra")),
                                             _p(out.get("xyz")), _p(out.get("rgb"))))
         return out
 
+    def _chain(self, table, ill, pidx, iidx, tw, width: int):
+        if not isinstance(iidx, torch.Tensor) or iidx.dim() != 2:
+            raise ValueError("iidx must be a [P, spp] CUDA tensor")
+        P, spp = iidx.shape
+        table = _dev_in(table, torch.float32, "palette", shape=(None, width))
+        ill = _dev_in(ill, torch.float32, "illuminants", shape=(None, width))
+        pidx = _dev_in(pidx, torch.uint8, "pidx", numel=P * spp * 4)
+        iidx = _dev_in(iidx, torch.uint8, "iidx", numel=P * spp)
+        tw = _dev_in(tw, torch.float32, "tw", numel=P * spp * 4)
+        return table, ill, pidx, iidx, tw, P, spp
+
     def multibounce_latent(self, pal_codes, ill_codes, pidx, iidx, tw, latent: bool = False,
                            out: Optional[dict] = None) -> dict:
-        P, spp = iidx.shape
+        pal_codes, ill_codes, pidx, iidx, tw, P, spp = self._chain(pal_codes, ill_codes, pidx, iidx, tw, self.k)
         if out is None:
             out = {"latent": self.ctx.empty(P, self.k) if latent else None,
                    "xyz": self.ctx.empty(P, 3), "rgb": self.ctx.empty(P, 3)}
+        for key, w in (("latent", self.k), ("xyz", 3), ("rgb", 3)):
+            _dev_out(out.get(key), key, (P, w))
         self.ctx.bind_stream()
         _check(_lib.lib().hc_multibounce_latent(self.h, _p(pal_codes), pal_codes.shape[0], _p(ill_codes),
                                                 ill_codes.shape[0], _p(pidx), _p(iidx), _p(tw), P, spp,
@@ -264,9 +351,12 @@ class Codec:
         return out
 
     def multibounce_spectral(self, pal_spectra, ill_spectra, pidx, iidx, tw, out: Optional[dict] = None) -> dict:
-        P, spp = iidx.shape
+        pal_spectra, ill_spectra, pidx, iidx, tw, P, spp = self._chain(pal_spectra, ill_spectra, pidx, iidx, tw,
+                                                                       self.n)
         if out is None:
             out = {"xyz": self.ctx.empty(P, 3), "rgb": self.ctx.empty(P, 3)}
+        for key in ("xyz", "rgb"):
+            _dev_out(out.get(key), key, (P, 3))
         self.ctx.bind_stream()
         _check(_lib.lib().hc_multibounce_spectral(self.h, _p(pal_spectra), pal_spectra.shape[0], _p(ill_spectra),
                                                   ill_spectra.shape[0], _p(pidx), _p(iidx), _p(tw), P, spp,
@@ -276,9 +366,12 @@ class Codec:
     def hadamard_loss(self, A: torch.Tensor, B: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         A = _cuda(A, torch.float32, "A")
         B = _cuda(B, torch.float32, "B")
-        pairs = A.numel() // self.n
+        pairs = self._rows(A, self.n, "A")
+        if B.numel() != A.numel():
+            raise ValueError("hadamard_loss: A and B must hold the same number of spectra")
         if out is None:
             out = self.ctx.empty(1, dtype=torch.float64)
+        _dev_out(out, "out", (1,), torch.float64)
         self.ctx.bind_stream()
         _check(_lib.lib().hc_hadamard_loss(self.h, _p(A), _p(B), pairs, _p(out)))
         return out
@@ -286,31 +379,42 @@ class Codec:
     # ------------------------------------------------------------ host-buffer (reference-facing) calls
     def shade_latent_host(self, pal_codes: np.ndarray, light_codes: np.ndarray, idx: np.ndarray,
                           cosv: np.ndarray, xyz: np.ndarray, rgb: np.ndarray) -> None:
-        lc = np.ascontiguousarray(light_codes, dtype=np.float32)
+        pal = _codes_table(pal_codes, self.k, "pal_codes")
+        lc = _codes_table(light_codes, self.k, "light_codes")
+        P = idx.size if isinstance(idx, np.ndarray) else 0
+        _host_arr(idx, (np.uint32, np.int32), "idx", P)
+        _host_arr(cosv, np.float32, "cosv", P * lc.shape[0])
+        _host_arr(xyz, np.float32, "xyz", P * 3, writable=True)
+        _host_arr(rgb, np.float32, "rgb", P * 3, writable=True)
         self.ctx.bind_stream()
-        _check(_lib.lib().hc_shade_latent_host(self.h, _np_ptr(pal_codes), pal_codes.shape[0], _np_ptr(lc),
-                                               lc.shape[0], _np_ptr(idx), _np_ptr(cosv), idx.size, _np_ptr(xyz),
-                                               _np_ptr(rgb)))
+        _check(_lib.lib().hc_shade_latent_host(self.h, _np_ptr(pal), pal.shape[0], _np_ptr(lc),
+                                               lc.shape[0], _np_ptr(idx), _np_ptr(cosv), P,
+                                               None if xyz is None else _np_ptr(xyz),
+                                               None if rgb is None else _np_ptr(rgb)))
 
     def shade_latent_host_frames(self, pal_codes: np.ndarray, light_codes: np.ndarray, frames) -> None:
         """A frame stream through one host-buffer pipeline (hc_shade_latent_host_frames).
 
         frames: sequence of (idx, cosv, xyz, rgb) host arrays of P pixels each (xyz / rgb may be
-        None); outputs are identical to one shade_latent_host call per frame."""
+        None); outputs are identical to one shade_latent_host call per frame.  Copies overlap
+        the kernels only for page-locked (pinned) buffers."""
         import ctypes as C
 
-        lc = np.ascontiguousarray(light_codes, dtype=np.float32)
+        pal = _codes_table(pal_codes, self.k, "pal_codes")
+        lc = _codes_table(light_codes, self.k, "light_codes")
         nf = len(frames)
         if nf == 0:
             return
-        P = frames[0][0].size
-        for f in frames:
-            if f[0].size != P or f[1].size != P * lc.shape[0]:
-                raise ValueError("all frames must have P pixels and L cos terms per pixel")
+        P = frames[0][0].size if isinstance(frames[0][0], np.ndarray) else 0
+        for i, f in enumerate(frames):
+            _host_arr(f[0], (np.uint32, np.int32), f"frames[{i}].idx", P)
+            _host_arr(f[1], np.float32, f"frames[{i}].cosv", P * lc.shape[0])
+            _host_arr(f[2], np.float32, f"frames[{i}].xyz", P * 3, writable=True)
+            _host_arr(f[3], np.float32, f"frames[{i}].rgb", P * 3, writable=True)
         tab = [(C.c_void_p * nf)(*[(_np_ptr(f[j]) if f[j] is not None else None) for f in frames])
                for j in range(4)]
         self.ctx.bind_stream()
-        _check(_lib.lib().hc_shade_latent_host_frames(self.h, _np_ptr(pal_codes), pal_codes.shape[0], _np_ptr(lc),
+        _check(_lib.lib().hc_shade_latent_host_frames(self.h, _np_ptr(pal), pal.shape[0], _np_ptr(lc),
                                                       lc.shape[0], nf, C.addressof(tab[0]), C.addressof(tab[1]), P,
                                                       C.addressof(tab[2]), C.addressof(tab[3])))
 
@@ -318,7 +422,11 @@ class Codec:
                        xyz: Optional[np.ndarray] = None, rgb: Optional[np.ndarray] = None) -> None:
         """Host-buffer round trip (encode -> decode_image -> image_to_linear_rgb); outputs may be None."""
         S = np.ascontiguousarray(S, dtype=np.float32)
+        if S.size % self.n:
+            raise ValueError(f"S: {S.size} elements is not a whole number of {self.n}-sample spectra")
         rows = S.size // self.n
+        for a, name, w in ((Z, "Z", self.k), (S2, "S2", self.n), (xyz, "xyz", 3), (rgb, "rgb", 3)):
+            _host_arr(a, np.float32, name, rows * w, writable=True)
         self.ctx.bind_stream()
         _check(_lib.lib().hc_roundtrip_host(self.h, _np_ptr(S), rows, *[None if a is None else _np_ptr(a)
                                                                         for a in (Z, S2, xyz, rgb)]))

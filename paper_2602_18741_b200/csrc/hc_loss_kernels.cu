@@ -30,8 +30,9 @@ __global__ void sum_partials_kernel(const double* partials, int count, double* o
 
 template <int N, int K>
 int loss_nk(hc_codec c, const float* A, const float* B, int64_t pairs, double* sum_dev) {
-  // 64-pair tiles x 2 stages = 83 KB smem: 2 CTAs / SM, one tile computing + one loading each
-  using Op = LossOp<N, K, HC_LOSS_T, HC_LOSS_T, HC_LOSS_STAGES>;
+  // 64-pair tiles (two 64-thread halves) x 2 stages = 96 KB smem: 2 CTAs / SM (8 warps), one
+  // tile computing + one loading each
+  using Op = LossOp<N, K, HC_LOSS_T, HC_LOSS_GROUPS * HC_LOSS_T, HC_LOSS_STAGES>;
   hc_ctx ctx = c->ctx;
   int rc = configure_tile_op<Op>();
   if (rc != HC_OK) return rc;
@@ -43,17 +44,13 @@ int loss_nk(hc_codec c, const float* A, const float* B, int64_t pairs, double* s
     ctx->partial_capacity = cap;
   }
   typename Op::Params p;
-  fill_codec_const<N, K>(c, &p.cc);
-  for (int j = 0; j < K; ++j)
-    for (int l = 0; l < K; ++l) {
-      double g = 0.0;
-      for (int i = 0; i < N; ++i) g += static_cast<double>(c->D[i * K + j]) * static_cast<double>(c->D[i * K + l]);
-      p.G[j * K + l] = static_cast<float>(g);
-    }
+  for (int i = 0; i < K * N; ++i) p.E[i] = static_cast<double>(c->E[i]);
+  for (int i = 0; i < N * K; ++i) p.D[i] = static_cast<double>(c->D[i]);
   p.a = A;
   p.b = B;
   p.partials = ctx->d_partials;
   p.partial_offset = 0;
+  p.pairs = pairs;
   // Main (TMA) pass over full tiles first, then the tail with offset partials.
   const bool aligned = al16(A) && al16(B);
   const int64_t full = aligned ? pairs / Op::T : 0;

@@ -22,15 +22,29 @@
 //   setup(p, extra_smem), compute(p, st, in[], out[], extra, item, global_item),
 //   finish(p, st, extra),
 //   kWarpSpecialized (run tile_pipeline_ws instead of tile_pipeline),
-//   kEvictFirstLoads (stream the inputs through L2 with an evict-first policy)
+//   kEvictFirstLoads (stream the inputs through L2 with an evict-first policy),
+//   optionally kLanesPerItem (default 1): that many threads call compute() for
+//   the same item -- threads item, item + THREADS/LPI, ... (warp groups) -- and
+//   the op splits the item's work by threadIdx.x / (THREADS/LPI)
 // Ragged tails and unaligned pointers go through tile_generic, which runs the
 // same compute on word copies (no TMA; the swizzle is applied in software).
 #pragma once
+
+#include <type_traits>
 
 #include "hc_common.cuh"
 #include "hc_tma.cuh"
 
 namespace hcb {
+
+template <class Op, class = void>
+struct LanesPerItem {
+  static constexpr int value = 1;
+};
+template <class Op>
+struct LanesPerItem<Op, std::void_t<decltype(Op::kLanesPerItem)>> {
+  static constexpr int value = Op::kLanesPerItem;
+};
 
 constexpr int kTileAlign = 1024;  // every stream tile starts 1024-byte aligned (swizzle requirement)
 
@@ -140,7 +154,8 @@ __global__ void __launch_bounds__(Op::THREADS)
     for (int i = 0; i < Op::NIN; ++i) ins[i] = in_base + s * Lay::kInTile + Lay::in_off(i);
 #pragma unroll
     for (int i = 0; i < Op::NOUT; ++i) outs[i] = out_base + s * Lay::kOutTile + Lay::out_off(i);
-    for (int item = tid; item < T; item += Op::THREADS)
+    constexpr int LPI = LanesPerItem<Op>::value;
+    for (int item = tid % (Op::THREADS / LPI); item < T; item += Op::THREADS / LPI)
       Op::compute(p, st, ins, outs, extra, item, tile * T + item);
     if (Op::NOUT > 0) fence_proxy_async_smem();
     __syncthreads();
@@ -332,7 +347,10 @@ __global__ void __launch_bounds__(Op::THREADS)
 #pragma unroll
     for (int i = 0; i < Op::NOUT; ++i) outs[i] = out_base + Lay::out_off(i);
     __syncthreads();
-    for (int item = tid; item < cnt; item += Op::THREADS)
+    // Ops with several lanes per item run every item of the tile (whole warps take
+    // part in their shuffles); they discard items at or past item_end themselves.
+    constexpr int LPI = LanesPerItem<Op>::value;
+    for (int item = tid % (Op::THREADS / LPI); item < (LPI > 1 ? T : cnt); item += Op::THREADS / LPI)
       Op::compute(p, st, ins, outs, extra, item, first + item);
     __syncthreads();
 #pragma unroll

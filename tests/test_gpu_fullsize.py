@@ -1,0 +1,40 @@
+"""Full-size parity on the bench's own tensors (SURVEY §8d "parity on the full outputs").
+
+`bench.py --verify` runs one step of each BASELINE config at its full size with the bench's
+inputs (seed, generators, buffer set 0) and checks the outputs against the reference compiled
+from its sources (oracle/_ref, all host threads) on the same inputs: configs 1, 2, 3, 5a and
+5b on the whole output, config 4 on every 16th row.  Those runs also cross the > 2^31-byte
+offsets (config 3 writes 2.69 GB of spectra, config 5b reads two 5.4 GB arrays, config 4
+reads a 4.3 GB throughput array).  Tolerances: 1e-5 relative (fp32 outputs, fp64 loss),
+1e-2 for the bf16 MLP.
+"""
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+def _verify(configs: str) -> list:
+    if not (ROOT / "oracle" / "_ref" / "libhcref81.so").exists():
+        pytest.skip("oracle/_ref not built")
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--verify", "--verify-configs", configs], cwd=ROOT,
+                       capture_output=True, text=True, timeout=1800)
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    for ln in lines:
+        print(json.dumps(ln))
+    assert lines, r.stderr[-3000:]
+    return lines
+
+
+@pytest.mark.parametrize("configs", ["1,2,3", "4,5a,5b"])
+def test_full_size_parity(configs):
+    lines = _verify(configs)
+    assert [ln["verify"] for ln in lines] == configs.split(",")
+    for ln in lines:
+        for c in ln["checks"]:
+            assert c["pass"], f"config {ln['verify']} {c}"
