@@ -405,6 +405,34 @@ int hc_synth_uniform(hc_ctx ctx, uint64_t key, int64_t first, int64_t count, flo
 /* Write `bytes` of garbage over a device buffer (L2 flush between timed steps). */
 int hc_flush_l2(hc_ctx ctx, void* buf, int64_t bytes);
 
+/* ------------------------------------------------------------------ several GPUs
+ * Replaces the renderer's row-scheduled thread pool (renderer.cpp:573-608,
+ * HADACODEC_THREADS :615-621) across devices: an image is cut into contiguous row
+ * bands, one per GPU, each driven by its own host thread, context and stream.
+ * hc_row_band: rows [*row0, *row0 + *rows) of rank `rank` of `world` over `height`
+ * rows; sizes differ by at most one row (the Python sharding module calls this too). */
+int hc_row_band(int rank, int world, int64_t height, int64_t* row0, int64_t* rows);
+typedef struct hc_group_s* hc_group;
+#define HC_GATHER_HOST 0 /* each device copies its band into the host image (own PCIe link) */
+#define HC_GATHER_NCCL 1 /* bands -> device 0 by grouped ncclSend / ncclRecv, one D2H copy */
+#define HC_GATHER_PEER 2 /* bands -> device 0 by cudaMemcpyPeerAsync, one D2H copy */
+/* devices[ndev] (distinct for HC_GATHER_NCCL: ncclCommInitAll); NCCL is loaded at run time
+ * (libnccl.so.2) and its absence is HC_EUNSUPPORTED for that mode. */
+int hc_group_create(const int* devices, int ndev, int gather, hc_group* out);
+int hc_group_destroy(hc_group g);
+int hc_group_size(hc_group g);
+/* Version of the NCCL library the group layer loaded (e.g. 22809), 0 if none. */
+int hc_group_nccl_version(void);
+/* One codec per device (the arguments of hc_codec_create). */
+int hc_group_codec_create(hc_group g, int k, int n, const float* E, const float* D, const double* cmf,
+                          double dlambda);
+/* hc_shade_latent_host over a width x height frame split into row bands across the group:
+ * host G-buffer in (idx [P], cosv [P][L]), host XYZ / sRGB out ([P][3], may be NULL);
+ * bit-identical to one hc_shade_latent_host call on the whole frame. */
+int hc_group_shade_latent_host(hc_group g, const float* pal_codes, int n_pal, const float* light_codes, int L,
+                               const uint32_t* idx, const float* cosv, int64_t width, int64_t height, float* xyz,
+                               float* rgb);
+
 #ifdef __cplusplus
 }
 #endif

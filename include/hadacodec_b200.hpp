@@ -17,16 +17,28 @@
 #pragma once
 
 #include <array>
+#include <cstddef>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <vector>
 
 #include "hadacodec_b200.h"
 
 namespace hadacodec {
 namespace b200 {
+
+// spectrum.hpp:10-21 — the reference's canonical grid (source compatibility: the
+// reference-signature overloads below default to it; the BASELINE grid is Grid::baseline81).
+inline constexpr int kSampleCount = 47;
+inline constexpr double kLambdaMin = 368.0;
+inline constexpr double kLambdaMax = 830.0;
+inline constexpr double kLambdaStep = (kLambdaMax - kLambdaMin) / (kSampleCount - 1);
+inline constexpr double kActiveBandMin = 400.0;
+inline constexpr double kActiveBandMax = 700.0;
+constexpr double wavelength_at(int i) { return kLambdaMin + kLambdaStep * i; }
 
 // spectrum.hpp:10-21 — runtime grid.
 struct Grid {
@@ -39,14 +51,28 @@ struct Grid {
   static Grid for_samples(int n);
 };
 
-// spectrum.hpp:25-39
+// spectrum.hpp:25-39.  Default-constructed curves have the reference's kSampleCount zero
+// samples (as its std::array); SpectralCurve(81) is a curve on the BASELINE grid.
 struct SpectralCurve {
   std::vector<double> v;
-  SpectralCurve() = default;
+  SpectralCurve() : v(static_cast<size_t>(kSampleCount), 0.0) {}
   explicit SpectralCurve(int n, double value = 0.0) : v(static_cast<size_t>(n), value) {}
   int size() const { return static_cast<int>(v.size()); }
   double& operator[](int i) { return v[static_cast<size_t>(i)]; }
   const double& operator[](int i) const { return v[static_cast<size_t>(i)]; }
+  static SpectralCurve flat(double value) { return SpectralCurve(kSampleCount, value); }
+  static SpectralCurve zero() { return SpectralCurve(); }
+  static SpectralCurve ones() { return flat(1.0); }
+  double max_value() const {
+    double m = v.empty() ? 0.0 : v[0];
+    for (double x : v) m = x > m ? x : m;
+    return m;
+  }
+  double sum() const {
+    double t = 0.0;
+    for (double x : v) t += x;
+    return t;
+  }
 };
 
 // codec.hpp:14-22
@@ -67,7 +93,7 @@ struct CodecTrainingMeta {
 // codec.hpp:34-43
 struct CodecWeights {
   int k = 6;
-  int n = 81;
+  int n = kSampleCount;
   double beta = 10.0;
   std::vector<double> raw_enc;  // k x n
   std::vector<double> raw_dec;  // n x k
@@ -328,6 +354,71 @@ std::vector<ShadedFrame> shade_latent_frames(const Codec& c, const std::vector<f
 // Naive n-sample path on the same G-buffer (palette_spectra n_pal x n, light_spectra L x n).
 ShadedFrame shade_spectral(const Codec& c, const std::vector<float>& palette_spectra,
                            const std::vector<float>& light_spectra, const GBuffer& g);
+
+// ===================================================================== reference signatures
+// The reference's free functions with its exact signatures (codec.hpp:60-78,
+// colorimetry.hpp:47-55, renderer.hpp:100-133, upsampler.hpp:32-40, spectrum.hpp:42-72,
+// rng.hpp), so code written against `hadacodec` compiles against `hadacodec::b200` with only
+// the namespace changed.  The GPU work runs on a per-thread default Device (CUDA device
+// HADACODEC_B200_DEVICE, default 0) with codecs / upsamplers cached by the weights they were
+// built from (a small per-thread LRU keyed by the weight arrays), so repeated calls with the
+// same weights pay the upload once.  Grids come from the curves / weights (47 or 81 samples).
+Device& default_device();
+
+// ---- spectrum.hpp:42-72 (host value helpers)
+bool curve_is_valid(const SpectralCurve& s, bool reflectance = false);
+SpectralCurve scale(const SpectralCurve& s, double alpha);  // std::domain_error for alpha < 0 / non-finite
+SpectralCurve add(const SpectralCurve& a, const SpectralCurve& b);
+SpectralCurve hadamard(const SpectralCurve& a, const SpectralCurve& b);
+SpectralCurve resample(const std::vector<double>& source_wavelengths, const std::vector<double>& source_values,
+                       bool zero_outside_active_band);  // onto the kSampleCount grid
+void zero_outside_active_band(SpectralCurve& s);
+SpectralCurve gaussian_curve(double center_nm, double sigma_nm, double amplitude);
+
+// ---- rng.hpp: the reference's deterministic streams (xoshiro256++ seeded by splitmix64)
+std::uint64_t fnv1a64(const void* data, std::size_t size, std::uint64_t basis = 0xcbf29ce484222325ull);
+std::uint64_t splitmix64_next(std::uint64_t& state);
+class Rng {
+ public:
+  explicit Rng(std::uint64_t seed);
+  static Rng stream(std::uint64_t seed, std::string_view purpose);
+  static Rng pixel_stream(std::uint64_t seed, int x, int y, int sample, std::uint32_t lane);
+  std::uint64_t next_u64();
+  double uniform();
+  double uniform(double a, double b);
+  double log_uniform(double a, double b);
+  std::uint32_t index(std::uint32_t n);
+  double normal();
+
+ private:
+  std::uint64_t s_[4];
+  double cached_normal_ = 0.0;
+  bool has_cached_normal_ = false;
+};
+
+// ---- codec.hpp:60-78
+void validate(const CodecWeights& w);  // n must be a supported grid (47 or 81)
+LatentCode encode(const EffectiveWeights& w, const SpectralCurve& s);
+LatentCode encode(const CodecWeights& w, const SpectralCurve& s);
+SpectralCurve decode(const EffectiveWeights& w, const LatentCode& z);  // std::domain_error on negative codes
+SpectralCurve decode(const CodecWeights& w, const LatentCode& z);
+
+// ---- colorimetry.hpp:47 (radiance convention, on the curve's grid)
+ColorTriple spectrum_to_xyz(const SpectralCurve& s);
+
+// ---- renderer.hpp:100-133
+ChannelImage render(const Scene& scene, const RenderJob& job, const CodecWeights* codec = nullptr);
+ChannelImage render_latent_multipass(const Scene& scene, const RenderJob& job, const CodecWeights& codec);
+ChannelImage decode_image(const ChannelImage& latent, const CodecWeights& w);
+ChannelImage image_to_linear_rgb(const ChannelImage& img);
+double exposure_for(const ChannelImage& img, double percentile = 99.5);
+std::vector<unsigned char> tonemap_srgb8(const ChannelImage& linear_rgb, double exposure);
+ErrorMap error_map(const ChannelImage& a, const ChannelImage& b);
+
+// ---- upsampler.hpp:32-40
+LatentCode upsample_raw(const UpsamplerWeights& w, const std::array<double, 3>& linear_rgb);
+LatentCode upsample(const UpsamplerWeights& w, const std::array<double, 3>& linear_rgb,
+                    std::uint64_t* clamped_entries = nullptr);
 
 }  // namespace b200
 }  // namespace hadacodec

@@ -47,6 +47,13 @@ SIGNATURES: dict[str, tuple] = {
     "hc_mlp_destroy": (i32, [vp]),
     "hc_mlp_forward": (i32, [vp, vp, i64, vp]),
     "hc_hadamard_loss": (i32, [vp, vp, vp, i64, vp]),
+    "hc_row_band": (i32, [i32, i32, i64, C.POINTER(i64), C.POINTER(i64)]),
+    "hc_group_create": (i32, [vp, i32, i32, C.POINTER(vp)]),
+    "hc_group_destroy": (i32, [vp]),
+    "hc_group_size": (i32, [vp]),
+    "hc_group_nccl_version": (i32, []),
+    "hc_group_codec_create": (i32, [vp, i32, i32, vp, vp, vp, f64]),
+    "hc_group_shade_latent_host": (i32, [vp, vp, i32, vp, i32, vp, vp, i64, i64, vp, vp]),
     "hc_exposure_for": (i32, [vp, vp, i64, i32, f64, C.POINTER(f64)]),
     "hc_tonemap_srgb8": (i32, [vp, vp, i64, f64, vp]),
     "hc_error_map": (i32, [vp, vp, i32, vp, i32, i64, vp, C.POINTER(f64)]),

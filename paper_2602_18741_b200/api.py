@@ -432,6 +432,59 @@ class Codec:
                                                                         for a in (Z, S2, xyz, rgb)]))
 
 
+GATHER_MODES = {"host": 0, "nccl": 1, "peer": 2}
+
+
+class Group:
+    """Several GPUs driven from this process (hc_group_*: one host thread, context and stream
+    per device, row bands, gather by host copies / NCCL / peer copies)."""
+
+    def __init__(self, devices: Sequence[int], gather: str = "host"):
+        arr = (C.c_int * len(devices))(*devices)
+        h = C.c_void_p()
+        _check(_lib.lib().hc_group_create(arr, len(devices), GATHER_MODES[gather], C.byref(h)))
+        self.h, self.devices, self.gather = h, list(devices), gather
+        self.k = self.n = None
+
+    @staticmethod
+    def nccl_version() -> int:
+        return int(_lib.lib().hc_group_nccl_version())
+
+    def set_codec(self, E: np.ndarray, D: np.ndarray) -> None:
+        E = np.ascontiguousarray(E, dtype=np.float32)
+        D = np.ascontiguousarray(D, dtype=np.float32)
+        k, n = E.shape
+        if D.shape != (n, k):
+            raise ValueError("codec weights: parameter array size mismatch")
+        cmf = np.ascontiguousarray(cmf_matrix(n), dtype=np.float64)
+        _check(_lib.lib().hc_group_codec_create(self.h, k, n, _np_ptr(E), _np_ptr(D), _np_ptr(cmf), grid(n)[1]))
+        self.k, self.n = k, n
+
+    def shade_latent_host(self, pal_codes: np.ndarray, light_codes: np.ndarray, idx: np.ndarray, cosv: np.ndarray,
+                          width: int, height: int, xyz: Optional[np.ndarray], rgb: Optional[np.ndarray]) -> None:
+        if self.k is None:
+            raise ValueError("group: set_codec first")
+        pal = _codes_table(pal_codes, self.k, "pal_codes")
+        lc = _codes_table(light_codes, self.k, "light_codes")
+        P = width * height
+        _host_arr(idx, (np.uint32, np.int32), "idx", P)
+        _host_arr(cosv, np.float32, "cosv", P * lc.shape[0])
+        _host_arr(xyz, np.float32, "xyz", P * 3, writable=True)
+        _host_arr(rgb, np.float32, "rgb", P * 3, writable=True)
+        _check(_lib.lib().hc_group_shade_latent_host(self.h, _np_ptr(pal), pal.shape[0], _np_ptr(lc), lc.shape[0],
+                                                     _np_ptr(idx), _np_ptr(cosv), width, height,
+                                                     None if xyz is None else _np_ptr(xyz),
+                                                     None if rgb is None else _np_ptr(rgb)))
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                _lib.lib().hc_group_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 def blockwise_hadamard(ctx: Context, A: torch.Tensor, B: torch.Tensor) -> torch.Tensor:
     """codec.cpp:77-85, batched over rows."""
     if A.shape != B.shape:

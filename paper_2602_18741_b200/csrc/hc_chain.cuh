@@ -132,11 +132,17 @@ __global__ void __launch_bounds__(256) chain_latent_kernel(const __grid_constant
 // re-associated (SURVEY Appendix A #7 allows it):
 //   thr_d = thr_{d-1} (.) a_d ;  s = sum_d t_d thr_d ;  rad = le (.) s
 // and each lane sums its samples in fp32 before the fp64 cross-lane reduction.
-template <int K>
+//
+// SHFL_ILL (n_ill <= 16, config 4): the illuminant codes live in registers instead — lane
+// l holds illuminant l % 16 — and each sample's illuminant code is fetched with 2*KP
+// shuffles, so only the 4 palette lookups per sample touch shared memory.  The L1 data
+// pipe (shared-memory wavefronts plus the sample records' global loads) is this kernel's
+// bottleneck (r01 ncu: 83 % busy); the shuffles do not use it.
+template <int K, bool SHFL_ILL>
 __global__ void __launch_bounds__(256) chain_latent_rep_kernel(const __grid_constant__ ChainLatentParams<K> p) {
   constexpr int KP = (K + 1) / 2;  // float2 per code
   extern __shared__ __align__(16) float2 rep[];
-  const int n_ent = p.n_pal + p.n_ill;
+  const int n_ent = SHFL_ILL ? p.n_pal : p.n_pal + p.n_ill;
   constexpr int R = 8;  // loads in flight per thread before its stores (block_load_table)
   for (int base = threadIdx.x; base < n_ent * KP * 16; base += R * blockDim.x) {
     float2 v[R];
@@ -159,6 +165,10 @@ __global__ void __launch_bounds__(256) chain_latent_rep_kernel(const __grid_cons
   const int lane = threadIdx.x & 31;
   const int g = lane & (kChainLanes - 1);
   const float2* mine = rep + (lane & 15);
+  float ill_reg[2 * KP];  // SHFL_ILL: illuminant lane % 16 (zero past n_ill)
+#pragma unroll
+  for (int j = 0; j < 2 * KP; ++j)
+    ill_reg[j] = SHFL_ILL && (lane & 15) < p.n_ill && j < K ? __ldg(p.ill + (lane & 15) * K + j) : 0.f;
   constexpr int kPixPerWarp = 32 / kChainLanes;
   const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -171,7 +181,9 @@ __global__ void __launch_bounds__(256) chain_latent_rep_kernel(const __grid_cons
     for (int j = 0; j < 2 * KP; ++j) part[j] = 0.f;
     const int64_t base = pix * p.spp;
     bool bad = false;
-    const int per_lane = valid ? p.spp / kChainLanes : 0;
+    // SHFL_ILL: every lane runs the sample loop (warp-wide shuffles); a past-the-end pixel's
+    // lanes load nothing and are never stored.
+    const int per_lane = valid || SHFL_ILL ? p.spp / kChainLanes : 0;
     {
       // Warm L2 with the next quad's sample records (no registers held): the 8 lanes
       // of a pixel group each touch one 128-byte line of the next pixel's streams.
@@ -197,7 +209,7 @@ __global__ void __launch_bounds__(256) chain_latent_rep_kernel(const __grid_cons
 #pragma unroll
       for (int m = 0; m < kGroup; ++m) {
         const int64_t s = base + g + static_cast<int64_t>(m0 + m) * kChainLanes;
-        const bool in = m0 + m < per_lane;
+        const bool in = m0 + m < per_lane && valid;
         pkg[m] = in ? __ldg(p.pidx + s) : 0u;
         lig[m] = in ? static_cast<uint32_t>(__ldg(p.iidx + s)) : 0u;
         t4g[m] = in ? ldg_stream(p.tw + s) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -232,12 +244,18 @@ __global__ void __launch_bounds__(256) chain_latent_rep_kernel(const __grid_cons
           }
         }
       }
-      const float2* lrow = mine + (npal + li) * (KP * 16);
+      if constexpr (SHFL_ILL) {
 #pragma unroll
-      for (int c2 = 0; c2 < KP; ++c2) {
-        const float2 le = lrow[c2 * 16];
-        part[2 * c2] = fmaf(le.x, acc[2 * c2], part[2 * c2]);
-        part[2 * c2 + 1] = fmaf(le.y, acc[2 * c2 + 1], part[2 * c2 + 1]);
+        for (int j = 0; j < 2 * KP; ++j)
+          part[j] = fmaf(__shfl_sync(0xffffffffu, ill_reg[j], static_cast<int>(li)), acc[j], part[j]);
+      } else {
+        const float2* lrow = mine + (npal + li) * (KP * 16);
+#pragma unroll
+        for (int c2 = 0; c2 < KP; ++c2) {
+          const float2 le = lrow[c2 * 16];
+          part[2 * c2] = fmaf(le.x, acc[2 * c2], part[2 * c2]);
+          part[2 * c2 + 1] = fmaf(le.y, acc[2 * c2 + 1], part[2 * c2 + 1]);
+        }
       }
     }
     }

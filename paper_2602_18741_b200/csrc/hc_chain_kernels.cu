@@ -59,10 +59,21 @@ int chain_latent_k(hc_codec c, const float* pal, int n_pal, const float* ill, in
   p.err = c->ctx->d_err;
   int grid = 0;
   if constexpr (K <= 6) {
+#ifndef HC_CHAIN_SHFL_ILL
+#define HC_CHAIN_SHFL_ILL 1
+#endif
+    if (HC_CHAIN_SHFL_ILL && n_ill <= 16) {  // illuminant codes by shuffle, palette in smem
+      const int smem = n_pal * ((K + 1) / 2) * 16 * 8;
+      int rc = chain_grid(c->ctx, chain_latent_rep_kernel<K, true>, smem, P, &grid);
+      if (rc != HC_OK) return rc;
+      chain_latent_rep_kernel<K, true><<<grid, 256, smem, c->ctx->stream>>>(p);
+      HC_CHECK_LAUNCH(c->ctx, "chain_latent_rep_kernel");
+      return HC_OK;
+    }
     const int smem = (n_pal + n_ill) * ((K + 1) / 2) * 16 * 8;  // replicated float2 tables
-    int rc = chain_grid(c->ctx, chain_latent_rep_kernel<K>, smem, P, &grid);
+    int rc = chain_grid(c->ctx, chain_latent_rep_kernel<K, false>, smem, P, &grid);
     if (rc != HC_OK) return rc;
-    chain_latent_rep_kernel<K><<<grid, 256, smem, c->ctx->stream>>>(p);
+    chain_latent_rep_kernel<K, false><<<grid, 256, smem, c->ctx->stream>>>(p);
     HC_CHECK_LAUNCH(c->ctx, "chain_latent_rep_kernel");
   } else {
     const int smem = (n_pal + n_ill) * K * 4;

@@ -32,7 +32,7 @@ template <int N, int K>
 int loss_nk(hc_codec c, const float* A, const float* B, int64_t pairs, double* sum_dev) {
   // 64-pair tiles (two 64-thread halves) x 2 stages = 96 KB smem: 2 CTAs / SM (8 warps), one
   // tile computing + one loading each
-  using Op = LossOp<N, K, HC_LOSS_T, HC_LOSS_GROUPS * HC_LOSS_T, HC_LOSS_STAGES>;
+  using Op = LossOp<N, K, HC_LOSS_T, (N % 3 == 0 ? 3 : 1) * HC_LOSS_T, HC_LOSS_STAGES>;
   hc_ctx ctx = c->ctx;
   int rc = configure_tile_op<Op>();
   if (rc != HC_OK) return rc;

@@ -458,6 +458,337 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ===================================================================== mlp2_kernel
+// Layer 1 on the CUDA cores, layers 2 and 3 on the tensor cores.
+//
+// mlp_kernel's per-tile chain is L1 round trip + epilogue 1 + L2 round trip + epilogue 2
+// (~1,900 cycles; tools/mma_latency.cu: a tcgen05.mma + commit round trip is ~474 cycles
+// whatever N), and TMEM holds 3 tile streams, so the SM finishes a tile every ~630 cycles
+// against a 224-cycle tensor-pipe floor.  Layer 1 is only 3 -> 64 (+ bias): per pixel
+// 192 FMAs, i.e. 96 packed FFMA2 (fma.rn.f32x2) on the epilogue thread that owns the
+// pixel's TMEM lane, with the same arithmetic as the tensor core (bf16 inputs and
+// weights, fp32 accumulation, one cvt.rn.relu.bf16x2 per hidden pair).  The thread
+// writes A2 straight into TMEM, so the layer-1 MMA, its commit round trip, the A1 smem
+// tile and epilogue 1's accumulator read all disappear.  A2 of tile t+1 is computed in
+// registers while layer 2 of tile t runs and stored as soon as that layer completes, so
+// a stream's period is one layer-2 round trip + epilogue 2 + the A2 store.
+//
+// Per stream (TMEM lane = pixel row of the tile): A2 [32 cols bf16x2] | A3 [32] | D [64
+// fp32] | D3 [16]; the constant-1 K chunk of A2 (b2 rides the fifth layer-2 MMA) is one
+// 8-column region shared by all streams.  Warps: 4 epilogue warps per stream (one per TMEM
+// lane quarter) + 1 issuer warp per stream (rgb bulk copies, MMAs).  Hand-offs:
+//   epilogue: [regs] A2(t+1) | wait l2(t) -> D3(t-1) -> relu(D) -> A3(t), arrive a3
+//             -> A2(t+1) -> TMEM, arrive a2 | softplus + stores of tile t-1's codes
+//   issuer:   wait a2(t) -> rgb load (t + R) -> L2(t) -> commit l2 | wait a3(t) -> L3(t) -> commit l3
+// One commit covers every earlier MMA of the thread, so l2(t) complete implies L3(t-1)
+// complete: D3(t-1) and the A3 region are free without waiting on l3.
+#ifndef HC_MLP2_STREAMS
+#define HC_MLP2_STREAMS 3
+#endif
+#ifndef HC_MLP2_RING
+#define HC_MLP2_RING 4
+#endif
+#ifndef HC_MLP2_L1_BF16  // 1: layer 1 in packed bf16 FMA (fma.rn.bf16x2) instead of fp32 FFMA2
+#define HC_MLP2_L1_BF16 0
+#endif
+constexpr int kS2 = HC_MLP2_STREAMS;
+constexpr int kRing2 = HC_MLP2_RING;
+constexpr int kEpi2 = 128 * kS2;
+constexpr int kThreads2 = kEpi2 + 32 * kS2;
+constexpr int kCols2 = 144;  // A2 32 | A3 32 | D 64 | D3 16
+constexpr int kColConst2 = kS2 * kCols2;
+static_assert(kColConst2 + 8 <= 512, "TMEM budget");
+constexpr int kOffW2b = 0;                    // W2' image (kW2Bytes)
+constexpr int kOffW3b = kW2Bytes;             // W3 image (kW3Bytes)
+constexpr int kOffRing2 = kW2Bytes + kW3Bytes;
+constexpr int kStream2Bytes = kRing2 * kInTile;
+constexpr int kOffBar2 = kOffRing2 + kS2 * kStream2Bytes;
+constexpr int kBars2 = kRing2 + 4;  // in[R], l2, l3, a2, a3
+constexpr int kSmem2 = kOffBar2 + kS2 * kBars2 * 8 + 16;
+
+struct Mlp2Params {
+  // layer 1, bf16-valued, as (hidden 2i, 2i + 1) pairs: w1p[c][i] = (W1[2i][c], W1[2i+1][c])
+  unsigned long long w1p[3][kHid / 2];
+  unsigned long long b1p[kHid / 2];
+  float b3[kN3];
+  const uint8_t* wimg;  // W2' | W3 canonical images (kW2Bytes + kW3Bytes)
+  const float* rgb;
+  float* out;
+  int64_t first_tile, ntiles, P;
+  int k;
+  int use_tma;
+  int vec2;  // codes rows 8-byte aligned (float2 stores for even k)
+};
+
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+// Layer 1 of one pixel: A2 word i = bf16x2(relu(W1 x + b1)) of hidden units (2i, 2i + 1),
+// element 2i in the low half (the layout epilogue_hidden writes), x = bf16(rgb).
+__device__ __forceinline__ void layer1_row(const Mlp2Params& p, float r, float g, float b, uint32_t (&w)[32]) {
+  const float x0 = __bfloat162float(__float2bfloat16_rn(r));
+  const float x1 = __bfloat162float(__float2bfloat16_rn(g));
+  const float x2 = __bfloat162float(__float2bfloat16_rn(b));
+#if HC_MLP2_L1_BF16
+  const __nv_bfloat162 R = __floats2bfloat162_rn(x0, x0), G = __floats2bfloat162_rn(x1, x1),
+                       B = __floats2bfloat162_rn(x2, x2);
+  auto bf2 = [](unsigned long long v) {
+    const float2 f = make_float2(__uint_as_float(static_cast<uint32_t>(v)), __uint_as_float(static_cast<uint32_t>(v >> 32)));
+    return __floats2bfloat162_rn(f.x, f.y);
+  };
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    __nv_bfloat162 h = __hfma2(R, bf2(p.w1p[0][i]), bf2(p.b1p[i]));
+    h = __hfma2(G, bf2(p.w1p[1][i]), h);
+    h = __hfma2_relu(B, bf2(p.w1p[2][i]), h);
+    w[i] = *reinterpret_cast<uint32_t*>(&h);
+  }
+#else
+  const uint64_t R = f2_pack(x0, x0), G = f2_pack(x1, x1), B = f2_pack(x2, x2);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    uint64_t h = ffma2(R, p.w1p[0][i], p.b1p[i]);
+    h = ffma2(G, p.w1p[1][i], h);
+    h = ffma2(B, p.w1p[2][i], h);
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(h));
+    w[i] = pack_relu_bf16(lo, hi);
+  }
+#endif
+}
+
+template <int ST>
+__device__ __forceinline__ void mlp2_issuer(const Mlp2Params& p, unsigned char* sm, float* ring, int64_t t0,
+                                            int64_t tstride) {
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kOffBar2) + ST * kBars2;
+  uint64_t* bar_in = bars;
+  uint64_t* bar_l2 = bars + kRing2;
+  uint64_t* bar_l3 = bars + kRing2 + 1;
+  uint64_t* bar_a2 = bars + kRing2 + 2;
+  uint64_t* bar_a3 = bars + kRing2 + 3;
+  constexpr uint32_t tA2 = ST * kCols2, tA3 = tA2 + 32, tD = tA2 + 64, tD3 = tA2 + 128, tC = kColConst2;
+  const bool elect = (threadIdx.x & 31) == 0;
+  const uint32_t sW2 = smem_u32(sm + kOffW2b), sW3 = smem_u32(sm + kOffW3b);
+  constexpr uint32_t id64 = idesc_bf16(kMlpM, kHid), id16 = idesc_bf16(kMlpM, kN3);
+  auto load_tile = [&](int64_t t, int s) {
+    mbar_arrive_expect_tx(&bar_in[s], kInTile);
+    bulk_g2s(ring + s * kMlpM * 3, p.rgb + (p.first_tile + t) * kMlpM * 3, kInTile, &bar_in[s]);
+  };
+  if (p.use_tma && elect)
+    for (int s = 0; s < kRing2; ++s)
+      if (t0 + s * tstride < p.ntiles) load_tile(t0 + s * tstride, s);
+  int it = 0;
+  for (int64_t t = t0; t < p.ntiles; t += tstride, ++it) {
+    mbar_wait(bar_a2, it & 1);  // A2(t) in TMEM; its rgb slot has been read
+    if (elect) {
+      if (p.use_tma && t + kRing2 * tstride < p.ntiles) load_tile(t + kRing2 * tstride, it % kRing2);
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < kK2 / 16; ++kk)
+        mma_ts(tD, kk < kHid / 16 ? tA2 + kk * 8 : tC, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128), id64,
+               kk > 0);
+      mma_commit(bar_l2);
+    }
+    __syncwarp();
+    mbar_wait(bar_a3, it & 1);  // A3(t) in TMEM, D(t) and D3(t - 1) read out
+    if (elect) {
+      tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < kK3 / 16; ++kk)
+        mma_ts(tD3, tA3 + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
+      mma_commit(bar_l3);
+    }
+    __syncwarp();
+  }
+  (void)bar_l3;
+}
+
+__global__ void __launch_bounds__(kThreads2, 1) mlp2_kernel(const __grid_constant__ Mlp2Params p) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const bool issuer = tid >= kEpi2;
+  const int st = issuer ? (tid - kEpi2) >> 5 : warp >> 2;
+  const int quarter = warp & 3;
+  const int r = tid & 127;
+  float* ring = reinterpret_cast<float*>(sm + kOffRing2 + st * kStream2Bytes);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kOffBar2) + st * kBars2;
+  uint64_t* bar_in = bars;               // [R] rgb tile landed
+  uint64_t* bar_l2 = bars + kRing2;      // layer-2 MMAs complete (and every earlier MMA)
+  uint64_t* bar_l3 = bars + kRing2 + 1;  // layer-3 MMAs complete
+  uint64_t* bar_a2 = bars + kRing2 + 2;  // A2 in TMEM (4 epilogue warps)
+  uint64_t* bar_a3 = bars + kRing2 + 3;  // A3 in TMEM, D and D3 read (4 epilogue warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + kOffBar2 + kS2 * kBars2 * 8);
+
+  for (int i = tid; i < (kW2Bytes + kW3Bytes) / 16; i += kThreads2)
+    reinterpret_cast<uint4*>(sm)[i] = reinterpret_cast<const uint4*>(p.wimg)[i];
+  if (issuer && (tid & 31) == 0) {
+    for (int i = 0; i < kRing2 + 2; ++i) mbar_init(&bars[i], 1);
+    mbar_init(bar_a2, 4);
+    mbar_init(bar_a3, 4);
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp < 4) {  // constant K chunk of A2: element 64 = 1 (b2), 65..79 = 0
+    uint32_t one[8] = {0x3F80u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(
+                     tmem + kColConst2 + (static_cast<uint32_t>(warp * 32) << 16)),
+                 "r"(one[0]), "r"(one[1]), "r"(one[2]), "r"(one[3]), "r"(one[4]), "r"(one[5]), "r"(one[6]),
+                 "r"(one[7])
+                 : "memory");
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tcol = tmem + st * kCols2;
+  const uint32_t tA2 = tcol, tA3 = tcol + 32, tD = tcol + 64, tD3 = tcol + 128, tC = tmem + kColConst2;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kS2 + st;
+  const int64_t tstride = static_cast<int64_t>(gridDim.x) * kS2;
+
+  if (issuer) {
+    // The stream index is a template argument and the TMEM base is 0 (the CTA owns all 512
+    // columns), so every MMA operand is warp-uniform at compile time: no per-MMA R2UR
+    // waterfall (tools/mma_probe3.cu's ~45 cycles per issued MMA came from it).
+    if (tmem != 0 && (tid & 31) == 0) __trap();
+    switch (st) {
+      case 0: mlp2_issuer<0>(p, sm, ring, t0, tstride); break;
+#if HC_MLP2_STREAMS > 1
+      case 1: mlp2_issuer<1>(p, sm, ring, t0, tstride); break;
+#endif
+#if HC_MLP2_STREAMS > 2
+      case 2: mlp2_issuer<2>(p, sm, ring, t0, tstride); break;
+#endif
+#if HC_MLP2_STREAMS > 3
+      case 3: mlp2_issuer<3>(p, sm, ring, t0, tstride); break;
+#endif
+      default: break;
+    }
+  } else {
+    const uint32_t lane_off = static_cast<uint32_t>(quarter * 32) << 16;
+    const int k = p.k;
+    uint32_t prev_v[kN3];
+    int64_t prev_row0 = -1;
+    int prev_rows = 0;
+    auto store_codes = [&]() {
+      if (prev_row0 < 0 || r >= prev_rows) return;
+      float* o = p.out + (prev_row0 + r) * k;
+      if (k == 6 && p.vec2) {
+        float y[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) y[j] = softplus1(__uint_as_float(prev_v[j]) + p.b3[j]);
+        reinterpret_cast<float2*>(o)[0] = make_float2(y[0], y[1]);
+        reinterpret_cast<float2*>(o)[1] = make_float2(y[2], y[3]);
+        reinterpret_cast<float2*>(o)[2] = make_float2(y[4], y[5]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < kMaxK; ++j)
+          if (j < k) o[j] = softplus1(__uint_as_float(prev_v[j]) + p.b3[j]);
+      }
+    };
+    auto handoff = [&](uint64_t* bar) {
+      tc_fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(bar);
+    };
+    auto rgb_row = [&](int64_t t, int it, float& x0, float& x1, float& x2) {
+      if (p.use_tma) {
+        const int s = it % kRing2;
+        mbar_wait(&bar_in[s], (it / kRing2) & 1);
+        const float* in = ring + s * kMlpM * 3 + r * 3;
+        x0 = in[0];
+        x1 = in[1];
+        x2 = in[2];
+      } else {
+        const int64_t row = (p.first_tile + t) * kMlpM + r;
+        x0 = x1 = x2 = 0.f;
+        if (row < p.P) {
+          const float* in = p.rgb + row * 3;
+          x0 = in[0];
+          x1 = in[1];
+          x2 = in[2];
+        }
+      }
+    };
+    auto store_a2 = [&](const uint32_t (&w)[32]) {
+      HC_TMEM_ST16(tA2 + lane_off, w);
+      HC_TMEM_ST16(tA2 + lane_off + 16, (&w[16]));
+      tmem_wait_st();
+      handoff(bar_a2);
+    };
+    uint32_t a2w[32];
+    if (t0 < p.ntiles) {
+      float x0, x1, x2;
+      rgb_row(t0, 0, x0, x1, x2);
+      layer1_row(p, x0, x1, x2, a2w);
+      store_a2(a2w);
+    }
+    int it = 0;
+    for (int64_t t = t0; t < p.ntiles; t += tstride, ++it) {
+      const int64_t tn = t + tstride;
+      const bool next = tn < p.ntiles;
+      if (next) {  // layer 1 of the next tile, in registers, under layer 2 of this one
+        float x0, x1, x2;
+        rgb_row(tn, it + 1, x0, x1, x2);
+        layer1_row(p, x0, x1, x2, a2w);
+      }
+      mbar_wait(bar_l2, it & 1);
+      tc_fence_after();
+      if (it > 0) {  // layer 3 of the previous tile is complete too (earlier MMA, same commit chain)
+        HC_TMEM_LD16(tD3 + lane_off, prev_v);
+      }
+      // relu(D) -> bf16 A3, in two 32-column halves (register budget: 480 threads)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t va[2][16], pk[16];
+        HC_TMEM_LD16(tD + lane_off + 32 * h, va[0]);
+        HC_TMEM_LD16(tD + lane_off + 32 * h + 16, va[1]);
+        tmem_wait_ld();  // (covers the D3 load too)
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            pk[q * 8 + j] = pack_relu_bf16(__uint_as_float(va[q][2 * j]), __uint_as_float(va[q][2 * j + 1]));
+        HC_TMEM_ST16(tA3 + lane_off + 16 * h, pk);
+      }
+      tmem_wait_st();
+      handoff(bar_a3);
+      if (next) store_a2(a2w);
+      store_codes();  // tile t - 1
+      const int64_t row0 = (p.first_tile + t) * kMlpM;
+      const int64_t left = p.P - row0;
+      prev_row0 = row0;
+      prev_rows = left < kMlpM ? static_cast<int>(left) : kMlpM;
+    }
+    if (it > 0) {
+      mbar_wait(bar_l3, (it - 1) & 1);
+      tc_fence_after();
+      HC_TMEM_LD16(tD3 + lane_off, prev_v);
+      tmem_wait_ld();
+      store_codes();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
 }  // namespace hcb
 
 using namespace hcb;
@@ -467,6 +798,7 @@ struct hc_mlp_s {
   int hidden = 0, k = 0;
   uint8_t* d_wimg = nullptr;
   MlpParams base{};
+  Mlp2Params base2{};
   int occ = 1;
 };
 
@@ -481,6 +813,23 @@ uint16_t to_bf16(float f) {
 
 // Canonical no-swizzle K-major image of an N x K bf16 matrix: element (n, k) at
 // (k / 8) * (N * 16) + n * 16 + (k % 8) * 2 bytes.
+float bf16_value(float f) {
+  const uint32_t u = static_cast<uint32_t>(to_bf16(f)) << 16;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
+// mlp2_kernel (layer 1 on the CUDA cores) unless HC_MLP_V1 is set or the build pins V1.
+#ifndef HC_MLP_V2
+#define HC_MLP_V2 1
+#endif
+bool use_v2() {
+  const char* v1 = std::getenv("HC_MLP_V1");
+  static const bool v2 = HC_MLP_V2 && !(v1 && *v1 && *v1 != '0');
+  return v2;
+}
+
 void put_kmajor(std::vector<uint8_t>& img, int off, int N, int K, int n, int k, float v) {
   const uint16_t b = to_bf16(v);
   std::memcpy(&img[off + (k / 8) * (N * 16) + n * 16 + (k % 8) * 2], &b, 2);
@@ -527,6 +876,28 @@ int hc_mlp_create(hc_ctx ctx, int hidden, int k, const float* w1, const float* b
   for (int i = 0; i < k; ++i) m->base.b3[i] = b3[i];
   m->base.wimg = m->d_wimg;
   m->base.k = k;
+  std::memset(&m->base2, 0, sizeof(m->base2));
+  auto pair = [](float lo, float hi) {
+    const float f[2] = {bf16_value(lo), bf16_value(hi)};
+    unsigned long long v;
+    std::memcpy(&v, f, 8);
+    return v;
+  };
+  for (int i = 0; i < kHid / 2; ++i) {
+    for (int c = 0; c < 3; ++c) m->base2.w1p[c][i] = pair(w1[(2 * i) * 3 + c], w1[(2 * i + 1) * 3 + c]);
+    m->base2.b1p[i] = pair(b1[2 * i], b1[2 * i + 1]);
+  }
+  for (int i = 0; i < k; ++i) m->base2.b3[i] = b3[i];
+  m->base2.wimg = m->d_wimg + kOffW2;  // W2' | W3 images are contiguous
+  m->base2.k = k;
+  if (use_v2()) {
+    e = cudaFuncSetAttribute(mlp2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2);
+    if (e != cudaSuccess) {
+      cudaFree(m->d_wimg);
+      delete m;
+      return cuda_error(e, "hc_mlp_create (mlp2_kernel)");
+    }
+  }
   *out = m;
   return HC_OK;
 }
@@ -544,11 +915,38 @@ int hc_mlp_forward(hc_mlp m, const float* rgb, int64_t P, float* codes) {
   if (P == 0) return HC_OK;
   if (!rgb || !codes) return set_error(HC_EINVAL, "mlp: null buffer");
   hc_ctx ctx = m->ctx;
+  const bool aligned = (reinterpret_cast<uintptr_t>(rgb) & 15u) == 0;  // rgb tiles arrive by bulk copy
+  if (use_v2()) {
+    Mlp2Params q = m->base2;
+    q.rgb = rgb;
+    q.out = codes;
+    q.P = P;
+    q.vec2 = (reinterpret_cast<uintptr_t>(codes) & 7u) == 0;  // float2 code stores need 8-byte rows
+    const int64_t full = aligned ? P / kMlpM : 0;
+    if (full > 0) {
+      q.first_tile = 0;
+      q.ntiles = full;
+      q.use_tma = 1;
+      const int grid = static_cast<int>(std::min<int64_t>((full + kS2 - 1) / kS2, ctx->sm_count));
+      mlp2_kernel<<<grid, kThreads2, kSmem2, ctx->stream>>>(q);
+      HC_CHECK_LAUNCH(ctx, "mlp2_kernel");
+    }
+    if (full * kMlpM < P) {
+      q.first_tile = full;
+      q.ntiles = (P - full * kMlpM + kMlpM - 1) / kMlpM;
+      q.use_tma = 0;
+      const int grid = static_cast<int>(std::min<int64_t>((q.ntiles + kS2 - 1) / kS2, ctx->sm_count));
+      mlp2_kernel<<<grid, kThreads2, kSmem2, ctx->stream>>>(q);
+      HC_CHECK_LAUNCH(ctx, "mlp2_kernel(tail)");
+    }
+    return HC_OK;
+  }
   MlpParams p = m->base;
   p.rgb = rgb;
   p.out = codes;
   p.P = P;
-  const bool aligned = (reinterpret_cast<uintptr_t>(rgb) & 15u) == 0;  // rgb tiles arrive by bulk copy
+  if (p.k == 6 && (reinterpret_cast<uintptr_t>(codes) & 7u) != 0)
+    return set_error(HC_EINVAL, "mlp: codes must be 8-byte aligned (HC_MLP_V1 kernel)");
   // codes tile = 128 * k * 4 bytes: 16-byte multiple for any k
   const int64_t full = aligned ? P / kMlpM : 0;
   if (full > 0) {

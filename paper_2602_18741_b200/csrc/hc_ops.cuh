@@ -21,9 +21,6 @@
 #include "hc_common.cuh"
 #include "hc_tma.cuh"
 
-#ifndef HC_LOSS_UNROLL
-#define HC_LOSS_UNROLL 8
-#endif
 
 namespace hcb {
 
@@ -421,6 +418,118 @@ struct ShadeSpectralOp {
   }
 };
 
+// ---------------------------------------------------------------- naive shading, packed
+// The naive n-sample shade of configs 2 (no spectra written), restated for the fp32x2
+// pipe: wavelengths are processed in pairs with packed FFMA2 (fma.rn.f32x2), so the
+// light sum (L FMAs), the reflectance product and the 3 CMF accumulations of two
+// wavelengths issue as L + 1 + 3 instructions instead of 2 (L + 4): the kernel was
+// issue-bound (ShadeSpectralOp, ~13 instructions per wavelength).  The arithmetic per
+// wavelength is unchanged (the same products and sums, fp32); XYZ sums the even- and
+// odd-wavelength partials at the end.  Palette rows are padded to an even length in
+// shared memory and read as float2; light SPD and CMF pairs are constant-bank operands.
+__device__ __forceinline__ uint64_t f2pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ uint64_t f2fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ float2 f2unpack(uint64_t v) {
+  float2 r;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(v));
+  return r;
+}
+
+template <int N, int L, int T_, int THREADS_, int STAGES_>
+struct ShadeSpectralF2Op {
+  static constexpr int T = T_, THREADS = THREADS_, STAGES = STAGES_;
+  static constexpr int NP = (N + 1) / 2 * 2;  // padded row length
+  static constexpr int NIN = 2;
+  __host__ __device__ static constexpr int in_bytes(int i) { return i == 0 ? 4 : L * 4; }
+  static constexpr int NOUT = 2;  // XYZ, sRGB
+  __host__ __device__ static constexpr int out_bytes(int) { return 12; }
+  static constexpr int EXTRA_SMEM = kMaxPalette * NP * 4;
+  static constexpr int kTensorStream = -1;
+  static constexpr bool kWarpSpecialized = false;
+  static constexpr bool kEvictFirstLoads = false;
+
+  struct Params {
+    unsigned long long light2[L * NP / 2];  // (L_l(2h), L_l(2h + 1)) pairs, [l][h]
+    unsigned long long cmf2[3 * NP / 2];    // dlambda * CMF pairs, [c][h]
+    float Crgb[9];
+    const uint32_t* idx;
+    const float* cosv;
+    const float* pal_spectra;
+    int n_pal;
+    float* xyz;
+    float* rgb;
+    int* err;
+  };
+  __host__ __device__ static const void* tensor_map(const Params&) { return nullptr; }
+  struct State {};
+  __device__ static void init_state(State&) {}
+  __host__ __device__ static const void* in_ptr(const Params& p, int i) {
+    return i == 0 ? static_cast<const void*>(p.idx) : static_cast<const void*>(p.cosv);
+  }
+  __host__ __device__ static void* out_ptr(const Params& p, int i) { return i == 0 ? p.xyz : p.rgb; }
+  __device__ static void setup(const Params& p, unsigned char* extra) {
+    float* pal = reinterpret_cast<float*>(extra);
+    for (int x = threadIdx.x; x < p.n_pal * NP; x += blockDim.x) {
+      const int r = x / NP, i = x - r * NP;
+      pal[x] = i < N ? __ldg(p.pal_spectra + r * N + i) : 0.f;
+    }
+  }
+  __device__ static void finish(const Params&, State&, unsigned char*) {}
+
+  __device__ static void compute(const Params& p, State&, const unsigned char* const* ins,
+                                 unsigned char* const* outs, unsigned char* extra, int item, int64_t) {
+    uint32_t id = reinterpret_cast<const uint32_t*>(ins[0])[item];
+    if (id >= static_cast<uint32_t>(p.n_pal)) {
+      atomicOr(p.err, kErrIndexRange);
+      id = 0;
+    }
+    const float* c = reinterpret_cast<const float*>(ins[1]) + item * L;
+    uint64_t w2[L];
+#pragma unroll
+    for (int l4 = 0; l4 < L; l4 += 4) {
+      const float4 w4 = *reinterpret_cast<const float4*>(c + l4);
+      w2[l4] = f2pack(w4.x, w4.x);
+      w2[l4 + 1] = f2pack(w4.y, w4.y);
+      w2[l4 + 2] = f2pack(w4.z, w4.z);
+      w2[l4 + 3] = f2pack(w4.w, w4.w);
+    }
+    const float2* R = reinterpret_cast<const float2*>(extra) + id * (NP / 2);
+    uint64_t acc[3] = {0ull, 0ull, 0ull};
+#pragma unroll
+    for (int h = 0; h < NP / 2; ++h) {
+      uint64_t il = f2fma(w2[0], p.light2[h], 0ull);
+#pragma unroll
+      for (int l = 1; l < L; ++l) il = f2fma(w2[l], p.light2[l * (NP / 2) + h], il);
+      const float2 r = R[h];
+      const uint64_t s = f2fma(f2pack(r.x, r.y), il, 0ull);
+#pragma unroll
+      for (int cc = 0; cc < 3; ++cc) acc[cc] = f2fma(p.cmf2[cc * (NP / 2) + h], s, acc[cc]);
+    }
+    float xyz[3], rgb[3];
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+      const float2 a = f2unpack(acc[cc]);
+      xyz[cc] = a.x + a.y;
+    }
+    xyz_to_rgb(p.Crgb, xyz, rgb);
+    float* ox = reinterpret_cast<float*>(outs[0]) + item * 3;
+    float* orgb = reinterpret_cast<float*>(outs[1]) + item * 3;
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+      ox[cc] = xyz[cc];
+      orgb[cc] = rgb[cc];
+    }
+  }
+};
+
 // ---------------------------------------------------------------- loss
 // sum over pairs and lambda of (D (E a (.) E b) - a (.) b)^2, computed the way the
 // reference computes it (forward_pair + mse_n, trainer.cpp:49-71): the residual
@@ -429,67 +538,48 @@ struct ShadeSpectralOp {
 // multiplicative, so r_l is routinely 1e-8 of a_l b_l; an fp32 residual (or the
 // expanded zp^T G zp - 2 zp.D^T(ab) + |ab|^2 form of round 1) is then rounding noise.
 //
-// The kernel is fp64-pipe bound next to HBM (~1650 fp64 ops per 648-byte pair), so it
-// is laid out for latency hiding and to keep shared memory off the critical path:
-//  * G warp groups share each pair (kLanesPerItem = G): group h (threads
-//    [h*T, (h+1)*T)) takes wavelengths [h*N/G, (h+1)*N/G) of every pair of the tile,
-//    which multiplies the warps per SM at the same TMA ring;
-//  * within a warp the wavelength is uniform, so the fp64 E / D coefficients are
-//    kernel parameters read at a uniform index (constant bank, no shared memory), and
-//    a lane's a_l / b_l reads (row stride 81 words, odd) are bank-conflict free;
+// ~1,650 fp64 operations per 648-byte pair put the fp64 pipe next to HBM, so the layout
+// is about feeding it:
+//  * G warp groups share each pair (kLanesPerItem = G; G = 3 for n = 81): group h
+//    (threads [h*T, (h+1)*T)) takes wavelengths [h*R, (h+1)*R) of every pair of the tile,
+//    which gives 3x the warps per SM at the same TMA ring;
+//  * a warp is always at one wavelength, so E comes from the constant bank at a uniform
+//    index and D from a shared-memory table as same-address double2 broadcasts (both in the
+//    constant bank thrash its cache: 73 % hits), and a lane's a_l / b_l reads (row stride
+//    81 words, odd) are bank-conflict free;
+//  * both passes are software pipelined: the floats of the next batch of wavelengths are
+//    loaded (LDS) and converted (F2F, variable latency) while the current batch's DFMAs
+//    issue;
 //  * pass 1 accumulates the group's partial codes, the groups exchange them through
-//    shared memory (one barrier), pass 2 decodes zp at the group's wavelengths starting
-//    from -a_l b_l (an exact fp64 product of two floats) and accumulates r_l^2.
+//    shared memory (one barrier; every group adds the partials in group order, so all hold
+//    the same zp), pass 2 decodes zp at the group's wavelengths starting from -a_l b_l (an
+//    exact fp64 product of two floats) and accumulates r_l^2.
 // Pairs accumulate in fp64 per thread, then per CTA into partials[].
-#ifndef HC_LOSS_GROUPS
-#define HC_LOSS_GROUPS 2
+#ifndef HC_LOSS_B1
+#define HC_LOSS_B1 9  // pass-1 batch (wavelengths); must divide N / G, else 1
 #endif
-#ifndef HC_LOSS_INTCVT
-#define HC_LOSS_INTCVT 0
+#ifndef HC_LOSS_B2
+#define HC_LOSS_B2 3  // pass-2 batch
 #endif
-#ifndef HC_LOSS_ETAB  // where pass 1 reads E: 0 = constant bank (kernel parameter), 1 = shared memory
-#define HC_LOSS_ETAB 0
-#endif
-#ifndef HC_LOSS_DTAB  // where pass 2 reads D: 0 = constant bank, 1 = shared memory
-#define HC_LOSS_DTAB 0
-#endif
-
-// float -> double.  HC_LOSS_INTCVT: integer re-bias of normal floats and zeros (fixed-latency
-// ALU ops instead of the variable-latency F2F), F2F only for subnormals / inf / nan.
-__device__ __forceinline__ double loss_f2d(float f) {
-#if HC_LOSS_INTCVT
-  const uint32_t u = __float_as_uint(f);
-  const uint32_t t = u & 0x7fffffffu;
-  uint32_t hi = (u & 0x80000000u) | ((t >> 3) + 0x38000000u);
-  hi = t ? hi : (u & 0x80000000u);
-  double d = __hiloint2double(static_cast<int>(hi), static_cast<int>(u << 29));
-  if (__builtin_expect(t - 1u >= 0x7f7fffffu, 0) && t) d = static_cast<double>(f);
-  return d;
-#else
-  return static_cast<double>(f);
-#endif
-}
 
 template <int N, int K, int T_, int THREADS_, int STAGES_>
 struct LossOp {
   static constexpr int T = T_, THREADS = THREADS_, STAGES = STAGES_;
-  static constexpr int G = HC_LOSS_GROUPS;  // warp groups per pair (wavelength ranges)
+  static constexpr int G = N % 3 == 0 ? 3 : 1;  // warp groups per pair
+  static constexpr int R = N / G;               // wavelengths per group
+  static constexpr int B1 = R % HC_LOSS_B1 == 0 ? HC_LOSS_B1 : 1;
+  static constexpr int B2 = R % HC_LOSS_B2 == 0 ? HC_LOSS_B2 : 1;
   static constexpr int kLanesPerItem = G;
   static_assert(THREADS == G * T && T % 32 == 0, "G whole warp groups per tile");
   static constexpr int NIN = 2;
   __host__ __device__ static constexpr int in_bytes(int) { return N * 4; }
   static constexpr int NOUT = 0;
   __host__ __device__ static constexpr int out_bytes(int) { return 0; }
-  static constexpr int kUnroll = HC_LOSS_UNROLL;
+  static constexpr int KP = (K + 1) / 2 * 2;
   // [group][2K][T] fp64 partial codes (item fastest: conflict-free 64-bit accesses)
   static constexpr int kXchg = G > 1 ? G * 2 * K * T * 8 : 0;
-  // optional fp64 tables in shared memory: [l][KP] (E^T) and [l][KP] (D), read as
-  // same-address double2 broadcasts (every lane of a warp is at the same wavelength)
-  static constexpr int KP = (K + 1) / 2 * 2;
-  static constexpr bool kETab = HC_LOSS_ETAB, kDTab = HC_LOSS_DTAB;
-  static constexpr int kTabE = kETab ? N * KP * 8 : 0;
-  static constexpr int kTabD = kDTab ? N * KP * 8 : 0;
-  static constexpr int EXTRA_SMEM = 32 * 8 + kXchg + kTabE + kTabD;
+  static constexpr int kTabD = N * KP * 8;  // D rows [l][KP], fp64
+  static constexpr int EXTRA_SMEM = 32 * 8 + kXchg + kTabD;
   static constexpr int kTensorStream = -1;
   static constexpr bool kWarpSpecialized = false;
   static constexpr bool kEvictFirstLoads = false;
@@ -513,52 +603,81 @@ struct LossOp {
   }
   __host__ __device__ static void* out_ptr(const Params&, int) { return nullptr; }
   __device__ static void setup(const Params& p, unsigned char* extra) {
-    double* te = reinterpret_cast<double*>(extra + 32 * 8 + kXchg);
-    double* td = te + kTabE / 8;
+    double* td = reinterpret_cast<double*>(extra + 32 * 8 + kXchg);
     for (int x = threadIdx.x; x < N * KP; x += blockDim.x) {
       const int l = x / KP, c = x % KP;
-      if (kETab) te[x] = c < K ? p.E[c * N + l] : 0.0;
-      if (kDTab) td[x] = c < K ? p.D[l * K + c] : 0.0;
+      td[x] = c < K ? p.D[l * K + c] : 0.0;
     }
   }
 
-  template <int H>
-  __device__ static double part(const Params& p, const float* a, const float* b, double* xchg, int item) {
-    constexpr int L0 = H * N / G, L1 = (H + 1) * N / G;
-    const double2* te = reinterpret_cast<const double2*>(xchg + kXchg / 8);
-    const double2* td = te + kTabE / 16;
-    // pass 1: partial za = E a, zb = E b over [L0, L1) (codec.cpp:36-46, trainer.cpp:52-53)
+  __device__ static void compute(const Params& p, State& st, const unsigned char* const* ins,
+                                 unsigned char* const*, unsigned char* extra, int item, int64_t g) {
+    // Every thread of the CTA gets here exactly once per tile (tile_generic runs all T
+    // pairs of a ragged tile), so the barrier below is uniform.
+    const int grp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x) / T, 0);  // warp-uniform
+    const int L0 = grp * R;
+    const float* a = reinterpret_cast<const float*>(ins[0]) + item * N + L0;
+    const float* b = reinterpret_cast<const float*>(ins[1]) + item * N + L0;
+    double* xchg = reinterpret_cast<double*>(extra + 32 * 8);
+    const double2* td = reinterpret_cast<const double2*>(extra + 32 * 8 + kXchg) + L0 * (KP / 2);
+    const double* E = p.E + L0;
+
+    // pass 1: partial za = E a, zb = E b over [L0, L0 + R) (codec.cpp:36-46, trainer.cpp:52-53)
     double za[K], zb[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) za[j] = zb[j] = 0.0;
-#pragma unroll kUnroll
-    for (int l = L0; l < L1; ++l) {
-      const double va = loss_f2d(a[l]), vb = loss_f2d(b[l]);
-      double e[KP];
+    {
+      float fa[B1], fb[B1];
+      double va[B1], vb[B1];
 #pragma unroll
-      for (int c = 0; c < KP / 2; ++c) {
-        if (kETab) {
-          const double2 v = te[l * (KP / 2) + c];
-          e[2 * c] = v.x;
-          e[2 * c + 1] = v.y;
-        } else {
-          e[2 * c] = p.E[(2 * c) * N + l];  // uniform index: constant bank
-          e[2 * c + 1] = 2 * c + 1 < K ? p.E[(2 * c + 1) * N + l] : 0.0;
+      for (int i = 0; i < B1; ++i) {
+        fa[i] = a[i];
+        fb[i] = b[i];
+      }
+#pragma unroll
+      for (int i = 0; i < B1; ++i) {
+        va[i] = static_cast<double>(fa[i]);
+        vb[i] = static_cast<double>(fb[i]);
+      }
+      if (B1 < R) {
+#pragma unroll
+        for (int i = 0; i < B1; ++i) {
+          fa[i] = a[B1 + i];
+          fb[i] = b[B1 + i];
         }
       }
+#pragma unroll 1
+      for (int l0 = 0; l0 < R; l0 += B1) {
 #pragma unroll
-      for (int j = 0; j < K; ++j) {
-        za[j] = fma(e[j], va, za[j]);
-        zb[j] = fma(e[j], vb, zb[j]);
+        for (int i = 0; i < B1; ++i)
+#pragma unroll
+          for (int j = 0; j < K; ++j) {
+            const double e = E[j * N + l0 + i];  // warp-uniform: constant bank
+            za[j] = fma(e, va[i], za[j]);
+            zb[j] = fma(e, vb[i], zb[j]);
+          }
+        if (l0 + B1 < R) {  // next batch: convert the floats loaded one batch ago, load the one after
+#pragma unroll
+          for (int i = 0; i < B1; ++i) {
+            va[i] = static_cast<double>(fa[i]);
+            vb[i] = static_cast<double>(fb[i]);
+          }
+          if (l0 + 2 * B1 < R) {
+#pragma unroll
+            for (int i = 0; i < B1; ++i) {
+              fa[i] = a[l0 + 2 * B1 + i];
+              fb[i] = b[l0 + 2 * B1 + i];
+            }
+          }
+        }
       }
     }
-    // exchange partial codes; every group sums the G partials in group order, so all
-    // hold bit-identical zp = za (.) zb (codec.cpp:77-85)
+    // exchange the groups' partial codes; zp = za (.) zb (codec.cpp:77-85)
     if constexpr (G > 1) {
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        xchg[(H * 2 * K + j) * T + item] = za[j];
-        xchg[(H * 2 * K + K + j) * T + item] = zb[j];
+        xchg[(grp * 2 * K + j) * T + item] = za[j];
+        xchg[(grp * 2 * K + K + j) * T + item] = zb[j];
       }
       __syncthreads();
 #pragma unroll
@@ -566,55 +685,53 @@ struct LossOp {
         za[j] = xchg[j * T + item];
         zb[j] = xchg[(K + j) * T + item];
 #pragma unroll
-        for (int g = 1; g < G; ++g) {
-          za[j] += xchg[(g * 2 * K + j) * T + item];
-          zb[j] += xchg[(g * 2 * K + K + j) * T + item];
+        for (int h = 1; h < G; ++h) {
+          za[j] += xchg[(h * 2 * K + j) * T + item];
+          zb[j] += xchg[(h * 2 * K + K + j) * T + item];
         }
       }
     }
 #pragma unroll
     for (int j = 0; j < K; ++j) za[j] *= zb[j];
-    // pass 2: r_l = (D zp)_l - a_l b_l over [L0, L1), sum of r_l^2 (trainer.cpp:56-71)
+
+    // pass 2: r_l = (D zp)_l - a_l b_l over [L0, L0 + R), sum of r_l^2 (trainer.cpp:56-71)
     double acc = 0.0;
-#pragma unroll kUnroll
-    for (int l = L0; l < L1; ++l) {
-      double s = -(loss_f2d(a[l]) * loss_f2d(b[l]));  // exact product
-      double d[KP];
+    {
+      float fa[B2], fb[B2];
+      double d[B2][KP];
+      auto load = [&](int l0) {
 #pragma unroll
-      for (int c = 0; c < KP / 2; ++c) {
-        if (kDTab) {
-          const double2 v = td[l * (KP / 2) + c];
-          d[2 * c] = v.x;
-          d[2 * c + 1] = v.y;
-        } else {
-          d[2 * c] = p.D[l * K + 2 * c];
-          d[2 * c + 1] = 2 * c + 1 < K ? p.D[l * K + 2 * c + 1] : 0.0;
+        for (int i = 0; i < B2; ++i) {
+          fa[i] = a[l0 + i];
+          fb[i] = b[l0 + i];
+#pragma unroll
+          for (int c = 0; c < KP / 2; ++c) {
+            const double2 v = td[(l0 + i) * (KP / 2) + c];  // same address in every lane: broadcast
+            d[i][2 * c] = v.x;
+            d[i][2 * c + 1] = v.y;
+          }
+        }
+      };
+      load(0);
+#pragma unroll 1
+      for (int l0 = 0; l0 < R; l0 += B2) {
+        double s[B2];
+#pragma unroll
+        for (int i = 0; i < B2; ++i) s[i] = -(static_cast<double>(fa[i]) * static_cast<double>(fb[i]));  // exact
+        double dc[B2][KP];
+#pragma unroll
+        for (int i = 0; i < B2; ++i)
+#pragma unroll
+          for (int c = 0; c < KP; ++c) dc[i][c] = d[i][c];
+        if (l0 + B2 < R) load(l0 + B2);
+#pragma unroll
+        for (int i = 0; i < B2; ++i) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) s[i] = fma(dc[i][j], za[j], s[i]);
+          acc = fma(s[i], s[i], acc);
         }
       }
-#pragma unroll
-      for (int j = 0; j < K; ++j) s = fma(d[j], za[j], s);
-      acc = fma(s, s, acc);
     }
-    return acc;
-  }
-
-  template <int H>
-  __device__ static double dispatch(const Params& p, const float* a, const float* b, double* xchg, int item,
-                                    int grp) {
-    if constexpr (H + 1 < G) {
-      if (grp != H) return dispatch<H + 1>(p, a, b, xchg, item, grp);
-    }
-    return part<H>(p, a, b, xchg, item);
-  }
-
-  __device__ static void compute(const Params& p, State& st, const unsigned char* const* ins,
-                                 unsigned char* const*, unsigned char* extra, int item, int64_t g) {
-    // Every thread of the CTA gets here exactly once per tile (tile_generic runs all T
-    // pairs of a ragged tile), so the barrier inside part() is uniform.
-    const float* a = reinterpret_cast<const float*>(ins[0]) + item * N;
-    const float* b = reinterpret_cast<const float*>(ins[1]) + item * N;
-    double* xchg = reinterpret_cast<double*>(extra + 32 * 8);
-    const double acc = dispatch<0>(p, a, b, xchg, item, threadIdx.x / T);
     if (g < p.pairs) st.acc += acc;
   }
   __device__ static void finish(const Params& p, State& st, unsigned char* extra) {

@@ -592,6 +592,9 @@ int hc_shade_latent_host_frames(hc_codec c, const float* pal_codes, int n_pal, c
   HC_CUDA_TRY(cudaEventRecord(ctx->ev_fork, ctx->stream));
   for (auto st : ctx->aux) HC_CUDA_TRY(cudaStreamWaitEvent(st, ctx->ev_fork, 0));
   cudaStream_t home = ctx->stream;
+  // On any error the aux streams are drained before returning: copies in flight read and
+  // write the caller's host buffers and the shared scratch.
+  auto enqueue = [&]() -> int {
   int64_t ci = 0;
   for (int f = 0; f < nframes; ++f) {
     for (int64_t p0 = 0; p0 < P; p0 += kChunk, ++ci) {
@@ -614,7 +617,16 @@ int hc_shade_latent_host_frames(hc_codec c, const float* pal_codes, int n_pal, c
       if (rgb[f]) HC_CUDA_TRY(cudaMemcpyAsync(rgb[f] + p0 * 3, d_rgb, sizeof(float) * n * 3, cudaMemcpyDeviceToHost, st));
     }
   }
-  for (auto st : ctx->aux) HC_CUDA_TRY(cudaStreamSynchronize(st));
+  return HC_OK;
+  };
+  const int rq = enqueue();
+  cudaError_t es = cudaSuccess;
+  for (auto st : ctx->aux) {
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (es == cudaSuccess) es = e;
+  }
+  if (rq != HC_OK) return rq;
+  if (es != cudaSuccess) return cuda_error(es, "shade_latent_host_frames");
   return hc_ctx_synchronize(ctx);
 }
 

@@ -261,6 +261,35 @@ int shade_spectral_nl(hc_codec c, const float* pal, int n_pal, const float* ligh
 #define HC_NAIVE_T 256  // measured: 128 -> 256 threads per CTA +9.5 % (tools/sweep_naive.sh)
 #endif
   constexpr int T = SPEC ? 64 : HC_NAIVE_T;
+#ifndef HC_NAIVE_F2
+#define HC_NAIVE_F2 1
+#endif
+  if constexpr (!SPEC && HC_NAIVE_F2 && L <= 8) {  // packed-FFMA2 variant (ShadeSpectralF2Op)
+    using Op2 = ShadeSpectralF2Op<N, L, T, T, 2>;
+    typename Op2::Params q;
+    constexpr int H = Op2::NP / 2;
+    auto pair = [](float lo, float hi) {
+      const float f[2] = {lo, hi};
+      unsigned long long v;
+      std::memcpy(&v, f, 8);
+      return v;
+    };
+    for (int l = 0; l < L; ++l)
+      for (int h = 0; h < H; ++h)
+        q.light2[l * H + h] = pair(light[l * N + 2 * h], 2 * h + 1 < N ? light[l * N + 2 * h + 1] : 0.f);
+    for (int cc = 0; cc < 3; ++cc)
+      for (int h = 0; h < H; ++h)
+        q.cmf2[cc * H + h] = pair(c->cmf_dl[cc * N + 2 * h], 2 * h + 1 < N ? c->cmf_dl[cc * N + 2 * h + 1] : 0.f);
+    for (int i = 0; i < 9; ++i) q.Crgb[i] = c->Crgb[i];
+    q.idx = idx;
+    q.cosv = cosv;
+    q.pal_spectra = pal;
+    q.n_pal = n_pal;
+    q.xyz = xyz;
+    q.rgb = rgb;
+    q.err = c->ctx->d_err;
+    return launch_tile_op<Op2>(c->ctx, q, P);
+  }
   using Op = ShadeSpectralOp<N, L, SPEC, T, T, 2>;
   typename Op::Params p;
   for (int i = 0; i < L * N; ++i) p.light[i] = light[i];

@@ -38,13 +38,17 @@ class Band:
 
 
 def row_band(rank: int, world: int, height: int, width: int) -> Band:
-    """Contiguous rows [row0, row1) of rank `rank`; sizes differ by at most one row."""
+    """Contiguous rows [row0, row1) of rank `rank`; sizes differ by at most one row.  The split
+    is the library's (hc_row_band), so Python ranks and the C++ device group agree."""
+    import ctypes as C
+
+    from . import _lib
+
     if not (0 <= rank < world) or height < 0:
         raise ValueError("row_band: bad rank / size")
-    base, extra = divmod(height, world)
-    row0 = rank * base + min(rank, extra)
-    row1 = row0 + base + (1 if rank < extra else 0)
-    return Band(rank, world, row0, row1, width)
+    r0, n = C.c_int64(), C.c_int64()
+    _lib.check(_lib.lib().hc_row_band(rank, world, height, C.byref(r0), C.byref(n)))
+    return Band(rank, world, r0.value, r0.value + n.value, width)
 
 
 def gather_rows(local: torch.Tensor, band: Band, height: int, dst: int = 0) -> torch.Tensor | None:

@@ -1,0 +1,4 @@
+// Compatibility include: the reference header name hadacodec/renderer.hpp maps onto the
+// drop-in header (namespace hadacodec::b200).
+#pragma once
+#include "hadacodec_b200.hpp"

@@ -37,6 +37,10 @@ def test_reference_arm_line():
     assert line["e2e"] == {"value": line["value"], "unit": "Mpixel/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
     assert line["config"]["workload"].startswith("1920x1080")
+    import bench
+
+    assert line["config"] == bench.config_dict("2")  # the GPU arm prints the same dict
+    assert "full 1920x1080 frame" in line["cpu_baseline"]["sample"]
 
 
 def test_reference_arm_other_ranks_exit_quietly():
@@ -46,10 +50,17 @@ def test_reference_arm_other_ranks_exit_quietly():
 
 @pytest.mark.gpu
 def test_gpu_arm_line():
-    (line,) = _run(["--steps", "40", "--warmup", "3", "--no-cpu-baseline"])
-    assert line["metric"] == BASELINE["metric"] and line["n_gpus"] == 1 and line["steps"] == 40
+    (line,) = _run(["--steps", "37", "--warmup", "3", "--no-cpu-baseline"])  # not a multiple of the rotation
+    import bench
+
+    assert line["metric"] == BASELINE["metric"] and line["n_gpus"] == 1 and line["steps"] == 37
+    assert line["config"] == bench.config_dict("2")
+    assert line["parity"]["pass"] and line["parity"]["rows"] == "full frame"
+    k9 = line["k9"]
+    assert k9["config"]["k"] == 9 and k9["value"] > 0 and 0 < k9["roofline"]["frac"] <= 1.0
+    assert k9["parity"]["pass"]
     assert line["value"] > 1e4 and 0 < line["roofline"]["frac"] <= 1.0 and line["roofline"]["bound"] == "hbm"
-    assert line["gpu_launches"] >= 40
+    assert line["gpu_launches"] >= 37
     e2e = line["e2e"]
     assert e2e["h2d_bytes_per_step"] == 1920 * 1080 * 36 and e2e["d2h_bytes_per_step"] == 1920 * 1080 * 24
     assert 0 < e2e["value"] < line["value"]

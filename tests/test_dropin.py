@@ -33,3 +33,29 @@ def test_dropin_reference_cases_on_gpu(tmp_path):
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stderr
     assert "0 failures" in r.stdout
+
+
+REF_UNIT = ROOT / "tests" / "cpp" / "bin" / "ref_unit_tests"
+
+
+def test_reference_unit_tests_compile_unchanged():
+    """The reference's test_codec.cpp / test_spectrum.cpp compile against the drop-in with only
+    `using namespace hadacodec;` -> `hadacodec::b200` (tests/cpp/build_ref_tests.py)."""
+    import sys
+
+    sys.path.insert(0, str(ROOT / "tests" / "cpp"))
+    import build_ref_tests
+
+    if not build_ref_tests.REF_TESTS.is_dir():
+        pytest.skip("/root/reference not present (the binary is built where it is)")
+    assert build_ref_tests.build() == REF_UNIT and REF_UNIT.exists()
+
+
+@pytest.mark.gpu
+def test_reference_unit_tests_pass_on_gpu():
+    if not REF_UNIT.exists():
+        pytest.skip("tests/cpp/bin/ref_unit_tests not built (python tests/cpp/build_ref_tests.py)")
+    r = subprocess.run([str(REF_UNIT)], capture_output=True, text=True, timeout=300)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "\n0 failures" in r.stdout
