@@ -700,7 +700,7 @@ class StepReplayer:
             self.per_step = ctx.launches - l0
         self.full = None
         self.rem = {}
-        if self.graph and max_steps >= R:
+        if self.graph:
             self.full = self._capture(R)
 
     def _capture(self, n: int):
@@ -726,6 +726,8 @@ class StepReplayer:
                 self.wl.step(i)
             return
         R = self.wl.R
+        if n % R and (n % R) not in self.rem:
+            self.prepare(n)  # (timed callers prepare beforehand)
         for _ in range(n // R):
             self.full.replay()
         if n % R:

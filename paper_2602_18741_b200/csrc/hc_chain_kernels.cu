@@ -60,7 +60,7 @@ int chain_latent_k(hc_codec c, const float* pal, int n_pal, const float* ill, in
   int grid = 0;
   if constexpr (K <= 6) {
 #ifndef HC_CHAIN_SHFL_ILL
-#define HC_CHAIN_SHFL_ILL 1
+#define HC_CHAIN_SHFL_ILL 0
 #endif
     if (HC_CHAIN_SHFL_ILL && n_ill <= 16) {  // illuminant codes by shuffle, palette in smem
       const int smem = n_pal * ((K + 1) / 2) * 16 * 8;

@@ -822,7 +822,7 @@ float bf16_value(float f) {
 
 // mlp2_kernel (layer 1 on the CUDA cores) unless HC_MLP_V1 is set or the build pins V1.
 #ifndef HC_MLP_V2
-#define HC_MLP_V2 1
+#define HC_MLP_V2 0
 #endif
 bool use_v2() {
   const char* v1 = std::getenv("HC_MLP_V1");

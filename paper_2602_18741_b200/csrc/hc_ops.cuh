@@ -556,10 +556,16 @@ struct ShadeSpectralF2Op {
 //    exact fp64 product of two floats) and accumulates r_l^2.
 // Pairs accumulate in fp64 per thread, then per CTA into partials[].
 #ifndef HC_LOSS_B1
-#define HC_LOSS_B1 9  // pass-1 batch (wavelengths); must divide N / G, else 1
+#define HC_LOSS_B1 27  // pass-1 batch (wavelengths); must divide N / G, else 1
 #endif
 #ifndef HC_LOSS_B2
-#define HC_LOSS_B2 3  // pass-2 batch
+#define HC_LOSS_B2 27  // pass-2 batch
+#endif
+#ifndef HC_LOSS_VLOAD
+#define HC_LOSS_VLOAD 0
+#endif
+#ifndef HC_LOSS_SPLIT  // pass 2: (D zp)_l as two interleaved 3-term chains
+#define HC_LOSS_SPLIT 0
 #endif
 
 template <int N, int K, int T_, int THREADS_, int STAGES_>
@@ -614,7 +620,8 @@ struct LossOp {
                                  unsigned char* const*, unsigned char* extra, int item, int64_t g) {
     // Every thread of the CTA gets here exactly once per tile (tile_generic runs all T
     // pairs of a ragged tile), so the barrier below is uniform.
-    const int grp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x) / T, 0);  // warp-uniform
+    // warp-uniform group (the shuffle lets the compiler see it; G = 1 ragged tiles run partial warps)
+    const int grp = G > 1 ? __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x) / T, 0) : 0;
     const int L0 = grp * R;
     const float* a = reinterpret_cast<const float*>(ins[0]) + item * N + L0;
     const float* b = reinterpret_cast<const float*>(ins[1]) + item * N + L0;
@@ -631,8 +638,13 @@ struct LossOp {
       double va[B1], vb[B1];
 #pragma unroll
       for (int i = 0; i < B1; ++i) {
+#if HC_LOSS_VLOAD  // pinned at the top: every LDS of the batch in flight before the first use
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(fa[i]) : "r"(smem_u32(a + i)));
+        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(fb[i]) : "r"(smem_u32(b + i)));
+#else
         fa[i] = a[i];
         fb[i] = b[i];
+#endif
       }
 #pragma unroll
       for (int i = 0; i < B1; ++i) {
@@ -726,8 +738,17 @@ struct LossOp {
         if (l0 + B2 < R) load(l0 + B2);
 #pragma unroll
         for (int i = 0; i < B2; ++i) {
+          if (HC_LOSS_SPLIT && K % 2 == 0) {
+            double s2 = dc[i][K / 2] * za[K / 2];
 #pragma unroll
-          for (int j = 0; j < K; ++j) s[i] = fma(dc[i][j], za[j], s[i]);
+            for (int j = 0; j < K / 2; ++j) s[i] = fma(dc[i][j], za[j], s[i]);
+#pragma unroll
+            for (int j = K / 2 + 1; j < K; ++j) s2 = fma(dc[i][j], za[j], s2);
+            s[i] += s2;
+          } else {
+#pragma unroll
+            for (int j = 0; j < K; ++j) s[i] = fma(dc[i][j], za[j], s[i]);
+          }
           acc = fma(s[i], s[i], acc);
         }
       }

@@ -265,7 +265,10 @@ int shade_spectral_nl(hc_codec c, const float* pal, int n_pal, const float* ligh
 #define HC_NAIVE_F2 1
 #endif
   if constexpr (!SPEC && HC_NAIVE_F2 && L <= 8) {  // packed-FFMA2 variant (ShadeSpectralF2Op)
-    using Op2 = ShadeSpectralF2Op<N, L, T, T, 2>;
+#ifndef HC_NAIVE_F2_T
+#define HC_NAIVE_F2_T 1024  // one 84 KB palette copy per 32 warps: 256 / 512 / 1024 -> 14.0 / 20.0 / 24.0 Gpix/s
+#endif
+    using Op2 = ShadeSpectralF2Op<N, L, HC_NAIVE_F2_T, HC_NAIVE_F2_T, 2>;
     typename Op2::Params q;
     constexpr int H = Op2::NP / 2;
     auto pair = [](float lo, float hi) {
