@@ -33,6 +33,8 @@ from pathlib import Path
 
 import numpy as np
 
+from paper_2602_18741_b200.colorimetry import cmf_analytic
+
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
@@ -45,7 +47,7 @@ N_SPEC = 81
 # Per-config shape, algorithmic bytes per unit and unit names.
 CONFIGS = {
     "1": dict(name="codec round trip N=2^20, n=81, k=6 -> codes+spectra+XYZ+sRGB", units=1 << 20, k=6,
-              unit="M spectra/s", bytes_per_unit=696, rot=2),
+              unit="M spectra/s", bytes_per_unit=696, rot=2, cmf="analytic"),
     "2": dict(name="1920x1080 G-buffer, k=6 (2 RGB passes), 8 lights, latent shade -> XYZ+sRGB",
               W=1920, H=1080, k=6, L=8, unit="Mpixel/s", bytes_per_unit=60, rot=8),
     "3": dict(name="3840x2160 G-buffer, k=9 (3 RGB passes), 32 lights, latent shade -> spectra(81)+sRGB",
@@ -418,7 +420,7 @@ def config_dict(key: str) -> dict:
     """The workload description both arms print (identical, so the driver can match them)."""
     cfg = CONFIGS[key]
     d = {"workload": cfg["name"], "config_id": key}
-    for f in ("W", "H", "units", "k", "L", "spp"):
+    for f in ("W", "H", "units", "k", "L", "spp", "cmf"):
         if f in cfg:
             d[f] = cfg[f]
     return d
@@ -469,7 +471,10 @@ class Workload:
         self.key = cfg_key
         k = cfg["k"]
         E, D = synth.codec_weights(SEED, k, N_SPEC)
-        self.codec = codec = api.Codec(ctx, E, D)
+        # config 1 projects with the analytic multi-lobe CIE 1931 fit BASELINE.json names; the
+        # other configs with the reference's tabulated CmfTable rows
+        cmf = cmf_analytic(N_SPEC) if cfg.get("cmf") == "analytic" else None
+        self.codec = codec = api.Codec(ctx, E, D, cmf=cmf)
         self.sets = []
         self.extra = {}  # workload facts added to the JSON line's config
         R = cfg["rot"]
@@ -1217,10 +1222,17 @@ def verify_config(key: str, rank: int = 0) -> dict:
         hS = S.cpu().numpy()
         want = {"codes": np.zeros((P, k), np.float32), "spectra": np.zeros((P, N_SPEC), np.float32),
                 "xyz": np.zeros((P, 3), np.float32), "rgb": np.zeros((P, 3), np.float32)}
-        ref.ref_codec_roundtrip(E, D, k, hS, P, want["codes"], want["spectra"], want["xyz"], want["rgb"], 0)
+        # codes and spectra: the compiled reference; XYZ / sRGB: the oracle's restatement of
+        # image_to_linear_rgb with the analytic CMF rows the config names (the reference's
+        # CmfTable is tabulated)
+        ref.ref_codec_roundtrip(E, D, k, hS, P, want["codes"], want["spectra"], None, None, 0)
+        orc = oracle.oracle()
+        junk = [np.zeros((P, d), np.float32) for d in (k, N_SPEC)]
+        orc.orc_codec_roundtrip(E, D, k, N_SPEC, cmf_analytic(N_SPEC), 5.0, hS, P, junk[0], junk[1], want["xyz"],
+                                want["rgb"])
         for name in ("codes", "spectra", "xyz", "rgb"):
             checks.append(_cmp(name, outs[name].cpu().numpy(), want[name], 1e-5))
-        sample = f"all {P} spectra"
+        sample = f"all {P} spectra (XYZ / sRGB with the analytic CMF fit)"
     elif key == "4":
         pidx, iidx, tw, outs = wl.sets[0]
         W, H, spp = cfg["W"], cfg["H"], cfg["spp"]

@@ -75,3 +75,31 @@ def white_xyz(n: int) -> tuple[float, float, float]:
             acc += scale * row[i] * d[i]
         out.append(acc)
     return tuple(out)
+
+
+# The analytic multi-lobe Gaussian fit of the CIE 1931 2-degree colour-matching functions
+# (Wyman, Sloan & Shirley, "Simple Analytic Approximations to the CIE XYZ Color Matching
+# Functions", JCGT 2(2), 2013): each function is a sum of piecewise Gaussians
+# g(l; mu, s1, s2) = exp(-(l - mu)^2 / (2 s^2)) with s = s1 below mu and s2 above.  BASELINE.json
+# config 1 names this fit; it lies within 1.4 % of the tabulated functions' peaks on the
+# 81-sample grid (tests/test_oracle.py pins that).
+_CMF_LOBES = {
+    "xbar": ((1.056, 599.8, 37.9, 31.0), (0.362, 442.0, 16.0, 26.7), (-0.065, 501.1, 20.4, 26.2)),
+    "ybar": ((0.821, 568.8, 46.9, 40.5), (0.286, 530.9, 16.3, 31.1)),
+    "zbar": ((1.217, 437.0, 11.8, 36.0), (0.681, 459.0, 26.0, 13.8)),
+}
+
+
+def _lobe(lam: np.ndarray, mu: float, s1: float, s2: float) -> np.ndarray:
+    s = np.where(lam < mu, s1, s2)
+    t = (lam - mu) / s
+    return np.exp(-0.5 * t * t)
+
+
+def cmf_analytic(n: int) -> np.ndarray:
+    """3 x n colour-matching rows of the analytic multi-lobe fit on the n-sample grid."""
+    lam = wavelengths(n)
+    rows = []
+    for name in ("xbar", "ybar", "zbar"):
+        rows.append(sum(a * _lobe(lam, mu, s1, s2) for a, mu, s1, s2 in _CMF_LOBES[name]))
+    return np.ascontiguousarray(np.stack(rows), dtype=np.float64)

@@ -152,6 +152,32 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Warp-wide variants: every lane of the issuing warp executes them and elect.sync picks the
+// one that issues.  Under `if (lane == 0)` with register operands the compiler wraps every
+// UTCHMMA in a per-thread "waterfall" loop (ELECT / R2UR.BROADCAST / BRA.U.ANY): ~54 cycles per
+// MMA from one thread (tools/mma_probe4.cu); warp-wide with elect.sync inside the asm: 17
+// cycles (N = 16) and the full tensor rate at N = 64 (32 cycles) from a single issuer.
+__device__ __forceinline__ void mma_ss_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_ts_w(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p, e;\nsetp.ne.b32 p, %4, 0;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n.reg .pred e;\nelect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
@@ -329,11 +355,9 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       if (elect && p.use_tma && t + 2 * tstride < p.ntiles) load_tile(t + 2 * tstride, s);
     };
     auto issue_l1 = [&]() {
-      if (elect) {
-        tc_fence_after();
-        mma_ss(tD, umma_desc(sA1, kChunkA, 128), umma_desc(sW1, kHid * 16, 128), id64, 0);
-        mma_commit(bar_l1);
-      }
+      tc_fence_after();
+      mma_ss_w(tD, umma_desc(sA1, kChunkA, 128), umma_desc(sW1, kHid * 16, 128), id64, 0);
+      mma_commit_w(bar_l1);
       __syncwarp();
     };
     if (t0 < p.ntiles) {
@@ -345,14 +369,12 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       const uint32_t ph = iter & 1;
       const int64_t tn = t + tstride;
       mbar_wait(bar_a2, ph);  // A2(t) in TMEM, D read out
-      if (elect) {
-        tc_fence_after();
+      tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < (kB2Epi ? kHid : kK2) / 16; ++kk)
-          mma_ts(tD, kk < kHid / 16 ? tA + kk * 8 : tC, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128),
+      for (int kk = 0; kk < (kB2Epi ? kHid : kK2) / 16; ++kk)
+        mma_ts_w(tD, kk < kHid / 16 ? tA + kk * 8 : tC, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128),
                  id64, kk > 0);
-        mma_commit(bar_l2);
-      }
+      mma_commit_w(bar_l2);
       __syncwarp();
       if (tn < p.ntiles) {
         mbar_wait(bar_l1, ph);  // layer 1 of tile t has read A1
@@ -365,13 +387,11 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       // A region the epilogue needs layer 3 done before it writes the next A2, so layer 3
       // goes first there.
       if (!kL3First && tn < p.ntiles) issue_l1();
-      if (elect) {
-        tc_fence_after();
+      tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < kK3 / 16; ++kk)
-          mma_ts(tD3, tA3 + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
-        mma_commit(bar_l3);
-      }
+      for (int kk = 0; kk < kK3 / 16; ++kk)
+        mma_ts_w(tD3, tA3 + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
+      mma_commit_w(bar_l3);
       __syncwarp();
       if (kL3First && tn < p.ntiles) issue_l1();
     }
@@ -588,24 +608,21 @@ __device__ __forceinline__ void mlp2_issuer(const Mlp2Params& p, unsigned char* 
   int it = 0;
   for (int64_t t = t0; t < p.ntiles; t += tstride, ++it) {
     mbar_wait(bar_a2, it & 1);  // A2(t) in TMEM; its rgb slot has been read
-    if (elect) {
-      if (p.use_tma && t + kRing2 * tstride < p.ntiles) load_tile(t + kRing2 * tstride, it % kRing2);
-      tc_fence_after();
+    if (elect && p.use_tma && t + kRing2 * tstride < p.ntiles) load_tile(t + kRing2 * tstride, it % kRing2);
+    __syncwarp();
+    tc_fence_after();
 #pragma unroll
-      for (int kk = 0; kk < kK2 / 16; ++kk)
-        mma_ts(tD, kk < kHid / 16 ? tA2 + kk * 8 : tC, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128), id64,
+    for (int kk = 0; kk < kK2 / 16; ++kk)
+      mma_ts_w(tD, kk < kHid / 16 ? tA2 + kk * 8 : tC, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128), id64,
                kk > 0);
-      mma_commit(bar_l2);
-    }
+    mma_commit_w(bar_l2);
     __syncwarp();
     mbar_wait(bar_a3, it & 1);  // A3(t) in TMEM, D(t) and D3(t - 1) read out
-    if (elect) {
-      tc_fence_after();
+    tc_fence_after();
 #pragma unroll
-      for (int kk = 0; kk < kK3 / 16; ++kk)
-        mma_ts(tD3, tA3 + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
-      mma_commit(bar_l3);
-    }
+    for (int kk = 0; kk < kK3 / 16; ++kk)
+      mma_ts_w(tD3, tA3 + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
+    mma_commit_w(bar_l3);
     __syncwarp();
   }
   (void)bar_l3;

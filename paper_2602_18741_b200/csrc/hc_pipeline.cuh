@@ -84,6 +84,15 @@ __device__ __forceinline__ unsigned char* aligned_smem_base(unsigned char* raw) 
   return raw + ((kTileAlign - (a & (kTileAlign - 1))) & (kTileAlign - 1));
 }
 
+#ifndef HC_PIPE_WARP  // 1: TMA issue from a whole warp (elect.sync), 0: from thread 0
+#define HC_PIPE_WARP 0
+#endif
+#if HC_PIPE_WARP
+#define HC_PW(fn) fn##_w
+#else
+#define HC_PW(fn) fn
+#endif
+
 template <class Op>
 __global__ void __launch_bounds__(Op::THREADS)
     tile_pipeline(const __grid_constant__ typename Op::Params p, int64_t ntiles) {
@@ -97,22 +106,23 @@ __global__ void __launch_bounds__(Op::THREADS)
   unsigned char* out_base = in_base + S * Lay::kInTile;
   unsigned char* extra = out_base + S * Lay::kOutTile;
   const int tid = threadIdx.x;
+  const bool issuer = HC_PIPE_WARP ? tid < 32 : tid == 0;  // warp 0 (elect.sync) or thread 0
 
   auto issue_loads = [&](int64_t tile, int s) {
     unsigned char* stage = in_base + s * Lay::kInTile;
-    mbar_arrive_expect_tx(&bar[s], Lay::kInBytes());
+    HC_PW(mbar_arrive_expect_tx)(&bar[s], Lay::kInBytes());
 #pragma unroll
     for (int i = 0; i < Op::NIN; ++i) {
       unsigned char* dst = stage + Lay::in_off(i);
       if (i == Op::kTensorStream) {
-        tma_load_2d(dst, Op::tensor_map(p), 0, static_cast<int>(tile * T), &bar[s]);
+        HC_PW(tma_load_2d)(dst, Op::tensor_map(p), 0, static_cast<int>(tile * T), &bar[s]);
       } else {
         const unsigned char* src = static_cast<const unsigned char*>(Op::in_ptr(p, i));
         if constexpr (Op::kEvictFirstLoads)
-          bulk_g2s_evict_first(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &bar[s],
-                               policy_evict_first());
+          HC_PW(bulk_g2s_evict_first)(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &bar[s],
+                                      policy_evict_first());
         else
-          bulk_g2s(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &bar[s]);
+          HC_PW(bulk_g2s)(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &bar[s]);
       }
     }
   };
@@ -129,7 +139,7 @@ __global__ void __launch_bounds__(Op::THREADS)
   pdl_wait_prior_grids();
   // The first STAGES tiles are requested before the op's table setup (e.g. the
   // palette copy) so the two latencies overlap at kernel start.
-  if (tid == 0) {
+  if (issuer) {
     for (int s = 0; s < S; ++s) {
       const int64_t tile = blockIdx.x + static_cast<int64_t>(s) * gridDim.x;
       if (tile < ntiles) issue_loads(tile, s);
@@ -144,7 +154,7 @@ __global__ void __launch_bounds__(Op::THREADS)
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++iter) {
     const int s = iter % S;
     const uint32_t phase = (iter / S) & 1;
-    if (tid == 0) bulk_wait_read<S - 1>();  // out[s] no longer read by the store of tile - S
+    if (issuer) bulk_wait_read<S - 1>();  // out[s] no longer read by the store of tile - S
     mbar_wait(&bar[s], phase);
     __syncthreads();
 
@@ -160,20 +170,20 @@ __global__ void __launch_bounds__(Op::THREADS)
     if (Op::NOUT > 0) fence_proxy_async_smem();
     __syncthreads();
 
-    if (tid == 0) {
+    if (issuer) {
       if (Op::NOUT > 0) {
 #pragma unroll
         for (int i = 0; i < Op::NOUT; ++i) {
           unsigned char* dst = static_cast<unsigned char*>(Op::out_ptr(p, i));
-          if (dst) bulk_s2g(dst + tile * T * Op::out_bytes(i), outs[i], T * Op::out_bytes(i));
+          if (dst) HC_PW(bulk_s2g)(dst + tile * T * Op::out_bytes(i), outs[i], T * Op::out_bytes(i));
         }
-        bulk_commit();
+        HC_PW(bulk_commit)();
       }
       const int64_t next = tile + static_cast<int64_t>(S) * gridDim.x;
       if (next < ntiles) issue_loads(next, s);
     }
   }
-  if (tid == 0) bulk_wait_all<0>();
+  if (issuer) bulk_wait_all<0>();
   Op::finish(p, st, extra);
 }
 
@@ -214,29 +224,30 @@ __global__ void __launch_bounds__(Op::THREADS + kProducerWarp)
   unsigned char* out_base = in_base + S * Lay::kInTile;
   unsigned char* extra = out_base + WsLayout<Op>::kOutSlots * Lay::kOutTile;
   const int tid = threadIdx.x;
-  const bool producer = tid == Op::THREADS;
+  // the producer is the extra warp (elect.sync issue) or its first thread
+  const bool producer = HC_PIPE_WARP ? tid >= Op::THREADS : tid == Op::THREADS;
 
   auto issue_loads = [&](int64_t tile, int s) {
     unsigned char* stage = in_base + s * Lay::kInTile;
-    mbar_arrive_expect_tx(&full[s], Lay::kInBytes());
+    HC_PW(mbar_arrive_expect_tx)(&full[s], Lay::kInBytes());
 #pragma unroll
     for (int i = 0; i < Op::NIN; ++i) {
       unsigned char* dst = stage + Lay::in_off(i);
       if (i == Op::kTensorStream) {
-        tma_load_2d(dst, Op::tensor_map(p), 0, static_cast<int>(tile * T), &full[s]);
+        HC_PW(tma_load_2d)(dst, Op::tensor_map(p), 0, static_cast<int>(tile * T), &full[s]);
       } else {
         const unsigned char* src = static_cast<const unsigned char*>(Op::in_ptr(p, i));
         if constexpr (Op::kEvictFirstLoads)
-          bulk_g2s_evict_first(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &full[s],
-                               policy_evict_first());
+          HC_PW(bulk_g2s_evict_first)(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &full[s],
+                                      policy_evict_first());
         else
-          bulk_g2s(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &full[s]);
+          HC_PW(bulk_g2s)(dst, src + tile * T * Op::in_bytes(i), T * Op::in_bytes(i), &full[s]);
       }
     }
   };
 
   pdl_launch_dependents();
-  if (producer) {
+  if (tid == Op::THREADS) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
@@ -250,7 +261,7 @@ __global__ void __launch_bounds__(Op::THREADS + kProducerWarp)
       const int64_t tile = blockIdx.x + static_cast<int64_t>(s) * gridDim.x;
       if (tile < ntiles) issue_loads(tile, s);
     }
-    for (int o = 0; o < SO; ++o) mbar_arrive(&ofree[o]);  // every output slot starts free
+    for (int o = 0; o < SO; ++o) HC_PW(mbar_arrive)(&ofree[o]);  // every output slot starts free
   }
   Op::setup(p, extra);
   __syncthreads();
@@ -286,15 +297,15 @@ __global__ void __launch_bounds__(Op::THREADS + kProducerWarp)
 #pragma unroll
         for (int i = 0; i < Op::NOUT; ++i) {
           unsigned char* dst = static_cast<unsigned char*>(Op::out_ptr(p, i));
-          if (dst) bulk_s2g(dst + tile * T * Op::out_bytes(i), ob + Lay::out_off(i), T * Op::out_bytes(i));
+          if (dst) HC_PW(bulk_s2g)(dst + tile * T * Op::out_bytes(i), ob + Lay::out_off(i), T * Op::out_bytes(i));
         }
-        bulk_commit();
+        HC_PW(bulk_commit)();
       }
       const int64_t next = tile + static_cast<int64_t>(S) * gridDim.x;
       if (next < ntiles) issue_loads(next, s);
       if (Op::NOUT > 0 && iter + 1 >= SO) {
         bulk_wait_read<SO - 1>();  // the store of tile iter + 1 - SO has read its slot
-        mbar_arrive(&ofree[(iter + 1) % SO]);
+        HC_PW(mbar_arrive)(&ofree[(iter + 1) % SO]);
       }
     }
     bulk_wait_all<0>();

@@ -109,6 +109,55 @@ __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// ---- warp-wide issue (`_w`): the whole warp calls, elect.sync inside the asm picks one lane
+// (the lowest active, so the same lane every time: bulk groups are per thread).  Issued from
+// `if (tid == 0)` with register operands, every UBLKCP / UTMALDG is wrapped by the compiler in a
+// per-thread ELECT / BRA.U.ANY loop (tools/mma_probe4.cu measured the same for tcgen05.mma:
+// 54 -> 17 cycles per instruction); warp-wide the instruction is straight-line.
+#define HC_ELECT_PRED "elect.sync _|e, 0xffffffff;\n"
+__device__ __forceinline__ void mbar_arrive_expect_tx_w(uint64_t* bar, uint32_t bytes) {
+  asm volatile("{\n.reg .pred e;\n" HC_ELECT_PRED
+               "@e mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_w(uint64_t* bar) {
+  asm volatile("{\n.reg .pred e;\n" HC_ELECT_PRED "@e mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n}\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_w(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("{\n.reg .pred e;\n" HC_ELECT_PRED
+               "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(
+                   smem_u32(dst_smem)),
+               "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s_evict_first_w(void* dst_smem, const void* src_gmem, uint32_t bytes,
+                                                       uint64_t* bar, uint64_t policy) {
+  asm volatile("{\n.reg .pred e;\n" HC_ELECT_PRED
+               "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+               "[%3], %4;\n}\n" ::"r"(smem_u32(dst_smem)),
+               "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_w(void* dst_smem, const void* tmap, int x, int y, uint64_t* bar) {
+  asm volatile("{\n.reg .pred e;\n" HC_ELECT_PRED
+               "@e cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+               "%3}], [%4];\n}\n" ::"r"(smem_u32(dst_smem)),
+               "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_w(void* dst_gmem, const void* src_smem, uint32_t bytes) {
+  asm volatile("{\n.reg .pred e;\n" HC_ELECT_PRED "@e cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n}\n" ::"l"(
+                   dst_gmem),
+               "r"(smem_u32(src_smem)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit_w() {
+  asm volatile("{\n.reg .pred e;\n" HC_ELECT_PRED "@e cp.async.bulk.commit_group;\n}\n" ::: "memory");
+}
+
 // Make generic-proxy shared-memory writes visible to the async (bulk) proxy.
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

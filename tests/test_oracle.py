@@ -301,3 +301,16 @@ def test_metric_tail_oracle_matches_compiled_reference(orc, n):
     orc.orc_delta_e94_report(xg, xt, P, white, d1, o1)
     ref.ref_delta_e94_report(xg, xt, P, d2, o2)
     assert np.array_equal(d1, d2) and np.array_equal(o1, o2)
+
+
+def test_analytic_cmf_fit_tracks_the_tabulated_cie1931():
+    """The analytic multi-lobe fit BASELINE config 1 names stays within 1.5 % of the peak of the
+    tabulated CIE 1931 functions the reference uses (CmfTable), on both grids."""
+    from paper_2602_18741_b200.colorimetry import cmf_analytic, cmf_matrix
+
+    for n in (81, 47):
+        fit, tab = cmf_analytic(n), cmf_matrix(n)
+        for r in range(3):
+            assert np.max(np.abs(fit[r] - tab[r])) <= 0.015 * tab[r].max()
+        # and it is a different function (not the table under another name)
+        assert np.max(np.abs(fit - tab)) > 1e-3
