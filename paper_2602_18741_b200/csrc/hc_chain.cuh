@@ -294,6 +294,211 @@ __global__ void __launch_bounds__(256) chain_latent_rep_kernel(const __grid_cons
   }
 }
 
+// k = 6 chain, instruction-lean (config 4).  chain_latent_rep_kernel is bounded by the L1
+// data pipe (the random code lookups: 5 x 24 B per sample) *and* by issue (~100
+// instructions per sample: per-lookup bounds checks, IMAD row addressing, 48 scalar FP ops).
+// This kernel keeps the lookup bytes (the codes are fp32) and cuts the instructions:
+//  * rows are 256 B: [c0..c3] as a float4 replicated 8x (LDS.128, each quarter-warp phase
+//    reads 8 distinct 16-byte slots = all 32 banks) then [c4 c5] as a float2 replicated 16x
+//    (LDS.64, conflict-free per half-warp), so a row address is (index << 8) | lane offset,
+//    built by ONE byte permute (PRMT) straight from the packed u8x4 palette word;
+//  * the palette table always has 256 rows (zero past n_pal), so a u8 index can never read
+//    out of bounds: out-of-range indices are detected once per pixel from a running byte-wise
+//    max (__vmaxu4) instead of per lookup; illuminant indices are clamped (min) and tracked;
+//  * the chain is evaluated in Horner form on packed pairs (fma.rn.f32x2 / mul.rn.f32x2):
+//      S = a0 (.) (t0 + a1 (.) (t1 + a2 (.) (t2 + t3 a3))),  part += le (.) S
+//    = sum_d t_d prod_{e<=d} a_e (.) le, the reference's rad (renderer.cpp:505-510, :530-533)
+//    re-associated: 5 packed ops per code pair, 15 per sample.
+// Shared memory: 64 KB palette + 256 B per illuminant + 6.2 KB of staging (config 4: 74 KB,
+// 3 CTAs / SM).
+#ifndef HC_CHAIN_IIDX128
+#define HC_CHAIN_IIDX128 0
+#endif
+constexpr int kChainV3Row = 256;
+constexpr int kChainV3Stage = 6 * 33;  // floats of per-warp staging for the pixel sums
+
+__device__ __forceinline__ uint64_t chain_fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t chain_mul2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t chain_dup(float x) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(d) : "f"(x));
+  return d;
+}
+
+// One sample of the v3 chain: the 5 lookups and the packed Horner chain into part[3].
+template <bool kCheckPal>
+__device__ __forceinline__ void chain_v3_sample(const unsigned char* tab3, const unsigned char* ill_tab, uint32_t offs,
+                                                uint32_t pk, uint32_t li_raw, float4 t4, uint32_t ill_last,
+                                                uint32_t& pmax, uint32_t& imax, uint64_t part[3]) {
+  if (kCheckPal) pmax = __vmaxu4(pmax, pk);
+  imax = max(imax, li_raw);
+  const uint32_t li = min(li_raw, ill_last);
+  uint64_t a[4][3];
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {
+    const uint32_t o4 = __byte_perm(pk, offs, 0x6604u | (d << 4));  // (idx << 8) | off4
+    const uint32_t o2 = __byte_perm(pk, offs, 0x6605u | (d << 4));  // (idx << 8) | off2
+    const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(tab3 + o4);
+    a[d][0] = v.x;
+    a[d][1] = v.y;
+    a[d][2] = *reinterpret_cast<const unsigned long long*>(tab3 + o2);
+  }
+  const uint32_t lo4 = __byte_perm(li, offs, 0x6604u), lo2 = __byte_perm(li, offs, 0x6605u);
+  const ulonglong2 lv = *reinterpret_cast<const ulonglong2*>(ill_tab + lo4);
+  const uint64_t le[3] = {lv.x, lv.y, *reinterpret_cast<const unsigned long long*>(ill_tab + lo2)};
+  const uint64_t T0 = chain_dup(t4.x), T1 = chain_dup(t4.y), T2 = chain_dup(t4.z), T3 = chain_dup(t4.w);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    uint64_t u = chain_fma2(a[3][j], T3, T2);
+    u = chain_fma2(a[2][j], u, T1);
+    u = chain_fma2(a[1][j], u, T0);
+    part[j] = chain_fma2(le[j], chain_mul2(a[0][j], u), part[j]);
+  }
+}
+
+// kCheckPal: n_pal < 256, so palette indices are range-checked (byte-wise running max).
+template <bool kCheckPal>
+__global__ void __launch_bounds__(256) chain_latent_v3_kernel(const __grid_constant__ ChainLatentParams<6> p) {
+  extern __shared__ __align__(16) unsigned char tab3[];
+  // Table fill: row r (palette r < 256, illuminant 256 + i), 16-byte chunk c of 16.
+  const int n_rows = 256 + p.n_ill;
+  for (int i = threadIdx.x; i < n_rows * 16; i += blockDim.x) {
+    const int r = i >> 4, c = i & 15;
+    const float* src = r < 256 ? (r < p.n_pal ? p.pal + r * 6 : nullptr) : p.ill + (r - 256) * 6;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (src) {
+      if (c < 8) v = make_float4(__ldg(src), __ldg(src + 1), __ldg(src + 2), __ldg(src + 3));
+      else v = make_float4(__ldg(src + 4), __ldg(src + 5), __ldg(src + 4), __ldg(src + 5));
+    }
+    *reinterpret_cast<float4*>(tab3 + r * kChainV3Row + c * 16) = v;
+  }
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31;
+  const int g = lane & (kChainLanes - 1);
+  // Byte 0: this lane's float4 replica offset, byte 1: its float2 replica offset.
+  const uint32_t offs = static_cast<uint32_t>((lane & 7) * 16) | (static_cast<uint32_t>(128 + (lane & 15) * 8) << 8);
+  const unsigned char* ill_tab = tab3 + 256 * kChainV3Row;
+  float* stg = reinterpret_cast<float*>(tab3 + n_rows * kChainV3Row) + (threadIdx.x >> 5) * kChainV3Stage;
+  constexpr int kPixPerWarp = 32 / kChainLanes;
+  const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t ill_last = static_cast<uint32_t>(p.n_ill - 1);
+  uint32_t pmax = 0, imax = 0;  // running maxima of the palette / illuminant indices
+  const int per_lane = p.spp / kChainLanes;
+  for (int64_t qd = warp_id; qd * kPixPerWarp < p.P; qd += nwarps) {
+    const int64_t pix = qd * kPixPerWarp + lane / kChainLanes;
+    const bool valid = pix < p.P;
+    uint64_t part[3] = {0ull, 0ull, 0ull};
+    const int64_t base = pix * p.spp;
+    {
+      const int64_t npix = (qd + nwarps) * kPixPerWarp + lane / kChainLanes;
+      if (npix < p.P) {
+        const int64_t nb = npix * p.spp;
+        const char* twl = reinterpret_cast<const char*>(p.tw + nb);
+        for (int off = g * 128; off < p.spp * 16; off += kChainLanes * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(twl + off));
+        const char* pkl = reinterpret_cast<const char*>(p.pidx + nb);
+        for (int off = g * 128; off < p.spp * 4; off += kChainLanes * 128)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(pkl + off));
+        if (g == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.iidx + nb));
+      }
+    }
+    // Samples in groups of kGroup per lane, every load of a group issued before any use
+    // (~170 B in flight per lane); a past-the-end pixel's lanes load zeros (index 0, weight 0).
+    constexpr int kGroup = 8;
+    const int full = per_lane - per_lane % kGroup;
+    for (int m0 = 0; m0 < full; m0 += kGroup) {
+      uint32_t pkg[kGroup], lig[kGroup];
+      float4 t4g[kGroup];
+#pragma unroll
+      for (int m = 0; m < kGroup; ++m) {
+        const int64_t s = base + g + static_cast<int64_t>(m0 + m) * kChainLanes;
+        pkg[m] = valid ? __ldg(p.pidx + s) : 0u;
+        if (!HC_CHAIN_IIDX128) lig[m] = valid ? static_cast<uint32_t>(__ldg(p.iidx + s)) : 0u;
+        t4g[m] = valid ? ldg_stream(p.tw + s) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (HC_CHAIN_IIDX128) {
+        // The group's 64 illuminant bytes of this pixel in 4 LDG.128 (the pixel group's 8 lanes
+        // load the same addresses: 2 L1 tag lookups per instruction instead of 8 byte loads at
+        // 2 each); lane g keeps words 2m + g/4 and extracts byte g % 4.  Needs spp % 16 == 0 and
+        // a 16-byte aligned iidx (checked by the launcher).
+        const uint4* blk = reinterpret_cast<const uint4*>(p.iidx + base + static_cast<int64_t>(m0) * kChainLanes);
+        const uint32_t hsel = static_cast<uint32_t>(g >> 2), bsel = 0x4440u | static_cast<uint32_t>(g & 3);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint4 w = valid ? __ldg(blk + q) : make_uint4(0u, 0u, 0u, 0u);
+          lig[2 * q] = __byte_perm(hsel ? w.y : w.x, 0u, bsel);
+          lig[2 * q + 1] = __byte_perm(hsel ? w.w : w.z, 0u, bsel);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < kGroup; ++m)
+        chain_v3_sample<kCheckPal>(tab3, ill_tab, offs, pkg[m], lig[m], t4g[m], ill_last, pmax, imax, part);
+    }
+    for (int m = full; m < per_lane; ++m) {
+      const int64_t s = base + g + static_cast<int64_t>(m) * kChainLanes;
+      chain_v3_sample<kCheckPal>(tab3, ill_tab, offs, valid ? __ldg(p.pidx + s) : 0u,
+                                 valid ? static_cast<uint32_t>(__ldg(p.iidx + s)) : 0u,
+                                 valid ? ldg_stream(p.tw + s) : make_float4(0.f, 0.f, 0.f, 0.f), ill_last, pmax,
+                                 imax, part);
+    }
+    // Pixel sums: the 8 lanes' fp32 partials are transposed through a per-warp staging area
+    // (6 rows of 33 words: conflict-free both ways), lane g < 6 of each pixel group adds the 8
+    // partials of code g in fp64 (renderer.cpp:548-551) and the group's lane 0 gathers the 6
+    // codes by shuffle for the XYZ / sRGB projection: 20 L1 wavefronts per pixel quad instead of
+    // the 36 of an fp64 butterfly (the kernel is bound by the L1 data pipe).
+    __syncwarp();  // the previous quad's staging reads are done
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      float2 f;
+      memcpy(&f, &part[j], 8);
+      stg[(2 * j) * 33 + lane] = f.x;
+      stg[(2 * j + 1) * 33 + lane] = f.y;
+    }
+    __syncwarp();
+    const int grp0 = lane & ~(kChainLanes - 1);
+    float z = 0.f;
+    if (g < 6) {
+      double acc = 0.0;
+#pragma unroll
+      for (int m = 0; m < kChainLanes; ++m) acc += static_cast<double>(stg[g * 33 + grp0 + m]);
+      z = static_cast<float>(acc * (1.0 / p.spp));
+      if (valid && p.latent) p.latent[pix * 6 + g] = z;
+    }
+    float zz[6];
+#pragma unroll
+    for (int j = 0; j < 6; ++j) zz[j] = __shfl_sync(0xffffffffu, z, grp0 + j);
+    if (valid && g == 0) {
+      float xyz[3], rgb[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float a = p.Mxyz[c * 6] * zz[0];
+#pragma unroll
+        for (int j = 1; j < 6; ++j) a = fmaf(p.Mxyz[c * 6 + j], zz[j], a);
+        xyz[c] = a;
+      }
+      xyz_to_rgb(p.Crgb, xyz, rgb);
+      if (p.xyz)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) p.xyz[pix * 3 + c] = xyz[c];
+      if (p.rgb)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) p.rgb[pix * 3 + c] = rgb[c];
+    }
+  }
+  const uint32_t pm = max(max(pmax & 0xffu, (pmax >> 8) & 0xffu), max((pmax >> 16) & 0xffu, pmax >> 24));
+  if (pm >= static_cast<uint32_t>(p.n_pal) || imax > ill_last) atomicOr(p.err, kErrIndexRange);
+}
+
 // Naive n-sample chain: the same recursion per wavelength.  Loop order is
 // wavelength-outer so per-lane state stays in registers; the pixel spectrum
 // value float(acc/spp) is projected to XYZ on the fly (colorimetry.cpp:75-87).

@@ -58,6 +58,20 @@ int chain_latent_k(hc_codec c, const float* pal, int n_pal, const float* ill, in
   p.rgb = rgb;
   p.err = c->ctx->d_err;
   int grid = 0;
+#ifndef HC_CHAIN_V3
+#define HC_CHAIN_V3 1
+#endif
+  if constexpr (K == 6) {
+    if (HC_CHAIN_V3 && (!HC_CHAIN_IIDX128 || (spp % 16 == 0 && (reinterpret_cast<uintptr_t>(iidx) & 15u) == 0))) {  // instruction-lean k = 6 kernel (256-row palette table, packed Horner chain)
+      const int smem = (256 + n_ill) * kChainV3Row + 8 * kChainV3Stage * 4;  // 8 warps of staging
+      auto fn = n_pal < 256 ? chain_latent_v3_kernel<true> : chain_latent_v3_kernel<false>;
+      int rc = chain_grid(c->ctx, fn, smem, P, &grid);
+      if (rc != HC_OK) return rc;
+      fn<<<grid, 256, smem, c->ctx->stream>>>(p);
+      HC_CHECK_LAUNCH(c->ctx, "chain_latent_v3_kernel");
+      return HC_OK;
+    }
+  }
   if constexpr (K <= 6) {
 #ifndef HC_CHAIN_SHFL_ILL
 #define HC_CHAIN_SHFL_ILL 0

@@ -69,7 +69,15 @@ constexpr bool kB2Epi = HC_MLP_B2_EPI;     // b2 added in the layer-2 epilogue i
 constexpr int kStreams = HC_MLP_STREAMS;    // tile streams per CTA
 constexpr bool kSepA3 = kStreams < 4;       // A3 in its own TMEM region (fits with 3 streams only)
 constexpr bool kL3First = HC_MLP_L3_FIRST;  // issue layer 3 of a tile before layer 1 of the next
-constexpr int kEpiThreads = 128 * kStreams; // epilogue warps: warp w -> stream w / 4, lane quarter w % 4
+#ifndef HC_MLP_EPI_WARPS
+#define HC_MLP_EPI_WARPS 4
+#endif
+// Epilogue warps per stream: 4 (one per TMEM lane quarter, all 64 accumulator columns) or 8
+// (two per lane quarter, 32 columns each: half the tcgen05.ld / cvt / tcgen05.st chain per warp).
+constexpr int kEpiW = HC_MLP_EPI_WARPS;
+static_assert(kEpiW == 4 || kEpiW == 8, "epilogue warps per stream");
+constexpr int kEpiCols = kHid * 4 / kEpiW;   // accumulator columns per epilogue warp
+constexpr int kEpiThreads = 32 * kEpiW * kStreams; // warp w -> stream w / kEpiW, lane quarter w % 4
 constexpr int kThreads = kEpiThreads + 32 * kStreams;  // + one MMA-issuer warp per stream
 constexpr int kK2 = 80;                     // layer 2 K: 64 hidden + constant-1 column (b2 rides the MMA)
 constexpr int kK3 = 64;                     // layer 3 K: b3 (6 values) is added in the epilogue instead of
@@ -223,20 +231,20 @@ __device__ __forceinline__ float softplus1(float x) {
 // Hidden-layer epilogue: fp32 accumulator row (64 TMEM columns of this thread's
 // lane) -> bf16 relu(acc [+ bias]) packed in pairs (element 2j in the low half)
 // -> 32 TMEM columns of the next layer's A operand.
-template <bool kBias>
+// kCols accumulator columns starting at tmem_acc -> kCols / 2 packed A columns at tmem_a.
+template <bool kBias, int kCols = 64>
 __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem_a, const float* bias) {
 #ifdef HC_MLP_PROBE_NOEPI  // timing probe only: no accumulator read-out (wrong results)
   return;
 #endif
-  uint32_t va[4][16];
-  HC_TMEM_LD16(tmem_acc + 0, va[0]);
-  HC_TMEM_LD16(tmem_acc + 16, va[1]);
-  HC_TMEM_LD16(tmem_acc + 32, va[2]);
-  HC_TMEM_LD16(tmem_acc + 48, va[3]);
-  tmem_wait_ld();
-  uint32_t pk[2][16];
+  constexpr int kQ = kCols / 16;
+  uint32_t va[kQ][16];
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
+  for (int q = 0; q < kQ; ++q) HC_TMEM_LD16(tmem_acc + q * 16, va[q]);
+  tmem_wait_ld();
+  uint32_t pk[kQ / 2][16];
+#pragma unroll
+  for (int q = 0; q < kQ; ++q)
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       float lo = __uint_as_float(va[q][2 * j]), hi = __uint_as_float(va[q][2 * j + 1]);
@@ -246,8 +254,8 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem
       }
       pk[q >> 1][(q & 1) * 8 + j] = pack_relu_bf16(lo, hi);
     }
-  HC_TMEM_ST16(tmem_a + 0, pk[0]);
-  HC_TMEM_ST16(tmem_a + 16, pk[1]);
+#pragma unroll
+  for (int q = 0; q < kQ / 2; ++q) HC_TMEM_ST16(tmem_a + q * 16, pk[q]);
   tmem_wait_st();
 }
 
@@ -256,8 +264,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const bool issuer = tid >= kEpiThreads;
-  const int st = issuer ? (tid - kEpiThreads) >> 5 : warp >> 2;  // tile stream
-  const int quarter = warp & 3;                                    // TMEM lane quarter (epilogue warps)
+  const int st = issuer ? (tid - kEpiThreads) >> 5 : warp / kEpiW;  // tile stream
+  const int quarter = warp & 3;                                       // TMEM lane quarter (epilogue warps)
+  const int half = kEpiW == 8 ? (warp >> 2) & 1 : 0;                  // column half (8 epilogue warps)
+  const bool codes_warp = half == 0;  // reads D3 and stores the codes
   const int r = tid & 127;                                         // tile row = TMEM lane (epilogue)
   unsigned char* A1 = sm + kOffStreams + st * kStreamBytes;
   float* in_tiles = reinterpret_cast<float*>(A1 + kA1Bytes);
@@ -275,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
     reinterpret_cast<uint4*>(sm)[i] = reinterpret_cast<const uint4*>(p.wimg)[i];
   if (issuer && (tid & 31) == 0) {
     for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
-    for (int i = 5; i < 8; ++i) mbar_init(&bars[i], 4);
+    for (int i = 5; i < 8; ++i) mbar_init(&bars[i], i == 5 ? 4 : kEpiW);
     fence_mbar_init();
   }
   if (warp == 0) {
@@ -405,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
     int prev_rows = 0;
     const int k = p.k;
     auto store_codes = [&]() {
-      if (prev_row0 < 0 || r >= prev_rows) return;
+      if (!codes_warp || prev_row0 < 0 || r >= prev_rows) return;
       float* o = p.out + (prev_row0 + r) * k;
       if (k == 6) {
         float y[6];
@@ -432,22 +442,25 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       const int64_t row0 = (p.first_tile + t) * kMlpM;
       const int64_t left = p.P - row0;
       const int rows = left < kMlpM ? static_cast<int>(left) : kMlpM;
-      long long* tr = (p.trace && blockIdx.x == 0 && r == 0 && iter < 32) ? p.trace + (st * 32 + iter) * 8 : nullptr;
+      long long* tr = (p.trace && blockIdx.x == 0 && r == 0 && half == 0 && iter < 32) ? p.trace + (st * 32 + iter) * 8 : nullptr;
       if (tr) tr[0] = clock64();
       if (!kSepA3 && iter > 0) {  // layer 3 of the previous tile has read A3 (the A region) and written D3
         mbar_wait(bar_l3, ph ^ 1);
         tc_fence_after();
-        HC_TMEM_LD16(tD3 + lane_off, prev_v);
-        tmem_wait_ld();
+        if (codes_warp) {
+          HC_TMEM_LD16(tD3 + lane_off, prev_v);
+          tmem_wait_ld();
+        }
       }
       if (tr) tr[1] = clock64();
       mbar_wait(bar_l1, ph);
       if (tr) tr[2] = clock64();
       tc_fence_after();
-      epilogue_hidden<false>(tD + lane_off, tA + lane_off, nullptr);  // A2 over A3 of t-1
+      epilogue_hidden<false, kEpiCols>(tD + lane_off + half * kEpiCols, tA + lane_off + half * (kEpiCols / 2),
+                                       nullptr);  // A2 over A3 of t-1
       handoff(bar_a2);
       if (tr) tr[3] = clock64();
-      if (kSepA3 && iter > 0) {  // layer 3 of the previous tile, read under this tile's layer 2
+      if (kSepA3 && iter > 0 && codes_warp) {  // layer 3 of the previous tile, read under this tile's layer 2
         mbar_wait(bar_l3, ph ^ 1);
         tc_fence_after();
         HC_TMEM_LD16(tD3 + lane_off, prev_v);
@@ -458,14 +471,15 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       mbar_wait(bar_l2, ph);
       if (tr) tr[5] = clock64();
       tc_fence_after();
-      epilogue_hidden<kB2Epi>(tD + lane_off, tA3 + lane_off, p.b2);  // A3 (over A2 unless kSepA3)
+      epilogue_hidden<kB2Epi, kEpiCols>(tD + lane_off + half * kEpiCols, tA3 + lane_off + half * (kEpiCols / 2),
+                                        p.b2 + half * kEpiCols);  // A3 (over A2 unless kSepA3)
       handoff(bar_a3);
       prev_row0 = row0;
       prev_rows = rows;
       if (tr) tr[6] = clock64();
       if (tr) tr[7] = clock64();
     }
-    if (iter > 0) {  // the last tile's codes
+    if (iter > 0 && codes_warp) {  // the last tile's codes
       mbar_wait(bar_l3, (iter - 1) & 1);
       tc_fence_after();
       HC_TMEM_LD16(tD3 + lane_off, prev_v);

@@ -372,6 +372,50 @@ def test_multibounce_vs_oracle(api, ctx, orc, spp, k, n):
     _check("chain naive rgb", host(nv["rgb"]), R)
 
 
+@pytest.mark.parametrize("n_pal,n_ill,spp,k", [(100, 5, 72, 6), (256, 200, 64, 6), (1, 1, 8, 6), (37, 16, 136, 6),
+                                                (100, 5, 72, 3), (37, 16, 24, 9)])
+def test_multibounce_small_tables(api, ctx, orc, n_pal, n_ill, spp, k):
+    """Palettes / illuminant sets smaller than the u8 index range (the k = 6 kernel range-checks
+    palette indices only when n_pal < 256), large illuminant sets, and spp with a sample tail
+    (spp / 8 not a multiple of the 8-sample load group)."""
+    codec, E, D = _codec(api, ctx, k)
+    pal = synth.palette(SEED, n_pal, 81)
+    ill = synth.lights(SEED, n_ill, 81, purpose="scene.illuminants")
+    pal_codes = codec.encode(torch.from_numpy(pal).cuda())
+    ill_codes = codec.encode(torch.from_numpy(ill).cuda())
+    P = 777
+    rng = np.random.default_rng(n_pal * 1000 + spp)
+    ph = rng.integers(0, n_pal, (P, spp, 4), dtype=np.uint8)
+    ih = rng.integers(0, n_ill, (P, spp), dtype=np.uint8)
+    th = rng.uniform(0.0, 1.5, (P, spp, 4)).astype(np.float32)
+    out = codec.multibounce_latent(pal_codes, ill_codes, torch.from_numpy(ph).cuda(), torch.from_numpy(ih).cuda(),
+                                   torch.from_numpy(th).cuda(), latent=True)
+    ctx.synchronize()
+    lat = np.zeros((P, k), np.float32)
+    orc.orc_chain(k, host(pal_codes), host(ill_codes), ph, ih, th, P, spp, 4, lat)
+    _check(f"chain latent n_pal={n_pal} n_ill={n_ill} spp={spp}", host(out["latent"]), lat)
+
+
+@pytest.mark.parametrize("which", ["pal", "ill"])
+@pytest.mark.parametrize("k", [6, 9])
+def test_multibounce_index_out_of_range_is_reported(api, ctx, which, k):
+    codec, E, D = _codec(api, ctx, k)
+    pal_codes = codec.encode(torch.from_numpy(synth.palette(SEED, 100, 81)).cuda())
+    ill_codes = codec.encode(torch.from_numpy(synth.lights(SEED, 5, 81, purpose="scene.illuminants")).cuda())
+    P, spp = 300, 64
+    ph = np.zeros((P, spp, 4), np.uint8)
+    ih = np.zeros((P, spp), np.uint8)
+    if which == "pal":
+        ph[123, 17, 2] = 100
+    else:
+        ih[299, 63] = 5
+    th = np.full((P, spp, 4), 0.5, np.float32)
+    codec.multibounce_latent(pal_codes, ill_codes, torch.from_numpy(ph).cuda(), torch.from_numpy(ih).cuda(),
+                             torch.from_numpy(th).cuda())
+    with pytest.raises(ValueError):
+        ctx.synchronize()
+
+
 def test_multibounce_golden(api, ctx, golden):
     codec = api.Codec(ctx, golden["E6"], golden["D6"])
     t = {k: torch.from_numpy(np.ascontiguousarray(golden[k])).cuda()

@@ -67,9 +67,18 @@ def main():
     pal = torch.from_numpy(synth.palette(3, 256, n)).cuda()
     ill = torch.from_numpy(synth.lights(3, 16, n, purpose="scene.illuminants")).cuda()
     pidx, iidx, tw = api.synth_chain(ctx, 3, 0, 37, 64, 256, 16)
-    ch = codec.multibounce_latent(codec.encode(pal), codec.encode(ill), pidx, iidx, tw)
+    pc, ic = codec.encode(pal), codec.encode(ill)
+    ch = codec.multibounce_latent(pc, ic, pidx, iidx, tw, latent=True)
     nch = codec.multibounce_spectral(pal, ill, pidx, iidx, tw)
-    assert rel(ch["rgb"].cpu().numpy(), nch["rgb"].cpu().numpy()) < 5e-2  # latent vs naive: codec error
+    ph, ih, th = (x.cpu().numpy() for x in (pidx, iidx, tw))
+    lat = np.zeros((37, 6), np.float32)
+    orc.orc_chain(6, pc.cpu().numpy(), ic.cpu().numpy(), ph, ih, th, 37, 64, 4, lat)
+    assert rel(ch["latent"].cpu().numpy(), lat) < 1e-5
+    spec = np.zeros((37, n), np.float32)
+    X, R = np.zeros((37, 3), np.float32), np.zeros((37, 3), np.float32)
+    orc.orc_chain(n, pal.cpu().numpy(), ill.cpu().numpy(), ph, ih, th, 37, 64, 4, spec)
+    orc.orc_spectra_to_outputs(cmf_matrix(n), grid(n)[1], n, spec, 37, X, R)
+    assert rel(nch["rgb"].cpu().numpy(), R) < 1e-5
     print("chain: ok", flush=True)
     # MLP (tcgen05 / TMEM), both kernels
     w = synth.mlp_weights(3, 6, 64)
