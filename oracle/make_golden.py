@@ -2,7 +2,8 @@
 
 Runs only in the build container (needs /root/reference and `make -C oracle ref`).
 Outputs (committed):
-  paper_2602_18741_b200/data/cmf_n{47,81}.json  CmfTable rows (colorimetry.cpp:45-61)
+  (checks) paper_2602_18741_b200/data/cmf_n{47,81}.json against CmfTable of the compiled reference
+          (the files themselves are written by tools/make_cmf_tables.py from the CIE tables)
   tests/golden/ref_rng.json                      Rng streams / pixel streams / FNV (rng.cpp)
   tests/golden/ref_generators.json               gaussian_curve / blackbody_curve / Glorot init
   tests/golden/ref_small_cases.npz               small seeded cases of every config, outputs
@@ -30,7 +31,8 @@ GOLD = ROOT / "tests" / "golden"
 
 
 def cmf_files() -> None:
-    DATA.mkdir(parents=True, exist_ok=True)
+    """The package CMF rows (tools/make_cmf_tables.py: CIE tables + an in-repo resampler) must equal
+    CmfTable of the compiled reference bit for bit (colorimetry.cpp:45-61)."""
     for n in (47, 81):
         ref = oracle.reference(n)
         t = np.zeros(7 * n)
@@ -38,15 +40,9 @@ def cmf_files() -> None:
         t = t.reshape(7, n)
         lo, step = ref.ref_lambda_min(), ref.ref_lambda_step()
         assert (lo, step) == grid(n), (lo, step, grid(n))
-        doc = {
-            "source": "CmfTable (colorimetry.cpp:45-61) of the compiled reference "
-                      f"(oracle/_ref/libhcref{n}.so): CIE 1931 2-degree observer and D65, "
-                      "linearly resampled onto the grid",
-            "n": n, "lambda_min": lo, "lambda_step": step,
-            "xbar": [float(v) for v in t[0]], "ybar": [float(v) for v in t[1]],
-            "zbar": [float(v) for v in t[2]], "d65": [float(v) for v in t[3]],
-        }
-        (DATA / f"cmf_n{n}.json").write_text(json.dumps(doc, indent=1) + "\n")
+        d = json.loads((DATA / f"cmf_n{n}.json").read_text())
+        for i, key in enumerate(("xbar", "ybar", "zbar", "d65")):
+            assert d[key] == [float(v) for v in t[i]], f"cmf_n{n}.json {key} differs from the reference CmfTable"
 
 
 def rng_file() -> None:

@@ -6,8 +6,10 @@ with wavelength_at(i) = lambda_min + step * i.
 
 CMF rows are the reference's CmfTable (colorimetry.cpp:45-61: CIE 1931 2-degree
 1 nm tables linearly resampled onto the grid, plus D65).  They are shipped as
-package data generated from the compiled reference by oracle/make_golden.py;
-at n = 81 every 5 nm sample falls exactly on a 1 nm table entry.  XYZ uses the
+package data made by tools/make_cmf_tables.py (the published CIE tables + an
+in-repo resampler; oracle/make_golden.py checks them bit-exact against the
+compiled reference's CmfTable); at n = 81 every 5 nm sample falls exactly on a
+1 nm table entry.  XYZ uses the
 radiance convention dlambda * sum cmf * s (colorimetry.cpp:75-87); sRGB the
 IEC 61966-2-1 matrix (colorimetry.cpp:22-26).
 """
@@ -46,7 +48,7 @@ def cmf_table(n: int) -> dict:
     """xbar, ybar, zbar, d65 on the n-grid as float64 arrays (+ 'cmf' 3 x n)."""
     path = DATA / f"cmf_n{n}.json"
     if not path.exists():
-        raise FileNotFoundError(f"{path} missing (generate with `python oracle/make_golden.py`)")
+        raise FileNotFoundError(f"{path} missing (generate with `python tools/make_cmf_tables.py`)")
     d = json.loads(path.read_text())
     out = {k: np.array(d[k], dtype=np.float64) for k in ("xbar", "ybar", "zbar", "d65")}
     out["cmf"] = np.stack([out["xbar"], out["ybar"], out["zbar"]])

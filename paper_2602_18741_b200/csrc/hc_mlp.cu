@@ -67,7 +67,13 @@ constexpr int kMaxK = 9;
 #endif
 constexpr bool kB2Epi = HC_MLP_B2_EPI;     // b2 added in the layer-2 epilogue instead of a 5th MMA
 constexpr int kStreams = HC_MLP_STREAMS;    // tile streams per CTA
-constexpr bool kSepA3 = kStreams < 4;       // A3 in its own TMEM region (fits with 3 streams only)
+#ifndef HC_MLP_A3_SMEM
+#define HC_MLP_A3_SMEM 0
+#endif
+// A3 in shared memory (canonical K-major image written by the layer-2 epilogue, layer 3 is an
+// SS MMA): frees 32 TMEM columns per stream, so 4 streams fit without A3 over A2.
+constexpr bool kA3Smem = HC_MLP_A3_SMEM;
+constexpr bool kSepA3 = kA3Smem || kStreams < 4;  // A3 not over A2 (own TMEM region or smem)
 constexpr bool kL3First = HC_MLP_L3_FIRST;  // issue layer 3 of a tile before layer 1 of the next
 #ifndef HC_MLP_EPI_WARPS
 #define HC_MLP_EPI_WARPS 4
@@ -76,6 +82,7 @@ constexpr bool kL3First = HC_MLP_L3_FIRST;  // issue layer 3 of a tile before la
 // (two per lane quarter, 32 columns each: half the tcgen05.ld / cvt / tcgen05.st chain per warp).
 constexpr int kEpiW = HC_MLP_EPI_WARPS;
 static_assert(kEpiW == 4 || kEpiW == 8, "epilogue warps per stream");
+static_assert(!(HC_MLP_A3_SMEM && kEpiW != 4), "A3 in smem: 4 epilogue warps");
 constexpr int kEpiCols = kHid * 4 / kEpiW;   // accumulator columns per epilogue warp
 constexpr int kEpiThreads = 32 * kEpiW * kStreams; // warp w -> stream w / kEpiW, lane quarter w % 4
 constexpr int kThreads = kEpiThreads + 32 * kStreams;  // + one MMA-issuer warp per stream
@@ -83,8 +90,9 @@ constexpr int kK2 = 80;                     // layer 2 K: 64 hidden + constant-1
 constexpr int kK3 = 64;                     // layer 3 K: b3 (6 values) is added in the epilogue instead of
                                             // paying a fifth >= 45-cycle N = 16 MMA
 constexpr int kColA = 0;                    // packed bf16 A2 (and A3 of the same tile unless kSepA3): 32 columns
-constexpr int kColA3 = kSepA3 ? 32 : 0;     // packed bf16 A3
-constexpr int kColD = kSepA3 ? 64 : 32;     // fp32 accumulator of layers 1 / 2: 64 columns
+constexpr bool kA3Tmem = kSepA3 && !kA3Smem;
+constexpr int kColA3 = kA3Tmem ? 32 : 0;    // packed bf16 A3
+constexpr int kColD = kA3Tmem ? 64 : 32;    // fp32 accumulator of layers 1 / 2: 64 columns
 constexpr int kColD3 = kColD + 64;          // fp32 accumulator of layer 3: 16 columns (separate, so layer 1
                                             // of the next tile can run while layer 3 still reads A3)
 constexpr int kColsPerStream = kColD3 + 16; // TMEM columns per stream (4 x 112 or 3 x 144 of the 512)
@@ -101,7 +109,8 @@ constexpr int kOffW2 = kOffW1 + kW1Bytes;
 constexpr int kOffW3 = kOffW2 + kW2Bytes;
 constexpr int kA1Bytes = kMlpM * kK1 * 2;            // 4 KB
 constexpr int kInTile = kMlpM * 3 * 4;               // 1536 B
-constexpr int kStreamBytes = kA1Bytes + 2 * kInTile;
+constexpr int kA3Bytes = kA3Smem ? kMlpM * kK3 * 2 : 0;  // 16 KB A3 image (kA3Smem)
+constexpr int kStreamBytes = kA1Bytes + 2 * kInTile + kA3Bytes;
 constexpr int kOffStreams = kWBytes;
 constexpr int kOffBar = kOffStreams + kStreams * kStreamBytes;
 constexpr int kBarsPerStream = 8;  // in[2], l1, l2, l3, a1, a2, a3
@@ -259,6 +268,33 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem
   tmem_wait_st();
 }
 
+// Layer-2 epilogue with A3 in shared memory: relu(acc + bias) -> bf16 pairs -> the canonical
+// no-swizzle K-major image (element (row, k) at (k / 8) * 2048 + row * 16 + (k % 8) * 2): eight
+// 16-byte stores per row, a warp's 32 rows contiguous per store (conflict-free).
+template <bool kBias>
+__device__ __forceinline__ void epilogue_hidden_smem(uint32_t tmem_acc, unsigned char* a3, int row, const float* bias) {
+  uint32_t va[4][16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) HC_TMEM_LD16(tmem_acc + q * 16, va[q]);
+  tmem_wait_ld();
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    uint32_t w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int e = c * 8 + 2 * j;  // element pair (e, e + 1)
+      float lo = __uint_as_float(va[e >> 4][e & 15]), hi = __uint_as_float(va[e >> 4][(e & 15) + 1]);
+      if (kBias) {
+        lo += bias[e];
+        hi += bias[e + 1];
+      }
+      w[j] = pack_relu_bf16(lo, hi);
+    }
+    *reinterpret_cast<uint4*>(a3 + c * (kMlpM * 16) + row * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  fence_proxy_async_smem();  // the tensor core (async proxy) reads the image
+}
+
 __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant__ MlpParams p) {
   extern __shared__ __align__(1024) unsigned char sm[];
   const int tid = threadIdx.x;
@@ -271,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
   const int r = tid & 127;                                         // tile row = TMEM lane (epilogue)
   unsigned char* A1 = sm + kOffStreams + st * kStreamBytes;
   float* in_tiles = reinterpret_cast<float*>(A1 + kA1Bytes);
+  unsigned char* A3s = A1 + kA1Bytes + 2 * kInTile;  // kA3Smem
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + kOffBar) + st * kBarsPerStream;
   uint64_t* bar_in = bars;         // [2] rgb tile landed (TMA transaction count)
   uint64_t* bar_l1 = bars + 2;     // layer-1 MMAs complete (tcgen05.commit)
@@ -399,8 +436,13 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       if (!kL3First && tn < p.ntiles) issue_l1();
       tc_fence_after();
 #pragma unroll
-      for (int kk = 0; kk < kK3 / 16; ++kk)
-        mma_ts_w(tD3, tA3 + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
+      for (int kk = 0; kk < kK3 / 16; ++kk) {
+        if constexpr (kA3Smem)
+          mma_ss_w(tD3, umma_desc(smem_u32(A3s) + kk * 2 * (kMlpM * 16), kMlpM * 16, 128),
+                   umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
+        else
+          mma_ts_w(tD3, tA3 + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
+      }
       mma_commit_w(bar_l3);
       __syncwarp();
       if (kL3First && tn < p.ntiles) issue_l1();
@@ -471,8 +513,11 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       mbar_wait(bar_l2, ph);
       if (tr) tr[5] = clock64();
       tc_fence_after();
-      epilogue_hidden<kB2Epi, kEpiCols>(tD + lane_off + half * kEpiCols, tA3 + lane_off + half * (kEpiCols / 2),
-                                        p.b2 + half * kEpiCols);  // A3 (over A2 unless kSepA3)
+      if constexpr (kA3Smem)
+        epilogue_hidden_smem<kB2Epi>(tD + lane_off, A3s, r, p.b2);
+      else
+        epilogue_hidden<kB2Epi, kEpiCols>(tD + lane_off + half * kEpiCols, tA3 + lane_off + half * (kEpiCols / 2),
+                                          p.b2 + half * kEpiCols);  // A3 (over A2 unless kSepA3)
       handoff(bar_a3);
       prev_row0 = row0;
       prev_rows = rows;

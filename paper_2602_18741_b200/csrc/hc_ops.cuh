@@ -567,6 +567,12 @@ struct ShadeSpectralF2Op {
 #ifndef HC_LOSS_SPLIT  // pass 2: (D zp)_l as two interleaved 3-term chains
 #define HC_LOSS_SPLIT 0
 #endif
+#ifndef HC_LOSS_ABREG  // a_l b_l formed in pass 1 and kept in registers (pass 2 reads no a / b)
+#define HC_LOSS_ABREG 0
+#endif
+#ifndef HC_LOSS_CE  // pass 1 specialised per warp group: E as compile-time constant-bank operands
+#define HC_LOSS_CE 0
+#endif
 
 template <int N, int K, int T_, int THREADS_, int STAGES_>
 struct LossOp {
@@ -616,6 +622,30 @@ struct LossOp {
     }
   }
 
+  // Pass 1 of warp group GRP with every E offset a compile-time constant, so each DFMA takes
+  // its E value straight from the constant bank (c[0x0][imm] operand) instead of through a
+  // uniform-register load (LDCU) on the dependency chain; all R floats of a and b are loaded
+  // up front.
+  template <int GRP>
+  __device__ static void pass1_ce(const Params& p, const float* a, const float* b, double za[K], double zb[K]) {
+    float fa[R], fb[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      fa[i] = a[i];
+      fb[i] = b[i];
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const double va = static_cast<double>(fa[i]), vb = static_cast<double>(fb[i]);
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const double e = p.E[j * N + GRP * R + i];
+        za[j] = fma(e, va, za[j]);
+        zb[j] = fma(e, vb, zb[j]);
+      }
+    }
+  }
+
   __device__ static void compute(const Params& p, State& st, const unsigned char* const* ins,
                                  unsigned char* const*, unsigned char* extra, int item, int64_t g) {
     // Every thread of the CTA gets here exactly once per tile (tile_generic runs all T
@@ -630,10 +660,21 @@ struct LossOp {
     const double* E = p.E + L0;
 
     // pass 1: partial za = E a, zb = E b over [L0, L0 + R) (codec.cpp:36-46, trainer.cpp:52-53)
+    constexpr bool kAbReg = HC_LOSS_ABREG && B1 == R && B2 == R;
+    double ab[kAbReg ? R : 1];  // kAbReg: a_l b_l (exact fp64 products of two floats)
     double za[K], zb[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) za[j] = zb[j] = 0.0;
-    {
+    if constexpr (HC_LOSS_CE && !kAbReg) {
+      if constexpr (G == 1) {
+        pass1_ce<0>(p, a, b, za, zb);
+      } else {
+        static_assert(G == 1 || G == 3, "warp groups");
+        if (grp == 0) pass1_ce<0>(p, a, b, za, zb);
+        else if (grp == 1) pass1_ce<G == 3 ? 1 : 0>(p, a, b, za, zb);
+        else pass1_ce<G == 3 ? 2 : 0>(p, a, b, za, zb);
+      }
+    } else {
       float fa[B1], fb[B1];
       double va[B1], vb[B1];
 #pragma unroll
@@ -668,6 +709,10 @@ struct LossOp {
             za[j] = fma(e, va[i], za[j]);
             zb[j] = fma(e, vb[i], zb[j]);
           }
+        if constexpr (kAbReg) {
+#pragma unroll
+          for (int i = 0; i < B1; ++i) ab[i] = va[i] * vb[i];
+        }
         if (l0 + B1 < R) {  // next batch: convert the floats loaded one batch ago, load the one after
 #pragma unroll
           for (int i = 0; i < B1; ++i) {
@@ -714,8 +759,10 @@ struct LossOp {
       auto load = [&](int l0) {
 #pragma unroll
         for (int i = 0; i < B2; ++i) {
-          fa[i] = a[l0 + i];
-          fb[i] = b[l0 + i];
+          if constexpr (!kAbReg) {
+            fa[i] = a[l0 + i];
+            fb[i] = b[l0 + i];
+          }
 #pragma unroll
           for (int c = 0; c < KP / 2; ++c) {
             const double2 v = td[(l0 + i) * (KP / 2) + c];  // same address in every lane: broadcast
@@ -729,7 +776,8 @@ struct LossOp {
       for (int l0 = 0; l0 < R; l0 += B2) {
         double s[B2];
 #pragma unroll
-        for (int i = 0; i < B2; ++i) s[i] = -(static_cast<double>(fa[i]) * static_cast<double>(fb[i]));  // exact
+        for (int i = 0; i < B2; ++i)
+          s[i] = kAbReg ? -ab[i] : -(static_cast<double>(fa[i]) * static_cast<double>(fb[i]));  // exact
         double dc[B2][KP];
 #pragma unroll
         for (int i = 0; i < B2; ++i)
