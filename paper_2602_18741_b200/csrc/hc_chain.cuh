@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(256) chain_latent_rep_kernel(const __grid_cons
 #endif
 constexpr int kChainV3Row = 256;
 constexpr int kChainV3Stage = 6 * 33;  // floats of per-warp staging for the pixel sums
+__host__ __device__ constexpr int chain_v3_stage_bytes(int warps) { return (warps * kChainV3Stage * 4 + 15) / 16 * 16; }
 
 __device__ __forceinline__ uint64_t chain_fma2(uint64_t a, uint64_t b, uint64_t c) {
   uint64_t d;
@@ -364,9 +365,23 @@ __device__ __forceinline__ void chain_v3_sample(const unsigned char* tab3, const
   }
 }
 
+// kTma (spp == 64, 16-byte aligned pidx / iidx): a pixel quad's palette-index words and
+// illuminant bytes arrive by bulk copies (cp.async.bulk, one mbarrier per warp, double-buffered)
+// into per-pixel slots padded so the lanes' reads are conflict-free (pixel strides 288 B and
+// 80 B): 16 L1 wavefronts per quad for the two streams instead of ~48 through LDG (4 pixels =
+// 4 lines per 32-bit load, 2 per byte load), and the L2 prefetches of those streams go away.
+constexpr int kChainTmaPidx = 4 * 288;              // pidx slot: 4 pixels x (256 + 32 pad) B
+constexpr int kChainTmaSlot = kChainTmaPidx + 4 * 80;  // + iidx: 4 pixels x (64 + 16 pad) B
+constexpr int kChainTmaWarp = 16 + 2 * kChainTmaSlot;  // mbarrier + two slots
+#ifndef HC_CHAIN_TMA_T
+#define HC_CHAIN_TMA_T 384
+#endif
+constexpr int kChainTmaThreads = HC_CHAIN_TMA_T;
+
 // kCheckPal: n_pal < 256, so palette indices are range-checked (byte-wise running max).
-template <bool kCheckPal>
-__global__ void __launch_bounds__(256) chain_latent_v3_kernel(const __grid_constant__ ChainLatentParams<6> p) {
+template <bool kCheckPal, bool kTma = false>
+__global__ void __launch_bounds__(kTma ? kChainTmaThreads : 256, kTma ? 2 : 0)
+    chain_latent_v3_kernel(const __grid_constant__ ChainLatentParams<6> p) {
   extern __shared__ __align__(16) unsigned char tab3[];
   // Table fill: row r (palette r < 256, illuminant 256 + i), 16-byte chunk c of 16.
   const int n_rows = 256 + p.n_ill;
@@ -391,6 +406,30 @@ __global__ void __launch_bounds__(256) chain_latent_v3_kernel(const __grid_const
   constexpr int kPixPerWarp = 32 / kChainLanes;
   const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  // kTma: this warp's mbarrier and two record slots
+  unsigned char* tma_w = tab3 + n_rows * kChainV3Row + chain_v3_stage_bytes(blockDim.x >> 5) +
+                         (threadIdx.x >> 5) * kChainTmaWarp;
+  uint64_t* tbar = reinterpret_cast<uint64_t*>(tma_w);
+  auto issue_quad = [&](int64_t q, int slot) {  // whole warp; elect.sync issues
+    unsigned char* dst = tma_w + 16 + slot * kChainTmaSlot;
+    const int64_t left = p.P - q * kPixPerWarp;
+    const int npx = left < kPixPerWarp ? static_cast<int>(left) : kPixPerWarp;
+    mbar_arrive_expect_tx_w(tbar, npx * (64 * 4 + 64));
+    for (int pp = 0; pp < npx; ++pp) {
+      const int64_t px = q * kPixPerWarp + pp;
+      bulk_g2s_w(dst + pp * 288, p.pidx + px * 64, 64 * 4, tbar);
+      bulk_g2s_w(dst + kChainTmaPidx + pp * 80, p.iidx + px * 64, 64, tbar);
+    }
+  };
+  if constexpr (kTma) {
+    if ((threadIdx.x & 31) == 0) {
+      mbar_init(tbar, 1);
+      fence_mbar_init();
+    }
+    __syncwarp();
+    if (warp_id * kPixPerWarp < p.P) issue_quad(warp_id, 0);
+  }
+  int titer = 0;
   const uint32_t ill_last = static_cast<uint32_t>(p.n_ill - 1);
   uint32_t pmax = 0, imax = 0;  // running maxima of the palette / illuminant indices
   const int per_lane = p.spp / kChainLanes;
@@ -406,12 +445,35 @@ __global__ void __launch_bounds__(256) chain_latent_v3_kernel(const __grid_const
         const char* twl = reinterpret_cast<const char*>(p.tw + nb);
         for (int off = g * 128; off < p.spp * 16; off += kChainLanes * 128)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(twl + off));
-        const char* pkl = reinterpret_cast<const char*>(p.pidx + nb);
-        for (int off = g * 128; off < p.spp * 4; off += kChainLanes * 128)
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(pkl + off));
-        if (g == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.iidx + nb));
+        if constexpr (!kTma) {
+          const char* pkl = reinterpret_cast<const char*>(p.pidx + nb);
+          for (int off = g * 128; off < p.spp * 4; off += kChainLanes * 128)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(pkl + off));
+          if (g == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.iidx + nb));
+        }
       }
     }
+    if constexpr (kTma) {  // spp == 64: one group of 8 samples per lane, records from the slot
+      const int slot = titer & 1;
+      mbar_wait(tbar, titer & 1);  // one quad in flight per warp: completions in quad order
+      const unsigned char* src = tma_w + 16 + slot * kChainTmaSlot;
+      const int pp = lane / kChainLanes;
+      uint32_t pkg[8], lig[8];
+      float4 t4g[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int smp = g + m * kChainLanes;
+        pkg[m] = valid ? *reinterpret_cast<const uint32_t*>(src + pp * 288 + smp * 4) : 0u;
+        lig[m] = valid ? static_cast<uint32_t>(src[kChainTmaPidx + pp * 80 + smp]) : 0u;
+        t4g[m] = valid ? ldg_stream(p.tw + base + smp) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      // the other slot was read one quad ago: refill it with the next quad's records
+      if (qd + nwarps < (p.P + kPixPerWarp - 1) / kPixPerWarp) issue_quad(qd + nwarps, slot ^ 1);
+      ++titer;
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        chain_v3_sample<kCheckPal>(tab3, ill_tab, offs, pkg[m], lig[m], t4g[m], ill_last, pmax, imax, part);
+    } else {
     // Samples in groups of kGroup per lane, every load of a group issued before any use
     // (~170 B in flight per lane); a past-the-end pixel's lanes load zeros (index 0, weight 0).
     constexpr int kGroup = 8;
@@ -451,6 +513,7 @@ __global__ void __launch_bounds__(256) chain_latent_v3_kernel(const __grid_const
                                  valid ? ldg_stream(p.tw + s) : make_float4(0.f, 0.f, 0.f, 0.f), ill_last, pmax,
                                  imax, part);
     }
+    }  // !kTma
     // Pixel sums: the 8 lanes' fp32 partials are transposed through a per-warp staging area
     // (6 rows of 33 words: conflict-free both ways), lane g < 6 of each pixel group adds the 8
     // partials of code g in fp64 (renderer.cpp:548-551) and the group's lane 0 gathers the 6

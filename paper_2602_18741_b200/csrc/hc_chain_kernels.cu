@@ -13,7 +13,7 @@ namespace hcb {
 // Occupancy per (kernel, dynamic smem) is cached: the launchers also run inside
 // CUDA-graph capture, where attribute / occupancy queries are best avoided.
 template <class KernelFn>
-int chain_grid(hc_ctx ctx, KernelFn fn, int smem, int64_t P, int* grid) {
+int chain_grid(hc_ctx ctx, KernelFn fn, int smem, int64_t P, int* grid, int threads = 256) {
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, int> cache;
   int occ = 0;
@@ -27,12 +27,13 @@ int chain_grid(hc_ctx ctx, KernelFn fn, int smem, int64_t P, int* grid) {
       HC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       HC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                        cudaSharedmemCarveoutMaxShared));
-      HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, smem));
+      HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));
       cache[key] = occ;
     }
   }
   if (occ < 1) return set_error(HC_EUNSUPPORTED, "chain kernel does not fit on an SM");
-  const int64_t blocks_needed = (P + 31) / 32;  // 32 pixels per 256-thread block iteration
+  const int64_t px_per_block = threads / 8;  // 8 lanes per pixel
+  const int64_t blocks_needed = (P + px_per_block - 1) / px_per_block;
   *grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(blocks_needed, static_cast<int64_t>(occ) * ctx->sm_count)));
   return HC_OK;
 }
@@ -63,11 +64,20 @@ int chain_latent_k(hc_codec c, const float* pal, int n_pal, const float* ill, in
 #endif
   if constexpr (K == 6) {
     if (HC_CHAIN_V3 && (!HC_CHAIN_IIDX128 || (spp % 16 == 0 && (reinterpret_cast<uintptr_t>(iidx) & 15u) == 0))) {  // instruction-lean k = 6 kernel (256-row palette table, packed Horner chain)
-      const int smem = (256 + n_ill) * kChainV3Row + 8 * kChainV3Stage * 4;  // 8 warps of staging
-      auto fn = n_pal < 256 ? chain_latent_v3_kernel<true> : chain_latent_v3_kernel<false>;
-      int rc = chain_grid(c->ctx, fn, smem, P, &grid);
+#ifndef HC_CHAIN_TMA
+#define HC_CHAIN_TMA 1
+#endif
+      // palette-index / illuminant records by bulk copy: spp == 64, 16-byte aligned streams
+      const bool tma = HC_CHAIN_TMA && spp == 64 && (reinterpret_cast<uintptr_t>(pidx) & 15u) == 0 &&
+                       (reinterpret_cast<uintptr_t>(iidx) & 15u) == 0;
+      const int threads = tma ? kChainTmaThreads : 256;
+      const int smem = (256 + n_ill) * kChainV3Row + chain_v3_stage_bytes(threads / 32) +
+                       (tma ? (threads / 32) * kChainTmaWarp : 0);
+      auto fn = n_pal < 256 ? (tma ? chain_latent_v3_kernel<true, true> : chain_latent_v3_kernel<true, false>)
+                            : (tma ? chain_latent_v3_kernel<false, true> : chain_latent_v3_kernel<false, false>);
+      int rc = chain_grid(c->ctx, fn, smem, P, &grid, threads);
       if (rc != HC_OK) return rc;
-      fn<<<grid, 256, smem, c->ctx->stream>>>(p);
+      fn<<<grid, threads, smem, c->ctx->stream>>>(p);
       HC_CHECK_LAUNCH(c->ctx, "chain_latent_v3_kernel");
       return HC_OK;
     }

@@ -570,6 +570,9 @@ struct ShadeSpectralF2Op {
 #ifndef HC_LOSS_ABREG  // a_l b_l formed in pass 1 and kept in registers (pass 2 reads no a / b)
 #define HC_LOSS_ABREG 0
 #endif
+#ifndef HC_LOSS_WS  // warp-specialised pipeline; the code exchange syncs only the G warps of a 32-pair slice
+#define HC_LOSS_WS 0
+#endif
 #ifndef HC_LOSS_CE  // pass 1 specialised per warp group: E as compile-time constant-bank operands
 #define HC_LOSS_CE 0
 #endif
@@ -593,7 +596,7 @@ struct LossOp {
   static constexpr int kTabD = N * KP * 8;  // D rows [l][KP], fp64
   static constexpr int EXTRA_SMEM = 32 * 8 + kXchg + kTabD;
   static constexpr int kTensorStream = -1;
-  static constexpr bool kWarpSpecialized = false;
+  static constexpr bool kWarpSpecialized = HC_LOSS_WS;
   static constexpr bool kEvictFirstLoads = false;
 
   struct Params {
@@ -736,7 +739,12 @@ struct LossOp {
         xchg[(grp * 2 * K + j) * T + item] = za[j];
         xchg[(grp * 2 * K + K + j) * T + item] = zb[j];
       }
-      __syncthreads();
+      // Warp-specialised: only the G warps holding this 32-pair slice exchange (named barrier
+      // 1 + slice); the CTA-barrier pipelines use the CTA barrier.
+      if constexpr (kWarpSpecialized)
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + item / 32), "r"(32 * G) : "memory");
+      else
+        __syncthreads();
 #pragma unroll
       for (int j = 0; j < K; ++j) {
         za[j] = xchg[j * T + item];
@@ -747,6 +755,8 @@ struct LossOp {
           zb[j] += xchg[(h * 2 * K + K + j) * T + item];
         }
       }
+      // ws: the slice's next tile overwrites these partials; no CTA barrier separates tiles there
+      if constexpr (kWarpSpecialized) asm volatile("bar.sync %0, %1;" ::"r"(1 + item / 32), "r"(32 * G) : "memory");
     }
 #pragma unroll
     for (int j = 0; j < K; ++j) za[j] *= zb[j];

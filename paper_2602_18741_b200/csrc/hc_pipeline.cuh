@@ -281,7 +281,8 @@ __global__ void __launch_bounds__(Op::THREADS + kProducerWarp)
       for (int i = 0; i < Op::NIN; ++i) ins[i] = in_base + s * Lay::kInTile + Lay::in_off(i);
 #pragma unroll
       for (int i = 0; i < Op::NOUT; ++i) outs[i] = out_base + o * Lay::kOutTile + Lay::out_off(i);
-      for (int item = tid; item < T; item += Op::THREADS)
+      constexpr int LPI = LanesPerItem<Op>::value;
+      for (int item = tid % (Op::THREADS / LPI); item < T; item += Op::THREADS / LPI)
         Op::compute(p, st, ins, outs, extra, item, tile * T + item);
       if (Op::NOUT > 0) fence_proxy_async_smem();
       __syncwarp();
