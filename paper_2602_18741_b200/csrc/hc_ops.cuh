@@ -573,6 +573,9 @@ struct ShadeSpectralF2Op {
 #ifndef HC_LOSS_WS  // warp-specialised pipeline; the code exchange syncs only the G warps of a 32-pair slice
 #define HC_LOSS_WS 0
 #endif
+#ifndef HC_LOSS_CE2  // both passes per warp group with E / D from the constant bank, a_l b_l in registers
+#define HC_LOSS_CE2 0
+#endif
 #ifndef HC_LOSS_CE  // pass 1 specialised per warp group: E as compile-time constant-bank operands
 #define HC_LOSS_CE 0
 #endif
@@ -649,6 +652,44 @@ struct LossOp {
     }
   }
 
+  // HC_LOSS_CE2: pass 1 also forms a_l b_l (exact) into registers; pass 2 is then pure DFMA with
+  // D at compile-time constant-bank offsets, j outer so the R residual chains run side by side.
+  template <int GRP>
+  __device__ static void pass1_ce2(const Params& p, const float* a, const float* b, double za[K], double zb[K],
+                                   double ab[R]) {
+    float fa[R], fb[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      fa[i] = a[i];
+      fb[i] = b[i];
+    }
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const double va = static_cast<double>(fa[i]), vb = static_cast<double>(fb[i]);
+      ab[i] = va * vb;
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const double e = p.E[j * N + GRP * R + i];
+        za[j] = fma(e, va, za[j]);
+        zb[j] = fma(e, vb, zb[j]);
+      }
+    }
+  }
+  template <int GRP>
+  __device__ static double pass2_ce2(const Params& p, const double zp[K], const double ab[R]) {
+    double r[R];
+#pragma unroll
+    for (int i = 0; i < R; ++i) r[i] = -ab[i];
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+#pragma unroll
+      for (int i = 0; i < R; ++i) r[i] = fma(p.D[(GRP * R + i) * K + j], zp[j], r[i]);
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) acc = fma(r[i], r[i], acc);
+    return acc;
+  }
+
   __device__ static void compute(const Params& p, State& st, const unsigned char* const* ins,
                                  unsigned char* const*, unsigned char* extra, int item, int64_t g) {
     // Every thread of the CTA gets here exactly once per tile (tile_generic runs all T
@@ -668,7 +709,13 @@ struct LossOp {
     double za[K], zb[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) za[j] = zb[j] = 0.0;
-    if constexpr (HC_LOSS_CE && !kAbReg) {
+    constexpr bool kCe2 = HC_LOSS_CE2 && (G == 1 || G == 3);
+    double abv[kCe2 ? R : 1];
+    if constexpr (kCe2) {
+      if (G == 1 || grp == 0) pass1_ce2<0>(p, a, b, za, zb, abv);
+      else if (grp == 1) pass1_ce2<G == 3 ? 1 : 0>(p, a, b, za, zb, abv);
+      else pass1_ce2<G == 3 ? 2 : 0>(p, a, b, za, zb, abv);
+    } else if constexpr (HC_LOSS_CE && !kAbReg) {
       if constexpr (G == 1) {
         pass1_ce<0>(p, a, b, za, zb);
       } else {
@@ -763,7 +810,11 @@ struct LossOp {
 
     // pass 2: r_l = (D zp)_l - a_l b_l over [L0, L0 + R), sum of r_l^2 (trainer.cpp:56-71)
     double acc = 0.0;
-    {
+    if constexpr (kCe2) {
+      if (G == 1 || grp == 0) acc = pass2_ce2<0>(p, za, abv);
+      else if (grp == 1) acc = pass2_ce2<G == 3 ? 1 : 0>(p, za, abv);
+      else acc = pass2_ce2<G == 3 ? 2 : 0>(p, za, abv);
+    } else {
       float fa[B2], fb[B2];
       double d[B2][KP];
       auto load = [&](int l0) {

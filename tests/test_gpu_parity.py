@@ -396,6 +396,30 @@ def test_multibounce_small_tables(api, ctx, orc, n_pal, n_ill, spp, k):
     _check(f"chain latent n_pal={n_pal} n_ill={n_ill} spp={spp}", host(out["latent"]), lat)
 
 
+@pytest.mark.parametrize("offset", [1, 16])
+def test_multibounce_unaligned_records(api, ctx, orc, offset):
+    """k = 6 at spp = 64 takes the bulk-copy record path only for 16-byte aligned index streams;
+    an illuminant-index stream at a 1-byte offset runs the LDG path, 16 bytes the bulk-copy path
+    (ragged last pixel quad in both: P % 4 == 1)."""
+    codec, E, D = _codec(api, ctx, 6)
+    pal_codes = codec.encode(torch.from_numpy(synth.palette(SEED, 256, 81)).cuda())
+    ill_codes = codec.encode(torch.from_numpy(synth.lights(SEED, 16, 81, purpose="scene.illuminants")).cuda())
+    P, spp = 1001, 64
+    rng = np.random.default_rng(offset)
+    ph = rng.integers(0, 256, (P, spp, 4), dtype=np.uint8)
+    ih = rng.integers(0, 16, (P, spp), dtype=np.uint8)
+    th = rng.uniform(0.0, 1.5, (P, spp, 4)).astype(np.float32)
+    buf = torch.empty(P * spp + offset, dtype=torch.uint8, device="cuda")
+    iidx = buf[offset:].view(P, spp)
+    iidx.copy_(torch.from_numpy(ih))
+    out = codec.multibounce_latent(pal_codes, ill_codes, torch.from_numpy(ph).cuda(), iidx,
+                                   torch.from_numpy(th).cuda(), latent=True)
+    ctx.synchronize()
+    lat = np.zeros((P, 6), np.float32)
+    orc.orc_chain(6, host(pal_codes), host(ill_codes), ph, ih, th, P, spp, 4, lat)
+    _check(f"chain latent iidx offset {offset}", host(out["latent"]), lat)
+
+
 @pytest.mark.parametrize("which", ["pal", "ill"])
 @pytest.mark.parametrize("k", [6, 9])
 def test_multibounce_index_out_of_range_is_reported(api, ctx, which, k):
