@@ -135,7 +135,10 @@ int hc_shade_spectral(hc_codec codec, const float* pal_spectra, int n_pal,
                       int64_t P, float* spectra, float* xyz, float* rgb);
 
 /* Multi-bounce accumulation (config 4; renderer.cpp:457-551, evaluation.cpp:50-76):
- * depth 4, spp a multiple of 8.  Latent: codes; spectral: spectra. */
+ * depth 4, spp a multiple of 8, 1 <= n_pal, n_ill <= 256, pidx 4-byte and tw 16-byte aligned.
+ * Latent: codes; spectral: spectra.  Out-of-range palette / illuminant indices are latched
+ * and reported as HC_EINVAL by hc_ctx_synchronize.  Performance note (k = 6): spp == 64 with
+ * 16-byte aligned pidx and iidx takes the bulk-copy record path (config 4's layout). */
 int hc_multibounce_latent(hc_codec codec, const float* pal_codes, int n_pal, const float* ill_codes,
                           int n_ill, const uint8_t* pidx, const uint8_t* iidx, const float* tw,
                           int64_t P, int spp, float* latent, float* xyz, float* rgb);
