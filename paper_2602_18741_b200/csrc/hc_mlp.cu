@@ -211,6 +211,18 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
                  "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])   \
                : "memory")
 
+#define HC_TMEM_LD8(taddr, r)                                                                           \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                   \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]) \
+               : "r"(taddr))
+// The layer-3 accumulator has 16 columns (N = 16) but only k are codes: k <= 8 reads 8
+// (TMEM reads, not writes, are the scarce direction).  k is uniform, the load warp-collective.
+#define HC_TMEM_LD_D3(taddr, r, k)     \
+  do {                                 \
+    if ((k) <= 8) HC_TMEM_LD8(taddr, r); \
+    else HC_TMEM_LD16(taddr, r);       \
+  } while (0)
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -490,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
         mbar_wait(bar_l3, ph ^ 1);
         tc_fence_after();
         if (codes_warp) {
-          HC_TMEM_LD16(tD3 + lane_off, prev_v);
+          HC_TMEM_LD_D3(tD3 + lane_off, prev_v, p.k);
           tmem_wait_ld();
         }
       }
@@ -505,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       if (kSepA3 && iter > 0 && codes_warp) {  // layer 3 of the previous tile, read under this tile's layer 2
         mbar_wait(bar_l3, ph ^ 1);
         tc_fence_after();
-        HC_TMEM_LD16(tD3 + lane_off, prev_v);
+        HC_TMEM_LD_D3(tD3 + lane_off, prev_v, p.k);
         tmem_wait_ld();
       }
       store_codes();  // the previous tile's codes, under this tile's layer 2
@@ -527,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
     if (iter > 0 && codes_warp) {  // the last tile's codes
       mbar_wait(bar_l3, (iter - 1) & 1);
       tc_fence_after();
-      HC_TMEM_LD16(tD3 + lane_off, prev_v);
+      HC_TMEM_LD_D3(tD3 + lane_off, prev_v, p.k);
       tmem_wait_ld();
       store_codes();
     }
@@ -827,7 +839,7 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp2_kernel(const __grid_constan
       mbar_wait(bar_l2, it & 1);
       tc_fence_after();
       if (it > 0) {  // layer 3 of the previous tile is complete too (earlier MMA, same commit chain)
-        HC_TMEM_LD16(tD3 + lane_off, prev_v);
+        HC_TMEM_LD_D3(tD3 + lane_off, prev_v, p.k);
       }
       // relu(D) -> bf16 A3, in two 32-column halves (register budget: 480 threads)
 #pragma unroll
@@ -855,7 +867,7 @@ __global__ void __launch_bounds__(kThreads2, 1) mlp2_kernel(const __grid_constan
     if (it > 0) {
       mbar_wait(bar_l3, (it - 1) & 1);
       tc_fence_after();
-      HC_TMEM_LD16(tD3 + lane_off, prev_v);
+      HC_TMEM_LD_D3(tD3 + lane_off, prev_v, p.k);
       tmem_wait_ld();
       store_codes();
     }
