@@ -254,6 +254,192 @@ int shade_latent_launch(hc_codec c, const float* pal, int n_pal, const float* li
                  xyz, rgb);
 }
 
+// ---------------------------------------------------------------- naive, lanes over wavelengths
+// The thread-per-pixel naive shade (ShadeSpectralOp) needs, per wavelength, the L light SPD
+// values as shared-memory broadcasts (L / 4 LDS.128 per L FMAs): at L = 32 it ran at 12 % of its
+// fp32-issue bound.  Here a warp shades one pixel at a time with the lanes over wavelengths:
+// lane j owns lambda j, j + 32, j + 64 and keeps those wavelengths of all L light SPDs in
+// registers (packed pairs for lambda j, j + 32 -> FFMA2), so the only per-pixel broadcast is
+// the pixel's L cosines (L / 4 LDS.128 from a per-warp staging of 32 pixels' G-buffer rows).
+// Per pixel: S(lambda) = R_idx(lambda) * sum_l c_l L_l(lambda) (renderer.cpp:187-190 at C = n,
+// :505-510), the spectra row written coalesced, XYZ = dlambda * CMF . S as per-lane partials
+// reduced across the warp (colorimetry.cpp:75-87), sRGB.  The light sum runs in 4 partial
+// chains (l mod 4): fp32, re-associated against the reference's order (within 1e-6).
+constexpr int kLanesThreads = 384;  // 12 warps, one CTA per SM (~140 registers per thread)
+
+template <int N, int L>
+struct NaiveLanesParams {
+  float light[L * N];
+  float cmf[3 * N];
+  float Crgb[9];
+  const uint32_t* idx;
+  const float* cosv;
+  const float* pal;
+  int n_pal;
+  int64_t P;
+  float* spectra;
+  float* xyz;
+  float* rgb;
+  int* err;
+};
+
+__device__ __forceinline__ uint64_t nl_pack(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ uint64_t nl_fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ float2 nl_unpack(uint64_t v) {
+  float2 f;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(f.x), "=f"(f.y) : "l"(v));
+  return f;
+}
+
+template <int N, int L>
+__global__ void __launch_bounds__(kLanesThreads, 1) naive_lanes_kernel(const __grid_constant__ NaiveLanesParams<N, L> p) {
+  static_assert(N > 64 && N <= 96 && L % 16 == 0, "three wavelength slots per lane, L a multiple of 16");
+  // per warp: 32 pixels' cosine rows (32 x L floats), then the XYZ partials [3][32 px][32 lanes]
+  extern __shared__ __align__(16) float stage_dyn[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int l0 = lane, l1 = lane + 32, l2 = lane + 64;
+  const bool has2 = l2 < N;
+  uint64_t L01[L];  // (L_l(lambda j), L_l(lambda j + 32))
+  float L2[L];      // L_l(lambda j + 64)
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    L01[l] = nl_pack(p.light[l * N + l0], p.light[l * N + l1]);
+    L2[l] = has2 ? p.light[l * N + l2] : 0.f;
+  }
+  float cm[3][3];
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    cm[c][0] = p.cmf[c * N + l0];
+    cm[c][1] = p.cmf[c * N + l1];
+    cm[c][2] = has2 ? p.cmf[c * N + l2] : 0.f;
+  }
+  float* st = stage_dyn + wib * (32 * L + 3 * 32 * 32);
+  float* red = st + 32 * L;
+  const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t npal = static_cast<uint32_t>(p.n_pal);
+  bool bad = false;
+  for (int64_t r0 = warp_id * 32; r0 < p.P; r0 += nwarps * 32) {
+    const int cnt = p.P - r0 < 32 ? static_cast<int>(p.P - r0) : 32;
+    // stage the 32 pixels' cosine rows (32 x L floats, contiguous in the G-buffer)
+    __syncwarp();
+    const float4* src = reinterpret_cast<const float4*>(p.cosv + r0 * L);
+#pragma unroll
+    for (int i = 0; i < L / 4; ++i) {
+      const int q = i * 32 + lane;  // float4 index within the round
+      const float4 v = q < cnt * (L / 4) ? ldg_stream(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      reinterpret_cast<float4*>(st)[q] = v;
+    }
+    uint32_t my_id = lane < cnt ? __ldg(p.idx + r0 + lane) : 0u;
+    if (my_id >= npal) {
+      bad = true;
+      my_id = 0;
+    }
+    __syncwarp();
+    float my_x = 0.f, my_y = 0.f, my_z = 0.f;
+    for (int q = 0; q < cnt; ++q) {
+      const uint32_t id = __shfl_sync(0xffffffffu, my_id, q);
+      const float4* row = reinterpret_cast<const float4*>(st + q * L);
+      uint64_t a01[4] = {0ull, 0ull, 0ull, 0ull};
+      float a2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int l4 = 0; l4 < L / 4; ++l4) {
+        const float4 c4 = row[l4];  // same address in every lane: broadcast
+        const float cs[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int l = 4 * l4 + u;
+          a01[u] = nl_fma2(L01[l], nl_pack(cs[u], cs[u]), a01[u]);
+          a2[u] = fmaf(L2[l], cs[u], a2[u]);
+        }
+      }
+      const float2 s01a = nl_unpack(a01[0]), s01b = nl_unpack(a01[1]), s01c = nl_unpack(a01[2]),
+                   s01d = nl_unpack(a01[3]);
+      const float il0 = (s01a.x + s01b.x) + (s01c.x + s01d.x);
+      const float il1 = (s01a.y + s01b.y) + (s01c.y + s01d.y);
+      const float il2 = (a2[0] + a2[1]) + (a2[2] + a2[3]);
+      const float* R = p.pal + static_cast<int64_t>(id) * N;
+      const float s0 = __ldg(R + l0) * il0, s1 = __ldg(R + l1) * il1, s2 = has2 ? __ldg(R + l2) * il2 : 0.f;
+      if (p.spectra) {
+        float* o = p.spectra + (r0 + q) * N;
+        __stcs(o + l0, s0);
+        __stcs(o + l1, s1);
+        if (has2) __stcs(o + l2, s2);
+      }
+      // this lane's XYZ partial of pixel q, column (lane + q) mod 32 (conflict-free both ways)
+      const int col = (lane + q) & 31;
+      red[(0 * 32 + q) * 32 + col] = fmaf(cm[0][2], s2, fmaf(cm[0][1], s1, cm[0][0] * s0));
+      red[(1 * 32 + q) * 32 + col] = fmaf(cm[1][2], s2, fmaf(cm[1][1], s1, cm[1][0] * s0));
+      red[(2 * 32 + q) * 32 + col] = fmaf(cm[2][2], s2, fmaf(cm[2][1], s1, cm[2][0] * s0));
+    }
+    __syncwarp();
+    if (lane < cnt) {  // lane q adds the 32 lanes' partials of its pixel
+      float xs[4] = {0.f, 0.f, 0.f, 0.f}, ys[4] = {0.f, 0.f, 0.f, 0.f}, zs[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int col = (i + lane) & 31;
+        xs[i & 3] += red[(0 * 32 + lane) * 32 + col];
+        ys[i & 3] += red[(1 * 32 + lane) * 32 + col];
+        zs[i & 3] += red[(2 * 32 + lane) * 32 + col];
+      }
+      my_x = (xs[0] + xs[1]) + (xs[2] + xs[3]);
+      my_y = (ys[0] + ys[1]) + (ys[2] + ys[3]);
+      my_z = (zs[0] + zs[1]) + (zs[2] + zs[3]);
+    }
+    if (lane < cnt) {
+      const float xyz[3] = {my_x, my_y, my_z};
+      float rgb[3];
+      xyz_to_rgb(p.Crgb, xyz, rgb);
+      const int64_t px = r0 + lane;
+      if (p.xyz)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) p.xyz[px * 3 + c] = xyz[c];
+      if (p.rgb)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) p.rgb[px * 3 + c] = rgb[c];
+    }
+  }
+  if (bad) atomicOr(p.err, kErrIndexRange);
+}
+
+template <int N, int L>
+int naive_lanes_launch(hc_codec c, const float* pal, int n_pal, const float* light, const uint32_t* idx,
+                       const float* cosv, int64_t P, float* spectra, float* xyz, float* rgb) {
+  NaiveLanesParams<N, L> p;
+  for (int i = 0; i < L * N; ++i) p.light[i] = light[i];
+  for (int i = 0; i < 3 * N; ++i) p.cmf[i] = c->cmf_dl[i];
+  for (int i = 0; i < 9; ++i) p.Crgb[i] = c->Crgb[i];
+  p.idx = idx;
+  p.cosv = cosv;
+  p.pal = pal;
+  p.n_pal = n_pal;
+  p.P = P;
+  p.spectra = spectra;
+  p.xyz = xyz;
+  p.rgb = rgb;
+  p.err = c->ctx->d_err;
+  const int64_t rounds = (P + 31) / 32;
+  const int warps = kLanesThreads / 32;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((rounds + warps - 1) / warps, c->ctx->sm_count)));
+  const int smem = kLanesThreads / 32 * (32 * L + 3 * 32 * 32) * 4;
+  static bool configured = false;  // (a benign race: the attribute call is idempotent)
+  if (!configured) {
+    HC_CUDA_TRY(cudaFuncSetAttribute(naive_lanes_kernel<N, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = true;
+  }
+  naive_lanes_kernel<N, L><<<grid, kLanesThreads, smem, c->ctx->stream>>>(p);
+  HC_CHECK_LAUNCH(c->ctx, "naive_lanes_kernel");
+  return HC_OK;
+}
+
 template <int N, int L, bool SPEC>
 int shade_spectral_nl(hc_codec c, const float* pal, int n_pal, const float* light, const uint32_t* idx,
                       const float* cosv, int64_t P, float* spectra, float* xyz, float* rgb) {
@@ -292,6 +478,14 @@ int shade_spectral_nl(hc_codec c, const float* pal, int n_pal, const float* ligh
     q.rgb = rgb;
     q.err = c->ctx->d_err;
     return launch_tile_op<Op2>(c->ctx, q, P);
+  }
+#ifndef HC_NAIVE_LANES
+#define HC_NAIVE_LANES 1
+#endif
+  // L = 32 (config 3): lanes over wavelengths; needs 16-byte aligned cosine rows
+  if constexpr (L % 16 == 0 && N > 64 && N <= 96) {
+    if (HC_NAIVE_LANES && (reinterpret_cast<uintptr_t>(cosv) & 15u) == 0)
+      return naive_lanes_launch<N, L>(c, pal, n_pal, light, idx, cosv, P, spectra, xyz, rgb);
   }
   using Op = ShadeSpectralOp<N, L, SPEC, T, T, 2>;
   typename Op::Params p;

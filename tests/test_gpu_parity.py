@@ -298,7 +298,8 @@ def test_multipass_equals_fused(api, ctx, k, L):
 
 @pytest.mark.parametrize("L,P,spec,n", [(8, 30_001, False, 81), (32, 5000, True, 81), (8, 2048, True, 81),
                                         (3, 1001, True, 81), (17, 999, False, 81), (8, 4099, True, 47),
-                                        (32, 1000, False, 47)])
+                                        (32, 1000, False, 47), (32, 777, False, 81), (32, 31, True, 81),
+                                        (32, 40_003, True, 81)])
 def test_shade_spectral_vs_oracle(api, ctx, orc, L, P, spec, n):
     codec, E, D, pal, lts, pal_d, _, _ = _scene(api, ctx, 6, L, n)
     idx, cosv = api.synth_gbuffer(ctx, SEED, 3, P, L, 256)
@@ -321,6 +322,16 @@ def test_latent_tracks_naive_on_shared_scene(api, ctx):
     nv = host(codec.shade_spectral(pal_d, lts, idx, cosv)["xyz"])
     assert np.all(np.isfinite(lat)) and np.all(np.isfinite(nv))
     assert np.corrcoef(lat[:, 1], nv[:, 1])[0, 1] > 0.5
+
+
+@pytest.mark.parametrize("L,spec", [(32, True), (32, False), (8, False)])
+def test_shade_spectral_index_out_of_range_is_reported(api, ctx, L, spec):
+    codec, E, D, pal, lts, pal_d, pal_codes, light_codes = _scene(api, ctx, 6, L)
+    idx, cosv = api.synth_gbuffer(ctx, SEED, 0, 1024, L, 256)
+    idx[1000] = 256
+    codec.shade_spectral(pal_d, lts, idx, cosv, spectra=spec)
+    with pytest.raises(ValueError):
+        ctx.synchronize()
 
 
 def test_shade_index_out_of_range_is_reported(api, ctx):
