@@ -655,4 +655,120 @@ __global__ void __launch_bounds__(256) chain_spectral_kernel(const __grid_consta
   }
 }
 
+// Naive n-sample chain with the lanes over wavelengths (config 4 ground truth, n <= 96): a warp
+// takes one pixel, lane j owns lambda j, j + 32, j + 64.  Every random lookup of a sample is then
+// one palette row read by the whole warp at consecutive addresses (conflict-free, 128 B per
+// wavefront) instead of 32 random rows at stride n (bank conflicts: the thread-per-pixel kernel
+// above spends ~3 wavefronts per lookup).  A sample's records (u8x4 palette indices, u8
+// illuminant index, float4 throughput factors) are loaded by lane s % 32 (coalesced), staged per
+// warp in shared memory and read back as broadcasts.  Per sample and wavelength the chain is the
+// Horner form of chain_latent_v3_kernel (re-associated); each lane sums 8
+// samples in fp32, then in fp64 (renderer.cpp:548-551); XYZ partials reduce across the warp.
+constexpr int kChainLanesRow = 96;  // padded table row (floats)
+
+template <int N>
+__global__ void __launch_bounds__(256) chain_spectral_lanes_kernel(const __grid_constant__ ChainSpectralParams<N> p) {
+  static_assert(N > 64 && N <= kChainLanesRow, "three wavelength slots per lane");
+  extern __shared__ __align__(16) float ltab[];
+  float* pal = ltab;
+  float* ill = ltab + p.n_pal * kChainLanesRow;
+  for (int i = threadIdx.x; i < (p.n_pal + p.n_ill) * kChainLanesRow; i += blockDim.x) {
+    const int r = i / kChainLanesRow, l = i - r * kChainLanesRow;
+    float v = 0.f;
+    if (l < N) v = r < p.n_pal ? __ldg(p.pal + r * N + l) : __ldg(p.ill + (r - p.n_pal) * N + l);
+    ltab[i] = v;
+  }
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  // per-warp record staging: 32 samples x (u32 palette word, u32 illuminant index, float4 weights)
+  uint32_t* rec = reinterpret_cast<uint32_t*>(ltab + (p.n_pal + p.n_ill) * kChainLanesRow) + wib * 32 * 6;
+  __syncthreads();
+  const int l0 = lane, l1 = lane + 32, l2 = lane + 64;
+  const bool has2 = l2 < N;
+  const int64_t warp_id = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t npal = static_cast<uint32_t>(p.n_pal), nill = static_cast<uint32_t>(p.n_ill);
+  bool bad = false;
+  for (int64_t pix = warp_id; pix < p.P; pix += nwarps) {
+    const int64_t base = pix * p.spp;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    for (int c0 = 0; c0 < p.spp; c0 += 32) {
+      const int cnt = p.spp - c0 < 32 ? p.spp - c0 : 32;  // multiple of 8
+      __syncwarp();
+      if (lane < cnt) {
+        uint32_t pk = __ldg(p.pidx + base + c0 + lane);
+        uint32_t li = __ldg(p.iidx + base + c0 + lane);
+        const float4 t = ldg_stream(p.tw + base + c0 + lane);
+        if (li >= nill) { bad = true; li = 0; }
+#pragma unroll
+        for (int d = 0; d < 4; ++d)
+          if (((pk >> (8 * d)) & 0xffu) >= npal) { bad = true; pk &= ~(0xffu << (8 * d)); }
+        rec[lane * 6 + 0] = pk;
+        rec[lane * 6 + 1] = li;
+        *reinterpret_cast<float2*>(rec + lane * 6 + 2) = make_float2(t.x, t.y);
+        *reinterpret_cast<float2*>(rec + lane * 6 + 4) = make_float2(t.z, t.w);
+      }
+      __syncwarp();
+      for (int g0 = 0; g0 < cnt; g0 += 8) {
+        float part0 = 0.f, part1 = 0.f, part2 = 0.f;
+#pragma unroll 8
+        for (int q = g0; q < g0 + 8; ++q) {
+          const uint32_t pk = rec[q * 6 + 0], li = rec[q * 6 + 1];  // broadcasts
+          const float2 t01 = *reinterpret_cast<const float2*>(rec + q * 6 + 2);
+          const float2 t23 = *reinterpret_cast<const float2*>(rec + q * 6 + 4);
+          const float4 t = make_float4(t01.x, t01.y, t23.x, t23.y);
+          const float* r0 = pal + (pk & 0xffu) * kChainLanesRow;
+          const float* r1 = pal + ((pk >> 8) & 0xffu) * kChainLanesRow;
+          const float* r2 = pal + ((pk >> 16) & 0xffu) * kChainLanesRow;
+          const float* r3 = pal + (pk >> 24) * kChainLanesRow;
+          const float* le = ill + li * kChainLanesRow;
+          {
+            float u = fmaf(r3[l0], t.w, t.z);
+            u = fmaf(r2[l0], u, t.y);
+            u = fmaf(r1[l0], u, t.x);
+            part0 = fmaf(le[l0], r0[l0] * u, part0);
+          }
+          {
+            float u = fmaf(r3[l1], t.w, t.z);
+            u = fmaf(r2[l1], u, t.y);
+            u = fmaf(r1[l1], u, t.x);
+            part1 = fmaf(le[l1], r0[l1] * u, part1);
+          }
+          if (has2) {
+            float u = fmaf(r3[l2], t.w, t.z);
+            u = fmaf(r2[l2], u, t.y);
+            u = fmaf(r1[l2], u, t.x);
+            part2 = fmaf(le[l2], r0[l2] * u, part2);
+          }
+        }
+        acc0 += static_cast<double>(part0);
+        acc1 += static_cast<double>(part1);
+        acc2 += static_cast<double>(part2);
+      }
+    }
+    const double inv = 1.0 / p.spp;
+    const float s0 = static_cast<float>(acc0 * inv), s1 = static_cast<float>(acc1 * inv),
+                s2 = has2 ? static_cast<float>(acc2 * inv) : 0.f;
+    float xyz[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float v = fmaf(p.cmf[c * N + l1], s1, p.cmf[c * N + l0] * s0);
+      if (has2) v = fmaf(p.cmf[c * N + l2], s2, v);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      xyz[c] = v;
+    }
+    if (lane == 0) {
+      float rgb[3];
+      xyz_to_rgb(p.Crgb, xyz, rgb);
+      if (p.xyz)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) p.xyz[pix * 3 + c] = xyz[c];
+      if (p.rgb)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) p.rgb[pix * 3 + c] = rgb[c];
+    }
+  }
+  if (bad) atomicOr(p.err, kErrIndexRange);
+}
+
 }  // namespace hcb

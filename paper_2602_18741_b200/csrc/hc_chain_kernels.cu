@@ -149,8 +149,21 @@ int chain_spectral_ns(hc_codec c, const float* pal, int n_pal, const float* ill,
   p.xyz = xyz;
   p.rgb = rgb;
   p.err = c->ctx->d_err;
-  const int smem = (n_pal + n_ill) * N * 4;
   int grid = 0;
+#ifndef HC_CHAIN_NAIVE_LANES
+#define HC_CHAIN_NAIVE_LANES 1
+#endif
+  if constexpr (N > 64 && N <= kChainLanesRow) {
+    if (HC_CHAIN_NAIVE_LANES) {  // lanes over wavelengths (one pixel per warp)
+      const int smem = (n_pal + n_ill) * kChainLanesRow * 4 + 8 * 32 * 6 * 4;
+      int rc = chain_grid(c->ctx, chain_spectral_lanes_kernel<N>, smem, P * 8, &grid);  // 8 lanes-worth per pixel
+      if (rc != HC_OK) return rc;
+      chain_spectral_lanes_kernel<N><<<grid, 256, smem, c->ctx->stream>>>(p);
+      HC_CHECK_LAUNCH(c->ctx, "chain_spectral_lanes_kernel");
+      return HC_OK;
+    }
+  }
+  const int smem = (n_pal + n_ill) * N * 4;
   int rc = chain_grid(c->ctx, chain_spectral_kernel<N, SPL>, smem, P, &grid);
   if (rc != HC_OK) return rc;
   chain_spectral_kernel<N, SPL><<<grid, 256, smem, c->ctx->stream>>>(p);
