@@ -15,11 +15,13 @@ namespace hcb {
 template <class KernelFn>
 int chain_grid(hc_ctx ctx, KernelFn fn, int smem, int64_t P, int* grid, int threads = 256) {
   static std::mutex mu;
-  static std::map<std::pair<const void*, int>, int> cache;
+  static std::map<std::pair<std::pair<const void*, int>, int>, int> cache;  // ((kernel, smem), device)
   int occ = 0;
   {
     std::lock_guard<std::mutex> lk(mu);
-    auto key = std::make_pair(reinterpret_cast<const void*>(fn), smem);
+    int dev = 0;
+    HC_CUDA_TRY(cudaGetDevice(&dev));  // attributes are per device
+    auto key = std::make_pair(std::make_pair(reinterpret_cast<const void*>(fn), smem), dev);
     auto it = cache.find(key);
     if (it != cache.end()) {
       occ = it->second;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdint>
 #include <string>
 #include <vector>
 
@@ -51,6 +52,21 @@ void note_launch(hc_ctx ctx, int n = 1);
 // Grows the context scratch to >= bytes; the first `keep` bytes survive a reallocation.
 int ensure_scratch(hc_ctx ctx, size_t bytes, size_t keep = 0);
 int ensure_aux_streams(hc_ctx ctx);
+
+// Kernel attributes (cudaFuncSetAttribute: dynamic shared memory, carveout) are per device, so
+// one-time configuration is tracked per device (the group API drives several GPUs from one
+// process, one host thread each).  `mask` holds one bit per device ordinal (< 64).
+inline uint64_t current_device_bit() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return 1ull << (dev & 63);
+}
+inline bool configured_here(const std::atomic<uint64_t>& mask) {
+  return (mask.load(std::memory_order_acquire) & current_device_bit()) != 0;
+}
+inline void mark_configured_here(std::atomic<uint64_t>& mask) {
+  mask.fetch_or(current_device_bit(), std::memory_order_release);
+}
 
 #define HC_CUDA_TRY(expr)                                        \
   do {                                                           \

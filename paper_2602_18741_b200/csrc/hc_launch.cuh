@@ -14,11 +14,11 @@ namespace hcb {
 
 template <class Op>
 struct TileLaunchCache {
-  static std::atomic<int> configured;  // 0 = not yet, 1 = done
+  static std::atomic<uint64_t> configured;  // one bit per device (attributes are per device)
   static int occ_pipeline, occ_generic;  // occ_pipeline: of tile_pipeline_ws for warp-specialised ops
 };
 template <class Op>
-std::atomic<int> TileLaunchCache<Op>::configured{0};
+std::atomic<uint64_t> TileLaunchCache<Op>::configured{0};
 template <class Op>
 int TileLaunchCache<Op>::occ_pipeline = 1;
 template <class Op>
@@ -28,7 +28,7 @@ int TileLaunchCache<Op>::occ_generic = 1;
 template <class Op>
 int configure_tile_op() {
   using Cache = TileLaunchCache<Op>;
-  if (Cache::configured.load(std::memory_order_acquire)) return HC_OK;
+  if (configured_here(Cache::configured)) return HC_OK;
   const int smem = TileLayout<Op>::smem_bytes();
   HC_CUDA_TRY(cudaFuncSetAttribute(tile_pipeline<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   HC_CUDA_TRY(cudaFuncSetAttribute(tile_generic<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -52,7 +52,7 @@ int configure_tile_op() {
   if (a < 1 || b < 1 || w < 1) return set_error(HC_EUNSUPPORTED, "tile kernel does not fit on an SM");
   Cache::occ_pipeline = a;
   Cache::occ_generic = b;
-  Cache::configured.store(1, std::memory_order_release);
+  mark_configured_here(Cache::configured);
   return HC_OK;
 }
 

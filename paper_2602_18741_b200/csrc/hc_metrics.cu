@@ -679,12 +679,12 @@ int value_grid(hc_ctx ctx, int64_t P) {
 }
 
 int configure_producers() {
-  static int done = 0;
-  if (done) return HC_OK;
+  static std::atomic<uint64_t> done{0};  // per device (attributes are per device)
+  if (configured_here(done)) return HC_OK;
   HC_CUDA_TRY(cudaFuncSetAttribute(lum_keys_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopSmem));
   HC_CUDA_TRY(cudaFuncSetAttribute(de76_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopSmem));
   HC_CUDA_TRY(cudaFuncSetAttribute(de94_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kTopSmem));
-  done = 1;
+  mark_configured_here(done);
   return HC_OK;
 }
 

@@ -430,10 +430,10 @@ int naive_lanes_launch(hc_codec c, const float* pal, int n_pal, const float* lig
   const int warps = kLanesThreads / 32;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((rounds + warps - 1) / warps, c->ctx->sm_count)));
   const int smem = kLanesThreads / 32 * (32 * L + 3 * 32 * 32) * 4;
-  static bool configured = false;  // (a benign race: the attribute call is idempotent)
-  if (!configured) {
+  static std::atomic<uint64_t> configured{0};  // per device; the attribute call is idempotent
+  if (!configured_here(configured)) {
     HC_CUDA_TRY(cudaFuncSetAttribute(naive_lanes_kernel<N, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
+    mark_configured_here(configured);
   }
   naive_lanes_kernel<N, L><<<grid, kLanesThreads, smem, c->ctx->stream>>>(p);
   HC_CHECK_LAUNCH(c->ctx, "naive_lanes_kernel");
