@@ -851,6 +851,38 @@ def parity_gbuffer(wl, rows_stride: int = 1) -> dict:
     return res
 
 
+def parity_naive_gbuffer(wn, rows_stride: int = 16) -> dict:
+    """The naive n = 81 path (config 2 / 3 ground truth) on set 0 against the reference's
+    spectral shading (oracle/_ref, R1 at C = n) on every `rows_stride`-th row."""
+    import oracle
+
+    ref = oracle.reference(81)
+    cfg = wn.cfg
+    L, W = cfg["L"], cfg["W"]
+    idx, cosv, outs = wn.sets[0]
+    P = wn.units
+    rows = np.arange(0, P // W, rows_stride)
+    sel = (rows[:, None] * W + np.arange(W)[None, :]).reshape(-1)
+    h_idx = idx.cpu().numpy().view(np.uint32)[sel].copy()
+    h_cos = np.ascontiguousarray(cosv.cpu().numpy()[sel])
+    m = sel.size
+    spec = outs.get("spectra") is not None
+    r_spec = np.zeros((m, N_SPEC), np.float32) if spec else None
+    r_xyz = np.zeros((m, 3), np.float32)
+    r_rgb = np.zeros((m, 3), np.float32)
+    ref.ref_shade_spectral(np.ascontiguousarray(wn.pal_d.cpu().numpy()), np.ascontiguousarray(wn.lts, np.float32), L,
+                           h_idx, h_cos, m, r_spec, r_xyz, r_rgb, 0)
+    res = {}
+    for name, want in (("naive spectra", r_spec), ("naive xyz", r_xyz), ("naive rgb", r_rgb)):
+        key = name.split()[1]
+        if want is None or outs.get(key) is None:
+            continue
+        got = outs[key].cpu().numpy()[sel]
+        res[name] = {"max_rel": rel_err_rows(got, want), "max_abs": float(np.max(np.abs(got.astype(np.float64) - want))),
+                     "rows": f"every {rows_stride}th row", "pixels": int(m)}
+    return res
+
+
 def rel_err_rows(got, ref) -> float:
     """max |got - ref| / max(|ref|, ||ref_row||_inf), chunked for large arrays."""
     worst = 0.0
@@ -1215,7 +1247,14 @@ def verify_config(key: str, rank: int = 0) -> dict:
         for name in ("spectra", "xyz", "rgb"):
             if name in par:
                 checks.append({"name": name, **par[name], "tol": 1e-5, "pass": par[name]["max_rel"] <= 1e-5})
-        sample = f"full {cfg['W']}x{cfg['H']} frame"
+        # the naive n = 81 ground truth at full size too (every 16th row checked)
+        wn = Workload(api, ctx, key, rank, naive=True)
+        wn.step(0)
+        torch.cuda.synchronize()
+        for name, r in parity_naive_gbuffer(wn, 16).items():
+            checks.append({"name": name, **r, "tol": 1e-5, "pass": r["max_rel"] <= 1e-5})
+        del wn
+        sample = f"full {cfg['W']}x{cfg['H']} frame (naive: every 16th row)"
     elif key == "1":
         S, outs = wl.sets[0]
         P = wl.units
@@ -1251,7 +1290,15 @@ def verify_config(key: str, rank: int = 0) -> dict:
         ref.ref_multibounce_latent(E, D, k, pc, ic, h_p, h_i, h_t, m, spp, 4, None, X, R, 0)
         checks.append(_cmp("xyz", outs["xyz"][sel].cpu().numpy(), X, 1e-5))
         checks.append(_cmp("rgb", outs["rgb"][sel].cpu().numpy(), R, 1e-5))
-        sample = f"every 16th row ({m} px x {spp} spp)"
+        # the naive n = 81 chain (ground truth) on the same samples
+        nv = wl.codec.multibounce_spectral(torch.from_numpy(pal).cuda(), torch.from_numpy(ill).cuda(), pidx, iidx, tw)
+        torch.cuda.synchronize()
+        Xn, Rn = np.zeros((m, 3), np.float32), np.zeros((m, 3), np.float32)
+        ref.ref_multibounce_spectral(pal, ill, h_p, h_i, h_t, m, spp, 4, Xn, Rn, 0)
+        checks.append(_cmp("naive xyz", nv["xyz"][sel].cpu().numpy(), Xn, 1e-5))
+        checks.append(_cmp("naive rgb", nv["rgb"][sel].cpu().numpy(), Rn, 1e-5))
+        del nv
+        sample = f"every 16th row ({m} px x {spp} spp; latent and naive)"
     elif key == "5a":
         rgb, out = wl.sets[0]
         P = wl.units

@@ -3,7 +3,8 @@
 `bench.py --verify` runs one step of each BASELINE config at its full size with the bench's
 inputs (seed, generators, buffer set 0) and checks the outputs against the reference compiled
 from its sources (oracle/_ref, all host threads) on the same inputs: configs 1, 2, 3, 5a and
-5b on the whole output, config 4 on every 16th row.  Those runs also cross the > 2^31-byte
+5b on the whole output, config 4 on every 16th row, plus the naive n = 81 ground truths of
+configs 2, 3 and 4 on every 16th row.  Those runs also cross the > 2^31-byte
 offsets (config 3 writes 2.69 GB of spectra, config 5b reads two 5.4 GB arrays, config 4
 reads a 4.3 GB throughput array).  Tolerances: 1e-5 relative (fp32 outputs, fp64 loss),
 1e-2 for the bf16 MLP.
