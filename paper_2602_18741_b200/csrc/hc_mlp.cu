@@ -62,6 +62,9 @@ constexpr int kMaxK = 9;
 #ifndef HC_MLP_L3_FIRST
 #define HC_MLP_L3_FIRST 0
 #endif
+#ifndef HC_MLP_TMEM_WIDE  // epilogue TMEM access width: 0 = x16, 1 = x32 loads + one x32 store, 2 = x64 load
+#define HC_MLP_TMEM_WIDE 1
+#endif
 #ifndef HC_MLP_B2_EPI
 #define HC_MLP_B2_EPI 0
 #endif
@@ -223,6 +226,19 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
     else HC_TMEM_LD16(taddr, r);       \
   } while (0)
 
+#define HC_TMEM_LD64(taddr, r) \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];" \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63]) \
+               : "r"(taddr))
+#define HC_TMEM_LD32(taddr, r) \
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];" \
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]) \
+               : "r"(taddr))
+#define HC_TMEM_ST32(taddr, r) \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" \
+               ::"r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]) \
+               : "memory")
+
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -260,8 +276,18 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem
 #endif
   constexpr int kQ = kCols / 16;
   uint32_t va[kQ][16];
+#if HC_MLP_TMEM_WIDE  // 32-column (or, = 2 with 64 columns, one 64-column) loads and one 32-column store
+  static_assert(kQ % 2 == 0, "32-column chunks");
+  if constexpr (HC_MLP_TMEM_WIDE == 2 && kQ == 4) {
+    HC_TMEM_LD64(tmem_acc, (&va[0][0]));
+  } else {
+#pragma unroll
+    for (int q = 0; q < kQ; q += 2) HC_TMEM_LD32(tmem_acc + q * 16, (&va[q][0]));
+  }
+#else
 #pragma unroll
   for (int q = 0; q < kQ; ++q) HC_TMEM_LD16(tmem_acc + q * 16, va[q]);
+#endif
   tmem_wait_ld();
   uint32_t pk[kQ / 2][16];
 #pragma unroll
@@ -275,8 +301,13 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem
       }
       pk[q >> 1][(q & 1) * 8 + j] = pack_relu_bf16(lo, hi);
     }
+#if HC_MLP_TMEM_WIDE
+  static_assert(kQ / 2 == 2, "one 32-column store");
+  HC_TMEM_ST32(tmem_a, (&pk[0][0]));
+#else
 #pragma unroll
   for (int q = 0; q < kQ / 2; ++q) HC_TMEM_ST16(tmem_a + q * 16, pk[q]);
+#endif
   tmem_wait_st();
 }
 
