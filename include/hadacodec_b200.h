@@ -191,6 +191,11 @@ int hc_scene_color_report(hc_codec codec, const float* gt, int channels_gt, cons
  * from the same pass, as run_report writes next to the report (tools/main.cpp:604-623). */
 int hc_scene_color_report_dev(hc_codec codec, const float* gt, int channels_gt, const float* test,
                               int channels_test, int64_t P, double* out4_dev, uint8_t* test_srgb8);
+/* XYZ of rows of n fp64 values (device), fp64 out (device, rows x 3), in the reference's summation
+ * order: weights == NULL is the radiance convention spectrum_to_xyz (colorimetry.cpp:75-87: CMF
+ * rows, then x dlambda); otherwise `weights` (host, 3 x n) are CmfTable's D65-weighted rows and
+ * the result is xyz_of_reflectance (colorimetry.cpp:89-101). */
+int hc_spectra_to_xyz_f64(hc_codec codec, const double* S, int64_t rows, const double* weights, double* xyz);
 /* Per-pixel Delta E94 of multibounce_eval (evaluation.cpp:59-86): Lab of both XYZ images under
  * white_xyz (host, 3 doubles; CmfTable::white_xyz) scaled to the ground truth's max(Y, 1e-6).
  * out3 (host) = {mean, median, p95}; de[P] (may be NULL) per pixel.  HC_EDOMAIN for a

@@ -403,8 +403,37 @@ LatentCode encode(const CodecWeights& w, const SpectralCurve& s);
 SpectralCurve decode(const EffectiveWeights& w, const LatentCode& z);  // std::domain_error on negative codes
 SpectralCurve decode(const CodecWeights& w, const LatentCode& z);
 
-// ---- colorimetry.hpp:47 (radiance convention, on the curve's grid)
-ColorTriple spectrum_to_xyz(const SpectralCurve& s);
+// ---- colorimetry.hpp:25-77.  spectrum_to_xyz / xyz_of_reflectance run the fp64 GPU kernel
+// (hc_spectra_to_xyz_f64, the reference's summation order); CmfTable is the grid's tabulated
+// CIE 1931 / D65 rows (package data, tools/make_cmf_tables.py); the scalar Lab / Delta E / sRGB
+// helpers are the reference's formulas on one value (their per-pixel batched forms run on the
+// GPU in hc_scene_color_report / hc_delta_e94_report).
+class CmfTable {
+ public:
+  static const CmfTable& instance();       // the reference grid (kSampleCount = 47)
+  static const CmfTable& for_grid(int n);  // 47 or 81
+  const SpectralCurve& xbar() const { return xbar_; }
+  const SpectralCurve& ybar() const { return ybar_; }
+  const SpectralCurve& zbar() const { return zbar_; }
+  const SpectralCurve& d65() const { return d65_; }
+  const SpectralCurve& wx() const { return wx_; }  // D65-weighted rows, unit reflectance -> Y = 100
+  const SpectralCurve& wy() const { return wy_; }
+  const SpectralCurve& wz() const { return wz_; }
+  ColorTriple white_xyz() const;
+
+ private:
+  explicit CmfTable(int n);
+  SpectralCurve xbar_, ybar_, zbar_, d65_, wx_, wy_, wz_;
+};
+ColorTriple spectrum_to_xyz(const SpectralCurve& s);     // radiance convention, on the curve's grid
+ColorTriple xyz_of_reflectance(const SpectralCurve& r);  // reflectance convention
+ColorTriple linear_rgb_to_xyz(const ColorTriple& rgb);
+ColorTriple srgb_reference_white();
+ColorTriple xyz_to_lab(const ColorTriple& xyz, const ColorTriple& white);  // std::domain_error: white <= 0
+double delta_e76(const ColorTriple& lab_a, const ColorTriple& lab_b);
+double delta_e94(const ColorTriple& lab_reference, const ColorTriple& lab_sample);
+double srgb_encode(double linear);
+double srgb_decode(double encoded);
 
 // ---- renderer.hpp:100-133
 ChannelImage render(const Scene& scene, const RenderJob& job, const CodecWeights* codec = nullptr);

@@ -60,6 +60,7 @@ SIGNATURES: dict[str, tuple] = {
     "hc_scene_color_report": (i32, [vp, vp, i32, vp, i32, i64, vp]),
     "hc_scene_color_report_dev": (i32, [vp, vp, i32, vp, i32, i64, vp, vp]),
     "hc_delta_e94_report": (i32, [vp, vp, vp, i64, vp, vp, vp]),
+    "hc_spectra_to_xyz_f64": (i32, [vp, vp, i64, vp, vp]),
     "hc_format_g17": (i32, [vp, vp, i64, vp, vp]),
     "hc_codes_csv_write": (i32, [vp, vp, i64, i32, u64, vp, i64, C.POINTER(i64)]),
     "hc_codes_csv_write_ids": (i32, [vp, vp, i32, i64, i32, vp, vp, C.c_char_p, u64, vp, i64, C.POINTER(i64)]),

@@ -218,6 +218,36 @@ __global__ void __launch_bounds__(kThreads) spectra_to_rgb_d_kernel(const float*
   }
 }
 
+// Per-curve XYZ in fp64 (the by-value spectrum_to_xyz / xyz_of_reflectance of the drop-in,
+// colorimetry.cpp:75-101): radiance convention (CMF rows, then x dlambda) or, with `w` set,
+// the reflectance convention (D65-weighted rows, no scaling); sums in the reference's order.
+struct XyzRows {
+  double row[3][kMaxN];
+  double scale;  // dlambda (radiance) or 1 (reflectance)
+  int n;
+};
+__global__ void __launch_bounds__(kThreads) spectra_to_xyz_f64_kernel(const double* __restrict__ S, int64_t rows,
+                                                                      const __grid_constant__ XyzRows c,
+                                                                      double* __restrict__ xyz) {
+  for (int64_t p = blockIdx.x * int64_t(kThreads) + threadIdx.x; p < rows; p += int64_t(gridDim.x) * kThreads) {
+    const double* s = S + p * c.n;
+    double x = 0.0, y = 0.0, z = 0.0;
+    for (int i = 0; i < c.n; ++i) {
+      x += c.row[0][i] * s[i];
+      y += c.row[1][i] * s[i];
+      z += c.row[2][i] * s[i];
+    }
+    if (c.scale != 1.0) {
+      x *= c.scale;
+      y *= c.scale;
+      z *= c.scale;
+    }
+    xyz[p * 3] = x;
+    xyz[p * 3 + 1] = y;
+    xyz[p * 3 + 2] = z;
+  }
+}
+
 // error_map's per-pixel term (renderer.cpp:785-797): mean of squared channel differences.
 __device__ __forceinline__ double pixel_mse(const float* a, const float* b) {
   double acc = 0.0;
@@ -921,6 +951,23 @@ int hc_scene_color_report(hc_codec c, const float* gt, int channels_gt, const fl
   rc = scene_report_launch(c, s, gt, channels_gt, test, channels_test, P, s.results, nullptr);
   if (rc != HC_OK) return rc;
   return fetch_results(c->ctx, s, out4, 4);
+}
+
+int hc_spectra_to_xyz_f64(hc_codec c, const double* S, int64_t rows, const double* weights, double* xyz) {
+  HC_REQUIRE(c && xyz, HC_EINVAL, "spectra_to_xyz_f64: null argument");
+  HC_REQUIRE(rows >= 0, HC_EINVAL, "spectra_to_xyz_f64: negative row count");
+  if (rows == 0) return HC_OK;
+  HC_REQUIRE(S, HC_EINVAL, "spectra_to_xyz_f64: null spectra");
+  XyzRows r;
+  std::memset(&r, 0, sizeof(r));
+  r.n = c->n;
+  for (int row = 0; row < 3; ++row)
+    for (int i = 0; i < c->n; ++i) r.row[row][i] = weights ? weights[row * c->n + i] : c->cmf[row * c->n + i];
+  r.scale = weights ? 1.0 : c->dlambda;
+  hc_ctx ctx = c->ctx;
+  spectra_to_xyz_f64_kernel<<<value_grid(ctx, rows), kThreads, 0, ctx->stream>>>(S, rows, r, xyz);
+  HC_CHECK_LAUNCH(ctx, "spectra_to_xyz_f64_kernel");
+  return HC_OK;
 }
 
 int hc_delta_e94_report(hc_ctx ctx, const float* xyz_gt, const float* xyz_test, int64_t P, const double* white_xyz,

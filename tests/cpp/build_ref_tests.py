@@ -20,7 +20,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[2]
 REF_TESTS = Path("/root/reference/proj/tests")
-CASES = ("test_codec", "test_spectrum")  # codec.hpp / spectrum.hpp: the hot path's value API
+CASES = ("test_codec", "test_spectrum", "test_colorimetry")  # codec, spectrum and colorimetry value APIs
 OUT = ROOT / "tests" / "cpp" / "bin" / "ref_unit_tests"
 
 

@@ -39,7 +39,7 @@ REF_UNIT = ROOT / "tests" / "cpp" / "bin" / "ref_unit_tests"
 
 
 def test_reference_unit_tests_compile_unchanged():
-    """The reference's test_codec.cpp / test_spectrum.cpp compile against the drop-in with only
+    """The reference's test_codec.cpp / test_spectrum.cpp / test_colorimetry.cpp compile against the drop-in with only
     `using namespace hadacodec;` -> `hadacodec::b200` (tests/cpp/build_ref_tests.py)."""
     import sys
 
