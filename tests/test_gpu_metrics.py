@@ -180,3 +180,44 @@ def test_scene_report_dev_and_preview(api, ctx, orc):
     want = np.zeros(P * 3, np.uint8)
     orc.orc_tonemap_srgb8(b, P, sync["exposure"], want)
     assert np.array_equal(prev.cpu().numpy().reshape(-1), want)
+
+
+@pytest.mark.parametrize("n,rows,refl", [(81, 1, False), (81, 1000, False), (47, 777, False), (81, 513, True),
+                                         (47, 64, True)])
+def test_spectra_to_xyz_f64_matches_reference_order(api, ctx, n, rows, refl):
+    """hc_spectra_to_xyz_f64 (the drop-in's by-value spectrum_to_xyz / xyz_of_reflectance):
+    fp64 sums in the reference's order (colorimetry.cpp:75-101), so bit-identical to a sequential
+    numpy-scalar restatement; radiance rows are the CMF rows then x dlambda, reflectance rows the
+    D65-weighted rows scale * cmf * d65 (scale = 100 / sum(ybar d65))."""
+    from paper_2602_18741_b200 import _lib
+    from paper_2602_18741_b200.colorimetry import cmf_table
+
+    codec = _codec(api, ctx, n)
+    rng = np.random.default_rng(rows + n)
+    S = rng.random((rows, n)) * rng.lognormal(0.0, 1.0, (rows, 1))
+    t = cmf_table(n)
+    cmf = [t["xbar"], t["ybar"], t["zbar"]]
+    if refl:
+        norm = 0.0
+        for i in range(n):
+            norm += t["ybar"][i] * t["d65"][i]
+        scale = 100.0 / norm
+        w = np.array([[scale * row[i] * t["d65"][i] for i in range(n)] for row in cmf])
+        rows_used, mult = w, None
+    else:
+        w, rows_used, mult = None, np.array(cmf), grid(n)[1]
+    out = torch.empty(rows, 3, dtype=torch.float64, device="cuda")
+    Sd = dev(S)
+    wp = None if w is None else np.ascontiguousarray(w, np.float64).ctypes.data
+    rc = _lib.lib().hc_spectra_to_xyz_f64(codec.h, Sd.data_ptr(), rows, wp, out.data_ptr())
+    assert rc == 0
+    ctx.synchronize()
+    got = out.cpu().numpy()
+    for r in range(0, rows, max(1, rows // 50)):
+        want = []
+        for c in range(3):
+            acc = 0.0
+            for i in range(n):
+                acc += float(rows_used[c][i]) * float(S[r, i])
+            want.append(acc * mult if mult is not None else acc)
+        assert list(got[r]) == want, (r, got[r], want)
