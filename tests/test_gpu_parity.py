@@ -384,7 +384,7 @@ def test_multibounce_vs_oracle(api, ctx, orc, spp, k, n):
 
 
 @pytest.mark.parametrize("n_pal,n_ill,spp,k", [(100, 5, 72, 6), (256, 200, 64, 6), (1, 1, 8, 6), (37, 16, 136, 6),
-                                                (100, 5, 72, 3), (37, 16, 24, 9)])
+                                                (100, 5, 72, 3), (37, 16, 24, 9), (100, 5, 64, 6), (255, 16, 64, 6)])
 def test_multibounce_small_tables(api, ctx, orc, n_pal, n_ill, spp, k):
     """Palettes / illuminant sets smaller than the u8 index range (the k = 6 kernel range-checks
     palette indices only when n_pal < 256), large illuminant sets, and spp with a sample tail
