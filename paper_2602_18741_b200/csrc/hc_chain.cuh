@@ -314,6 +314,16 @@ __global__ void __launch_bounds__(256) chain_latent_rep_kernel(const __grid_cons
 #ifndef HC_CHAIN_IIDX128
 #define HC_CHAIN_IIDX128 0
 #endif
+// Bulk-copied records (kTma): a pixel's 64 illuminant bytes read as 4 LDS.128 that the pixel's 8
+// lanes share (one wavefront each for the warp's 4 pixels) instead of 8 byte loads per lane.
+#ifndef HC_CHAIN_TMA_IIDX128
+#define HC_CHAIN_TMA_IIDX128 1
+#endif
+// Pixel sums: 1 = fp32 reduce-scatter over the 8 lanes by shuffles (11 SHFL per quad),
+// 0 = fp32 partials staged through shared memory and added in fp64 (20 wavefronts per quad).
+#ifndef HC_CHAIN_SUM_SHFL
+#define HC_CHAIN_SUM_SHFL 1
+#endif
 constexpr int kChainV3Row = 256;
 constexpr int kChainV3Stage = 6 * 33;  // floats of per-warp staging for the pixel sums
 __host__ __device__ constexpr int chain_v3_stage_bytes(int warps) { return (warps * kChainV3Stage * 4 + 15) / 16 * 16; }
@@ -464,8 +474,21 @@ __global__ void __launch_bounds__(kTma ? kChainTmaThreads : 256, kTma ? 2 : 0)
       for (int m = 0; m < 8; ++m) {
         const int smp = g + m * kChainLanes;
         pkg[m] = valid ? *reinterpret_cast<const uint32_t*>(src + pp * 288 + smp * 4) : 0u;
-        lig[m] = valid ? static_cast<uint32_t>(src[kChainTmaPidx + pp * 80 + smp]) : 0u;
+        if (!HC_CHAIN_TMA_IIDX128) lig[m] = valid ? static_cast<uint32_t>(src[kChainTmaPidx + pp * 80 + smp]) : 0u;
         t4g[m] = valid ? ldg_stream(p.tw + base + smp) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (HC_CHAIN_TMA_IIDX128) {
+        // 16-byte chunk c holds samples 16c .. 16c+15: lane g's samples g + 16c and g + 8 + 16c are
+        // byte g % 4 of word g / 4 and of word 2 + g / 4.
+        const uint4* irow = reinterpret_cast<const uint4*>(src + kChainTmaPidx + pp * 80);
+        const uint32_t bsel = 0x4440u | static_cast<uint32_t>(g & 3);
+        const bool hw = g >= 4;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 w = valid ? irow[c] : make_uint4(0u, 0u, 0u, 0u);
+          lig[2 * c] = __byte_perm(hw ? w.y : w.x, 0u, bsel);
+          lig[2 * c + 1] = __byte_perm(hw ? w.w : w.z, 0u, bsel);
+        }
       }
       // the other slot was read one quad ago: refill it with the next quad's records
       if (qd + nwarps < (p.P + kPixPerWarp - 1) / kPixPerWarp) issue_quad(qd + nwarps, slot ^ 1);
@@ -519,6 +542,42 @@ __global__ void __launch_bounds__(kTma ? kChainTmaThreads : 256, kTma ? 2 : 0)
     // partials of code g in fp64 (renderer.cpp:548-551) and the group's lane 0 gathers the 6
     // codes by shuffle for the XYZ / sRGB projection: 20 L1 wavefronts per pixel quad instead of
     // the 36 of an fp64 butterfly (the kernel is bound by the L1 data pipe).
+    const int grp0 = lane & ~(kChainLanes - 1);
+    float zz[6];
+    if (HC_CHAIN_SUM_SHFL) {
+      // Reduce-scatter in fp32 over the 8 lanes (xor 4, 2, 1): 3 + 2 + 1 shuffles leave code
+      // 0, 1, 2, 2, 3, 4, 5, 5 in lanes g = 0..7, then the group's lane 0 gathers codes 1..5 (5
+      // shuffles): 11 L1 wavefronts per pixel quad instead of 20 through the staging area.
+      float pv[6];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        float2 f;
+        memcpy(&f, &part[j], 8);
+        pv[2 * j] = f.x;
+        pv[2 * j + 1] = f.y;
+      }
+      const bool b2 = (g & 4) != 0, b1 = (g & 2) != 0, b0 = (g & 1) != 0;
+      float q[3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const float r = __shfl_xor_sync(0xffffffffu, b2 ? pv[i] : pv[3 + i], 4);
+        q[i] = (b2 ? pv[3 + i] : pv[i]) + r;
+      }
+      const float r0 = __shfl_xor_sync(0xffffffffu, b1 ? q[0] : q[2], 2);
+      const float r1 = __shfl_xor_sync(0xffffffffu, q[1], 2);
+      const float s0 = (b1 ? q[2] : q[0]) + r0, s1 = q[1] + r1;  // s1 is used by b1 == 0 lanes only
+      const float r2 = __shfl_xor_sync(0xffffffffu, (!b1 && !b0) ? s1 : s0, 1);
+      const float t = ((!b1 && b0) ? s1 : s0) + r2;
+      const float z = static_cast<float>(static_cast<double>(t) * (1.0 / p.spp));
+      const int code = (b2 ? 3 : 0) + (b1 ? 2 : (b0 ? 1 : 0));
+      if (valid && p.latent && !(b1 && b0)) p.latent[pix * 6 + code] = z;
+      zz[0] = z;
+      zz[1] = __shfl_sync(0xffffffffu, z, grp0 + 1);
+      zz[2] = __shfl_sync(0xffffffffu, z, grp0 + 2);
+      zz[3] = __shfl_sync(0xffffffffu, z, grp0 + 4);
+      zz[4] = __shfl_sync(0xffffffffu, z, grp0 + 5);
+      zz[5] = __shfl_sync(0xffffffffu, z, grp0 + 6);
+    } else {
     __syncwarp();  // the previous quad's staging reads are done
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
@@ -528,7 +587,6 @@ __global__ void __launch_bounds__(kTma ? kChainTmaThreads : 256, kTma ? 2 : 0)
       stg[(2 * j + 1) * 33 + lane] = f.y;
     }
     __syncwarp();
-    const int grp0 = lane & ~(kChainLanes - 1);
     float z = 0.f;
     if (g < 6) {
       double acc = 0.0;
@@ -537,9 +595,9 @@ __global__ void __launch_bounds__(kTma ? kChainTmaThreads : 256, kTma ? 2 : 0)
       z = static_cast<float>(acc * (1.0 / p.spp));
       if (valid && p.latent) p.latent[pix * 6 + g] = z;
     }
-    float zz[6];
 #pragma unroll
     for (int j = 0; j < 6; ++j) zz[j] = __shfl_sync(0xffffffffu, z, grp0 + j);
+    }
     if (valid && g == 0) {
       float xyz[3], rgb[3];
 #pragma unroll
