@@ -314,10 +314,11 @@ __global__ void __launch_bounds__(256) chain_latent_rep_kernel(const __grid_cons
 #ifndef HC_CHAIN_IIDX128
 #define HC_CHAIN_IIDX128 0
 #endif
-// Bulk-copied records (kTma): a pixel's 64 illuminant bytes read as 4 LDS.128 that the pixel's 8
+// Bulk-copied records (kTma), option: a pixel's 64 illuminant bytes read as 4 LDS.128 that the pixel's 8
 // lanes share (one wavefront each for the warp's 4 pixels) instead of 8 byte loads per lane.
+// Measured neutral to slightly slower (72.0 vs 72.2-72.8 % with the shuffle sums), so off.
 #ifndef HC_CHAIN_TMA_IIDX128
-#define HC_CHAIN_TMA_IIDX128 1
+#define HC_CHAIN_TMA_IIDX128 0
 #endif
 // Pixel sums: 1 = fp32 reduce-scatter over the 8 lanes by shuffles (11 SHFL per quad),
 // 0 = fp32 partials staged through shared memory and added in fp64 (20 wavefronts per quad).
