@@ -56,8 +56,30 @@ constexpr int kHid = 64;      // hidden width
 constexpr int kK1 = 16;       // layer-1 K (3 inputs + bias column, padded)
 constexpr int kN3 = 16;       // layer-3 N (k padded)
 constexpr int kMaxK = 9;
+#ifndef HC_MLP_PP
+#define HC_MLP_PP 0
+#endif
+// Ping-pong TMEM layout (measured option, off: 63.8 Gpix/s with 4 streams against 63.1-63.3 for the
+// default 3 x 144 layout, 57.9 with 3 streams): each stream owns two 64-column regions X and Y.  Layer 1
+// accumulates into X and its epilogue writes A2 *in place* over X's first 32 columns (+ the 8-column
+// constant K chunk at X + 32); layer 2 reads A2 from X and accumulates into Y; its epilogue writes A3
+// in place over Y's first 32 columns and layer 3 accumulates into Y + 32.  X is free as soon as layer
+// 2 completes, so layer 1 of the next tile is issued then -- it runs under this tile's layer-2
+// epilogue instead of after it -- and a stream needs 128 columns instead of 144: 4 streams fit.
+// The stream's cycle is then layer-2 round trip + epilogue 2 + layer-3 round trip + accumulator read
+// (~2,000 cycles under load: layer 2 of the next tile overwrites Y, so layer 3 is on the cycle), which
+// 4 streams turn into ~500 cycles per tile -- the same as 3 streams of ~1,600.
+constexpr bool kPP = HC_MLP_PP;
+#ifndef HC_MLP_L3_SPLIT  // measured 37.2 Gpix/s: alternating two 16-column accumulators is far slower
+#define HC_MLP_L3_SPLIT 0
+#endif
+// Layer 3 as two independent two-step K chains into two 16-column accumulators (Y + 32, Y + 48)
+// summed by the codes epilogue: a dependent tcgen05.mma step costs ~100-135 cycles of latency
+// whatever N (tools/mma_latency.cu), and with kPP layer 3's latency is on the stream's cycle.
+constexpr bool kL3Split = HC_MLP_L3_SPLIT;
+static_assert(!kL3Split || kPP, "split layer 3 needs the ping-pong layout's free Y columns");
 #ifndef HC_MLP_STREAMS
-#define HC_MLP_STREAMS 3
+#define HC_MLP_STREAMS (HC_MLP_PP ? 4 : 3)
 #endif
 #ifndef HC_MLP_L3_FIRST
 #define HC_MLP_L3_FIRST 0
@@ -86,6 +108,7 @@ constexpr bool kL3First = HC_MLP_L3_FIRST;  // issue layer 3 of a tile before la
 constexpr int kEpiW = HC_MLP_EPI_WARPS;
 static_assert(kEpiW == 4 || kEpiW == 8, "epilogue warps per stream");
 static_assert(!(HC_MLP_A3_SMEM && kEpiW != 4), "A3 in smem: 4 epilogue warps");
+static_assert(!(HC_MLP_PP && (kEpiW != 4 || HC_MLP_A3_SMEM || HC_MLP_B2_EPI)), "ping-pong layout: 4 epilogue warps, A3 in TMEM, b2 by MMA");
 constexpr int kEpiCols = kHid * 4 / kEpiW;   // accumulator columns per epilogue warp
 constexpr int kEpiThreads = 32 * kEpiW * kStreams; // warp w -> stream w / kEpiW, lane quarter w % 4
 constexpr int kThreads = kEpiThreads + 32 * kStreams;  // + one MMA-issuer warp per stream
@@ -94,13 +117,16 @@ constexpr int kK3 = 64;                     // layer 3 K: b3 (6 values) is added
                                             // paying a fifth >= 45-cycle N = 16 MMA
 constexpr int kColA = 0;                    // packed bf16 A2 (and A3 of the same tile unless kSepA3): 32 columns
 constexpr bool kA3Tmem = kSepA3 && !kA3Smem;
-constexpr int kColA3 = kA3Tmem ? 32 : 0;    // packed bf16 A3
-constexpr int kColD = kA3Tmem ? 64 : 32;    // fp32 accumulator of layers 1 / 2: 64 columns
-constexpr int kColD3 = kColD + 64;          // fp32 accumulator of layer 3: 16 columns (separate, so layer 1
+constexpr int kColA3 = kPP ? 64 : kA3Tmem ? 32 : 0;    // packed bf16 A3
+constexpr int kColD = kPP ? 0 : kA3Tmem ? 64 : 32;     // fp32 accumulator of layer 1 (and 2 unless kPP): 64 columns
+constexpr int kColD2 = kPP ? 64 : kColD;    // fp32 accumulator of layer 2
+constexpr int kColD3 = kPP ? 96 : kColD + 64;  // fp32 accumulator of layer 3: 16 columns (separate, so layer 1
                                             // of the next tile can run while layer 3 still reads A3)
-constexpr int kColsPerStream = kColD3 + 16; // TMEM columns per stream (4 x 112 or 3 x 144 of the 512)
-constexpr int kColConst = kStreams * kColsPerStream;  // shared constant K chunk of A2: (1, 0 x 15) bf16
-static_assert(kColConst + 8 <= 512, "TMEM budget");
+constexpr int kColsPerStream = kPP ? 128 : kColD3 + 16; // TMEM columns per stream (4 x 128, 4 x 112 or 3 x 144 of the 512)
+// Constant K chunk of A2, (1, 0 x 15) bf16: one shared region after the streams, or (kPP) 8 columns
+// after each stream's A2, rewritten by every layer-1 epilogue (layer 1 overwrites X).
+constexpr int kColConst = kPP ? kColA + 32 : kStreams * kColsPerStream;
+static_assert(kPP ? kStreams * kColsPerStream <= 512 : kColConst + 8 <= 512, "TMEM budget");
 
 // Shared-memory image offsets (bytes).
 constexpr int kW1Bytes = kHid * kK1 * 2;   // 2 KB
@@ -226,6 +252,27 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
     else HC_TMEM_LD16(taddr, r);       \
   } while (0)
 
+// kL3Split: the two partial accumulators (16 columns apart) are read and summed.
+#define HC_TMEM_LD_D3S(taddr, r, k)                                                              \
+  do {                                                                                           \
+    if constexpr (kL3Split) {                                                                    \
+      uint32_t r2_[kN3];                                                                         \
+      if ((k) <= 8) {                                                                            \
+        HC_TMEM_LD8(taddr, r);                                                                   \
+        HC_TMEM_LD8((taddr) + kN3, r2_);                                                         \
+      } else {                                                                                   \
+        HC_TMEM_LD16(taddr, r);                                                                  \
+        HC_TMEM_LD16((taddr) + kN3, r2_);                                                        \
+      }                                                                                          \
+      tmem_wait_ld();                                                                            \
+      _Pragma("unroll") for (int j_ = 0; j_ < kN3; ++j_) if (j_ < 8 || (k) > 8)                  \
+          r[j_] = __float_as_uint(__uint_as_float(r[j_]) + __uint_as_float(r2_[j_]));            \
+    } else {                                                                                     \
+      HC_TMEM_LD_D3(taddr, r, k);                                                                \
+      tmem_wait_ld();                                                                            \
+    }                                                                                            \
+  } while (0)
+
 #define HC_TMEM_LD64(taddr, r) \
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];" \
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63]) \
@@ -269,7 +316,7 @@ __device__ __forceinline__ float softplus1(float x) {
 // lane) -> bf16 relu(acc [+ bias]) packed in pairs (element 2j in the low half)
 // -> 32 TMEM columns of the next layer's A operand.
 // kCols accumulator columns starting at tmem_acc -> kCols / 2 packed A columns at tmem_a.
-template <bool kBias, int kCols = 64>
+template <bool kBias, int kCols = 64, bool kConstChunk = false>
 __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem_a, const float* bias) {
 #ifdef HC_MLP_PROBE_NOEPI  // timing probe only: no accumulator read-out (wrong results)
   return;
@@ -308,6 +355,11 @@ __device__ __forceinline__ void epilogue_hidden(uint32_t tmem_acc, uint32_t tmem
 #pragma unroll
   for (int q = 0; q < kQ / 2; ++q) HC_TMEM_ST16(tmem_a + q * 16, pk[q]);
 #endif
+  if constexpr (kConstChunk) {  // K chunk (1, 0 x 15) bf16 after the 32 packed columns
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%2,%2,%2,%2,%2,%2};" ::"r"(tmem_a + kCols / 2),
+                 "r"(0x3F80u), "r"(0u)
+                 : "memory");
+  }
   tmem_wait_st();
 }
 
@@ -377,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (warp < 4) {
+  if (!kPP && warp < 4) {
     // Constant K chunk of every stream's layer-2 A operand: element 64 = 1 (bias b2),
     // 65..79 = 0.  Written once per CTA (warp w: lane quarter w); the fifth layer-2 MMA
     // of all streams reads it.
@@ -393,7 +445,8 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
   __syncthreads();
   tc_fence_after();
   const uint32_t tcol = tmem + st * kColsPerStream;  // stream base, lane 0
-  const uint32_t tA = tcol + kColA, tA3 = tcol + kColA3, tD = tcol + kColD, tD3 = tcol + kColD3, tC = tmem + kColConst;
+  const uint32_t tA = tcol + kColA, tA3 = tcol + kColA3, tD = tcol + kColD, tD2 = tcol + kColD2, tD3 = tcol + kColD3;
+  const uint32_t tC = (kPP ? tcol : tmem) + kColConst;
   const int64_t t0 = static_cast<int64_t>(blockIdx.x) * kStreams + st;
   const int64_t tstride = static_cast<int64_t>(gridDim.x) * kStreams;
   constexpr uint32_t kChunkA = kMlpM * 16;  // K-chunk stride of the 128-row A1 tile
@@ -462,7 +515,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < (kB2Epi ? kHid : kK2) / 16; ++kk)
-        mma_ts_w(tD, kk < kHid / 16 ? tA + kk * 8 : tC, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128),
+        mma_ts_w(tD2, kk < kHid / 16 ? tA + kk * 8 : tC, umma_desc(sW2 + kk * 2 * (kHid * 16), kHid * 16, 128),
                  id64, kk > 0);
       mma_commit_w(bar_l2);
       __syncwarp();
@@ -470,25 +523,35 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
         mbar_wait(bar_l1, ph);  // layer 1 of tile t has read A1
         prepare_a1(tn, iter + 1);
       }
+      if constexpr (kPP) {
+        // Layer 2 has read A2: X is free, layer 1 of the next tile runs under this tile's
+        // layer-2 epilogue.
+        mbar_wait(bar_l2, ph);
+        if (tn < p.ntiles) issue_l1();
+      }
       mbar_wait(bar_a3, ph);  // A3(t) in TMEM, D read out, D3(t - 1) read out
       // D and D3 are separate TMEM regions, so layer 1 of the next tile (D is free, A1 is
       // ready) and layer 3 of this one run back to back.  Dependent MMAs complete in order,
       // ~100 cycles apart after a ~470-cycle first one (tools/mma_latency.cu): with A3 in the
       // A region the epilogue needs layer 3 done before it writes the next A2, so layer 3
       // goes first there.
-      if (!kL3First && tn < p.ntiles) issue_l1();
+      if (!kPP && !kL3First && tn < p.ntiles) issue_l1();
       tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < kK3 / 16; ++kk) {
         if constexpr (kA3Smem)
           mma_ss_w(tD3, umma_desc(smem_u32(A3s) + kk * 2 * (kMlpM * 16), kMlpM * 16, 128),
                    umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
-        else
+        else if constexpr (kL3Split) {
+          const int kc = (kk & 1) * 2 + (kk >> 1);  // K chunks 0, 2, 1, 3: chains (0, 1) and (2, 3) interleaved
+          mma_ts_w(tD3 + (kc >> 1) * kN3, tA3 + kc * 8, umma_desc(sW3 + kc * 2 * (kN3 * 16), kN3 * 16, 128), id16,
+                   kc & 1);
+        } else
           mma_ts_w(tD3, tA3 + kk * 8, umma_desc(sW3 + kk * 2 * (kN3 * 16), kN3 * 16, 128), id16, kk > 0);
       }
       mma_commit_w(bar_l3);
       __syncwarp();
-      if (kL3First && tn < p.ntiles) issue_l1();
+      if (!kPP && kL3First && tn < p.ntiles) issue_l1();
     }
   } else {
     // ------------------------------------------------------------ epilogue warps
@@ -529,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       const int rows = left < kMlpM ? static_cast<int>(left) : kMlpM;
       long long* tr = (p.trace && blockIdx.x == 0 && r == 0 && half == 0 && iter < 32) ? p.trace + (st * 32 + iter) * 8 : nullptr;
       if (tr) tr[0] = clock64();
-      if (!kSepA3 && iter > 0) {  // layer 3 of the previous tile has read A3 (the A region) and written D3
+      if (!kPP && !kSepA3 && iter > 0) {  // layer 3 of the previous tile has read A3 (the A region) and written D3
         mbar_wait(bar_l3, ph ^ 1);
         tc_fence_after();
         if (codes_warp) {
@@ -541,11 +604,19 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       mbar_wait(bar_l1, ph);
       if (tr) tr[2] = clock64();
       tc_fence_after();
-      epilogue_hidden<false, kEpiCols>(tD + lane_off + half * kEpiCols, tA + lane_off + half * (kEpiCols / 2),
-                                       nullptr);  // A2 over A3 of t-1
+      epilogue_hidden<false, kEpiCols, kPP>(tD + lane_off + half * kEpiCols, tA + lane_off + half * (kEpiCols / 2),
+                                            nullptr);  // A2 over A3 of t-1 (kPP: in place over D)
+      if (kPP && iter > 0) {
+        // Layer 2 of this tile overwrites Y: layer 3 of the previous tile must have read A3 and
+        // its accumulator (Y + 32) must be in registers before a2 is signalled.  Layer 3 was
+        // issued a layer-1 wait + epilogue ago, so this wait is short.
+        mbar_wait(bar_l3, ph ^ 1);
+        tc_fence_after();
+        HC_TMEM_LD_D3S(tD3 + lane_off, prev_v, p.k);
+      }
       handoff(bar_a2);
       if (tr) tr[3] = clock64();
-      if (kSepA3 && iter > 0 && codes_warp) {  // layer 3 of the previous tile, read under this tile's layer 2
+      if (!kPP && kSepA3 && iter > 0 && codes_warp) {  // layer 3 of the previous tile, read under this tile's layer 2
         mbar_wait(bar_l3, ph ^ 1);
         tc_fence_after();
         HC_TMEM_LD_D3(tD3 + lane_off, prev_v, p.k);
@@ -557,10 +628,10 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
       if (tr) tr[5] = clock64();
       tc_fence_after();
       if constexpr (kA3Smem)
-        epilogue_hidden_smem<kB2Epi>(tD + lane_off, A3s, r, p.b2);
+        epilogue_hidden_smem<kB2Epi>(tD2 + lane_off, A3s, r, p.b2);
       else
-        epilogue_hidden<kB2Epi, kEpiCols>(tD + lane_off + half * kEpiCols, tA3 + lane_off + half * (kEpiCols / 2),
-                                          p.b2 + half * kEpiCols);  // A3 (over A2 unless kSepA3)
+        epilogue_hidden<kB2Epi, kEpiCols>(tD2 + lane_off + half * kEpiCols, tA3 + lane_off + half * (kEpiCols / 2),
+                                          p.b2 + half * kEpiCols);  // A3 (over A2 unless kSepA3; kPP: in place over D2)
       handoff(bar_a3);
       prev_row0 = row0;
       prev_rows = rows;
@@ -570,8 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1) mlp_kernel(const __grid_constant_
     if (iter > 0 && codes_warp) {  // the last tile's codes
       mbar_wait(bar_l3, (iter - 1) & 1);
       tc_fence_after();
-      HC_TMEM_LD_D3(tD3 + lane_off, prev_v, p.k);
-      tmem_wait_ld();
+      HC_TMEM_LD_D3S(tD3 + lane_off, prev_v, p.k);
       store_codes();
     }
   }
