@@ -579,6 +579,22 @@ struct ShadeSpectralF2Op {
 #ifndef HC_LOSS_CE  // pass 1 specialised per warp group: E as compile-time constant-bank operands
 #define HC_LOSS_CE 0
 #endif
+// Pass 2 on the fp64 tensor-core path (mma.sync m8n8k4), see LossOp::pass2_dmma.  Measured option,
+// off: 36.7-37.2 % of HBM against 53 % for the DFMA form (parity tests green either way) -- DMMA and
+// DFMA share one pipe and a mix of the two runs at ~60 % of either alone (profiles/r02/dmma_probe.txt),
+// and pass 1 stays DFMA (as MMAs its 6-of-8 code padding costs more than its 82 % DFMA rate).
+#ifndef HC_LOSS_DMMA
+#define HC_LOSS_DMMA 0
+#endif
+
+// C (8 x 8, fp64) += A (8 x 4, row) . B (4 x 8, col).  Fragments: A[i = lane / 4][k = lane % 4],
+// B[k = lane % 4][j = lane / 4], C[i = lane / 4][j = 2 (lane % 4) + {0, 1}] (tools/f2f_dfma_probe.cu
+// verifies the layout).  Each product-sum is an IEEE fp64 FMA chain over k.
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
 
 template <int N, int K, int T_, int THREADS_, int STAGES_>
 struct LossOp {
@@ -594,8 +610,13 @@ struct LossOp {
   static constexpr int NOUT = 0;
   __host__ __device__ static constexpr int out_bytes(int) { return 0; }
   static constexpr int KP = (K + 1) / 2 * 2;
-  // [group][2K][T] fp64 partial codes (item fastest: conflict-free 64-bit accesses)
-  static constexpr int kXchg = G > 1 ? G * 2 * K * T * 8 : 0;
+  // Pass 2 as fp64 MMAs (3 warp groups, whole warps of 32 pairs).
+  static constexpr bool kDmma = HC_LOSS_DMMA && !HC_LOSS_WS && !HC_LOSS_CE2 && G == 3 && T % 32 == 0;
+  // Row stride of the exchange buffer: + 4 doubles so the fragment reads (8 pairs x 4 codes per
+  // warp) spread over all banks.
+  static constexpr int TS = kDmma ? T + 4 : T;
+  // [group][2K][TS] fp64 partial codes (item fastest: conflict-free 64-bit accesses)
+  static constexpr int kXchg = G > 1 ? G * 2 * K * TS * 8 : 0;
   static constexpr int kTabD = N * KP * 8;  // D rows [l][KP], fp64
   static constexpr int EXTRA_SMEM = 32 * 8 + kXchg + kTabD;
   static constexpr int kTensorStream = -1;
@@ -690,6 +711,95 @@ struct LossOp {
     return acc;
   }
 
+  // Pass 2 on the fp64 tensor-core path.  The DFMA form needs one D value from shared memory or
+  // the constant bank per DFMA and ran at 34 % of the fp64 peak (profiles/r02/loss_mix_probe.txt);
+  // as MMAs the D rows are register fragments and one instruction does 8 pairs x 8 wavelengths
+  // x 4 codes.  The groups' partial codes go through the exchange buffer as before; each lane
+  // then reads the summed codes of the pairs / code slots of its A fragments
+  // (zp[pair 8m + lane / 4][code 4s + lane % 4]) and forms the products.  The wavelengths are
+  // re-split over the warp groups in 8-wide column tiles (81 -> 4 + 4 + 3 tiles), column
+  // 2c + e of a tile standing for wavelength c + 4e so a lane's two accumulator columns are 4
+  // words apart in the a / b rows (2-way instead of 4-way bank conflicts); the accumulators start
+  // at -a_l b_l (exact: two floats) and end as the residuals r_l = (D zp)_l - a_l b_l
+  // (trainer.cpp:56-71), squared and summed in fp64 per pair.
+  __device__ static void pass2_dmma(const Params& p, State& st, const unsigned char* const* ins,
+                                    unsigned char* extra, int grp, int item, int64_t g, const double* za,
+                                    const double* zb) {
+    constexpr int KS = (K + 3) / 4;          // k steps (4 codes each)
+    constexpr int NT = (N + 7) / 8;          // wavelength tiles
+    constexpr int TPG = (NT + G - 1) / G;    // tiles per warp group
+    double* xchg = reinterpret_cast<double*>(extra + 32 * 8);
+    const double* td = reinterpret_cast<const double*>(extra + 32 * 8 + kXchg);
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      xchg[(grp * 2 * K + j) * TS + item] = za[j];
+      xchg[(grp * 2 * K + K + j) * TS + item] = zb[j];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, fi = lane >> 2, fc = lane & 3;
+    const int pbase = item & ~31;  // the warp's first pair of the tile
+    double af[4][KS];
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+#pragma unroll
+      for (int s = 0; s < KS; ++s) {
+        const int j = 4 * s + fc, pl = pbase + 8 * m + fi;
+        double sa = 0.0, sb = 0.0;
+        if (j < K) {
+#pragma unroll
+          for (int h = 0; h < G; ++h) {  // the order of the DFMA path: group 0 + 1 + 2
+            sa += xchg[(h * 2 * K + j) * TS + pl];
+            sb += xchg[(h * 2 * K + K + j) * TS + pl];
+          }
+        }
+        af[m][s] = sa * sb;  // zp = za (.) zb (codec.cpp:77-85); 0 in the padding slots
+      }
+    const float* arow = reinterpret_cast<const float*>(ins[0]) + (pbase + fi) * N;
+    const float* brow = reinterpret_cast<const float*>(ins[1]) + (pbase + fi) * N;
+    double accm[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int t = 0; t < TPG; ++t) {
+      const int tn = grp * TPG + t;  // warp-uniform
+      if (tn < NT) {
+        const int wb = 8 * tn + (fi >> 1) + 4 * (fi & 1);  // B fragment column fi <-> wavelength
+        double bf[KS];
+#pragma unroll
+        for (int s = 0; s < KS; ++s)
+          bf[s] = (wb < N && 4 * s + fc < K) ? td[wb * KP + 4 * s + fc] : 0.0;
+        const int w0 = 8 * tn + fc, w1 = w0 + 4;  // accumulator columns 2 fc, 2 fc + 1
+        double c0[4], c1[4];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          float a0 = 0.f, b0 = 0.f, a1 = 0.f, b1 = 0.f;
+          if (w0 < N) {
+            a0 = arow[8 * m * N + w0];
+            b0 = brow[8 * m * N + w0];
+          }
+          if (w1 < N) {
+            a1 = arow[8 * m * N + w1];
+            b1 = brow[8 * m * N + w1];
+          }
+          c0[m] = -(static_cast<double>(a0) * static_cast<double>(b0));  // exact
+          c1[m] = -(static_cast<double>(a1) * static_cast<double>(b1));
+        }
+        // k step outer: the four pair blocks' MMAs are independent, a block's next step is 4 MMAs on
+#pragma unroll
+        for (int s = 0; s < KS; ++s)
+#pragma unroll
+          for (int m = 0; m < 4; ++m) dmma884(c0[m], c1[m], af[m][s], bf[s]);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          accm[m] = fma(c0[m], c0[m], accm[m]);
+          accm[m] = fma(c1[m], c1[m], accm[m]);
+        }
+      }
+    }
+    const int64_t g0 = g - item + pbase + fi;  // global index of the lane's first pair
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (g0 + 8 * m < p.pairs) st.acc += accm[m];
+  }
+
   __device__ static void compute(const Params& p, State& st, const unsigned char* const* ins,
                                  unsigned char* const*, unsigned char* extra, int item, int64_t g) {
     // Every thread of the CTA gets here exactly once per tile (tile_generic runs all T
@@ -778,6 +888,10 @@ struct LossOp {
           }
         }
       }
+    }
+    if constexpr (kDmma) {
+      pass2_dmma(p, st, ins, extra, grp, item, g, za, zb);
+      return;
     }
     // exchange the groups' partial codes; zp = za (.) zb (codec.cpp:77-85)
     if constexpr (G > 1) {
