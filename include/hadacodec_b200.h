@@ -424,6 +424,8 @@ typedef struct hc_group_s* hc_group;
 #define HC_GATHER_HOST 0 /* each device copies its band into the host image (own PCIe link) */
 #define HC_GATHER_NCCL 1 /* bands -> device 0 by grouped ncclSend / ncclRecv, one D2H copy */
 #define HC_GATHER_PEER 2 /* bands -> device 0 by cudaMemcpyPeerAsync, one D2H copy */
+#define HC_GATHER_FUSED 3 /* no gather step: each device's shade kernel stores its band straight into
+                           * device 0's frame through NVLink peer memory, one D2H copy */
 /* devices[ndev] (distinct for HC_GATHER_NCCL: ncclCommInitAll); NCCL is loaded at run time
  * (libnccl.so.2) and its absence is HC_EUNSUPPORTED for that mode. */
 int hc_group_create(const int* devices, int ndev, int gather, hc_group* out);

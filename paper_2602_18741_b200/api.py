@@ -432,7 +432,7 @@ class Codec:
                                                                         for a in (Z, S2, xyz, rgb)]))
 
 
-GATHER_MODES = {"host": 0, "nccl": 1, "peer": 2}
+GATHER_MODES = {"host": 0, "nccl": 1, "peer": 2, "fused": 3}
 
 
 class Group:

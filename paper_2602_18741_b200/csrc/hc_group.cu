@@ -12,7 +12,13 @@
 //                   one grouped ncclSend / ncclRecv per band over NVLink (NCCL has no Gather;
 //                   communicators from ncclCommInitAll), then copied to the host once;
 //   HC_GATHER_PEER  the same gather with cudaMemcpyPeerAsync (no NCCL; also valid when a
-//                   device appears twice, which the single-GPU tests use).
+//                   device appears twice, which the single-GPU tests use);
+//   HC_GATHER_FUSED no gather step at all: every device's shade kernel stores its band of
+//                   XYZ / sRGB straight into the first device's full-frame buffer through
+//                   NVLink peer memory (the kernel's bulk-copy stores take a peer address),
+//                   so the transfer rides under the band's compute tile by tile; one D2H
+//                   copy of the assembled frame follows.  Needs peer access from every
+//                   device to the first (HC_EUNSUPPORTED otherwise).
 // NCCL is loaded at run time (dlopen "libnccl.so.2": the copy PyTorch already loaded, else
 // the system one); HC_GATHER_NCCL fails with HC_EUNSUPPORTED when it is absent or the
 // devices are not distinct.
@@ -184,8 +190,9 @@ int hc_row_band(int rank, int world, int64_t height, int64_t* row0, int64_t* row
 
 int hc_group_create(const int* devices, int ndev, int gather, hc_group* out) {
   HC_REQUIRE(devices && ndev >= 1 && out, HC_EINVAL, "group: bad device list");
-  HC_REQUIRE(gather == HC_GATHER_HOST || gather == HC_GATHER_NCCL || gather == HC_GATHER_PEER, HC_EINVAL,
-             "group: unknown gather mode");
+  HC_REQUIRE(gather == HC_GATHER_HOST || gather == HC_GATHER_NCCL || gather == HC_GATHER_PEER ||
+                 gather == HC_GATHER_FUSED,
+             HC_EINVAL, "group: unknown gather mode");
   if (gather == HC_GATHER_NCCL) {
     if (!nccl().ok) return set_error(HC_EUNSUPPORTED, "group: " + nccl().why);
     for (int i = 0; i < ndev; ++i)
@@ -220,6 +227,24 @@ int hc_group_create(const int* devices, int ndev, int gather, hc_group* out) {
           cudaSetDevice(devices[0]);
           cudaDeviceEnablePeerAccess(devices[d], 0);
           cudaGetLastError();  // already enabled is fine
+        }
+      }
+  }
+  if (gather == HC_GATHER_FUSED) {  // every device's kernels store into the first device's memory
+    for (int d = 1; d < ndev; ++d)
+      if (devices[d] != devices[0]) {
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, devices[d], devices[0]);
+        if (!can) {
+          hc_group_destroy(g.release());
+          return set_error(HC_EUNSUPPORTED, "group: HC_GATHER_FUSED needs peer access to the first device");
+        }
+        cudaSetDevice(devices[d]);
+        const cudaError_t e = cudaDeviceEnablePeerAccess(devices[0], 0);
+        cudaGetLastError();
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+          hc_group_destroy(g.release());
+          return cuda_error(e, "cudaDeviceEnablePeerAccess");
         }
       }
   }
@@ -304,14 +329,15 @@ int hc_group_shade_latent_host(hc_group g, const float* pal_codes, int n_pal, co
   }
   const size_t pal_b = up(sizeof(float) * n_pal * k);
   auto in_bytes = [&](int64_t P) { return pal_b + up(sizeof(uint32_t) * P) + up(sizeof(float) * P * L); };
-  for (int d = 0; d < nd; ++d) {  // device 0: full-frame outputs; others: their band's
-    const int64_t outP = d == 0 ? Pall : max_band;
+  const bool fused = g->gather == HC_GATHER_FUSED;
+  for (int d = 0; d < nd; ++d) {  // device 0: full-frame outputs; others: their band's (none when fused)
+    const int64_t outP = d == 0 ? Pall : fused ? 0 : max_band;
     const int rc = ensure_buf(g, d, in_bytes(max_band) + 2 * up(sizeof(float) * outP * 3));
     if (rc != HC_OK) return rc;
   }
   auto layout = [&](int d, float*& d_pal, uint32_t*& d_idx, float*& d_cos, float*& d_xyz, float*& d_rgb) {
     char* b = static_cast<char*>(g->buf[d]);
-    const int64_t outP = d == 0 ? Pall : max_band;
+    const int64_t outP = d == 0 ? Pall : fused ? 0 : max_band;
     d_pal = reinterpret_cast<float*>(b);
     d_idx = reinterpret_cast<uint32_t*>(b + pal_b);
     d_cos = reinterpret_cast<float*>(b + pal_b + up(sizeof(uint32_t) * max_band));
@@ -327,6 +353,13 @@ int hc_group_shade_latent_host(hc_group g, const float* pal_codes, int n_pal, co
     float *d_pal, *d_cos, *d_xyz, *d_rgb;
     uint32_t* d_idx;
     layout(d, d_pal, d_idx, d_cos, d_xyz, d_rgb);
+    if (fused && d > 0) {  // this band's slice of the first device's frame (peer memory)
+      float *x0, *g0, *unused_p, *unused_c;
+      uint32_t* unused_i;
+      layout(0, unused_p, unused_i, unused_c, x0, g0);
+      d_xyz = x0 + p0 * 3;
+      d_rgb = g0 + p0 * 3;
+    }
     // device 0 shades straight into its slice of the full frame (its band starts at row 0)
     HC_CUDA_TRY(cudaMemcpyAsync(d_pal, pal_codes, sizeof(float) * n_pal * k, cudaMemcpyHostToDevice, s));
     HC_CUDA_TRY(cudaMemcpyAsync(d_idx, idx + p0, sizeof(uint32_t) * P, cudaMemcpyHostToDevice, s));
@@ -356,7 +389,7 @@ int hc_group_shade_latent_host(hc_group g, const float* pal_codes, int n_pal, co
       const ncclResult_t e2 = N.GroupEnd();
       if (e != ncclSuccess) return nccl_error(e, "ncclSend/ncclRecv");
       if (e2 != ncclSuccess) return nccl_error(e2, "ncclGroupEnd");
-    } else if (d > 0) {  // PEER
+    } else if (d > 0 && !fused) {  // PEER
       float *x0, *g0, *unused_p, *unused_c;
       uint32_t* unused_i;
       layout(0, unused_p, unused_i, unused_c, x0, g0);

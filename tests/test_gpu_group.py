@@ -44,7 +44,8 @@ def reference_frame(api):
 
 
 @pytest.mark.parametrize("devices,gather", [([0], "host"), ([0], "peer"), ([0], "nccl"), ([0, 0], "host"),
-                                            ([0, 0], "peer"), ([0, 0, 0], "peer")])
+                                            ([0, 0], "peer"), ([0, 0, 0], "peer"), ([0], "fused"),
+                                            ([0, 0], "fused"), ([0, 0, 0, 0, 0], "fused")])
 def test_group_matches_single_context(api, reference_frame, devices, gather):
     E, D, pc, lc, idx, cosv, xyz_ref, rgb_ref = reference_frame
     g = api.Group(devices, gather)
