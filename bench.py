@@ -685,10 +685,15 @@ class Workload:
 
 
 class StepReplayer:
-    """Replays exactly n steps of a workload: CUDA graphs of one full buffer rotation
-    (R steps) plus a graph of the remainder, so any --steps is honoured exactly.
+    """Replays exactly n steps of a workload from CUDA graphs, so any --steps is honoured
+    exactly: up to MAX_NODES steps are one graph of exactly n steps (the buffer rotation runs
+    through it, and every launch overlaps its predecessor's tail by programmatic dependent
+    launch -- at 22 us per step the gap between two graph launches is visible); longer runs
+    replay a chunk graph (a whole number of buffer rotations) plus one graph of the remainder.
     Configs whose step cannot be captured (host-side setup / synchronisation inside the
     call) run the steps as plain library calls."""
+
+    MAX_NODES = 512
 
     def __init__(self, torch, wl, warmup: int, stream, max_steps: int):
         self.torch, self.wl, self.stream = torch, wl, stream
@@ -703,10 +708,10 @@ class StepReplayer:
             wl.step(0)
             torch.cuda.synchronize()
             self.per_step = ctx.launches - l0
-        self.full = None
-        self.rem = {}
+        self.graphs = {}
+        self.chunk = max(R, self.MAX_NODES // max(1, self.per_step) // R * R)  # steps per chunk graph
         if self.graph:
-            self.full = self._capture(R)
+            self.prepare(R)
 
     def _capture(self, n: int):
         torch = self.torch
@@ -719,10 +724,22 @@ class StepReplayer:
         torch.cuda.synchronize()
         return g
 
+    def _parts(self, n: int):
+        """(graph size, replays) pairs that add up to exactly n steps."""
+        if n <= self.chunk:
+            return [(n, 1)] if n else []
+        parts = [(self.chunk, n // self.chunk)]
+        if n % self.chunk:
+            parts.append((n % self.chunk, 1))
+        return parts
+
     def prepare(self, n: int) -> None:
-        """Capture the remainder graph for n steps (outside any timed region)."""
-        if self.graph and n % self.wl.R and (n % self.wl.R) not in self.rem:
-            self.rem[n % self.wl.R] = self._capture(n % self.wl.R)
+        """Capture the graphs n steps need (outside any timed region)."""
+        if not self.graph:
+            return
+        for size, _ in self._parts(n):
+            if size not in self.graphs:
+                self.graphs[size] = self._capture(size)
 
     def run(self, n: int) -> None:
         """Issue exactly n steps on the stream (no synchronisation)."""
@@ -730,13 +747,10 @@ class StepReplayer:
             for i in range(n):
                 self.wl.step(i)
             return
-        R = self.wl.R
-        if n % R and (n % R) not in self.rem:
-            self.prepare(n)  # (timed callers prepare beforehand)
-        for _ in range(n // R):
-            self.full.replay()
-        if n % R:
-            self.rem[n % R].replay()
+        self.prepare(n)  # (timed callers prepare beforehand; a no-op then)
+        for size, reps in self._parts(n):
+            for _ in range(reps):
+                self.graphs[size].replay()
 
 
 def C_int64():
@@ -769,6 +783,11 @@ def time_steps(torch, dist, world: int, rep: StepReplayer, steps: int, stream, c
     with cm:
         w0 = time.perf_counter()
         with torch.cuda.stream(stream):
+            if rep.graph:
+                # A ~200 us spin kernel ahead of the start event: the device is still busy while the
+                # host enqueues the graph, so the event interval starts when the first step can start
+                # instead of containing the host's graph-launch latency (visible at --steps 20).
+                torch.cuda._sleep(400_000)
             e0.record(stream)
             rep.run(steps)
             e1.record(stream)
@@ -1121,8 +1140,11 @@ def run_ours(args) -> int:
             "method": {
                 "l2": (f"{R} rotating input/output buffer sets ({'each' if R == 1 else 'rotation'} > 2x 126 MB L2)"
                        if cfg.get("graph", True) else "compute-bound step (no L2 rotation needed)"),
-                "timing": ("CUDA graphs (one buffer rotation + the remainder) replaying exactly K steps; CUDA "
-                           "events on the launching stream; max over ranks" if cfg.get("graph", True) else
+                "timing": ("CUDA graphs (one graph of exactly K steps up to 512 launches, else chunk graphs + the "
+                           "remainder) replaying exactly K steps; CUDA "
+                           "events on the launching stream, the start event queued behind a 200 us spin kernel so "
+                           "the host's graph-launch latency is outside the interval; max over ranks"
+                           if cfg.get("graph", True) else
                            "K library calls (host-side setup included); CUDA events; max over ranks"),
                 "parallelism": (f"row bands, {args.scaling} scaling, {world} rank(s), one process per GPU, "
                                 "no data-path collective")},
