@@ -1057,6 +1057,45 @@ def run_ours(args) -> int:
         extra["with_gather"] = {"value": wl.units * world * gsteps / (gms / 1e3) / 1e6, "unit": cfg["unit"],
                                 "ms_per_step": gms / gsteps,
                                 "gathered": "linear-sRGB row bands -> rank 0 (sharding.gather_rows, NCCL)"}
+        if args.gather == "fused" and args.config == "2":
+            # Opt-in: no gather step -- every rank's shade kernel stores its sRGB band straight into
+            # rank 0's frame through NVLink peer memory (sharding.PeerFrame, CUDA IPC mapping); one
+            # frame per buffer-rotation slot.  Not the default: this run has one GPU, so the path is
+            # covered by the two-process test on one device only (tests/test_gpu_group.py).
+            from paper_2602_18741_b200.sharding import PeerFrame
+
+            rows_all = H * world if not strong else H
+            frames = [PeerFrame(band, rows_all, device=dev) for _ in range(R)]
+
+            def fused_step(i):
+                idx, cosv, outs = wl.sets[i % R]
+                wl.codec.shade_latent(wl.pal_codes, wl.light_codes, idx, cosv,
+                                      out={**outs, "rgb": frames[i % R].local})
+
+            with torch.cuda.stream(stream):
+                for i in range(R):
+                    fused_step(i)
+            dist.barrier()
+            torch.cuda.synchronize()
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+                for i in range(gsteps):
+                    fused_step(i)
+                e1.record(stream)
+            torch.cuda.synchronize()
+            dist.barrier()
+            fms = _max_over_ranks(torch, dist, world, e0.elapsed_time(e1))
+            ok = True
+            if rank == 0:  # rank 0's own band of the last frame equals its device-buffer result
+                last = (gsteps - 1) % R
+                ok = bool(torch.equal(frames[last].local, wl.sets[last][-1]["rgb"]))
+            extra["with_gather_fused"] = {
+                "value": wl.units * world * gsteps / (fms / 1e3) / 1e6, "unit": cfg["unit"],
+                "ms_per_step": fms / gsteps, "rank0_band_matches": ok,
+                "gathered": "each rank's shade kernel stores its sRGB band into rank 0's frame through peer "
+                            "memory (sharding.PeerFrame: CUDA IPC mapping, no gather step, plain launches)"}
+            for f in frames:
+                f.close()
 
     # ---- e2e through the host-buffer C-ABI call (config 2)
     e2e = None
@@ -1382,6 +1421,9 @@ def main(argv=None) -> int:
     ap.add_argument("--config", choices=sorted(CONFIGS), default="2")
     ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
                     help="weak: one frame per GPU (default); strong: one frame split into row bands")
+    ap.add_argument("--gather", choices=("nccl", "fused"), default="nccl",
+                    help="N > 1: 'fused' adds a with_gather_fused record (bands stored straight into rank 0's "
+                         "frame through peer memory) next to the NCCL gather")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-naive", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)

@@ -443,6 +443,18 @@ int hc_group_shade_latent_host(hc_group g, const float* pal_codes, int n_pal, co
                                const uint32_t* idx, const float* cosv, int64_t width, int64_t height, float* xyz,
                                float* rgb);
 
+/* One process per GPU (torch.distributed / MPI ranks): the fused gather across processes.  The
+ * destination rank allocates the full frame with hc_ipc_alloc and publishes the 64-byte handle
+ * (CUDA IPC); every other rank maps it with hc_ipc_open (peer access from its own device is
+ * enabled by the mapping) and passes its band's slice as the output pointer of hc_shade_latent,
+ * so its kernels store straight into the destination GPU's frame over NVLink.  hc_ipc_close
+ * unmaps (openers), hc_ipc_free releases (owner). */
+#define HC_IPC_HANDLE_BYTES 64
+int hc_ipc_alloc(int device, int64_t bytes, void** dptr, unsigned char* handle);
+int hc_ipc_open(int device, const unsigned char* handle, void** dptr);
+int hc_ipc_close(int device, void* dptr);
+int hc_ipc_free(int device, void* dptr);
+
 #ifdef __cplusplus
 }
 #endif

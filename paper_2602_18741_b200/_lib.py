@@ -54,6 +54,10 @@ SIGNATURES: dict[str, tuple] = {
     "hc_group_nccl_version": (i32, []),
     "hc_group_codec_create": (i32, [vp, i32, i32, vp, vp, vp, f64]),
     "hc_group_shade_latent_host": (i32, [vp, vp, i32, vp, i32, vp, vp, i64, i64, vp, vp]),
+    "hc_ipc_alloc": (i32, [i32, i64, C.POINTER(vp), vp]),
+    "hc_ipc_open": (i32, [i32, vp, C.POINTER(vp)]),
+    "hc_ipc_close": (i32, [i32, vp]),
+    "hc_ipc_free": (i32, [i32, vp]),
     "hc_exposure_for": (i32, [vp, vp, i64, i32, f64, C.POINTER(f64)]),
     "hc_tonemap_srgb8": (i32, [vp, vp, i64, f64, vp]),
     "hc_error_map": (i32, [vp, vp, i32, vp, i32, i64, vp, C.POINTER(f64)]),

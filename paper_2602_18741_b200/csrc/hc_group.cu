@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <condition_variable>
+#include <cstring>
 #include <memory>
 #include <functional>
 #include <mutex>
@@ -414,6 +415,53 @@ int hc_group_shade_latent_host(hc_group g, const float* pal_codes, int n_pal, co
         return HC_OK;
       },
       {0});
+}
+
+// ------------------------------------------------------------------ CUDA IPC frames
+// One process per GPU: the destination rank's frame mapped into every rank, so each rank's
+// shade kernel stores its band straight into it (the fused gather of hc_group, across
+// processes).
+static_assert(sizeof(cudaIpcMemHandle_t) == HC_IPC_HANDLE_BYTES, "CUDA IPC handle size");
+
+int hc_ipc_alloc(int device, int64_t bytes, void** dptr, unsigned char* handle) {
+  HC_REQUIRE(dptr && handle && bytes > 0, HC_EINVAL, "ipc_alloc: bad arguments");
+  HC_CUDA_TRY(cudaSetDevice(device));
+  void* p = nullptr;
+  HC_CUDA_TRY(cudaMalloc(&p, static_cast<size_t>(bytes)));
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, p);
+  if (e != cudaSuccess) {
+    cudaFree(p);
+    return cuda_error(e, "cudaIpcGetMemHandle");
+  }
+  std::memcpy(handle, &h, sizeof(h));
+  *dptr = p;
+  return HC_OK;
+}
+
+int hc_ipc_open(int device, const unsigned char* handle, void** dptr) {
+  HC_REQUIRE(dptr && handle, HC_EINVAL, "ipc_open: bad arguments");
+  HC_CUDA_TRY(cudaSetDevice(device));  // the device whose kernels will store into the frame
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  HC_CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *dptr = p;
+  return HC_OK;
+}
+
+int hc_ipc_close(int device, void* dptr) {
+  if (!dptr) return HC_OK;
+  HC_CUDA_TRY(cudaSetDevice(device));
+  HC_CUDA_TRY(cudaIpcCloseMemHandle(dptr));
+  return HC_OK;
+}
+
+int hc_ipc_free(int device, void* dptr) {
+  if (!dptr) return HC_OK;
+  HC_CUDA_TRY(cudaSetDevice(device));
+  HC_CUDA_TRY(cudaFree(dptr));
+  return HC_OK;
 }
 
 }  // extern "C"

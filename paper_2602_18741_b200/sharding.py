@@ -6,7 +6,9 @@ rank; each rank generates its own band of inputs from GLOBAL element indices
 (counter streams, so values do not depend on the number of ranks), shades it on
 its GPU, and — only when the caller wants the image on one rank — the linear-sRGB
 (or XYZ) bands are gathered to rank 0 with one collective (NCCL over NVLink on
-the B200 box, gloo in the CPU tests).  Nothing else crosses a GPU boundary.
+the B200 box, gloo in the CPU tests), or not gathered at all: with a `PeerFrame` every
+rank's shade kernel stores its band straight into rank 0's frame through NVLink peer memory
+(CUDA IPC mapping), so compute and gather are one kernel.  Nothing else crosses a GPU boundary.
 """
 from __future__ import annotations
 
@@ -74,3 +76,59 @@ def gather_rows(local: torch.Tensor, band: Band, height: int, dst: int = 0) -> t
         b = row_band(r, world, height, band.width)
         out.append(parts[r][: b.pixels])
     return torch.cat(out, dim=0)
+
+
+class _DevicePointer:
+    """A raw device pointer as a __cuda_array_interface__ object (float32, C-contiguous)."""
+
+    def __init__(self, ptr: int, shape: tuple):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<f4", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+class PeerFrame:
+    """The [height * width, channels] float32 image on rank `dst`'s GPU, mapped into every rank.
+
+    `dst` allocates the frame (hc_ipc_alloc) and broadcasts its CUDA IPC handle; the other ranks map
+    it (hc_ipc_open enables peer access from their own device).  `local` is this rank's band of rows
+    as a CUDA tensor — peer memory on every rank but `dst` — to be passed as the `out=` tensor of
+    `Codec.shade_latent`, whose kernel then stores the band straight into `dst`'s frame over NVLink:
+    no gather step, no staging copy.  After a `dist.barrier()` that follows every rank's stream
+    synchronisation, `image` (on `dst`) holds the assembled frame.  Works with any backend that can
+    broadcast a Python object (NCCL on the GPU box; gloo in the one-GPU two-process test)."""
+
+    def __init__(self, band: Band, height: int, channels: int = 3, device: int | None = None, dst: int = 0):
+        import ctypes as C
+
+        from . import _lib
+
+        self.band, self.height, self.channels, self.dst = band, height, channels, dst
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.owner = band.rank == dst
+        nbytes = height * band.width * channels * 4
+        ptr = C.c_void_p()
+        handle = (C.c_ubyte * 64)()
+        if self.owner:
+            _lib.check(_lib.lib().hc_ipc_alloc(self.device, nbytes, C.byref(ptr), handle))
+        box = [bytes(handle) if self.owner else None]
+        if band.world > 1:
+            dist.broadcast_object_list(box, src=dst)
+        if not self.owner:
+            handle = (C.c_ubyte * 64).from_buffer_copy(box[0])
+            _lib.check(_lib.lib().hc_ipc_open(self.device, handle, C.byref(ptr)))
+        self.ptr = ptr.value
+        px = height * band.width
+        # the pointer belongs to dst's device; torch only needs a CUDA tensor around it
+        self.image = torch.as_tensor(_DevicePointer(self.ptr, (px, channels)), device="cuda")
+        self.local = self.image[band.first_pixel:band.first_pixel + band.pixels]
+
+    def close(self) -> None:
+        from . import _lib
+
+        if getattr(self, "ptr", None):
+            self.image = self.local = None
+            if self.owner:
+                _lib.check(_lib.lib().hc_ipc_free(self.device, self.ptr))
+            else:
+                _lib.check(_lib.lib().hc_ipc_close(self.device, self.ptr))
+            self.ptr = None

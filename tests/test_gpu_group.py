@@ -95,6 +95,59 @@ def _rank(rank: int, world: int, port: int, out_path: str):
     dist.destroy_process_group()
 
 
+def _rank_fused(rank: int, world: int, port: int, out_path: str):
+    """The fused gather across processes: every rank's kernel stores its band into rank 0's frame
+    (CUDA IPC mapping; on this one-GPU box both ranks use cuda:0, on a node each its own GPU)."""
+    import torch.distributed as dist
+
+    from paper_2602_18741_b200 import api as a
+    from paper_2602_18741_b200.sharding import PeerFrame, row_band
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    ctx = a.Context(0)
+    E, D = synth.codec_weights(SEED, K, 81)
+    codec = a.Codec(ctx, E, D)
+    pal = codec.encode(torch.from_numpy(synth.palette(SEED, 256, 81)).cuda())
+    lc = codec.encode(torch.from_numpy(synth.lights(SEED, L, 81)).cuda()).cpu().numpy()
+    band = row_band(rank, world, H, W)
+    idx, cosv = a.synth_gbuffer(ctx, SEED, band.first_pixel, band.pixels, L, 256)
+    rgb, xyz = PeerFrame(band, H, device=0), PeerFrame(band, H, device=0)
+    if rank == 0:
+        rgb.image.fill_(-1.0)
+        xyz.image.fill_(-1.0)
+        torch.cuda.synchronize()
+    dist.barrier()
+    for _ in range(3):  # repeated frames into the same mapping
+        codec.shade_latent(pal, lc, idx, cosv, out={"latent": None, "spectra": None, "xyz": xyz.local,
+                                                    "rgb": rgb.local})
+    torch.cuda.synchronize()
+    dist.barrier()  # every rank's stores are complete
+    if rank == 0:
+        np.save(out_path, np.concatenate([rgb.image.cpu().numpy(), xyz.image.cpu().numpy()], axis=1))
+    dist.barrier()
+    rgb.close()
+    xyz.close()
+    dist.destroy_process_group()
+
+
+def test_two_ranks_fused_gather_through_peer_memory(api, tmp_path):
+    import torch.multiprocessing as mp
+
+    out = str(tmp_path / "fused.npy")
+    mp.spawn(_rank_fused, args=(2, _free_port(), out), nprocs=2, join=True)
+    ctx = api.Context(0)
+    E, D = synth.codec_weights(SEED, K, 81)
+    codec = api.Codec(ctx, E, D)
+    pal = codec.encode(torch.from_numpy(synth.palette(SEED, 256, 81)).cuda())
+    lc = codec.encode(torch.from_numpy(synth.lights(SEED, L, 81)).cuda()).cpu().numpy()
+    idx, cosv = api.synth_gbuffer(ctx, SEED, 0, W * H, L, 256)
+    want = codec.shade_latent(pal, lc, idx, cosv)
+    got = np.load(out)
+    assert np.array_equal(got[:, :3], want["rgb"].cpu().numpy())
+    assert np.array_equal(got[:, 3:], want["xyz"].cpu().numpy())
+
+
 def test_two_ranks_on_the_gpu_match_one_process(api, tmp_path):
     import torch.multiprocessing as mp
 
