@@ -555,8 +555,9 @@ int hc_hadamard_loss(hc_codec c, const float* A, const float* B, int64_t pairs, 
 // and chunk i-2's D2H overlap, and stream order alone orders each slot's reuse.
 // Measured on the B200 host (tools/e2e_sweep.sh): 256K-pixel chunks
 // balance the ~4 us per-copy cost against pipeline fill / drain; role streams (all H2D
-// on one stream, all D2H on another), a ramped chunk schedule and letting the kernel
-// write pinned outputs over PCIe (zero copy) all measured slower.  With several frames
+// on one stream, all D2H on another), a ramped chunk schedule, letting the kernel
+// write pinned outputs over PCIe (zero copy) and letting its bulk loads read the pinned
+// inputs over PCIe (1.08-1.16 against 1.34 Gpix/s, any chunk size) all measured slower.  With several frames
 // per call the pipeline does not drain between frames: frame f + 1's first uploads
 // run under frame f's last downloads.
 int hc_shade_latent_host_frames(hc_codec c, const float* pal_codes, int n_pal, const float* light_codes, int L,
