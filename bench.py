@@ -697,6 +697,9 @@ class StepReplayer:
 
     def __init__(self, torch, wl, warmup: int, stream, max_steps: int):
         self.torch, self.wl, self.stream = torch, wl, stream
+        from paper_2602_18741_b200 import api as _api
+
+        self.api = _api
         self.graph = wl.cfg.get("graph", True)
         R = wl.R
         ctx = wl.codec.ctx
@@ -787,7 +790,7 @@ def time_steps(torch, dist, world: int, rep: StepReplayer, steps: int, stream, c
                 # A ~200 us spin kernel ahead of the start event: the device is still busy while the
                 # host enqueues the graph, so the event interval starts when the first step can start
                 # instead of containing the host's graph-launch latency (visible at --steps 20).
-                torch.cuda._sleep(400_000)
+                rep.api.spin(rep.wl.codec.ctx, 400_000)
             e0.record(stream)
             rep.run(steps)
             e1.record(stream)

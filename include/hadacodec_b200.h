@@ -412,6 +412,10 @@ int hc_synth_chain(hc_ctx ctx, uint64_t key_pidx, uint64_t key_iidx, uint64_t ke
 int hc_synth_uniform(hc_ctx ctx, uint64_t key, int64_t first, int64_t count, float* out);
 /* Write `bytes` of garbage over a device buffer (L2 flush between timed steps). */
 int hc_flush_l2(hc_ctx ctx, void* buf, int64_t bytes);
+/* Keep the context's stream busy for `cycles` SM clocks (one spinning thread).  Measurement helper:
+ * a start event queued behind it is stamped when the work after it can start, not while the
+ * host is still enqueuing that work. */
+int hc_spin(hc_ctx ctx, int64_t cycles);
 
 /* ------------------------------------------------------------------ several GPUs
  * Replaces the renderer's row-scheduled thread pool (renderer.cpp:573-608,

@@ -97,6 +97,7 @@ SIGNATURES: dict[str, tuple] = {
     "hc_synth_chain": (i32, [vp, u64, u64, u64, i64, i64, i32, i32, i32, vp, vp, vp]),
     "hc_synth_uniform": (i32, [vp, u64, i64, i64, vp]),
     "hc_flush_l2": (i32, [vp, vp, i64]),
+    "hc_spin": (i32, [vp, i64]),
 }
 
 _lib = None

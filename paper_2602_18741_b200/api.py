@@ -1250,6 +1250,12 @@ def synth_uniform(ctx: Context, seed: int, purpose: str, first: int, count: int)
     return out
 
 
+def spin(ctx: Context, cycles: int) -> None:
+    """Keep the bound stream busy for `cycles` SM clocks (measurement helper, hc_spin)."""
+    ctx.bind_stream()
+    _check(_lib.lib().hc_spin(ctx.h, int(cycles)))
+
+
 def flush_l2(ctx: Context, buf: torch.Tensor) -> None:
     ctx.bind_stream()
     _check(_lib.lib().hc_flush_l2(ctx.h, _p(buf), buf.numel() * buf.element_size()))

@@ -170,6 +170,13 @@ __global__ void uniform_kernel(uint64_t key, int64_t first, int64_t count, float
     out[i] = u24(ctr_u64(key, static_cast<uint64_t>(first + i)));
 }
 
+// One thread that returns after `cycles` SM clocks (measurement helper, see hc_spin).
+__global__ void spin_kernel(long long cycles) {
+  const long long t0 = clock64();
+  while (clock64() - t0 < cycles) {
+  }
+}
+
 __global__ void flush_kernel(uint4* buf, int64_t n16, uint32_t salt) {
   const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n16; i += stride)
@@ -705,6 +712,13 @@ int hc_synth_uniform(hc_ctx ctx, uint64_t key, int64_t first, int64_t count, flo
   if (count == 0) return HC_OK;
   uniform_kernel<<<grid_for(ctx, count), 256, 0, ctx->stream>>>(key, first, count, out);
   HC_CHECK_LAUNCH(ctx, "uniform_kernel");
+  return HC_OK;
+}
+
+int hc_spin(hc_ctx ctx, int64_t cycles) {
+  HC_REQUIRE(ctx && cycles >= 0, HC_EINVAL, "spin: bad argument");
+  spin_kernel<<<1, 1, 0, ctx->stream>>>(cycles);
+  HC_CHECK_LAUNCH(ctx, "spin_kernel");
   return HC_OK;
 }
 
