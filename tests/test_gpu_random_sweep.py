@@ -1,0 +1,133 @@
+"""Seeded random sweep of the shading / codec entry points against the oracle: grid, code size,
+light count, palette size, row count, which outputs are requested and whether the inputs and
+outputs sit at 16-byte-aligned or 4-byte-offset addresses are all drawn at random, so the
+combinations the hand-written parity cases do not name (generic light counts with partial
+outputs, small palettes on the bulk-copy path, offset inputs with aligned outputs, ...) are hit
+too.  Same tolerance as test_gpu_parity.py (1e-5 relative, row-infinity-norm denominator)."""
+import numpy as np
+import pytest
+
+from conftest import rel_err
+from paper_2602_18741_b200 import synth
+from paper_2602_18741_b200.colorimetry import cmf_matrix, grid
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+CASES = 48
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2602_18741_b200 import api as a
+
+    return a
+
+
+@pytest.fixture(scope="module")
+def ctx(api):
+    return api.Context(0)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def _place(t: torch.Tensor, offset: int) -> torch.Tensor:
+    """The same values at `offset` elements past an aligned allocation (a contiguous view)."""
+    if offset == 0:
+        return t
+    flat = torch.empty(t.numel() + 16, dtype=t.dtype, device=t.device)
+    v = flat[offset:offset + t.numel()].view(t.shape)
+    v.copy_(t)
+    return v
+
+
+def _out(rows: int, width: int, offset: int) -> torch.Tensor:
+    flat = torch.full((rows * width + 16,), float("nan"), dtype=torch.float32, device="cuda")
+    return flat[offset:offset + rows * width].view(rows, width)
+
+
+def _draw(rng):
+    n = int(rng.choice([81, 81, 47]))
+    k = int(rng.choice([3, 6, 9]))
+    L = int(rng.choice([1, 2, 5, 8, 8, 13, 32, 32, 64]))
+    n_pal = int(rng.choice([1, 7, 100, 256, 256]))
+    P = int(rng.choice([1, 31, 64, 255, 256, 257, 1000, 4097, 12_289]))
+    return n, k, L, n_pal, P
+
+
+@pytest.mark.parametrize("case", range(CASES))
+def test_random_shade_latent(api, ctx, orc, case):
+    rng = np.random.default_rng(1000 + case)
+    n, k, L, n_pal, P = _draw(rng)
+    E, D = synth.codec_weights(77 + case, k, n)
+    codec = api.Codec(ctx, E, D)
+    pal = synth.palette(77 + case, n_pal, n)
+    lts = synth.lights(77 + case, L, n)
+    pal_codes = codec.encode(torch.from_numpy(pal).cuda())
+    light_codes = codec.encode(torch.from_numpy(lts).cuda()).cpu().numpy()
+    idx, cosv = api.synth_gbuffer(ctx, 77 + case, int(rng.integers(0, 1 << 20)), P, L, n_pal)
+    off_in, off_out = int(rng.choice([0, 0, 1, 3])), int(rng.choice([0, 0, 1, 2]))
+    want = {key: bool(rng.integers(0, 2)) for key in ("latent", "spectra", "xyz", "rgb")}
+    if not any(want.values()):
+        want["rgb"] = True
+    widths = {"latent": k, "spectra": n, "xyz": 3, "rgb": 3}
+    out = {key: _out(P, widths[key], off_out) if want[key] else None for key in widths}
+    codec.shade_latent(_place(pal_codes, off_in), light_codes, _place(idx, off_in), _place(cosv, off_in), out=out)
+    ref = [np.zeros((P, widths[key]), np.float32) for key in ("latent", "spectra", "xyz", "rgb")]
+    orc.orc_shade_latent(D, k, n, cmf_matrix(n), grid(n)[1], host(pal_codes), light_codes, L,
+                         host(idx).view(np.uint32), host(cosv), P, *ref)
+    tag = f"case {case}: n={n} k={k} L={L} n_pal={n_pal} P={P} in+{off_in} out+{off_out}"
+    for key, r in zip(("latent", "spectra", "xyz", "rgb"), ref):
+        if want[key]:
+            e = rel_err(host(out[key]), r)
+            assert e <= TOL, f"{tag} {key}: rel err {e:.3e}"
+
+
+@pytest.mark.parametrize("case", range(CASES // 2))
+def test_random_shade_spectral(api, ctx, orc, case):
+    rng = np.random.default_rng(5000 + case)
+    n, _, L, n_pal, P = _draw(rng)
+    E, D = synth.codec_weights(177 + case, 6, n)
+    codec = api.Codec(ctx, E, D)
+    pal = synth.palette(177 + case, n_pal, n)
+    lts = synth.lights(177 + case, L, n)
+    idx, cosv = api.synth_gbuffer(ctx, 177 + case, int(rng.integers(0, 1 << 20)), P, L, n_pal)
+    off_in, off_out = int(rng.choice([0, 0, 1, 3])), int(rng.choice([0, 0, 1, 2]))
+    spec = bool(rng.integers(0, 2))
+    out = {"spectra": _out(P, n, off_out) if spec else None, "xyz": _out(P, 3, off_out), "rgb": _out(P, 3, off_out)}
+    codec.shade_spectral(_place(torch.from_numpy(pal).cuda(), off_in), lts, _place(idx, off_in), _place(cosv, off_in),
+                         spectra=spec, out=out)
+    ref = [np.zeros((P, d), np.float32) for d in (n, 3, 3)]
+    orc.orc_shade_spectral(n, cmf_matrix(n), grid(n)[1], pal, lts, L, host(idx).view(np.uint32), host(cosv), P, *ref)
+    tag = f"case {case}: n={n} L={L} n_pal={n_pal} P={P} in+{off_in} out+{off_out} spectra={spec}"
+    for key, r in zip(("spectra", "xyz", "rgb"), ref):
+        if out[key] is not None:
+            e = rel_err(host(out[key]), r)
+            assert e <= TOL, f"{tag} {key}: rel err {e:.3e}"
+
+
+@pytest.mark.parametrize("case", range(CASES // 2))
+def test_random_roundtrip(api, ctx, orc, case):
+    rng = np.random.default_rng(9000 + case)
+    n, k, _, _, rows = _draw(rng)
+    E, D = synth.codec_weights(277 + case, k, n)
+    codec = api.Codec(ctx, E, D)
+    S = api.synth_gm_spectra(ctx, 277 + case, "sweep.spectra", int(rng.integers(0, 1 << 20)), rows, n)
+    off_in, off_out = int(rng.choice([0, 0, 1, 3])), int(rng.choice([0, 0, 1, 2]))
+    want = {key: bool(rng.integers(0, 2)) for key in ("codes", "spectra", "xyz", "rgb")}
+    if not any(want.values()):
+        want["codes"] = True
+    widths = {"codes": k, "spectra": n, "xyz": 3, "rgb": 3}
+    out = {key: _out(rows, widths[key], off_out) if want[key] else None for key in widths}
+    codec.roundtrip(_place(S, off_in), out=out)
+    ref = [np.zeros((rows, widths[key]), np.float32) for key in ("codes", "spectra", "xyz", "rgb")]
+    orc.orc_codec_roundtrip(E, D, k, n, cmf_matrix(n), grid(n)[1], host(S), rows, *ref)
+    tag = f"case {case}: n={n} k={k} rows={rows} in+{off_in} out+{off_out}"
+    for key, r in zip(("codes", "spectra", "xyz", "rgb"), ref):
+        if want[key]:
+            e = rel_err(host(out[key]), r)
+            assert e <= TOL, f"{tag} {key}: rel err {e:.3e}"
