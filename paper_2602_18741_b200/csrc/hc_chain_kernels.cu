@@ -26,7 +26,16 @@ int chain_grid(hc_ctx ctx, KernelFn fn, int smem, int64_t P, int* grid, int thre
     if (it != cache.end()) {
       occ = it->second;
     } else {
-      HC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      // The dynamic shared-memory limit is one attribute per kernel and device, while the table
+      // sizes (and so `smem`) vary per call: only ever raise it.  (Setting it to each new size
+      // lowered it under an earlier, cached, larger size, whose next launch then failed with
+      // "invalid argument" -- found by tests/test_gpu_random_sweep.py.)
+      static std::map<std::pair<const void*, int>, int> attr_max;  // (kernel, device) -> configured limit
+      int& limit = attr_max[std::make_pair(reinterpret_cast<const void*>(fn), dev)];
+      if (smem > limit) {
+        HC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        limit = smem;
+      }
       HC_CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                        cudaSharedmemCarveoutMaxShared));
       HC_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem));

@@ -131,3 +131,62 @@ def test_random_roundtrip(api, ctx, orc, case):
         if want[key]:
             e = rel_err(host(out[key]), r)
             assert e <= TOL, f"{tag} {key}: rel err {e:.3e}"
+
+
+@pytest.mark.parametrize("case", range(CASES // 2))
+def test_random_chain(api, ctx, orc, case):
+    """Latent chain: random k, table sizes, samples per pixel (multiples of 8: the ABI's constraint),
+    pixel counts (ragged pixel quads) and throughput ranges."""
+    rng = np.random.default_rng(13000 + case)
+    k = int(rng.choice([3, 6, 6, 9]))
+    n_pal = int(rng.choice([1, 2, 37, 100, 255, 256]))
+    n_ill = int(rng.choice([1, 5, 16, 200, 256]))
+    spp = 8 * int(rng.choice([1, 2, 3, 4, 8, 8, 9, 17]))
+    P = int(rng.choice([1, 3, 4, 5, 127, 777, 2049]))
+    E, D = synth.codec_weights(377 + case, k, 81)
+    codec = api.Codec(ctx, E, D)
+    pal_codes = codec.encode(torch.from_numpy(synth.palette(377 + case, n_pal, 81)).cuda())
+    ill_codes = codec.encode(torch.from_numpy(synth.lights(377 + case, n_ill, 81, purpose="scene.illuminants")).cuda())
+    ph = rng.integers(0, n_pal, (P, spp, 4), dtype=np.uint8)
+    ih = rng.integers(0, n_ill, (P, spp), dtype=np.uint8)
+    th = rng.uniform(0.0, float(rng.choice([0.5, 1.0, 1.5])), (P, spp, 4)).astype(np.float32)
+    out = codec.multibounce_latent(pal_codes, ill_codes, torch.from_numpy(ph).cuda(), torch.from_numpy(ih).cuda(),
+                                   torch.from_numpy(th).cuda(), latent=True)
+    ctx.synchronize()
+    lat = np.zeros((P, k), np.float32)
+    orc.orc_chain(k, host(pal_codes), host(ill_codes), ph, ih, th, P, spp, 4, lat)
+    tag = f"case {case}: k={k} n_pal={n_pal} n_ill={n_ill} spp={spp} P={P}"
+    e = rel_err(host(out["latent"]), lat)
+    assert e <= TOL, f"{tag} latent: rel err {e:.3e}"
+    S2, X, R = np.zeros((P, 81), np.float32), np.zeros((P, 3), np.float32), np.zeros((P, 3), np.float32)
+    orc.orc_decode(D, k, 81, lat, P, S2)
+    orc.orc_spectra_to_outputs(cmf_matrix(81), grid(81)[1], 81, S2, P, X, R)
+    for key, r in (("xyz", X), ("rgb", R)):
+        e = rel_err(host(out[key]), r)
+        assert e <= TOL, f"{tag} {key}: rel err {e:.3e}"
+
+
+@pytest.mark.parametrize("case", range(CASES // 4))
+def test_random_mlp_and_loss(api, ctx, orc, case):
+    rng = np.random.default_rng(17000 + case)
+    k = int(rng.choice([3, 6, 9]))
+    P = int(rng.choice([1, 127, 128, 129, 1000, 128 * 37 + 5, 128 * 450]))
+    w = synth.mlp_weights(477 + case, k, 64)
+    mlp = api.CodeMLP(ctx, w)
+    off = int(rng.choice([0, 0, 1, 4]))
+    rgb = _place(api.synth_uniform(ctx, 477 + case, "sweep.rgb", 0, P * 3).reshape(P, 3), off)
+    got = host(mlp.forward(rgb))
+    ref = np.zeros((P, k), np.float32)
+    orc.orc_mlp_forward(host(rgb), P, 64, k, w["w1"], w["b1"], w["w2"], w["b2"], w["w3"], w["b3"], ref)
+    e = rel_err(got, ref)
+    assert e <= 1e-2 and np.all(got >= 0), f"case {case}: mlp k={k} P={P} rgb+{off}: rel err {e:.3e}"
+
+    n = int(rng.choice([81, 81, 47]))
+    pairs = int(rng.choice([1, 63, 64, 65, 1000, 64 * 50 + 1]))
+    E, D = synth.codec_weights(477 + case, k, n)
+    codec = api.Codec(ctx, E, D)
+    A = _place(api.synth_gm_spectra(ctx, 477 + case, "sweep.a", 0, pairs, n), off)
+    B = _place(api.synth_gm_spectra(ctx, 477 + case, "sweep.b", 0, pairs, n), off)
+    got = float(host(codec.hadamard_loss(A, B))[0])
+    want = orc.orc_hadamard_loss(E, D, k, n, host(A), host(B), pairs)
+    assert got == pytest.approx(want, rel=TOL), f"case {case}: loss n={n} k={k} pairs={pairs} +{off}"
