@@ -190,3 +190,66 @@ def test_random_mlp_and_loss(api, ctx, orc, case):
     got = float(host(codec.hadamard_loss(A, B))[0])
     want = orc.orc_hadamard_loss(E, D, k, n, host(A), host(B), pairs)
     assert got == pytest.approx(want, rel=TOL), f"case {case}: loss n={n} k={k} pairs={pairs} +{off}"
+
+
+def test_random_call_sequence_on_one_context(api, ctx, orc):
+    """State carried between calls (scratch buffers that grow, cached launch configurations, the
+    frame pipeline's slots): one context and one codec per k serve a random sequence of host-buffer
+    and device calls with sizes going up and down; every result is compared with the device path
+    (bit-identical: the same kernels) and spot-checked against the oracle."""
+    rng = np.random.default_rng(4711)
+    codecs = {}
+    for k in (6, 9, 3):
+        E, D = synth.codec_weights(900 + k, k, 81)
+        codecs[k] = (api.Codec(ctx, E, D), E, D)
+    group = api.Group([0, 0, 0], "fused")
+    group_k = None
+    for step in range(40):
+        k = int(rng.choice([6, 6, 9, 3]))
+        codec, E, D = codecs[k]
+        L = int(rng.choice([8, 8, 32, 5]))
+        n_pal = int(rng.choice([256, 256, 17]))
+        W, H = int(rng.choice([1, 64, 333, 1920])), int(rng.choice([1, 2, 7, 67, 300]))
+        P = W * H
+        pal = synth.palette(900 + step, n_pal, 81)
+        lts = synth.lights(900 + step, L, 81)
+        pal_codes = codec.encode(torch.from_numpy(pal).cuda())
+        light_codes = codec.encode(torch.from_numpy(lts).cuda()).cpu().numpy()
+        idx, cosv = api.synth_gbuffer(ctx, 900 + step, 0, P, L, n_pal)
+        dev = codec.shade_latent(pal_codes, light_codes, idx, cosv)
+        want_xyz, want_rgb = host(dev["xyz"]), host(dev["rgb"])
+        h_pal, h_idx, h_cos = host(pal_codes), host(idx), host(cosv)
+        kind = str(rng.choice(["host", "frames", "group", "roundtrip"]))
+        tag = f"step {step}: {kind} k={k} L={L} n_pal={n_pal} {W}x{H}"
+        if kind == "host":
+            xyz, rgb = np.zeros((P, 3), np.float32), np.zeros((P, 3), np.float32)
+            codec.shade_latent_host(h_pal, light_codes, h_idx, h_cos, xyz, rgb)
+            assert np.array_equal(xyz, want_xyz) and np.array_equal(rgb, want_rgb), tag
+        elif kind == "frames":
+            nf = int(rng.integers(1, 5))
+            frames = [(h_idx, h_cos, np.zeros((P, 3), np.float32), np.zeros((P, 3), np.float32)) for _ in range(nf)]
+            codec.shade_latent_host_frames(h_pal, light_codes, frames)
+            for f in frames:
+                assert np.array_equal(f[2], want_xyz) and np.array_equal(f[3], want_rgb), tag
+        elif kind == "group":
+            if group_k != k:
+                group.set_codec(E, D)
+                group_k = k
+            xyz, rgb = np.zeros((P, 3), np.float32), np.zeros((P, 3), np.float32)
+            group.shade_latent_host(h_pal, light_codes, h_idx, h_cos, W, H, xyz, rgb)
+            assert np.array_equal(xyz, want_xyz) and np.array_equal(rgb, want_rgb), tag
+        else:
+            rows = max(1, P // 7)
+            S = host(api.synth_gm_spectra(ctx, 900 + step, "seq.spectra", 0, rows, 81))
+            Z, S2 = np.zeros((rows, k), np.float32), np.zeros((rows, 81), np.float32)
+            X, R = np.zeros((rows, 3), np.float32), np.zeros((rows, 3), np.float32)
+            codec.roundtrip_host(S, Z, S2, X, R)
+            ref = [np.zeros((rows, d), np.float32) for d in (k, 81, 3, 3)]
+            orc.orc_codec_roundtrip(E, D, k, 81, cmf_matrix(81), grid(81)[1], S, rows, *ref)
+            for name, got, r in zip(("codes", "spectra", "xyz", "rgb"), (Z, S2, X, R), ref):
+                assert rel_err(got, r) <= TOL, f"{tag} {name}"
+        if step % 8 == 0:  # the device path itself against the oracle
+            ref = [np.zeros((P, d), np.float32) for d in (k, 81, 3, 3)]
+            orc.orc_shade_latent(D, k, 81, cmf_matrix(81), grid(81)[1], h_pal, light_codes, L,
+                                 h_idx.view(np.uint32), h_cos, P, *ref)
+            assert rel_err(want_xyz, ref[2]) <= TOL and rel_err(want_rgb, ref[3]) <= TOL, tag
