@@ -253,3 +253,50 @@ def test_random_call_sequence_on_one_context(api, ctx, orc):
             orc.orc_shade_latent(D, k, 81, cmf_matrix(81), grid(81)[1], h_pal, light_codes, L,
                                  h_idx.view(np.uint32), h_cos, P, *ref)
             assert rel_err(want_xyz, ref[2]) <= TOL and rel_err(want_rgb, ref[3]) <= TOL, tag
+
+
+def _metric_images(rng, P, n):
+    """Linear RGB / spectra with zeros, duplicates (percentile ties), negatives and a wide range."""
+    a = (rng.lognormal(-1.0, 1.5, (P, 3)) * (rng.random((P, 3)) > 0.05)).astype(np.float32)
+    if rng.random() < 0.5 and P > 4:  # many exact ties around the percentile
+        a[rng.integers(0, P, P // 2)] = a[0]
+    if rng.random() < 0.3:
+        a[rng.integers(0, P, max(1, P // 10))] *= -1.0
+    b = (a * rng.normal(1.0, 0.05, (P, 3))).astype(np.float32)
+    s = (rng.random((P, n)) * rng.lognormal(0.0, 1.0, (P, 1))).astype(np.float32)
+    return a, b, s
+
+
+@pytest.mark.parametrize("case", range(CASES // 2))
+def test_random_metric_tail(api, ctx, orc, case):
+    """exposure_for (an exact order statistic), the 8-bit tone map and the per-pixel MSE map are
+    bit-exact; the Delta E report within 1e-12 (test_gpu_metrics.py's bars) -- at random pixel
+    counts (around the radix-select block and pass boundaries), percentiles and exposures."""
+    rng = np.random.default_rng(21000 + case)
+    n = int(rng.choice([81, 81, 47]))
+    P = int(rng.choice([1, 2, 3, 255, 256, 257, 1023, 1025, 4096, 65_537, 131_071, 262_145]))
+    E, D = synth.codec_weights(577, 6, n)
+    codec = api.Codec(ctx, E, D)
+    a, b, s = _metric_images(rng, P, n)
+    dev_ = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    ybar = np.ascontiguousarray(cmf_matrix(n)[1])
+    tag = f"case {case}: n={n} P={P}"
+    for pct in (99.5, float(rng.uniform(0, 100)), float(rng.choice([0.0, 100.0, 50.0]))):
+        assert api.exposure_for(codec, dev_(a), pct) == orc.orc_exposure_for(a, P, 3, None, grid(n)[1], pct), (tag, pct)
+        assert api.exposure_for(codec, dev_(s), pct) == orc.orc_exposure_for(s, P, n, ybar, grid(n)[1], pct), (tag, pct)
+    e = float(rng.choice([1.0, 0.37, 4.0, rng.uniform(0.01, 20.0)]))
+    got = api.tonemap_srgb8(ctx, dev_(a), e).cpu().numpy().reshape(-1)
+    want = np.zeros(P * 3, np.uint8)
+    orc.orc_tonemap_srgb8(a, P, e, want)
+    assert np.array_equal(got, want), f"{tag}: tone map, {int(np.sum(got != want))} bytes differ"
+    mse, mean = api.error_map(codec, dev_(s), dev_(b))
+    wmse = np.zeros(P, np.float32)
+    wmean = orc.orc_error_map(s, n, b, 3, P, cmf_matrix(n), grid(n)[1], wmse)
+    assert np.array_equal(mse.cpu().numpy(), wmse), f"{tag}: error map"
+    assert mean == pytest.approx(wmean, rel=1e-12), tag
+    rep = api.scene_color_report(codec, dev_(a), dev_(b))
+    wrep = np.zeros(4)
+    orc.orc_scene_color_report(a, 3, b, 3, P, cmf_matrix(n), grid(n)[1], wrep)
+    assert rep["exposure"] == wrep[3], tag
+    for key, w in (("mean_de76", wrep[0]), ("p95_de76", wrep[1]), ("mse", wrep[2])):
+        assert rep[key] == pytest.approx(w, rel=1e-12), (tag, key)
