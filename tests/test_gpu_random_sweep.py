@@ -300,3 +300,45 @@ def test_random_metric_tail(api, ctx, orc, case):
     assert rep["exposure"] == wrep[3], tag
     for key, w in (("mean_de76", wrep[0]), ("p95_de76", wrep[1]), ("mse", wrep[2])):
         assert rep[key] == pytest.approx(w, rel=1e-12), (tag, key)
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_random_render_vs_compiled_reference(api, ctx, case):
+    """The path tracer at random image sizes, sample counts, depths (fixed and
+    Russian roulette), seeds and modes: images and shading-evaluation counts bit-identical to the
+    compiled reference's render()."""
+    import ctypes as C
+
+    import oracle
+
+    rng = np.random.default_rng(25000 + case)
+    n = int(rng.choice([81, 47]))
+    ref = oracle.reference(n)
+    if ref is None:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    mode = str(rng.choice(["spectral", "latent", "rgb"]))
+    k = int(rng.choice([3, 6, 9]))
+    W, H = int(rng.integers(1, 70)), int(rng.integers(1, 50))
+    spp = int(rng.choice([1, 2, 5, 8, 16]))
+    depth = int(rng.choice([-1, 0, 1, 2, 3, 5]))
+    seed = int(rng.integers(0, 1 << 31))
+    block = bool(rng.integers(0, 2))
+    multipass = mode == "latent" and depth >= 0 and bool(rng.integers(0, 2))
+    E, D = synth.codec_weights(11 + case, k, n)
+    codec = api.Codec(ctx, E, D)
+    scene = synth.cornell_scene(n, block)
+    got = api.render(codec, scene, mode, W, H, spp, depth, seed, multipass=multipass)
+    sc, keep = api.scene_struct(scene, n)
+    job = api.HcRenderJob(api.RENDER_MODES[mode], W, H, spp, depth, seed)
+    ch = {"spectral": n, "latent": k, "rgb": 3}[mode]
+    img = np.zeros((H, W, ch), np.float32)
+    hashes = np.zeros(W * H, np.uint64)
+    ev = C.c_uint64()
+    rc = ref.ref_render(C.addressof(sc), C.addressof(job), k, E, D, int(multipass), img.reshape(-1), hashes,
+                        C.byref(ev))
+    assert rc == 0
+    g = got["image"].cpu().numpy()
+    tag = f"case {case}: {mode} n={n} k={k} {W}x{H} spp={spp} depth={depth} seed={seed} multipass={multipass}"
+    assert g.shape == img.shape, tag
+    assert np.array_equal(g, img), f"{tag}: {int(np.sum(g != img))} values differ"
+    assert got["shading_evals"] == ev.value, tag
