@@ -342,3 +342,38 @@ def test_random_render_vs_compiled_reference(api, ctx, case):
     assert g.shape == img.shape, tag
     assert np.array_equal(g, img), f"{tag}: {int(np.sum(g != img))} values differ"
     assert got["shading_evals"] == ev.value, tag
+
+
+@pytest.mark.parametrize("case", range(16))
+def test_random_training_step_vs_compiled_reference(api, ctx, case):
+    """The codec training step at random batch sizes (around the reduction's
+    30-row warps and ring slots), code sizes, betas and loss weights, with both softplus branches
+    and zero rows: losses and gradients bit-identical to the compiled reference (47-sample grid,
+    the grid its trainer is built for)."""
+    import oracle
+
+    ref = oracle.reference(47)
+    if ref is None:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    N = 47
+    rng = np.random.default_rng(29000 + case)
+    k = int(rng.choice([3, 6, 9]))
+    m = int(rng.choice([1, 2, 29, 30, 31, 59, 60, 61, 127, 128, 129, 999, 4097]))
+    beta = float(rng.choice([1.0, 10.0, 25.0]))
+    lw = tuple(float(x) for x in (rng.uniform(0, 2, 5) * (rng.random(5) > 0.3)))
+    re_ = rng.uniform(-0.5, 0.5, (k, N)) / np.sqrt(N)
+    rd = rng.uniform(-0.5, 0.5, (N, k)) / np.sqrt(k)
+    re_[0, :3] = [40.0 / beta, -35.0 / beta, 0.0]  # beta * raw > 30 and < -30, and 0
+    refl = rng.uniform(0, 1, (m, N))
+    illum = rng.uniform(0, 1, (m, N)) * rng.uniform(0.5, 2.0, (m, 1))
+    refl[rng.integers(0, m)] = 0.0
+    losses, ge, gd = api.codec_train_grad(ctx, re_, rd, beta, torch.from_numpy(refl).cuda(),
+                                          torch.from_numpy(illum).cuda(), loss_weights=lw)
+    rge, rgd, rl = np.zeros(k * N), np.zeros(N * k), np.zeros(6)
+    assert ref.ref_codec_gradients(k, beta, re_.reshape(-1), rd.reshape(-1), np.ascontiguousarray(refl.reshape(-1)),
+                                   np.ascontiguousarray(illum.reshape(-1)), m, np.array(lw),
+                                   rge.ctypes.data, rgd.ctypes.data, rl) == 0
+    tag = f"case {case}: k={k} m={m} beta={beta} lw={lw}"
+    assert ge.reshape(-1).tobytes() == rge.tobytes(), f"{tag}: encoder gradient"
+    assert gd.reshape(-1).tobytes() == rgd.tobytes(), f"{tag}: decoder gradient"
+    assert np.array(list(losses.values())).tobytes() == rl.tobytes(), f"{tag}: losses"
