@@ -377,3 +377,42 @@ def test_random_training_step_vs_compiled_reference(api, ctx, case):
     assert ge.reshape(-1).tobytes() == rge.tobytes(), f"{tag}: encoder gradient"
     assert gd.reshape(-1).tobytes() == rgd.tobytes(), f"{tag}: decoder gradient"
     assert np.array(list(losses.values())).tobytes() == rl.tobytes(), f"{tag}: losses"
+
+
+@pytest.mark.parametrize("case", range(CASES // 4))
+def test_random_passes_and_small_entry_points(api, ctx, orc, case):
+    """The k/3 three-channel passes + reassembly (bit-identical to the fused shade), encode /
+    decode / spectra_to_xyz_rgb as separate calls and blockwise_hadamard, at random sizes."""
+    rng = np.random.default_rng(33000 + case)
+    n = int(rng.choice([81, 47]))
+    k = int(rng.choice([3, 6, 9]))
+    L = int(rng.choice([1, 8, 32, 11]))
+    P = int(rng.choice([1, 5, 255, 257, 3001, 20_011]))
+    E, D = synth.codec_weights(677 + case, k, n)
+    codec = api.Codec(ctx, E, D)
+    pal_codes = codec.encode(torch.from_numpy(synth.palette(677 + case, 256, n)).cuda())
+    light_codes = codec.encode(torch.from_numpy(synth.lights(677 + case, L, n)).cuda()).cpu().numpy()
+    idx, cosv = api.synth_gbuffer(ctx, 677 + case, 0, P, L, 256)
+    fused = codec.shade_latent(pal_codes, light_codes, idx, cosv, latent=True)["latent"]
+    passes = [codec.shade_latent_pass(b, pal_codes, light_codes, idx, cosv) for b in range(k // 3)]
+    multi = api.reassemble(ctx, passes)
+    tag = f"case {case}: n={n} k={k} L={L} P={P}"
+    assert torch.equal(multi, fused), f"{tag}: passes + reassembly differ from the fused shade"
+
+    S = api.synth_gm_spectra(ctx, 677 + case, "small.spectra", 0, P, n)
+    Z = codec.encode(S)
+    Zr = np.zeros((P, k), np.float32)
+    orc.orc_encode(E, k, n, host(S), P, None, Zr)
+    assert rel_err(host(Z), Zr) <= TOL, f"{tag}: encode"
+    dec = codec.decode(torch.from_numpy(Zr).cuda(), spectra=True, xyz=True, rgb=True)
+    Sr, X, R = np.zeros((P, n), np.float32), np.zeros((P, 3), np.float32), np.zeros((P, 3), np.float32)
+    orc.orc_decode(D, k, n, Zr, P, Sr)
+    orc.orc_spectra_to_outputs(cmf_matrix(n), grid(n)[1], n, Sr, P, X, R)
+    for name, got, r in (("spectra", dec["spectra"], Sr), ("xyz", dec["xyz"], X), ("rgb", dec["rgb"], R)):
+        assert rel_err(host(got), r) <= TOL, f"{tag}: decode {name}"
+    proj = codec.spectra_to_xyz_rgb(S)
+    orc.orc_spectra_to_outputs(cmf_matrix(n), grid(n)[1], n, host(S), P, X, R)
+    assert rel_err(host(proj["xyz"]), X) <= TOL and rel_err(host(proj["rgb"]), R) <= TOL, f"{tag}: project"
+    A = api.synth_uniform(ctx, 677 + case, "small.a", 0, P * k).reshape(P, k)
+    B = api.synth_uniform(ctx, 677 + case, "small.b", 0, P * k).reshape(P, k)
+    assert np.array_equal(host(api.blockwise_hadamard(ctx, A, B)), host(A) * host(B)), f"{tag}: hadamard"
