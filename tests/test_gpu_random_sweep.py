@@ -416,3 +416,52 @@ def test_random_passes_and_small_entry_points(api, ctx, orc, case):
     A = api.synth_uniform(ctx, 677 + case, "small.a", 0, P * k).reshape(P, k)
     B = api.synth_uniform(ctx, 677 + case, "small.b", 0, P * k).reshape(P, k)
     assert np.array_equal(host(api.blockwise_hadamard(ctx, A, B)), host(A) * host(B)), f"{tag}: hadamard"
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_random_encode_decode_tools_vs_compiled_reference(api, ctx, tmp_path, case):
+    """The `encode` / `decode` tools on random measurement grids (regular and
+    irregular, narrower and wider than the codec's band, 1 to ~700 samples), row counts, id columns,
+    value precisions, blank lines and k: output files byte-identical to the compiled reference."""
+    import ctypes
+
+    import oracle
+
+    ref = oracle.reference(47)
+    if ref is None:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    N = 47
+    rng = np.random.default_rng(37000 + case)
+    k = int(rng.choice([3, 6, 9]))
+    re_ = rng.uniform(-0.5, 0.5, (k, N)) / np.sqrt(N)
+    rd = rng.uniform(-0.5, 0.5, (N, k)) / np.sqrt(N)
+    codec = api.Codec.from_raw(ctx, re_, rd, beta=10.0)
+    m = int(rng.choice([1, 2, 17, 61, 95, 300, 700]))
+    lo = float(rng.uniform(300, 450))
+    if rng.random() < 0.5:
+        wl = lo + np.arange(m) * float(rng.choice([0.5, 1.0, 2.0, 5.0, 10.0]))
+    else:
+        wl = np.cumsum(np.r_[lo, rng.uniform(0.3, 9.0, m - 1)]) if m > 1 else np.array([lo])
+    rows = int(rng.choice([1, 2, 33, 257, 1500]))
+    ids = bool(rng.integers(0, 2))
+    head = (["id"] if ids else []) + ["%.9g" % w for w in wl]
+    lines = [",".join(head)]
+    for r in range(rows):
+        v = np.clip(rng.normal(0.5, 0.3, m), 0, None) * rng.uniform(0.1, 3.0)
+        cells = (["s%05d" % r] if ids else []) + ["%.*g" % (int(rng.integers(3, 17)), x) for x in v]
+        lines.append(", ".join(cells) if r % 7 == 0 else ",".join(cells))
+        if r % 11 == 0:
+            lines.append("  ")
+    data = ("\n".join(lines) + "\n").encode()
+    src, codes_ref, spec_ref = tmp_path / "s.csv", tmp_path / "codes.csv", tmp_path / "dec.csv"
+    src.write_bytes(data)
+    err = ctypes.create_string_buffer(512)
+    flat = lambda a: np.ascontiguousarray(a.reshape(-1))
+    tag = f"case {case}: k={k} grid={m} samples from {lo:.1f} nm, rows={rows}, ids={ids}"
+    assert ref.ref_run_encode(str(src).encode(), k, 10.0, flat(re_), flat(rd), str(codes_ref).encode(), err,
+                              512) == 0, (tag, err.value)
+    got = api.encode_tool(codec, data)
+    assert got == codes_ref.read_bytes(), f"{tag}: encode tool output differs"
+    assert ref.ref_run_decode(str(codes_ref).encode(), k, 10.0, flat(re_), flat(rd), str(spec_ref).encode(), err,
+                              512) == 0, (tag, err.value)
+    assert api.decode_tool(codec, got) == spec_ref.read_bytes(), f"{tag}: decode tool output differs"
