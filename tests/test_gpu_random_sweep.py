@@ -465,3 +465,38 @@ def test_random_encode_decode_tools_vs_compiled_reference(api, ctx, tmp_path, ca
     assert ref.ref_run_decode(str(codes_ref).encode(), k, 10.0, flat(re_), flat(rd), str(spec_ref).encode(), err,
                               512) == 0, (tag, err.value)
     assert api.decode_tool(codec, got) == spec_ref.read_bytes(), f"{tag}: decode tool output differs"
+
+
+@pytest.mark.parametrize("case", range(12))
+def test_random_upsampler_vs_compiled_reference(api, ctx, case):
+    """The reference's fp64 SiLU upsampler (upsampler.cpp:42-72, :170-190) at random widths, code
+    sizes, texel counts and input ranges: codes within 1e-13 of the compiled reference (SiLU's exp
+    is CUDA's), clamp counts exact."""
+    import ctypes
+
+    import oracle
+
+    ref = oracle.reference(81)
+    if ref is None:
+        pytest.skip("compiled reference (oracle/_ref) not built")
+    rng = np.random.default_rng(41000 + case)
+    k = int(rng.choice([3, 6, 9, 12]))
+    hidden = int(rng.choice([1, 7, 17, 32, 64, 100, 128, 257, 512]))
+    P = int(rng.choice([1, 31, 32, 33, 1000, 4097]))
+    clamp = bool(rng.integers(0, 2))
+    lim = lambda fi, fo: np.sqrt(6.0 / (fi + fo))  # noqa: E731
+    w = {"w1": rng.uniform(-lim(3, hidden), lim(3, hidden), (hidden, 3)), "b1": rng.normal(0, 0.1, hidden),
+         "w2": rng.uniform(-lim(hidden, hidden), lim(hidden, hidden), (hidden, hidden)),
+         "b2": rng.normal(0, 0.1, hidden),
+         "w3": rng.uniform(-lim(hidden, k), lim(hidden, k), (k, hidden)), "b3": rng.normal(0, 0.1, k)}
+    rgb = rng.uniform(-0.1, float(rng.choice([1.0, 1.2, 50.0])), (P, 3))
+    got, n = api.Upsampler(ctx, w).forward(torch.from_numpy(rgb).cuda(), clamp=clamp)
+    got = got.cpu().numpy()
+    want = np.zeros((P, k))
+    rn = ctypes.c_uint64(0)
+    arrs = [np.ascontiguousarray(w[x].reshape(-1)) for x in api.Upsampler.KEYS]
+    assert ref.ref_upsample(k, hidden, *arrs, np.ascontiguousarray(rgb.reshape(-1)), P, int(clamp),
+                            want.reshape(-1), ctypes.byref(rn)) == 0
+    tag = f"case {case}: k={k} hidden={hidden} P={P} clamp={clamp}"
+    assert n == rn.value, f"{tag}: clamp count {n} vs {rn.value}"
+    np.testing.assert_allclose(got, want, rtol=1e-13, atol=1e-13 * max(np.abs(want).max(), 1e-300), err_msg=tag)
