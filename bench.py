@@ -1100,6 +1100,28 @@ def run_ours(args) -> int:
             for f in frames:
                 f.close()
 
+    # ---- config 5b across ranks: the per-rank fp64 partial sums are all-reduced (the one exchange
+    # step this path has); compute + all-reduce per step, N > 1 only
+    if world > 1 and args.config == "5b":
+        from paper_2602_18741_b200.sharding import reduce_loss
+
+        gsteps = min(steps, 20)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for i in range(gsteps):
+                wl.step(i)
+                reduce_loss(wl.sum)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ams = _max_over_ranks(torch, dist, world, e0.elapsed_time(e1))
+        extra["with_allreduce"] = {"value": wl.units * world * gsteps / (ams / 1e3) / 1e6, "unit": cfg["unit"],
+                                   "ms_per_step": ams / gsteps, "total_loss": float(wl.sum.item()),
+                                   "reduced": "per-rank fp64 partial sums -> total on every rank "
+                                              "(sharding.reduce_loss: one NCCL all-reduce of one double)"}
+
     # ---- e2e through the host-buffer C-ABI call (config 2)
     e2e = None
     if args.config == "2":

@@ -78,6 +78,24 @@ def gather_rows(local: torch.Tensor, band: Band, height: int, dst: int = 0) -> t
     return torch.cat(out, dim=0)
 
 
+def pair_range(rank: int, world: int, pairs: int) -> tuple[int, int]:
+    """Contiguous index range [first, first + count) of rank `rank` over `pairs` items (spectra, pairs,
+    texels): the row-band split with one item per row."""
+    b = row_band(rank, world, pairs, 1)
+    return b.first_pixel, b.pixels
+
+
+def reduce_loss(partial: torch.Tensor) -> torch.Tensor:
+    """The near-multiplicativity loss over sharded pairs: every rank's fp64 partial sum
+    (`Codec.hadamard_loss` on its own pairs) is summed over the ranks by one all-reduce -- the only
+    exchange step this path has.  Returns the total on every rank (in place)."""
+    if partial.dtype != torch.float64:
+        raise TypeError("reduce_loss: the partial sums are fp64")
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(partial, op=dist.ReduceOp.SUM)
+    return partial
+
+
 class _DevicePointer:
     """A raw device pointer as a __cuda_array_interface__ object (float32, C-contiguous)."""
 

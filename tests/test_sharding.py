@@ -13,7 +13,7 @@ import torch.multiprocessing as mp
 
 from paper_2602_18741_b200 import synth
 from paper_2602_18741_b200.colorimetry import cmf_matrix, grid
-from paper_2602_18741_b200.sharding import gather_rows, row_band
+from paper_2602_18741_b200.sharding import gather_rows, pair_range, reduce_loss, row_band
 
 W, H, L, K, SEED = 37, 23, 8, 6, 5
 
@@ -81,3 +81,49 @@ def test_two_rank_gloo_gather_matches_single_process(tmp_path):
     want = _shade_rows(oracle.oracle(), 0, W * H)
     assert got.shape == want.shape
     assert np.array_equal(got, want)
+
+
+# ---- config 5b across ranks: pairs split by index range, fp64 partial sums all-reduced
+PAIRS = 1001
+
+
+def _loss_pairs(first: int, count: int):
+    a = synth.gm_spectra_ctr(SEED, "loss.a", first, count, 81)
+    b = synth.gm_spectra_ctr(SEED, "loss.b", first, count, 81)
+    return np.ascontiguousarray(a, np.float32), np.ascontiguousarray(b, np.float32)
+
+
+def _loss_worker(rank: int, world: int, port: int, out_path: str):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+
+    orc = oracle.oracle()
+    E, D = synth.codec_weights(SEED, K, 81)
+    first, count = pair_range(rank, world, PAIRS)
+    a, b = _loss_pairs(first, count)
+    partial = torch.tensor([orc.orc_hadamard_loss(E, D, K, 81, a, b, count)], dtype=torch.float64)
+    total = reduce_loss(partial)
+    np.save(out_path + f".{rank}.npy", total.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_pair_ranges_partition_the_pairs():
+    for world in (1, 2, 3, 8):
+        rs = [pair_range(r, world, PAIRS) for r in range(world)]
+        assert rs[0][0] == 0 and rs[-1][0] + rs[-1][1] == PAIRS
+        assert all(a[0] + a[1] == b[0] for a, b in zip(rs, rs[1:]))
+
+
+def test_two_rank_gloo_loss_allreduce_matches_single_process(tmp_path):
+    import oracle
+
+    out = str(tmp_path / "loss")
+    mp.spawn(_loss_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    E, D = synth.codec_weights(SEED, K, 81)
+    a, b = _loss_pairs(0, PAIRS)
+    want = oracle.oracle().orc_hadamard_loss(E, D, K, 81, a, b, PAIRS)
+    got = [float(np.load(out + f".{rank}.npy")[0]) for rank in range(2)]
+    assert got[0] == got[1]  # every rank holds the same total
+    assert got[0] == pytest.approx(want, rel=1e-12)  # two fp64 partials vs one sequential sum
