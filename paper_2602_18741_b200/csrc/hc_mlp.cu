@@ -18,13 +18,16 @@
 // MMA reads directly ("A from TMEM").  With A in shared memory (SS) the 128 x 16 A
 // tile is re-read from smem by every MMA and smem bandwidth was the limit.
 //
-// One CTA per SM, 4 tile streams.  Each stream owns 112 TMEM columns of the CTA's
-// 512: [0,32) the packed bf16 A operand (A2 of a tile, then its A3), [32,96) the
-// fp32 layer-1/2 accumulator, [96,112) the layer-3 accumulator; the constant K chunk
-// of A2 (the b2 column) is one 8-column region at 448 shared by all streams.  With D3
-// separate, layer 1 of the next tile runs while layer 3 still reads A3; 4 streams
-// instead of 3 keep more tiles in flight, which is what the latency-bound chain needs
-// (the epilogue warps spend most of their time waiting on MMA completions).
+// One CTA per SM, 3 tile streams (default).  Each stream owns 144 TMEM columns of the CTA's
+// 512: [0,32) the packed bf16 A2 operand, [32,64) the packed bf16 A3 operand, [64,128) the fp32
+// layer-1/2 accumulator, [128,144) the layer-3 accumulator; the constant K chunk of A2 (the b2
+// column) is one 8-column region at 432 shared by all streams.  With A3 and D3 in their own
+// regions, layer 1 of the next tile is issued right after epilogue 2 (ahead of this tile's
+// layer 3) and no epilogue waits for its own layer 3.  The chain per tile is two commit round
+// trips (~470 cycles each, whatever the number of MMAs) + two epilogues (~290 each); throughput
+// is tiles in flight over that latency, and TMEM caps the tiles in flight (measured variants:
+// HC_MLP_STREAMS=4 with A3 over A2, 112 columns per stream; HC_MLP_PP ping-pong layout, 128
+// columns; HC_MLP_A3_SMEM -- profiles/r02/mlp_ceiling_probe.txt, mma_chains.txt).
 // A stream also has a 4 KB A1 tile and a 2-deep ring of rgb tiles fetched by 1-D
 // bulk copies (TMA), 4 epilogue warps (one per TMEM lane quarter) and one MMA-issuer
 // warp: tools/mma_probe3.cu measured that one thread can issue a tcgen05.mma only
