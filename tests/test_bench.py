@@ -68,3 +68,21 @@ def test_gpu_arm_line():
     assert line["clocks"]["sm_max_mhz"] > 0
     d = line["ms_per_step_dist"]
     assert d["p10"] <= d["p50"] <= d["p90"]
+
+
+def test_step_replayer_splits_any_step_count_exactly():
+    """The graph schedule of the timed region: one graph of exactly K steps up to the chunk size,
+    else whole chunks (multiples of the buffer rotation) plus one remainder graph -- always K steps."""
+    import bench
+
+    rep = bench.StepReplayer.__new__(bench.StepReplayer)
+    for R, per_step in ((8, 1), (2, 1), (1, 1), (4, 3)):
+        rep.chunk = max(R, bench.StepReplayer.MAX_NODES // per_step // R * R)
+        assert rep.chunk % R == 0
+        for n in (0, 1, 7, 20, 37, 400, rep.chunk - 1, rep.chunk, rep.chunk + 1, 3 * rep.chunk + 5, 5000):
+            parts = rep._parts(n)
+            assert sum(size * reps for size, reps in parts) == n
+            assert all(0 < size <= rep.chunk and reps >= 1 for size, reps in parts)
+            assert len(parts) <= 2
+            if n > rep.chunk:  # every graph but the last starts and ends on a rotation boundary
+                assert parts[0][0] == rep.chunk
